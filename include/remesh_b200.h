@@ -1,0 +1,134 @@
+/*
+ * remesh_b200.h -- C-ABI of the B200-native re-indexing hot path.
+ *
+ * The reference (remeshx 0.1.0, /root/reference/pkg) is a pure Python/numpy
+ * package with no FFI; its operator API is the module-level Python function
+ *
+ *     reindex(mesh: Mesh) -> tuple[Mesh, ReindexScratch]      pipeline.py:133-157
+ *
+ * re-exported at __init__.py:12-15 and bound by name in ops.py:7, cli.py:17,
+ * bench.py:19 and testing.py:18.  This header is the native boundary that
+ * the Python drop-in (paper_2109_09812_b200.pipeline.reindex) calls through
+ * ctypes.  Plain pointers and sizes only; no torch types.  All pointers
+ * except the host-side `rmx_scratch` struct itself are DEVICE pointers; every
+ * call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy default)
+ * and never allocates: the caller owns every buffer, including the
+ * workspace sized by rmx_workspace_bytes().
+ *
+ * Vertex data is handled exclusively as uint32 words (the reference's
+ * `vertex_bits`, mesh.py:91-94): ordering is raw unsigned bit order,
+ * component 0 most significant (primitives.py:23-27); equality is bitwise.
+ */
+#ifndef REMESH_B200_H
+#define REMESH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define RMX_OK        0
+#define RMX_EINVAL    1   /* bad shape/pointer/size (reference: MeshError, mesh.py:55-60) */
+#define RMX_ERANGE    2   /* n_vertices >= 2^32 (reference: MeshError, mesh.py:59-60)    */
+#define RMX_ECUDA     3   /* a CUDA runtime call failed                                 */
+#define RMX_ENOSPC    4   /* workspace smaller than rmx_workspace_bytes()               */
+
+/* bits of the device status word written by the pipeline */
+#define RMX_STATUS_INDEX_OUT_OF_RANGE 1u   /* reference: InvalidMeshError, mesh.py:103-105 */
+
+/* largest vertex dimension the CUDA path accepts (reference: unbounded) */
+#define RMX_MAX_DIM 32
+
+/* Optional intermediates of one run (reference ReindexScratch, pipeline.py:24-38).
+ * Any field may be NULL; all are device pointers of length n_vertices. */
+typedef struct rmx_scratch {
+    uint8_t*  is_used;   /* bool per input vertex          (pipeline.py:41-51)   */
+    uint32_t* org_id;    /* origin of each sorted slot      (pipeline.py:66-69)   */
+    uint8_t*  nodup;     /* first-occurrence flag per slot  (pipeline.py:72-83)   */
+    uint32_t* new_idx;   /* compacted destination per slot  (pipeline.py:86-94)   */
+    uint32_t* perm;      /* inverse of org_id               (pipeline.py:103-113) */
+} rmx_scratch;
+
+/* Library identification. */
+const char* rmx_version(void);
+const char* rmx_strerror(int code);
+
+/* Bytes of device workspace rmx_reindex needs for this problem size
+ * (the "two copies of vertex and index data" of SPEC.md are the caller's
+ * in/out buffers; this is the sort ping-pong, flags, map and look-back state). */
+size_t rmx_workspace_bytes(uint64_t n_vertices, uint32_t dim,
+                           uint64_t n_elements, uint32_t arity);
+
+/*
+ * Full re-indexing pipeline.  Replaces remeshx.reindex (pipeline.py:133-157)
+ * and every step it calls:
+ *   require_valid    mesh.py:103-105       -> status bit, checked by caller
+ *   mark_used        pipeline.py:41-51     -> K1  mark scatter
+ *   overwrite_unused pipeline.py:54-63     -> K1b replace + row build + digit histograms
+ *   compute_sort_permutation / key_value_sort / bitwise_sort_order
+ *                    pipeline.py:66-69, primitives.py:23-40 -> K2 onesweep LSD passes
+ *   flag_first_occurrences, compute_new_indices, compact_vertices, invert_permutation
+ *                    pipeline.py:72-113    -> K3 head flag + look-back scan + map + gather
+ *   remap_elements   pipeline.py:116-130   -> K4 remap
+ *
+ * vtx_bits     [n_vertices * dim]   input vertex words (row-major)
+ * idx          [n_elements * arity] input element indices (row-major)
+ * out_vtx_bits [n_vertices * dim]   capacity; the first *d_new_count rows are the result
+ * out_idx      [n_elements * arity] remapped indices
+ * d_new_count  device uint64: number of output vertices
+ * d_status     device uint32: RMX_STATUS_* bits (non-zero => outputs are undefined)
+ * scratch      NULL, or host struct of device pointers to fill
+ * stream       cudaStream_t
+ * Zero elements: writes new_count = 0 and is_used = all false, like pipeline.py:142-146.
+ */
+int rmx_reindex(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim,
+                const uint32_t* idx, uint64_t n_elements, uint32_t arity,
+                uint32_t* out_vtx_bits, uint32_t* out_idx,
+                uint64_t* d_new_count, uint32_t* d_status,
+                void* workspace, size_t workspace_bytes,
+                const rmx_scratch* scratch, void* stream);
+
+/* Same as rmx_reindex, additionally recording `events[k]` (cudaEvent_t
+ * handles created by the caller) on `stream` after the k-th stage boundary,
+ * k = 0 .. min(n_events, rmx_stage_count(dim)) - 1.  Stage 0 is the start.
+ * Used by bench.py to time each kernel live inside the timed region. */
+int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim,
+                         const uint32_t* idx, uint64_t n_elements, uint32_t arity,
+                         uint32_t* out_vtx_bits, uint32_t* out_idx,
+                         uint64_t* d_new_count, uint32_t* d_status,
+                         void* workspace, size_t workspace_bytes,
+                         const rmx_scratch* scratch, void* stream,
+                         void* const* events, int n_events);
+
+/* Number of stage-boundary events rmx_reindex_profiled records for `dim`, and
+ * the name of the kernel that runs between event k-1 and event k. */
+int rmx_stage_count(uint32_t dim);
+const char* rmx_stage_name(uint32_t dim, int k);
+
+/* Sort passes actually executed by the last call on this thread (digit
+ * passes whose 8-bit digit is constant over all keys are skipped). Host-side
+ * diagnostic: reads the device plan, so it synchronises `stream`. */
+int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream);
+
+/*
+ * Synthetic lattice soups of BASELINE.md section 3 (bench input generator;
+ * not part of the reference interface).  kind 0 = triangles (dim 3, arity 3,
+ * cells nx*ny), kind 1 = Kuhn tetrahedra (dim 4, arity 4, cells nx*ny*nz).
+ * Writes n_vertices*dim words to out_vtx_bits and n_elem_take*arity indices
+ * to out_idx, bit-identical to oracle/lattice.py:lattice_soup.
+ * rmx_lattice_sizes reports (n_elements_total, n_vertices_for_take).
+ */
+int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz,
+                      uint64_t n_elem_take, uint64_t* n_elements, uint64_t* n_vertices);
+int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed,
+                         uint64_t n_elem_take, uint32_t* out_vtx_bits, uint32_t* out_idx,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REMESH_B200_H */

@@ -1,0 +1,419 @@
+// rmx_capi.cu -- C-ABI entry points (include/remesh_b200.h) and the host-side
+// stream orchestration of the re-indexing pipeline.  No allocation, no
+// synchronisation on the hot path: every launch is stream-ordered on the
+// caller's stream and reads its control words (status, plan) from device
+// memory, so the whole sequence is CUDA-graph capturable.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/remesh_b200.h"
+#include "rmx_kernels.cuh"
+
+namespace {
+
+using namespace rmx;
+
+thread_local char g_err[256] = "";
+
+int fail_cuda(cudaError_t e, const char* what) {
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return RMX_ECUDA;
+}
+
+#define RMX_CHECK(call)                                         \
+    do {                                                        \
+        cudaError_t e_ = (call);                                \
+        if (e_ != cudaSuccess) return fail_cuda(e_, #call);     \
+    } while (0)
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+// Per-W kernel choices (items per thread).  W = dim + 1.
+constexpr int kSortIptNarrow = 16;  // W <= 2
+constexpr int kSortIpt = 8;         // W in 3..5
+constexpr int kSortIptWide = 2;     // generic W
+constexpr int kUniqIpt = 8;
+constexpr int kUniqIptWide = 2;
+
+int sort_tile(int W) { return kBlock * (W <= 2 ? kSortIptNarrow : (W <= 5 ? kSortIpt : kSortIptWide)); }
+int uniq_tile(int W) { return kBlock * (W <= 5 ? kUniqIpt : kUniqIptWide); }
+
+struct Layout {
+    int D, W, P;
+    uint32_t ntiles, ntiles3;
+    size_t flags, rows0, rows1, map, plan;
+    size_t ctl_begin, hist, counters, desc, desc3, ctl_end;
+    size_t total;
+};
+
+Layout make_layout(uint64_t V, uint32_t D) {
+    Layout L{};
+    L.D = static_cast<int>(D);
+    L.W = L.D + 1;
+    L.P = 4 * L.D;
+    L.ntiles = static_cast<uint32_t>((V + sort_tile(L.W) - 1) / sort_tile(L.W));
+    L.ntiles3 = static_cast<uint32_t>((V + uniq_tile(L.W) - 1) / uniq_tile(L.W));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = off;
+        off = align_up(off + bytes);
+        return at;
+    };
+    const size_t row_bytes = static_cast<size_t>(V) * L.W * 4 + 16;  // +16: bulk copies round up
+    L.flags = take(V);
+    L.rows0 = take(row_bytes);
+    L.rows1 = take(row_bytes);
+    L.map = take(static_cast<size_t>(V) * 4);
+    L.plan = take(plan_words(L.P) * 4);
+    L.ctl_begin = off;
+    L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
+    L.counters = take(static_cast<size_t>(L.P + 2) * 4);
+    L.desc = take(static_cast<size_t>(L.ntiles) * 256 * 8);
+    L.desc3 = take(static_cast<size_t>(L.ntiles3) * 8);
+    L.ctl_end = off;
+    L.total = off;
+    return L;
+}
+
+// ---- per-device cached launch facts -------------------------------------
+struct DeviceFacts {
+    int sms = 0;
+};
+std::mutex g_mu;
+DeviceFacts g_dev[64];
+
+int device_sms(int& sms) {
+    int dev = 0;
+    RMX_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return fail_cuda(cudaErrorInvalidDevice, "device id");
+    if (g_dev[dev].sms == 0) RMX_CHECK(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+    sms = g_dev[dev].sms;
+    return RMX_OK;
+}
+
+// Persistent grid size for a kernel: resident CTAs per SM x SMs.
+template <typename K>
+int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
+    int sms = 0;
+    int rc = device_sms(sms);
+    if (rc) return rc;
+    if (smem > 48 * 1024) RMX_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    RMX_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
+    if (per_sm < 1) per_sm = 1;
+    uint64_t g = static_cast<uint64_t>(per_sm) * sms;
+    if (work_items < g) g = work_items;
+    grid = static_cast<int>(g < 1 ? 1 : g);
+    return RMX_OK;
+}
+
+// ---- kernel dispatch by compile-time width --------------------------------
+template <int D_CT>
+int launch_build(const BuildArgs& a, cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(4 * a.dim) * 256 * 4;
+    int grid = 0;
+    int rc = persistent_grid(k_build_rows<D_CT>, smem, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
+    if (rc) return rc;
+    k_build_rows<D_CT><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+template <int W_CT, int IPT>
+int launch_pass(const SortArgs& a, cudaStream_t s) {
+    const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
+    int grid = 0;
+    int rc = persistent_grid(k_sort_pass<W_CT, IPT>, smem, a.ntiles, grid);
+    if (rc) return rc;
+    k_sort_pass<W_CT, IPT><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+template <int W_CT, int IPT>
+int launch_unique(const UniqueArgs& a, cudaStream_t s) {
+    const size_t smem = UniqueTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
+    int grid = 0;
+    int rc = persistent_grid(k_unique<W_CT, IPT>, smem, a.ntiles, grid);
+    if (rc) return rc;
+    k_unique<W_CT, IPT><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int dispatch_build(const BuildArgs& a, cudaStream_t s) {
+    switch (a.dim) {
+        case 1: return launch_build<1>(a, s);
+        case 2: return launch_build<2>(a, s);
+        case 3: return launch_build<3>(a, s);
+        case 4: return launch_build<4>(a, s);
+        default: return launch_build<0>(a, s);
+    }
+}
+
+int dispatch_pass(const SortArgs& a, cudaStream_t s) {
+    switch (a.dim + 1) {
+        case 2: return launch_pass<2, kSortIptNarrow>(a, s);
+        case 3: return launch_pass<3, kSortIpt>(a, s);
+        case 4: return launch_pass<4, kSortIpt>(a, s);
+        case 5: return launch_pass<5, kSortIpt>(a, s);
+        default: return launch_pass<0, kSortIptWide>(a, s);
+    }
+}
+
+int dispatch_unique(const UniqueArgs& a, cudaStream_t s) {
+    switch (a.dim + 1) {
+        case 2: return launch_unique<2, kUniqIpt>(a, s);
+        case 3: return launch_unique<3, kUniqIpt>(a, s);
+        case 4: return launch_unique<4, kUniqIpt>(a, s);
+        case 5: return launch_unique<5, kUniqIpt>(a, s);
+        default: return launch_unique<0, kUniqIptWide>(a, s);
+    }
+}
+
+int grid_for_stream(uint64_t items, int& grid) {
+    int sms = 0;
+    int rc = device_sms(sms);
+    if (rc) return rc;
+    uint64_t g = (items + kBlock - 1) / kBlock;
+    const uint64_t cap = static_cast<uint64_t>(sms) * 16;
+    if (g > cap) g = cap;
+    grid = static_cast<int>(g < 1 ? 1 : g);
+    return RMX_OK;
+}
+
+struct Recorder {
+    void* const* events;
+    int n;
+    int k = 0;
+    cudaStream_t s;
+    int mark() {
+        if (events && k < n && events[k]) RMX_CHECK(cudaEventRecord(static_cast<cudaEvent_t>(events[k]), s));
+        ++k;
+        return RMX_OK;
+    }
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* idx, uint64_t E, uint32_t K,
+                 uint32_t* out_vtx, uint32_t* out_idx, uint64_t* d_count, uint32_t* d_status, void* ws,
+                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events) {
+    g_err[0] = '\0';
+    if (D < 1 || K < 1) {
+        std::snprintf(g_err, sizeof(g_err), "dim and arity must be >= 1 (got %u, %u)", D, K);
+        return RMX_EINVAL;
+    }
+    if (D > RMX_MAX_DIM) {
+        std::snprintf(g_err, sizeof(g_err), "dim %u exceeds the CUDA path limit %d", D, RMX_MAX_DIM);
+        return RMX_EINVAL;
+    }
+    if (V >= (1ull << 32)) {
+        std::snprintf(g_err, sizeof(g_err), "vertex count %llu exceeds 32-bit index range",
+                      static_cast<unsigned long long>(V));
+        return RMX_ERANGE;
+    }
+    if (!d_count || !d_status) {
+        std::snprintf(g_err, sizeof(g_err), "d_new_count and d_status are required");
+        return RMX_EINVAL;
+    }
+    const uint64_t I = E * K;
+    Recorder rec{events, n_events, 0, s};
+    int rc = rec.mark();
+    if (rc) return rc;
+    RMX_CHECK(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s));
+    RMX_CHECK(cudaMemsetAsync(d_status, 0, sizeof(uint32_t), s));
+    if (E == 0) {  // pipeline.py:142-146: every vertex unused, empty result
+        if (sc && sc->is_used && V) RMX_CHECK(cudaMemsetAsync(sc->is_used, 0, V, s));
+        return RMX_OK;
+    }
+    if ((V && !vtx) || !idx || !out_idx || (V && !out_vtx)) {
+        std::snprintf(g_err, sizeof(g_err), "null buffer");
+        return RMX_EINVAL;
+    }
+    const Layout L = make_layout(V, D);
+    if (!ws || ws_bytes < L.total) {
+        std::snprintf(g_err, sizeof(g_err), "workspace %zu bytes < required %zu", ws_bytes, L.total);
+        return RMX_ENOSPC;
+    }
+    char* base = static_cast<char*>(ws);
+    uint8_t* flags = (sc && sc->is_used) ? sc->is_used : reinterpret_cast<uint8_t*>(base + L.flags);
+    uint32_t* rows0 = reinterpret_cast<uint32_t*>(base + L.rows0);
+    uint32_t* rows1 = reinterpret_cast<uint32_t*>(base + L.rows1);
+    uint32_t* map = reinterpret_cast<uint32_t*>(base + L.map);
+    uint32_t* plan = reinterpret_cast<uint32_t*>(base + L.plan);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
+    uint32_t* counters = reinterpret_cast<uint32_t*>(base + L.counters);
+    uint64_t* desc = reinterpret_cast<uint64_t*>(base + L.desc);
+    uint64_t* desc3 = reinterpret_cast<uint64_t*>(base + L.desc3);
+
+    RMX_CHECK(cudaMemsetAsync(base + L.ctl_begin, 0, L.ctl_end - L.ctl_begin, s));
+    if (V) RMX_CHECK(cudaMemsetAsync(flags, 0, V, s));
+
+    // K1 mark
+    {
+        MarkArgs a{idx, I, V, flags, d_status, aligned16(idx) ? 1 : 0};
+        int grid = 0;
+        rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
+        if (rc) return rc;
+        k_mark<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(cudaGetLastError());
+    }
+    if ((rc = rec.mark())) return rc;
+    if (V == 0) {  // every index is out of range; status is set
+        return RMX_OK;
+    }
+    // K1b rows + histograms
+    {
+        BuildArgs a{vtx, flags, idx, rows0, hist, d_status, static_cast<uint32_t>(V), L.D};
+        if ((rc = dispatch_build(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    k_plan<<<1, kBlock, 0, s>>>(hist, plan, L.P, static_cast<uint32_t>(V), d_status);
+    RMX_CHECK(cudaGetLastError());
+    if ((rc = rec.mark())) return rc;
+    // K2 onesweep passes, least significant digit first
+    for (int p = 0; p < L.P; ++p) {
+        SortArgs a{rows0, rows1, plan, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p};
+        if ((rc = dispatch_pass(a, s))) return rc;
+        if ((rc = rec.mark())) return rc;
+    }
+    // K3 unique
+    {
+        UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, d_status, map, out_vtx,
+                     reinterpret_cast<unsigned long long*>(d_count),
+                     sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
+                     sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D};
+        if ((rc = dispatch_unique(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    // K4 remap
+    {
+        RemapArgs a{idx, map, out_idx, I, d_status, (aligned16(idx) && aligned16(out_idx)) ? 1 : 0};
+        int grid = 0;
+        rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
+        if (rc) return rc;
+        k_remap<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(cudaGetLastError());
+    }
+    return rec.mark();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rmx_version(void) { return "paper_2109_09812_b200 0.1.0 (sm_100a)"; }
+
+const char* rmx_strerror(int code) {
+    switch (code) {
+        case RMX_OK: return "ok";
+        case RMX_EINVAL: return g_err[0] ? g_err : "invalid argument";
+        case RMX_ERANGE: return g_err[0] ? g_err : "vertex count exceeds 32-bit index range";
+        case RMX_ECUDA: return g_err[0] ? g_err : "CUDA error";
+        case RMX_ENOSPC: return g_err[0] ? g_err : "workspace too small";
+        default: return "unknown error";
+    }
+}
+
+size_t rmx_workspace_bytes(uint64_t n_vertices, uint32_t dim, uint64_t n_elements, uint32_t arity) {
+    (void)n_elements;
+    (void)arity;
+    if (dim < 1 || dim > RMX_MAX_DIM) return 0;
+    return make_layout(n_vertices, dim).total;
+}
+
+int rmx_reindex(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,
+                uint64_t n_elements, uint32_t arity, uint32_t* out_vtx_bits, uint32_t* out_idx,
+                uint64_t* d_new_count, uint32_t* d_status, void* workspace, size_t workspace_bytes,
+                const rmx_scratch* scratch, void* stream) {
+    return run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
+                        d_status, workspace, workspace_bytes, scratch, static_cast<cudaStream_t>(stream), nullptr,
+                        0);
+}
+
+int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,
+                         uint64_t n_elements, uint32_t arity, uint32_t* out_vtx_bits, uint32_t* out_idx,
+                         uint64_t* d_new_count, uint32_t* d_status, void* workspace, size_t workspace_bytes,
+                         const rmx_scratch* scratch, void* stream, void* const* events, int n_events) {
+    return run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
+                        d_status, workspace, workspace_bytes, scratch, static_cast<cudaStream_t>(stream), events,
+                        n_events);
+}
+
+int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6; }
+
+const char* rmx_stage_name(uint32_t dim, int k) {
+    static thread_local char buf[32];
+    const int P = static_cast<int>(4 * dim);
+    if (k == 0) return "start";
+    if (k == 1) return "mark";
+    if (k == 2) return "build_rows";
+    if (k == 3) return "plan";
+    if (k >= 4 && k < 4 + P) {
+        std::snprintf(buf, sizeof(buf), "sort_pass_%d", k - 4);
+        return buf;
+    }
+    if (k == 4 + P) return "unique";
+    if (k == 5 + P) return "remap";
+    return "";
+}
+
+int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream) {
+    if (!workspace || dim < 1 || dim > RMX_MAX_DIM) return -1;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t v = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(&v, static_cast<char*>(workspace) + L.plan + 4, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return -1;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+    return static_cast<int>(v);
+}
+
+int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n_elem_take, uint64_t* n_elements,
+                      uint64_t* n_vertices) {
+    if (kind != 0 && kind != 1) return RMX_EINVAL;
+    const uint64_t K = kind == 0 ? 3 : 4;
+    const uint64_t E = kind == 0 ? 2ull * nx * ny : 6ull * nx * ny * nz;
+    const uint64_t take = n_elem_take < E ? n_elem_take : E;
+    const uint64_t n_unused = (E * K) / 20;
+    if (n_elements) *n_elements = E;
+    if (n_vertices) *n_vertices = take * K + (E ? (take * n_unused) / E : 0);
+    return RMX_OK;
+}
+
+int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed, uint64_t n_elem_take,
+                         uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream) {
+    if (kind != 0 && kind != 1) return RMX_EINVAL;
+    GenArgs g{};
+    g.kind = kind;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    const uint64_t K = kind == 0 ? 3 : 4;
+    g.n_elem = kind == 0 ? 2ull * nx * ny : 6ull * nx * ny * nz;
+    g.take = n_elem_take < g.n_elem ? n_elem_take : g.n_elem;
+    g.n_unused = (g.n_elem * K) / 20;
+    if (g.take == 0) return RMX_OK;
+    int bits = 0;
+    while ((1ull << bits) < g.n_elem) ++bits;  // bit length of n-1
+    if (bits < 2) bits = 2;
+    bits += bits & 1;
+    g.half = static_cast<uint32_t>(bits / 2);
+    g.mask = (1ull << g.half) - 1;
+    for (int r = 0; r < 4; ++r) g.keys[r] = splitmix64(static_cast<uint64_t>(r) + seed * 4 + 1);
+    g.useed = splitmix64(seed + 0x5555);
+    g.vtx = out_vtx_bits;
+    g.idx = out_idx;
+    int grid = 0;
+    int rc = grid_for_stream(g.take, grid);
+    if (rc) return rc;
+    k_gen_lattice<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(g);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+}  // extern "C"

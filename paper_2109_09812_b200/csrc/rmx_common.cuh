@@ -1,0 +1,151 @@
+// rmx_common.cuh -- sm_100a device helpers shared by the re-indexing kernels:
+// warp intrinsics, relaxed GPU-scope atomics for decoupled look-back,
+// mbarrier + cp.async.bulk (TMA bulk copy) tile staging.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rmx {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t lanemask_le() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+    return m;
+}
+
+// ---- GPU-scope relaxed accesses for look-back descriptors -----------------
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Look-back descriptor: [63:34] epoch, [33:32] flag, [31:0] value.
+// The value is a count of rows, bounded by n_vertices < 2^32.
+constexpr uint32_t kAggregate = 1u;
+constexpr uint32_t kPrefix = 2u;
+
+__device__ __forceinline__ uint64_t pack_desc(uint32_t epoch, uint32_t flag, uint32_t value) {
+    return (static_cast<uint64_t>(epoch) << 34) | (static_cast<uint64_t>(flag) << 32) | value;
+}
+__device__ __forceinline__ uint32_t desc_epoch(uint64_t d) { return static_cast<uint32_t>(d >> 34); }
+__device__ __forceinline__ uint32_t desc_flag(uint64_t d) { return static_cast<uint32_t>(d >> 32) & 3u; }
+__device__ __forceinline__ uint32_t desc_value(uint64_t d) { return static_cast<uint32_t>(d); }
+
+// Spin until the descriptor carries this epoch and a non-empty flag.
+__device__ __forceinline__ uint64_t wait_desc(const uint64_t* p, uint32_t epoch) {
+    uint64_t d = ld_relaxed(p);
+    while (desc_epoch(d) != epoch || desc_flag(d) == 0u) {
+        __nanosleep(32);
+        d = ld_relaxed(p);
+    }
+    return d;
+}
+
+// ---- mbarrier + bulk async copy (TMA, non-tensor) --------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Order this thread's earlier generic-proxy shared-memory accesses (made
+// visible to it by a preceding __syncthreads) before later async-proxy writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// Global -> shared bulk copy completing `bytes` of transaction on `bar`.
+// dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "RMX_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra RMX_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Stage `bytes` (rounded up to 16) from global `src` into shared `dst`.
+// Called by one thread; everybody then waits on `bar` with `parity`.
+__device__ __forceinline__ void stage_tile(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    const uint32_t b16 = (bytes + 15u) & ~15u;
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, b16);
+    // one bulk op per 32 KiB keeps each request modest and lets the copy
+    // engine pipeline the pieces
+    constexpr uint32_t kChunk = 32768u;
+    const char* s = static_cast<const char*>(src);
+    char* d = static_cast<char*>(dst);
+    for (uint32_t off = 0; off < b16; off += kChunk) {
+        const uint32_t n = (b16 - off) < kChunk ? (b16 - off) : kChunk;
+        bulk_g2s(d + off, s + off, n, bar);
+    }
+}
+
+// ---- block scan over one value per thread ----------------------------------
+// Exclusive scan of `v` across a block of NW warps; `s_warp` holds NW words and
+// must not be reused until a later __syncthreads.
+template <int NW>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t& total) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= static_cast<uint32_t>(o)) x += y;
+    }
+    if (lane == 31u) s_warp[warp] = x;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const uint32_t t = s_warp[w];
+        before += (static_cast<uint32_t>(w) < warp) ? t : 0u;
+        all += t;
+    }
+    total = all;
+    return before + x - v;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+}  // namespace rmx

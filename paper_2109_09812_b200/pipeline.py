@@ -1,0 +1,336 @@
+"""Drop-in ``reindex``: the reference operator API over the CUDA C-ABI.
+
+Reference interface (``pkg/src/remeshx/pipeline.py:133-157``)::
+
+    reindex(mesh: Mesh) -> tuple[Mesh, ReindexScratch]
+
+Same argument meaning, same result types and the same errors:
+
+* out-of-range indices    -> ``InvalidMeshError`` with the reference's ``Issue``
+  list (``mesh.py:103-105``; detected on the GPU by K1, listed on the cold path);
+* zero elements           -> ``Mesh.empty(dim, arity)`` and an all-false
+  ``is_used`` (``pipeline.py:142-146``);
+* ``n_vertices >= 2**32`` -> ``MeshError`` (``mesh.py:59-60``).
+
+Three entry levels share one native call (``rmx_reindex``):
+
+* :func:`reindex`         -- numpy in, numpy out (the reference signature);
+* :class:`Reindexer`      -- fixed-capacity device + pinned host buffers for
+  repeated host-to-host calls (the end-to-end path bench.py times);
+* :func:`reindex_tensors` -- device-resident torch tensors in and out.
+
+PyTorch is only the buffer/stream plumbing; all arithmetic is in the CUDA
+library.  There is no CPU fallback: a missing library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .mesh import InvalidMeshError, Mesh, MeshError, validate
+
+_SCRATCH_FIELDS = ("is_used", "org_id", "nodup", "new_idx", "perm")
+
+
+def _device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2109_09812_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def workspace_bytes(n_vertices: int, dim: int, n_elements: int = 0, arity: int = 1) -> int:
+    return int(_native.lib().rmx_workspace_bytes(n_vertices, dim, n_elements, arity))
+
+
+def _raise_for(rc: int) -> None:
+    if rc == _native.RMX_OK:
+        return
+    msg = _native.lib().rmx_strerror(rc).decode()
+    if rc in (_native.RMX_EINVAL, _native.RMX_ERANGE):
+        raise MeshError(msg)
+    raise RuntimeError(f"CUDA re-indexing failed ({rc}): {msg}")
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+@dataclass
+class DeviceResult:
+    """Device-resident result of :func:`reindex_tensors`.
+
+    ``vertices`` is an int32 ``(U, dim)`` bit view, ``elements`` int32
+    ``(E, arity)``; ``scratch`` maps the ReindexScratch field names to device
+    tensors when requested.
+    """
+
+    vertices: torch.Tensor
+    elements: torch.Tensor
+    new_count: int
+    scratch: dict | None
+
+
+def launch(vtx: torch.Tensor, n_vertices: int, dim: int, idx: torch.Tensor, n_elements: int, arity: int,
+           out_vtx: torch.Tensor, out_idx: torch.Tensor, info: torch.Tensor, workspace: torch.Tensor,
+           scratch: dict | None = None, stream: torch.cuda.Stream | None = None, events=None) -> None:
+    """Enqueue the pipeline on ``stream`` (no synchronisation).
+
+    ``info`` is an int64 device tensor of 2 elements: [0] receives the output
+    vertex count, the low word of [1] the status bits.  ``events`` is an
+    optional sequence of raw cudaEvent_t handles recorded at stage boundaries.
+    """
+    lib = _native.lib()
+    sc = None
+    if scratch is not None:
+        sc = _native.Scratch(*[_ptr(scratch.get(f)) for f in _SCRATCH_FIELDS])
+    s = (stream or torch.cuda.current_stream(vtx.device if vtx is not None else idx.device)).cuda_stream
+    base = info.data_ptr()
+    args = (_ptr(vtx), n_vertices, dim, _ptr(idx), n_elements, arity, _ptr(out_vtx), _ptr(out_idx),
+            base, base + 8, workspace.data_ptr() if workspace is not None else None,
+            workspace.numel() if workspace is not None else 0,
+            ctypes.byref(sc) if sc is not None else None, s)
+    if events:
+        arr = (ctypes.c_void_p * len(events))(*events)
+        rc = lib.rmx_reindex_profiled(*args, arr, len(events))
+    else:
+        rc = lib.rmx_reindex(*args)
+    _raise_for(rc)
+
+
+def _alloc_scratch(n_vertices: int, device) -> dict:
+    return dict(is_used=torch.empty(n_vertices, dtype=torch.uint8, device=device),
+                org_id=torch.empty(n_vertices, dtype=torch.int32, device=device),
+                nodup=torch.empty(n_vertices, dtype=torch.uint8, device=device),
+                new_idx=torch.empty(n_vertices, dtype=torch.int32, device=device),
+                perm=torch.empty(n_vertices, dtype=torch.int32, device=device))
+
+
+def reindex_tensors(vertex_bits: torch.Tensor, elements: torch.Tensor, *, scratch: bool = False,
+                    stream: torch.cuda.Stream | None = None) -> DeviceResult:
+    """Re-index device-resident data: ``vertex_bits`` (V, D) int32/uint32 words,
+    ``elements`` (E, K) int32/uint32 indices, both contiguous on one CUDA device.
+
+    Synchronises once to learn the output size.  Raises InvalidMeshError (with
+    issues found on the device) for out-of-range indices.
+    """
+    if vertex_bits.dim() != 2 or elements.dim() != 2:
+        raise MeshError("vertex_bits must be (V, D) and elements (E, K)")
+    if vertex_bits.element_size() != 4 or elements.element_size() != 4:
+        raise MeshError("vertex_bits and elements must hold 32-bit words")
+    vertex_bits = vertex_bits.contiguous()
+    elements = elements.contiguous()
+    dev = vertex_bits.device
+    V, D = vertex_bits.shape
+    E, K = elements.shape
+    if V >= 1 << 32:
+        raise MeshError(f"vertex count {V} exceeds 32-bit index range")
+    out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
+    out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(max(workspace_bytes(V, D, E, K), 1) if E else 1, dtype=torch.uint8, device=dev)
+    sc = _alloc_scratch(V, dev) if scratch else None
+    launch(vertex_bits, V, D, elements, E, K, out_v, out_e, info, ws, sc, stream)
+    count, status = (int(x) for x in info.cpu())
+    if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+        bad = torch.nonzero(elements.to(torch.int64) & 0xFFFFFFFF >= V).cpu().numpy()
+        host = elements.cpu().numpy().view(np.uint32)
+        from .mesh import Issue
+        raise InvalidMeshError([Issue(int(e), int(s), int(host[e, s])) for e, s in bad])
+    if E == 0:
+        out_v = out_v[:0]
+    else:
+        out_v = out_v[:count]
+    return DeviceResult(out_v, out_e, count, sc)
+
+
+class ReindexScratch:
+    """Intermediates of one run (reference ``ReindexScratch``, pipeline.py:24-38).
+
+    ``new_count`` is known immediately.  The array fields are materialised on
+    first access by re-running the (deterministic) device pipeline with
+    scratch outputs enabled, so the hot path never pays for them.
+    """
+
+    __slots__ = ("_src", "_count", "_arrays", "_device")
+
+    def __init__(self, vertices: np.ndarray, elements: np.ndarray, new_count: int, device):
+        object.__setattr__(self, "_src", (vertices, elements))
+        object.__setattr__(self, "_count", int(new_count))
+        object.__setattr__(self, "_arrays", None)
+        object.__setattr__(self, "_device", device)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("ReindexScratch is immutable")
+
+    @property
+    def new_count(self) -> int:
+        return self._count
+
+    def _materialise(self) -> dict:
+        if self._arrays is None:
+            vertices, elements = self._src
+            V, D = vertices.shape
+            E, K = elements.shape
+            dev = self._device
+            with torch.cuda.device(dev):
+                vtx_d = torch.from_numpy(np.ascontiguousarray(vertices).view(np.int32).reshape(V, D)).to(dev)
+                idx_d = torch.from_numpy(np.ascontiguousarray(elements).view(np.int32).reshape(E, K)).to(dev)
+                res = reindex_tensors(vtx_d, idx_d, scratch=True)
+                sc = res.scratch
+                n = V if E else 0
+                arrays = dict(
+                    is_used=sc["is_used"].cpu().numpy().astype(bool),
+                    org_id=sc["org_id"][:n].cpu().numpy().view(np.uint32),
+                    nodup=sc["nodup"][:n].cpu().numpy().astype(bool),
+                    new_idx=sc["new_idx"][:n].cpu().numpy().view(np.uint32),
+                    perm=sc["perm"][:n].cpu().numpy().view(np.uint32))
+            for a in arrays.values():
+                a.flags.writeable = False
+            object.__setattr__(self, "_arrays", arrays)
+        return self._arrays
+
+    @property
+    def is_used(self) -> np.ndarray:
+        return self._materialise()["is_used"]
+
+    @property
+    def org_id(self) -> np.ndarray:
+        return self._materialise()["org_id"]
+
+    @property
+    def nodup(self) -> np.ndarray:
+        return self._materialise()["nodup"]
+
+    @property
+    def new_idx(self) -> np.ndarray:
+        return self._materialise()["new_idx"]
+
+    @property
+    def perm(self) -> np.ndarray:
+        return self._materialise()["perm"]
+
+    def __repr__(self):
+        return f"ReindexScratch(new_count={self._count})"
+
+
+def _host_arrays(mesh) -> tuple[np.ndarray, np.ndarray]:
+    """float32/uint32 C-contiguous arrays of a Mesh (or any .vertices/.elements object)."""
+    if isinstance(mesh, Mesh):
+        return mesh.vertices, mesh.elements
+    v = np.ascontiguousarray(mesh.vertices, dtype=np.float32)
+    e = np.ascontiguousarray(mesh.elements, dtype=np.uint32)
+    if v.ndim != 2 or v.shape[1] < 1 or e.ndim != 2 or e.shape[1] < 1:
+        raise MeshError(f"bad mesh shapes {v.shape} / {e.shape}")
+    if v.shape[0] >= 1 << 32:
+        raise MeshError(f"vertex count {v.shape[0]} exceeds 32-bit index range")
+    if v.flags.writeable or e.flags.writeable:     # snapshot for the lazy scratch
+        v, e = v.copy(), e.copy()
+        v.flags.writeable = False
+        e.flags.writeable = False
+    return v, e
+
+
+def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
+    """Remove duplicate and unused vertices (reference pipeline.py:133-157).
+
+    Output vertices are the bitwise-sorted unique used rows; element indices
+    are remapped accordingly; the soup is preserved bit for bit.
+    """
+    vertices, elements = _host_arrays(mesh)
+    dev = _device(device)
+    V, D = vertices.shape
+    E, K = elements.shape
+    if E == 0:
+        return Mesh.empty(dim=D, arity=K), ReindexScratch(vertices, elements, 0, dev)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
+        idx_d = torch.empty((E, K), dtype=torch.int32, device=dev)
+        vtx_d.copy_(torch.from_numpy(vertices.view(np.int32)))
+        idx_d.copy_(torch.from_numpy(elements.view(np.int32)))
+        out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
+        out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
+        info = torch.zeros(2, dtype=torch.int64, device=dev)
+        ws = torch.empty(workspace_bytes(V, D, E, K), dtype=torch.uint8, device=dev)
+        launch(vtx_d, V, D, idx_d, E, K, out_v, out_e, info, ws, None, stream)
+        count, status = (int(x) for x in info.cpu())
+        if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+            raise InvalidMeshError(validate(_Arrays(vertices, elements)))
+        host_v = out_v[:count].cpu().numpy().view(np.float32)
+        host_e = out_e.cpu().numpy().view(np.uint32)
+    return Mesh._adopt(host_v, host_e), ReindexScratch(vertices, elements, count, dev)
+
+
+class _Arrays:
+    __slots__ = ("vertices", "elements")
+
+    def __init__(self, vertices, elements):
+        self.vertices = vertices
+        self.elements = elements
+
+
+class Reindexer:
+    """Fixed-capacity buffers for repeated host-to-host re-indexing.
+
+    ``run(vertices_pinned, elements_pinned)`` copies the inputs host->device,
+    runs the pipeline, and copies the result back into pinned host buffers;
+    returns numpy views ``(vertices (U, D) float32, elements (E, K) uint32)``
+    valid until the next call.  Inputs should be pinned torch tensors (see
+    :meth:`pinned_inputs`) so the copies run at full PCIe speed.
+    """
+
+    def __init__(self, n_vertices: int, dim: int, n_elements: int, arity: int, device=None):
+        self.device = _device(device)
+        self.V, self.D, self.E, self.K = int(n_vertices), int(dim), int(n_elements), int(arity)
+        dev = self.device
+        self.vtx_d = torch.empty((self.V, self.D), dtype=torch.int32, device=dev)
+        self.idx_d = torch.empty((self.E, self.K), dtype=torch.int32, device=dev)
+        self.out_v = torch.empty((self.V, self.D), dtype=torch.int32, device=dev)
+        self.out_e = torch.empty((self.E, self.K), dtype=torch.int32, device=dev)
+        self.info = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.ws = torch.empty(max(1, workspace_bytes(self.V, self.D, self.E, self.K)), dtype=torch.uint8,
+                              device=dev)
+        self.host_v = torch.empty((self.V, self.D), dtype=torch.int32, pin_memory=True)
+        self.host_e = torch.empty((self.E, self.K), dtype=torch.int32, pin_memory=True)
+        self.host_info = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.stream = torch.cuda.Stream(dev)
+
+    def pinned_inputs(self, vertices: np.ndarray, elements: np.ndarray) -> tuple[torch.Tensor, torch.Tensor]:
+        v = torch.empty((self.V, self.D), dtype=torch.int32, pin_memory=True)
+        e = torch.empty((self.E, self.K), dtype=torch.int32, pin_memory=True)
+        v.numpy()[:] = np.ascontiguousarray(vertices, dtype=np.float32).view(np.int32)
+        e.numpy()[:] = np.ascontiguousarray(elements, dtype=np.uint32).view(np.int32)
+        return v, e
+
+    def bytes_per_call(self, count: int) -> tuple[int, int]:
+        h2d = self.V * self.D * 4 + self.E * self.K * 4
+        d2h = 16 + count * self.D * 4 + self.E * self.K * 4
+        return h2d, d2h
+
+    def run(self, vertices_pinned: torch.Tensor, elements_pinned: torch.Tensor):
+        s = self.stream
+        with torch.cuda.device(self.device), torch.cuda.stream(s):
+            self.vtx_d.copy_(vertices_pinned, non_blocking=True)
+            self.idx_d.copy_(elements_pinned, non_blocking=True)
+            launch(self.vtx_d, self.V, self.D, self.idx_d, self.E, self.K, self.out_v, self.out_e,
+                   self.info, self.ws, None, s)
+            self.host_info.copy_(self.info, non_blocking=True)
+            # the element result size is known up front: start it before the count arrives
+            self.host_e.copy_(self.out_e, non_blocking=True)
+            s.synchronize()
+            count, status = (int(x) for x in self.host_info)
+            if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+                host_v = vertices_pinned.numpy().view(np.float32)
+                host_e = elements_pinned.numpy().view(np.uint32)
+                raise InvalidMeshError(validate(_Arrays(host_v, host_e)))
+            if count:
+                self.host_v[:count].copy_(self.out_v[:count], non_blocking=True)
+            s.synchronize()
+        self.last_count = count
+        return (self.host_v[:count].numpy().view(np.float32), self.host_e.numpy().view(np.uint32))
