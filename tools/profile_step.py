@@ -1,0 +1,57 @@
+"""One generated config + N re-indexing steps on cuda:0 (the command ncu wraps).
+
+    python tools/profile_step.py --config C2 --steps 2
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2109_09812_b200 import _native, pipeline  # noqa: E402
+
+CFG = {"C1": (0, 625, 800, 0, 3), "C2": (0, 5000, 5000, 0, 3), "C3": (1, 150, 150, 148, 4)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--steps", type=int, default=2)
+    a = ap.parse_args()
+    kid, nx, ny, nz, D = CFG[a.config]
+    lib = _native.lib()
+    E, V = ctypes.c_uint64(), ctypes.c_uint64()
+    lib.rmx_lattice_sizes(kid, nx, ny, nz, 1 << 63, ctypes.byref(E), ctypes.byref(V))
+    E, V = E.value, V.value
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.current_stream(dev)
+    vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
+    idx = torch.empty((E, D), dtype=torch.int32, device=dev)
+    _native.check(lib.rmx_gen_lattice_soup(kid, nx, ny, nz, 0, 1 << 63, vtx.data_ptr(), idx.data_ptr(), s.cuda_stream))
+    out_v = torch.empty_like(vtx)
+    out_e = torch.empty_like(idx)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(pipeline.workspace_bytes(V, D, E, D), dtype=torch.uint8, device=dev)
+    n_ev = lib.rmx_stage_count(D)
+    names = [lib.rmx_stage_name(D, k).decode() for k in range(n_ev)]
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    for e in evs:
+        e.record(s)
+    for _ in range(a.steps):
+        pipeline.launch(vtx, V, D, idx, E, D, out_v, out_e, info, ws, None, s, [e.cuda_event for e in evs])
+    torch.cuda.synchronize()
+    print("count", int(info[0]), "status", int(info[1]))
+    tot = 0.0
+    for k in range(1, n_ev):
+        ms = evs[k - 1].elapsed_time(evs[k])
+        tot += ms
+        print(f"{names[k]:>14s} {ms:8.3f} ms")
+    print(f"{'total':>14s} {tot:8.3f} ms")
+
+
+if __name__ == "__main__":
+    main()
