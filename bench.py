@@ -313,7 +313,7 @@ def run_b200(args):
             "stage_ms": stage_ms,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": (4 * D + 5) * args.steps,
+            "gpu_launches": (4 * D + 7) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -4,6 +4,7 @@
 // caller's stream and reads its control words (status, plan) from device
 // memory, so the whole sequence is CUDA-graph capturable.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -30,21 +31,101 @@ int fail_cuda(cudaError_t e, const char* what) {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
-// Per-W kernel choices (items per thread).  W = dim + 1.
-constexpr int kSortIptNarrow = 16;  // W <= 2
-constexpr int kSortIpt = 8;         // W in 3..5
-constexpr int kSortIptWide = 2;     // generic W
-constexpr int kUniqIpt = 8;
-constexpr int kUniqIptWide = 2;
+// Per-W kernel configurations.  W = dim + 1.  For the hot width (W = 4,
+// float3 keys) a menu of sort / unique variants is compiled in and one is
+// selected by RMX_SORT_CFG / RMX_UNIQ_CFG (tuning); other widths use one
+// configuration each.
+struct SortCfg { int ipt; bool reg; int pf; };
+struct UniqCfg { int ipt; };
 
-int sort_tile(int W) { return kBlock * (W <= 2 ? kSortIptNarrow : (W <= 5 ? kSortIpt : kSortIptWide)); }
-int uniq_tile(int W) { return kBlock * (W <= 5 ? kUniqIpt : kUniqIptWide); }
+#define RMX_SORT_MENU(X) \
+    X(0, 10, true, 1)    \
+    X(1, 8, false, 0)    \
+    X(2, 12, false, 1)   \
+    X(3, 8, true, 0)     \
+    X(4, 16, false, 0)   \
+    X(5, 6, false, 1)    \
+    X(6, 8, false, 1)    \
+    X(7, 10, false, 1)   \
+    X(8, 12, false, 0)
+#define RMX_UNIQ_MENU(X) \
+    X(0, 8)              \
+    X(1, 12)             \
+    X(2, 16)             \
+    X(3, 6)
+
+int env_choice(const char* name, int n, int dflt) {
+    const char* e = std::getenv(name);
+    if (!e || !*e) return dflt;
+    const int v = (*e >= 'A' && *e <= 'Z') ? *e - 'A' : ((*e >= 'a' && *e <= 'z') ? *e - 'a' : std::atoi(e));
+    return (v >= 0 && v < n) ? v : dflt;
+}
+int sort_choice() {
+    static int c = env_choice("RMX_SORT_CFG", 9, 8);
+    return c;
+}
+int uniq_choice() {
+    static int c = env_choice("RMX_UNIQ_CFG", 4, 0);
+    return c;
+}
+
+SortCfg sort_cfg(int W) {
+    if (W == 4) {
+        switch (sort_choice()) {
+#define X(id, ipt, reg, pf) case id: return SortCfg{ipt, reg, pf};
+            RMX_SORT_MENU(X)
+#undef X
+        }
+    }
+    switch (W) {
+        case 2: return SortCfg{16, true, 0};
+        case 3: return SortCfg{12, true, 0};
+        case 5: return SortCfg{8, true, 0};
+        default: return SortCfg{2, false, 0};
+    }
+}
+UniqCfg uniq_cfg(int W) {
+    if (W == 4) {
+        switch (uniq_choice()) {
+#define X(id, ipt) case id: return UniqCfg{ipt};
+            RMX_UNIQ_MENU(X)
+#undef X
+        }
+    }
+    switch (W) {
+        case 2: return UniqCfg{16};
+        case 3: return UniqCfg{12};
+        case 5: return UniqCfg{8};
+        default: return UniqCfg{2};
+    }
+}
+int sort_tile(int W) { return kBlock * sort_cfg(W).ipt; }
+int uniq_tile(int W) { return kBlock * uniq_cfg(W).ipt; }
+
+// tuning-only ablation switches (RMX_ABLATE bitmask; results are invalid when set)
+int ablate_bits() {
+    static int v = [] {
+        const char* e = std::getenv("RMX_ABLATE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
+// warp ranking variant (RMX_RANK=ballot selects the 8-ballot multi-split)
+int rank_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("RMX_RANK");
+        return (e && std::strcmp(e, "ballot") == 0) ? kRankBallot : kRankMatch;
+    }();
+    return mode;
+}
 
 struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, hist, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, hist, vary, fill, counters, desc, desc3, ctl_end;
+    int bucket_shift;
     size_t total;
 };
 
@@ -69,6 +150,11 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.plan = take(plan_words(L.P) * 4);
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
+    L.vary = take(static_cast<size_t>(L.D) * 4);
+    L.fill = take(256 * 4);
+    int bits = 0;
+    while (bits < 40 && (1ull << bits) < V) ++bits;
+    L.bucket_shift = bits > 8 ? bits - 8 : 0;
     L.counters = take(static_cast<size_t>(L.P + 2) * 4);
     L.desc = take(static_cast<size_t>(L.ntiles) * 256 * 8);
     L.desc3 = take(static_cast<size_t>(L.ntiles3) * 8);
@@ -113,7 +199,7 @@ int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
 // ---- kernel dispatch by compile-time width --------------------------------
 template <int D_CT>
 int launch_build(const BuildArgs& a, cudaStream_t s) {
-    const size_t smem = static_cast<size_t>(4 * a.dim) * 256 * 4;
+    const size_t smem = 0;
     int grid = 0;
     int rc = persistent_grid(k_build_rows<D_CT>, smem, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
     if (rc) return rc;
@@ -122,24 +208,26 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     return RMX_OK;
 }
 
-template <int W_CT, int IPT>
+template <int W_CT, int IPT, int RANK, bool REG, int PF>
 int launch_pass(const SortArgs& a, cudaStream_t s) {
-    const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
+    auto kern = k_sort_pass<W_CT, IPT, RANK, REG, PF>;
+    const size_t smem = SortTraits<W_CT, IPT, REG, PF>::smem_bytes(a.dim + 1);
     int grid = 0;
-    int rc = persistent_grid(k_sort_pass<W_CT, IPT>, smem, a.ntiles, grid);
+    int rc = persistent_grid(kern, smem, a.ntiles, grid);
     if (rc) return rc;
-    k_sort_pass<W_CT, IPT><<<grid, kBlock, smem, s>>>(a);
+    kern<<<grid, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
 
 template <int W_CT, int IPT>
 int launch_unique(const UniqueArgs& a, cudaStream_t s) {
+    auto kern = k_unique<W_CT, IPT>;
     const size_t smem = UniqueTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
     int grid = 0;
-    int rc = persistent_grid(k_unique<W_CT, IPT>, smem, a.ntiles, grid);
+    int rc = persistent_grid(kern, smem, a.ntiles, grid);
     if (rc) return rc;
-    k_unique<W_CT, IPT><<<grid, kBlock, smem, s>>>(a);
+    kern<<<grid, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -154,23 +242,40 @@ int dispatch_build(const BuildArgs& a, cudaStream_t s) {
     }
 }
 
-int dispatch_pass(const SortArgs& a, cudaStream_t s) {
+template <int RANK>
+int dispatch_pass_r(const SortArgs& a, cudaStream_t s) {
     switch (a.dim + 1) {
-        case 2: return launch_pass<2, kSortIptNarrow>(a, s);
-        case 3: return launch_pass<3, kSortIpt>(a, s);
-        case 4: return launch_pass<4, kSortIpt>(a, s);
-        case 5: return launch_pass<5, kSortIpt>(a, s);
-        default: return launch_pass<0, kSortIptWide>(a, s);
+        case 2: return launch_pass<2, 16, RANK, true, 0>(a, s);
+        case 3: return launch_pass<3, 12, RANK, true, 0>(a, s);
+        case 4:
+            switch (sort_choice()) {
+#define X(id, ipt, reg, pf) case id: return launch_pass<4, ipt, RANK, reg, pf>(a, s);
+                RMX_SORT_MENU(X)
+#undef X
+            }
+            return RMX_EINVAL;
+        case 5: return launch_pass<5, 8, RANK, true, 0>(a, s);
+        default: return launch_pass<0, 2, RANK, false, 0>(a, s);
     }
+}
+
+int dispatch_pass(const SortArgs& a, cudaStream_t s) {
+    return rank_mode() == kRankBallot ? dispatch_pass_r<kRankBallot>(a, s) : dispatch_pass_r<kRankMatch>(a, s);
 }
 
 int dispatch_unique(const UniqueArgs& a, cudaStream_t s) {
     switch (a.dim + 1) {
-        case 2: return launch_unique<2, kUniqIpt>(a, s);
-        case 3: return launch_unique<3, kUniqIpt>(a, s);
-        case 4: return launch_unique<4, kUniqIpt>(a, s);
-        case 5: return launch_unique<5, kUniqIpt>(a, s);
-        default: return launch_unique<0, kUniqIptWide>(a, s);
+        case 2: return launch_unique<2, 16>(a, s);
+        case 3: return launch_unique<3, 12>(a, s);
+        case 4:
+            switch (uniq_choice()) {
+#define X(id, ipt) case id: return launch_unique<4, ipt>(a, s);
+                RMX_UNIQ_MENU(X)
+#undef X
+            }
+            return RMX_EINVAL;
+        case 5: return launch_unique<5, 8>(a, s);
+        default: return launch_unique<0, 2>(a, s);
     }
 }
 
@@ -246,6 +351,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint32_t* map = reinterpret_cast<uint32_t*>(base + L.map);
     uint32_t* plan = reinterpret_cast<uint32_t*>(base + L.plan);
     uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
+    uint32_t* vary = reinterpret_cast<uint32_t*>(base + L.vary);
     uint32_t* counters = reinterpret_cast<uint32_t*>(base + L.counters);
     uint64_t* desc = reinterpret_cast<uint64_t*>(base + L.desc);
     uint64_t* desc3 = reinterpret_cast<uint64_t*>(base + L.desc3);
@@ -268,26 +374,44 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     // K1b rows + histograms
     {
-        BuildArgs a{vtx, flags, idx, rows0, hist, d_status, static_cast<uint32_t>(V), L.D};
+        BuildArgs a{vtx,     flags, idx, rows0, hist, vary, d_status, static_cast<uint32_t>(V), L.D,
+                    (aligned16(vtx) && aligned16(flags)) ? 1 : 0};
         if ((rc = dispatch_build(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    k_plan<<<1, kBlock, 0, s>>>(hist, plan, L.P, static_cast<uint32_t>(V), d_status);
+    k_plan<<<1, 32, 0, s>>>(vary, plan, L.D, d_status);
     RMX_CHECK(cudaGetLastError());
+    {
+        HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D};
+        int grid = 0;
+        rc = grid_for_stream(V, grid);
+        if (rc) return rc;
+        k_first_hist<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(cudaGetLastError());
+    }
     if ((rc = rec.mark())) return rc;
     // K2 onesweep passes, least significant digit first
     for (int p = 0; p < L.P; ++p) {
-        SortArgs a{rows0, rows1, plan, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p};
+        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p,
+                   ablate_bits()};
         if ((rc = dispatch_pass(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
-    // K3 unique
+    // K3 unique + bucketed pairs, K3b map fill
     {
-        UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, d_status, map, out_vtx,
-                     reinterpret_cast<unsigned long long*>(d_count),
+        UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, reinterpret_cast<uint32_t*>(base + L.fill), d_status,
+                     out_vtx, reinterpret_cast<unsigned long long*>(d_count),
                      sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
-                     sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D};
+                     sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D, L.bucket_shift};
         if ((rc = dispatch_unique(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    {
+        const uint64_t threads = (V + 1) / 2;
+        k_map_fill<<<static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s>>>(plan, rows0, rows1, map,
+                                                                                          static_cast<uint32_t>(V),
+                                                                                          d_status);
+        RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
     // K4 remap
@@ -344,7 +468,7 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
                         n_events);
 }
 
-int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6; }
+int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 7; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
     static thread_local char buf[32];
@@ -358,7 +482,8 @@ const char* rmx_stage_name(uint32_t dim, int k) {
         return buf;
     }
     if (k == 4 + P) return "unique";
-    if (k == 5 + P) return "remap";
+    if (k == 5 + P) return "map_fill";
+    if (k == 6 + P) return "remap";
     return "";
 }
 

@@ -2,16 +2,20 @@
 //
 //   K1   k_mark         isUsed scatter over the index buffer + range check
 //                       (reference mark_used pipeline.py:41-51, require_valid mesh.py:103-105)
-//   K1b  k_build_rows   unused -> replacement, AoS (key words, origin) rows, and
-//                       the 8-bit digit histograms of every LSD pass
-//                       (overwrite_unused pipeline.py:54-63, fill_sequence primitives.py:16-20)
-//   plan k_plan         digit-pass skipping, ping-pong schedule, global digit offsets
-//   K2   k_sort_pass    one onesweep LSD pass: TMA-bulk tile staging, warp
-//                       match_any ranking, decoupled look-back, smem reorder
+//   K1b  k_build_rows   unused -> replacement, AoS (key words, origin) rows,
+//                       per-component varying-bit masks, component D-1 digit
+//                       histograms (overwrite_unused pipeline.py:54-63,
+//                       fill_sequence primitives.py:16-20)
+//   plan k_plan         digit-pass skipping, ping-pong schedule, pass chaining
+//   hist k_first_hist   histogram of the first executed pass if K1b lacks it
+//   K2   k_sort_pass    one onesweep LSD pass: double-buffered TMA-bulk tile
+//                       staging, warp multi-split ranking, windowed decoupled
+//                       look-back, smem reorder, next pass's histogram
 //                       (bitwise_sort_order / key_value_sort primitives.py:23-40)
 //   K3   k_unique       adjacent-compare head flags + decoupled look-back scan,
-//                       old->new map scatter and unique-row compaction
+//                       unique-row compaction, bucketed (org, new_idx) pairs
 //                       (pipeline.py:72-113, primitives.py:43-69)
+//   K3b  k_map_fill     map[org] = new_idx from the bucket-major pairs
 //   K4   k_remap        out_idx = map[idx] (remap_elements pipeline.py:116-130)
 //   gen  k_gen_lattice  synthetic bench input (oracle/lattice.py recipe)
 //
@@ -23,6 +27,7 @@
 // component D-1-p/4, pass 0 first.
 #pragma once
 
+#include "../../include/remesh_b200.h"
 #include "rmx_common.cuh"
 
 namespace rmx {
@@ -33,10 +38,11 @@ constexpr int kWarps = kBlock / 32;
 // ---------------------------------------------------------------------------
 // Plan layout (uint32 words, lives in the workspace):
 //   [0] buffer holding the final sorted rows   [1] executed passes
+//   [2] first executed pass                    [3] first pass needs k_first_hist
 //   [4 + p]            pass p executes (digit not constant)
 //   [4 + P + p]        source buffer of pass p
-//   [4 + 2P + 256p + d] global exclusive start of digit d in pass p
-__host__ __device__ inline size_t plan_words(int P) { return 4 + 2 * static_cast<size_t>(P) + 256 * static_cast<size_t>(P); }
+//   [4 + 2P + p]       next executed pass after p (P = none)
+__host__ __device__ inline size_t plan_words(int P) { return 4 + 3 * static_cast<size_t>(P); }
 
 // ---------------------------------------------------------------------------
 // K1: mark used vertices; any index >= n_vtx sets the status bit.
@@ -77,16 +83,20 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K1b: cleaned rows + all digit histograms.
+// K1b: cleaned AoS rows, the per-component "varying bits" masks that decide
+// which digit passes execute, and the digit histograms of component D-1
+// (passes 0..3: the first executed pass is almost always among them).
 struct BuildArgs {
     const uint32_t* vtx;
     const uint8_t* flags;
     const uint32_t* idx;  // idx[0] is the replacement vertex (pipeline.py:148)
     uint32_t* rows;
-    uint32_t* hist;       // [4D][256]
+    uint32_t* hist;       // [4D][256]; this kernel fills passes 0..3
+    uint32_t* vary;       // [D]: OR over rows of (key ^ replacement key)
     const uint32_t* status;
     uint32_t n;
     int dim;
+    int vec;              // vtx 16-byte aligned (4-row vector groups for D == 3)
 };
 
 // Run-length privatised histogram update: consecutive equal digits seen by a
@@ -105,9 +115,10 @@ template <int D_CT>
 __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
     const int D = D_CT > 0 ? D_CT : a.dim;
     const int W = D + 1;
-    const int P = 4 * D;
-    extern __shared__ __align__(16) uint32_t s_hist[];  // P * 256
-    for (int i = threadIdx.x; i < P * 256; i += kBlock) s_hist[i] = 0u;
+    __shared__ uint32_t s_hist[4 * 256];
+    __shared__ uint32_t s_vary[RMX_MAX_DIM];
+    for (int i = threadIdx.x; i < 4 * 256; i += kBlock) s_hist[i] = 0u;
+    if (threadIdx.x < RMX_MAX_DIM) s_vary[threadIdx.x] = 0u;
     __syncthreads();
     if (*a.status) return;  // uniform: written by K1, stable here
 
@@ -115,17 +126,21 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
     const uint32_t* repl = a.vtx + static_cast<size_t>(r0) * D;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    uint32_t rl[4] = {0u, 0u, 0u, 0u};
 
     if constexpr (D_CT > 0) {
-        uint32_t rl[4 * D_CT];
+        uint32_t ref[D_CT], vor[D_CT];
 #pragma unroll
-        for (int p = 0; p < 4 * D_CT; ++p) rl[p] = 0u;
-        for (uint64_t i = start; i < a.n; i += stride) {
-            const bool used = a.flags[i] != 0;
-            const uint32_t* srow = used ? a.vtx + i * D_CT : repl;
-            uint32_t k[D_CT];
+        for (int c = 0; c < D_CT; ++c) {
+            ref[c] = __ldg(repl + c);
+            vor[c] = 0u;
+        }
+        auto emit = [&](uint64_t i, uint32_t (&k)[D_CT]) {
 #pragma unroll
-            for (int c = 0; c < D_CT; ++c) k[c] = __ldg(srow + c);
+            for (int c = 0; c < D_CT; ++c) vor[c] |= k[c] ^ ref[c];
+            const uint32_t last = k[D_CT - 1];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) rl_push(rl[b], (last >> (8 * b)) & 255u, s_hist + b * 256);
             if constexpr (D_CT == 3) {
                 reinterpret_cast<uint4*>(a.rows)[i] = make_uint4(k[0], k[1], k[2], static_cast<uint32_t>(i));
             } else {
@@ -134,15 +149,45 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
                 for (int c = 0; c < D_CT; ++c) dst[c] = k[c];
                 dst[D_CT] = static_cast<uint32_t>(i);
             }
+        };
+        uint64_t done = 0;
+        if constexpr (D_CT == 3) {
+            if (a.vec) {  // 4 rows = 3 x 16 B of vertex words + one 32-bit flag word
+                const uint64_t ng = a.n >> 2;
+                const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
+                const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
+                for (uint64_t g = start; g < ng; g += stride) {
+                    const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
+                    const uint32_t f = __ldcs(f4 + g);
+                    uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
 #pragma unroll
-            for (int p = 0; p < 4 * D_CT; ++p) {
-                const int c = D_CT - 1 - (p >> 2);
-                rl_push(rl[p], (k[c] >> (8 * (p & 3))) & 255u, s_hist + p * 256);
+                    for (int j = 0; j < 4; ++j) {
+                        if (((f >> (8 * j)) & 255u) == 0u) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
+                        }
+                        emit(4 * g + j, k[j]);
+                    }
+                }
+                done = ng << 2;
             }
         }
+        for (uint64_t i = done + start; i < a.n; i += stride) {
+            const bool used = a.flags[i] != 0;
+            uint32_t k[D_CT];
 #pragma unroll
-        for (int p = 0; p < 4 * D_CT; ++p)
-            if ((rl[p] >> 8) != 0u) atomicAdd(s_hist + p * 256 + (rl[p] & 255u), rl[p] >> 8);
+            for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
+            if (!used) {
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) k[c] = ref[c];
+            }
+            emit(i, k);
+        }
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) {
+            const uint32_t v = __reduce_or_sync(kFull, vor[c]);
+            if ((threadIdx.x & 31u) == 0u && v) atomicOr(s_vary + c, v);
+        }
     } else {
         for (uint64_t i = start; i < a.n; i += stride) {
             const bool used = a.flags[i] != 0;
@@ -151,54 +196,96 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
             for (int c = 0; c < D; ++c) {
                 const uint32_t k = __ldg(srow + c);
                 dst[c] = k;
-                const int pbase = 4 * (D - 1 - c);
-#pragma unroll
-                for (int b = 0; b < 4; ++b) atomicAdd(s_hist + (pbase + b) * 256 + ((k >> (8 * b)) & 255u), 1u);
+                const uint32_t x = k ^ __ldg(repl + c);
+                if (x) atomicOr(s_vary + c, x);
+                if (c == D - 1)
+                    for (int b = 0; b < 4; ++b) rl_push(rl[b], (k >> (8 * b)) & 255u, s_hist + b * 256);
             }
             dst[D] = static_cast<uint32_t>(i);
         }
     }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+        if ((rl[b] >> 8) != 0u) atomicAdd(s_hist + b * 256 + (rl[b] & 255u), rl[b] >> 8);
     __syncthreads();
-    for (int i = threadIdx.x; i < P * 256; i += kBlock)
+    for (int i = threadIdx.x; i < 4 * 256; i += kBlock)
         if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
+    if (threadIdx.x < static_cast<unsigned>(D) && s_vary[threadIdx.x]) atomicOr(a.vary + threadIdx.x, s_vary[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
-// plan: skip passes whose digit is constant, assign ping-pong buffers, and
-// exclusive-scan each digit histogram into global bucket starts.
-__global__ void __launch_bounds__(kBlock) k_plan(const uint32_t* hist, uint32_t* plan, int P, uint32_t n,
-                                                  const uint32_t* status) {
-    if (*status) return;
-    __shared__ uint32_t s_warp[kWarps];
-    uint32_t cur = 0, executed = 0;
+// plan: a pass executes iff its digit is not constant over all keys (some
+// bit of that byte differs from the replacement key in some row); assign
+// ping-pong buffers and chain each executed pass to the next one.
+__global__ void k_plan(const uint32_t* vary, uint32_t* plan, int D, const uint32_t* status) {
+    if (*status || threadIdx.x != 0) return;
+    const int P = 4 * D;
+    uint32_t cur = 0, executed = 0, first = static_cast<uint32_t>(P), prev = static_cast<uint32_t>(P);
     for (int p = 0; p < P; ++p) {
-        const uint32_t c = hist[p * 256 + threadIdx.x];
-        const int constant = __syncthreads_or(c == n);
-        uint32_t tot;
-        const uint32_t ex = block_exclusive_scan<kWarps>(c, s_warp, tot);
-        plan[4 + 2 * P + p * 256 + threadIdx.x] = ex;
-        if (threadIdx.x == 0) {
-            plan[4 + p] = constant ? 0u : 1u;
-            plan[4 + P + p] = cur;
-        }
-        if (!constant) {
+        const int comp = D - 1 - (p >> 2);
+        const bool ex = ((vary[comp] >> (8 * (p & 3))) & 255u) != 0u;
+        plan[4 + p] = ex ? 1u : 0u;
+        plan[4 + P + p] = cur;
+        plan[4 + 2 * P + p] = static_cast<uint32_t>(P);
+        if (ex) {
+            if (first == static_cast<uint32_t>(P)) first = p;
+            if (prev != static_cast<uint32_t>(P)) plan[4 + 2 * P + prev] = p;
+            prev = p;
             cur ^= 1u;
             ++executed;
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        plan[0] = cur;
-        plan[1] = executed;
-    }
+    plan[0] = cur;
+    plan[1] = executed;
+    plan[2] = first;
+    plan[3] = (first < static_cast<uint32_t>(P) && first >= 4u) ? 1u : 0u;  // histogram not made by K1b
+}
+
+// Histogram of the first executed pass when it lies outside component D-1
+// (only then; exits immediately otherwise).
+struct HistArgs {
+    const uint32_t* rows;
+    uint32_t* hist;
+    const uint32_t* plan;
+    const uint32_t* status;
+    uint32_t n;
+    int dim;
+};
+
+__global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
+    if (*a.status || a.plan[3] == 0u) return;
+    __shared__ uint32_t s_h[256];
+    s_h[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint32_t p = a.plan[2];
+    const int comp = a.dim - 1 - static_cast<int>(p >> 2);
+    const int shift = 8 * static_cast<int>(p & 3u);
+    const int W = a.dim + 1;
+    uint32_t rl = 0u;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < a.n;
+         i += static_cast<uint64_t>(gridDim.x) * kBlock)
+        rl_push(rl, (__ldcs(a.rows + i * W + comp) >> shift) & 255u, s_h);
+    if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);
+    __syncthreads();
+    if (s_h[threadIdx.x]) atomicAdd(a.hist + p * 256 + threadIdx.x, s_h[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
-// K2: one onesweep LSD pass (persistent CTAs, dynamic tile ids).
+// K2: one onesweep LSD pass.  Persistent CTAs take tile ids from an atomic
+// counter (forward progress for the look-back).  Tile data arrives by TMA
+// bulk copy.  PF = 1 double-buffers: the NEXT tile id is taken only after the
+// current tile has published its inclusive prefix (taking it earlier would
+// hold back that tile's aggregate and convoy the look-back of later tiles),
+// and its copy overlaps the reorder + write-out of the current tile.
+// REG = rows held in registers and reordered in place; otherwise a per-slot
+// source index (u16) drives the write-out straight from the staged tile.
+// Each pass also counts the digit of the next executed pass (>= 4), so the
+// global histogram of that pass is complete when it starts.
 struct SortArgs {
     uint32_t* rows0;
     uint32_t* rows1;
     const uint32_t* plan;
+    uint32_t* hist;      // [P][256]
     uint64_t* desc;      // [ntiles][256] look-back descriptors (shared by all passes, epoch-tagged)
     uint32_t* counters;  // [P] tile-id counters
     const uint32_t* status;
@@ -206,23 +293,35 @@ struct SortArgs {
     uint32_t ntiles;
     int dim;
     int pass;
+    int ablate;  // tuning only (results invalid): 1 no look-back wait, 2 no ranking, 4 no write-out
 };
 
-template <int W_CT, int IPT>
+constexpr int kRankMatch = 0;   // warp multi-split with match.any
+constexpr int kRankBallot = 1;  // warp multi-split with 8 ballots
+
+template <int W_CT, int IPT, bool REG, int PF>
 struct SortTraits {
     static constexpr int kTile = kBlock * IPT;
-    // W_CT > 0: rows are held in registers and reordered in place (one buffer);
-    // generic W: separate input and output staging buffers.
-    static constexpr int kBuffers = W_CT > 0 ? 1 : 2;
+    static constexpr int kBufs = PF ? 2 : 1;
     static __host__ __device__ size_t smem_bytes(int W) {
-        return static_cast<size_t>(kBuffers) * kTile * W * 4 + (kWarps * 256 + 512 + kWarps + 8) * 4 + 16;
+        return static_cast<size_t>(kBufs) * kTile * W * 4 + (kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16 +
+               (REG ? 0 : kTile * 2);
     }
 };
 
-template <int W_CT, int IPT>
-__global__ void __launch_bounds__(kBlock) k_sort_pass(SortArgs a) {
-    using T = SortTraits<W_CT, IPT>;
+template <int W_CT>
+__device__ __forceinline__ uint32_t pick_word(const uint32_t* reg, int comp) {
+    uint32_t k = reg[0];
+#pragma unroll
+    for (int c = 1; c < W_CT - 1; ++c) k = (comp == c) ? reg[c] : k;
+    return k;
+}
+
+template <int W_CT, int IPT, int RANK, bool REG, int PF>
+__global__ void __launch_bounds__(kBlock, REG ? 2 : 3) k_sort_pass(SortArgs a) {
+    using T = SortTraits<W_CT, IPT, REG, PF>;
     constexpr int TILE = T::kTile;
+    static_assert(!REG || W_CT > 0, "register rows need a compile-time width");
     const int W = W_CT > 0 ? W_CT : a.dim + 1;
     const int P = 4 * a.dim;
     if (*a.status) return;
@@ -231,157 +330,277 @@ __global__ void __launch_bounds__(kBlock) k_sort_pass(SortArgs a) {
     const uint32_t src = plan[4 + P + a.pass];
     const uint32_t* __restrict__ in = src ? a.rows1 : a.rows0;
     uint32_t* __restrict__ out = src ? a.rows0 : a.rows1;
-    const uint32_t* offs = plan + 4 + 2 * P + 256 * a.pass;
     const int comp = a.dim - 1 - (a.pass >> 2);
     const int shift = 8 * (a.pass & 3);
     const uint32_t epoch = static_cast<uint32_t>(a.pass) + 1u;
+    const int nxt = static_cast<int>(plan[4 + 2 * P + a.pass]);
+    // passes 0..3 are counted by K1b; later ones by the pass before them
+    const bool count_next = nxt < P && nxt >= 4;
+    const int ncomp = count_next ? a.dim - 1 - (nxt >> 2) : 0;
+    const int nshift = 8 * (nxt & 3);
+    uint32_t* ctr = a.counters + a.pass;
 
     extern __shared__ __align__(128) uint32_t smem[];
-    uint32_t* s_in = smem;
-    uint32_t* s_out = (W_CT > 0) ? s_in : s_in + static_cast<size_t>(TILE) * W;
-    uint32_t* s_whist = s_out + static_cast<size_t>(TILE) * W;  // [warp][256]
-    uint32_t* s_start = s_whist + kWarps * 256;                   // tile-local digit start
-    uint32_t* s_gdst = s_start + 256;                             // global row of local slot 0, per digit
-    uint32_t* s_warp = s_gdst + 256;
+    const size_t tw = static_cast<size_t>(TILE) * W;
+    uint32_t* s_buf = smem;                           // [kBufs][TILE * W]
+    uint32_t* s_whist = smem + T::kBufs * tw;         // [warp][256]
+    uint32_t* s_offs = s_whist + kWarps * 256;        // global exclusive digit starts
+    uint32_t* s_gdst = s_offs + 256;                  // global row of tile slot 0, per digit
+    uint32_t* s_hnext = s_gdst + 256;                 // histogram of the next executed pass
+    uint32_t* s_warp = s_hnext + 256;
     uint32_t* s_misc = s_warp + kWarps;
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_bar + 2);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    auto tile_rows = [&](uint32_t t) { return min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE)); };
+    auto load_tile = [&](uint32_t t, uint32_t buf) {
+        stage_tile(s_buf + buf * tw, in + static_cast<size_t>(t) * TILE * W, tile_rows(t) * W * 4u, s_bar + buf);
+    };
+
     if (tid == 0) {
         mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
         fence_mbar_init();
+        if (PF) {
+            const uint32_t t0 = atomicAdd(ctr, 1u);
+            s_misc[0] = t0;
+            if (t0 < a.ntiles) load_tile(t0, 0);
+        }
+    }
+    {
+        uint32_t tot;
+        const uint32_t h = a.hist[a.pass * 256 + tid];
+        s_offs[tid] = block_exclusive_scan<kWarps>(h, s_warp, tot);
+        s_hnext[tid] = 0u;
     }
     __syncthreads();
-
-    for (uint32_t iter = 0;; ++iter) {
-        if (tid == 0) s_misc[0] = atomicAdd(a.counters + a.pass, 1u);
+    uint32_t tile = PF ? s_misc[0] : 0u;
+    for (uint32_t it = 0;; ++it) {
+        const uint32_t b = PF ? (it & 1u) : 0u;
+        uint32_t* s_cur = s_buf + b * tw;
+        if (!PF && tid == 0) {
+            const uint32_t t = atomicAdd(ctr, 1u);
+            s_misc[0] = t;
+            if (t < a.ntiles) load_tile(t, 0);
+        }
         for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
         __syncthreads();
-        const uint32_t tile = s_misc[0];
+        if (!PF) tile = s_misc[0];
         if (tile >= a.ntiles) break;
-        const uint32_t base = tile * static_cast<uint32_t>(TILE);
-        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
-        if (tid == 0) stage_tile(s_in, in + static_cast<size_t>(base) * W, tile_n * W * 4u, s_bar);
-        mbar_wait(s_bar, iter & 1u);
+        const uint32_t tile_n = tile_rows(tile);
+        mbar_wait(s_bar + b, PF ? ((it >> 1) & 1u) : (it & 1u));
 
-        // ---- stable warp-level ranking: warp w owns rows [w*32*IPT, (w+1)*32*IPT)
+        // ---- stable warp-level ranking: warp w owns rows [w*32*IPT, (w+1)*32*IPT).
+        // Digits and peer masks of all IPT rounds are computed first (independent,
+        // so the match latencies overlap); only the short per-round counter
+        // read-modify-write chain is serial.
         uint32_t* wh = s_whist + warp * 256;
-        uint32_t rank[IPT];
-        uint32_t dig[IPT];
-        uint32_t reg[W_CT > 0 ? IPT * W_CT : 1];
+        uint32_t pk[IPT];  // digit, then digit << 16 | rank within the warp's rows of that digit
+        uint32_t pm[IPT];  // peers (lanes of this round with the same digit)
+        uint32_t reg[REG ? IPT * W_CT : 1];
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
             const bool valid = p < tile_n;
-            uint32_t d = 0;
+            uint32_t d = 256u;  // sentinel for rows past the end of the last tile
             if (valid) {
-                d = (s_in[static_cast<size_t>(p) * W + comp] >> shift) & 255u;
+                uint32_t key, nkey = 0;
                 if constexpr (W_CT == 4) {
-                    const uint4 v = reinterpret_cast<const uint4*>(s_in)[p];
-                    reg[r * 4 + 0] = v.x;
-                    reg[r * 4 + 1] = v.y;
-                    reg[r * 4 + 2] = v.z;
-                    reg[r * 4 + 3] = v.w;
-                } else if constexpr (W_CT > 0) {
+                    const uint4 v = reinterpret_cast<const uint4*>(s_cur)[p];
+                    if constexpr (REG) {
+                        reg[r * 4 + 0] = v.x;
+                        reg[r * 4 + 1] = v.y;
+                        reg[r * 4 + 2] = v.z;
+                        reg[r * 4 + 3] = v.w;
+                    }
+                    key = comp == 0 ? v.x : (comp == 1 ? v.y : v.z);
+                    if (count_next) nkey = ncomp == 0 ? v.x : (ncomp == 1 ? v.y : v.z);
+                } else if constexpr (REG) {
 #pragma unroll
-                    for (int c = 0; c < W_CT; ++c) reg[r * W_CT + c] = s_in[p * W_CT + c];
+                    for (int c = 0; c < W_CT; ++c) reg[r * W_CT + c] = s_cur[p * W_CT + c];
+                    key = pick_word<W_CT>(reg + r * W_CT, comp);
+                    if (count_next) nkey = pick_word<W_CT>(reg + r * W_CT, ncomp);
+                } else {
+                    key = s_cur[static_cast<size_t>(p) * W + comp];
+                    if (count_next) nkey = s_cur[static_cast<size_t>(p) * W + ncomp];
                 }
+                d = (key >> shift) & 255u;
+                if (count_next) atomicAdd(s_hnext + ((nkey >> nshift) & 255u), 1u);
             }
-            const uint32_t vmask = __ballot_sync(kFull, valid);
-            uint32_t peers = 0, before = 0;
-            if (valid) {
-                peers = __match_any_sync(vmask, d);
-                before = wh[d];
+            pk[r] = d;
+        }
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t d = pk[r];
+            if (a.ablate & 2) {
+                pm[r] = 1u << lane;
+                continue;
             }
+            if constexpr (RANK == kRankBallot) {
+                uint32_t peers = kFull;
+#pragma unroll
+                for (int bit = 0; bit < 9; ++bit) {
+                    const uint32_t bb = __ballot_sync(kFull, (d >> bit) & 1u);
+                    peers &= ((d >> bit) & 1u) ? bb : ~bb;
+                }
+                pm[r] = peers;
+            } else {
+                pm[r] = __match_any_sync(kFull, d);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t d = pk[r];
+            const uint32_t peers = pm[r];
+            uint32_t before = 0;
+            if (d < 256u) before = wh[d];
             __syncwarp();
-            if (valid && (peers & lanemask_lt()) == 0u) wh[d] = before + __popc(peers);
+            if (d < 256u && (peers & lanemask_lt()) == 0u) wh[d] = before + __popc(peers);
             __syncwarp();
-            rank[r] = before + __popc(peers & lanemask_lt());
-            dig[r] = d;
+            pk[r] = (d << 16) | (before + __popc(peers & lanemask_lt()));
         }
         __syncthreads();
 
-        // ---- per digit: warp offsets, tile count, publish, local start, look-back
+        // ---- per digit (thread d): tile count, publish, local start, windowed look-back
         {
             const uint32_t d = tid;
+            uint32_t wc[kWarps];
             uint32_t cnt = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-                const uint32_t c = s_whist[w * 256 + d];
-                s_whist[w * 256 + d] = cnt;
-                cnt += c;
+                wc[w] = s_whist[w * 256 + d];
+                cnt += wc[w];
             }
             uint64_t* mine = a.desc + static_cast<size_t>(tile) * 256 + d;
             st_relaxed(mine, pack_desc(epoch, tile == 0 ? kPrefix : kAggregate, cnt));
             uint32_t tot;
             const uint32_t start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
-            s_start[d] = start;
+            uint32_t run = start;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                s_whist[w * 256 + d] = run;  // slot of this warp's first row with digit d
+                run += wc[w];
+            }
             uint32_t excl = 0;
-            if (tile > 0) {
+            if (tile > 0 && !(a.ablate & 1)) {
                 int64_t t = static_cast<int64_t>(tile) - 1;
                 for (;;) {
-                    const uint64_t dd = wait_desc(a.desc + static_cast<size_t>(t) * 256 + d, epoch);
-                    excl += desc_value(dd);
-                    if (desc_flag(dd) == kPrefix) break;
-                    --t;
+                    constexpr int LB = 4;
+                    uint64_t v[LB];
+#pragma unroll
+                    for (int j = 0; j < LB; ++j)
+                        v[j] = (t - j >= 0) ? ld_relaxed(a.desc + static_cast<size_t>(t - j) * 256 + d)
+                                            : pack_desc(epoch, kPrefix, 0u);
+                    bool done = false;
+#pragma unroll
+                    for (int j = 0; j < LB; ++j) {
+                        if (!done) {
+                            while (desc_epoch(v[j]) != epoch || desc_flag(v[j]) == 0u) {
+                                __nanosleep(20);
+                                v[j] = ld_relaxed(a.desc + static_cast<size_t>(t - j) * 256 + d);
+                            }
+                            excl += desc_value(v[j]);
+                            done = desc_flag(v[j]) == kPrefix;
+                        }
+                    }
+                    if (done) break;
+                    t -= LB;
                 }
                 st_relaxed(mine, pack_desc(epoch, kPrefix, excl + cnt));
             }
-            s_gdst[d] = offs[d] + excl - start;  // mod 2^32; + local slot gives the global row
+            s_gdst[d] = s_offs[d] + excl - start;  // mod 2^32; + tile slot gives the global row
+        }
+        if (PF && tid == 0) {  // prefix published: now take the next tile and start its copy
+            const uint32_t t = atomicAdd(ctr, 1u);
+            s_misc[1] = t;
+            if (t < a.ntiles) load_tile(t, b ^ 1u);
         }
         __syncthreads();
 
-        // ---- reorder the tile into digit order in shared memory
+        // ---- reorder into digit order (in place from registers, or via a slot -> row index)
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
             if (p < tile_n) {
-                const uint32_t d = dig[r];
-                const uint32_t slot = s_start[d] + s_whist[warp * 256 + d] + rank[r];
-                if constexpr (W_CT == 4) {
-                    reinterpret_cast<uint4*>(s_out)[slot] =
-                        make_uint4(reg[r * 4 + 0], reg[r * 4 + 1], reg[r * 4 + 2], reg[r * 4 + 3]);
-                } else if constexpr (W_CT > 0) {
+                const uint32_t slot = s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu);
+                if constexpr (REG) {
+                    if constexpr (W_CT == 4) {
+                        reinterpret_cast<uint4*>(s_cur)[slot] =
+                            make_uint4(reg[r * 4 + 0], reg[r * 4 + 1], reg[r * 4 + 2], reg[r * 4 + 3]);
+                    } else {
 #pragma unroll
-                    for (int c = 0; c < W_CT; ++c) s_out[slot * W_CT + c] = reg[r * W_CT + c];
+                        for (int c = 0; c < W_CT; ++c) s_cur[slot * W_CT + c] = reg[r * W_CT + c];
+                    }
                 } else {
-                    for (int c = 0; c < W; ++c) s_out[static_cast<size_t>(slot) * W + c] = s_in[static_cast<size_t>(p) * W + c];
+                    s_src[slot] = static_cast<uint16_t>(p);
                 }
             }
         }
         __syncthreads();
 
         // ---- coalesced write-out: consecutive slots of one digit are consecutive rows
-        if constexpr (W_CT == 4) {
-            const uint4* s4 = reinterpret_cast<const uint4*>(s_out);
+        if (a.ablate & 4) {
+        } else if constexpr (W_CT == 4) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(s_cur);
             uint4* o4 = reinterpret_cast<uint4*>(out);
-            for (uint32_t p = tid; p < tile_n; p += kBlock) {
-                const uint32_t d = (s_out[p * 4 + comp] >> shift) & 255u;
-                o4[s_gdst[d] + p] = s4[p];
+            constexpr int U = 4;  // independent LDS -> LDS -> STG chains in flight per thread
+            for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
+                uint4 v[U];
+                uint32_t dst[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) v[u] = REG ? s4[q] : s4[s_src[q]];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) {
+                        const uint32_t key = comp == 0 ? v[u].x : (comp == 1 ? v[u].y : v[u].z);
+                        dst[u] = s_gdst[(key >> shift) & 255u] + q;
+                        if (a.ablate) dst[u] = min(dst[u], a.n - 1u);  // keep ablated runs in bounds
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) o4[dst[u]] = v[u];
+                }
             }
         } else {
             const uint32_t nw = tile_n * W;
             for (uint32_t q = tid; q < nw; q += kBlock) {
-                const uint32_t p = q / W;
-                const uint32_t c = q - p * W;
-                const uint32_t d = (s_out[static_cast<size_t>(p) * W + comp] >> shift) & 255u;
-                out[static_cast<size_t>(s_gdst[d] + p) * W + c] = s_out[q];
+                const uint32_t slot = q / W;
+                const uint32_t c = q - slot * W;
+                const size_t p = REG ? slot : s_src[slot];
+                const uint32_t d = (s_cur[p * W + comp] >> shift) & 255u;
+                out[static_cast<size_t>(s_gdst[d] + slot) * W + c] = s_cur[p * W + c];
             }
         }
+        if (PF) tile = s_misc[1];
         __syncthreads();
     }
+    if (count_next && s_hnext[tid]) atomicAdd(a.hist + nxt * 256 + tid, s_hnext[tid]);
 }
 
 // ---------------------------------------------------------------------------
-// K3: head flags, decoupled look-back scan, map scatter, unique compaction.
+// K3: head flags, decoupled look-back scan, unique compaction, and the
+// old->new pairs.  invert_permutation + remap (pipeline.py:103-130) need
+// map[org_id[j]] = new_idx[j]: a random 4-byte scatter over V entries that
+// costs ~35 B of DRAM traffic per row when done directly.  Instead each tile
+// buckets its (org, new_idx) pairs by the high bits of org in shared memory
+// and appends each bucket run to that bucket's contiguous region of a pair
+// array (the free ping-pong row buffer); K3b then streams the pairs bucket
+// by bucket, so its map stores stay inside an L2-resident window.
 struct UniqueArgs {
     const uint32_t* rows0;
     const uint32_t* rows1;
     const uint32_t* plan;
     uint64_t* desc;     // [ntiles]
     uint32_t* counter;  // tile-id counter
+    uint32_t* fill;     // [256] per-bucket append counters
     const uint32_t* status;
-    uint32_t* map;      // map[org_id] = new_idx
     uint32_t* out_vtx;  // [U][D]
     unsigned long long* count;
     uint32_t* sc_org;   // optional scratch outputs
@@ -391,13 +610,15 @@ struct UniqueArgs {
     uint32_t n;
     uint32_t ntiles;
     int dim;
+    int bucket_shift;   // bucket = org >> bucket_shift (<= 256 buckets)
 };
 
 template <int W_CT, int IPT>
 struct UniqueTraits {
     static constexpr int kTile = kBlock * IPT;
     static __host__ __device__ size_t smem_bytes(int W) {
-        return static_cast<size_t>(kTile) * W * 4 + (64 + kWarps + 8) * 4 + 16;
+        return static_cast<size_t>(kTile) * W * 4 + static_cast<size_t>(kTile) * 8 + (64 + 4 * 256 + 2 * kWarps + 8) * 4 +
+               16;
     }
 };
 
@@ -409,34 +630,48 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
     const int W = D + 1;
     if (*a.status) return;
     const uint32_t* __restrict__ rows = a.plan[0] ? a.rows1 : a.rows0;
+    uint2* __restrict__ pairs = reinterpret_cast<uint2*>(a.plan[0] ? const_cast<uint32_t*>(a.rows0)
+                                                                    : const_cast<uint32_t*>(a.rows1));
 
     extern __shared__ __align__(128) uint32_t smem[];
+    const size_t tw = static_cast<size_t>(TILE) * W;
     uint32_t* s_rows = smem;
-    uint32_t* s_prev = s_rows + static_cast<size_t>(TILE) * W;  // up to 64 words
-    uint32_t* s_warp = s_prev + 64;
-    uint32_t* s_misc = s_warp + kWarps;
+    uint2* s_pairs = reinterpret_cast<uint2*>(smem + tw);     // tile pairs, bucket order
+    uint32_t* s_prev = smem + tw + 2 * TILE;                   // up to 64 words
+    uint32_t* s_bcnt = s_prev + 64;                            // per-bucket count in tile
+    uint32_t* s_bcur = s_bcnt + 256;                           // running local slot per bucket
+    uint32_t* s_bglob = s_bcur + 256;                          // pair index of local slot 0, per bucket
+    uint32_t* s_bsave = s_bglob + 256;
+    uint32_t* s_warp = s_bsave + 256;
+    uint32_t* s_misc = s_warp + 2 * kWarps;
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const int bs = a.bucket_shift;
     if (tid == 0) {
         mbar_init(s_bar, 1);
         fence_mbar_init();
     }
-    __syncthreads();
-
-    for (uint32_t iter = 0;; ++iter) {
-        if (tid == 0) s_misc[0] = atomicAdd(a.counter, 1u);
+    for (uint32_t it = 0;; ++it) {
+        if (tid == 0) {
+            const uint32_t t = atomicAdd(a.counter, 1u);
+            s_misc[0] = t;
+            if (t < a.ntiles) {
+                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
+                stage_tile(s_rows, rows + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
+            }
+        }
+        s_bcnt[tid] = 0u;
         __syncthreads();
         const uint32_t tile = s_misc[0];
         if (tile >= a.ntiles) break;
         const uint32_t base = tile * static_cast<uint32_t>(TILE);
         const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
-        if (tid == 0) stage_tile(s_rows, rows + static_cast<size_t>(base) * W, tile_n * W * 4u, s_bar);
         if (tile > 0 && tid < static_cast<uint32_t>(D)) s_prev[tid] = rows[static_cast<size_t>(base - 1) * W + tid];
-        mbar_wait(s_bar, iter & 1u);
         __syncthreads();
+        mbar_wait(s_bar, it & 1u);
 
-        // ---- phase 1: head flags (warp-striped rows) and per-warp totals
+        // ---- phase 1: head flags (warp-striped rows), per-warp totals, bucket counts
         uint32_t bal[IPT];
         uint32_t wtotal = 0;
 #pragma unroll
@@ -444,10 +679,10 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
             const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
             bool head = false;
             if (p < tile_n) {
+                const uint32_t* cur = s_rows + static_cast<size_t>(p) * W;
                 if (base + p == 0u) {
                     head = true;
                 } else {
-                    const uint32_t* cur = s_rows + static_cast<size_t>(p) * W;
                     const uint32_t* prv = p ? cur - W : s_prev;
                     if constexpr (W_CT > 0) {
 #pragma unroll
@@ -456,6 +691,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
                         for (int c = 0; c < D; ++c) head |= cur[c] != prv[c];
                     }
                 }
+                atomicAdd(s_bcnt + (cur[D] >> bs), 1u);
             }
             bal[r] = __ballot_sync(kFull, head);
             wtotal += __popc(bal[r]);
@@ -469,8 +705,18 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
             wexcl += (static_cast<uint32_t>(w) < warp) ? t : 0u;
             ttotal += t;
         }
+        // bucket b (thread b): local start, and append space in the global pair array
+        {
+            const uint32_t cnt = s_bcnt[tid];
+            uint32_t tot;
+            const uint32_t start = block_exclusive_scan<kWarps>(cnt, s_warp + kWarps, tot);
+            s_bcur[tid] = start;
+            s_bsave[tid] = start;
+            if (cnt) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, cnt) - start;
+        }
 
-        // ---- decoupled look-back over tiles (warp 0, 32 predecessors per step)
+        // ---- decoupled look-back over tiles (warp 0, 32 predecessors per window;
+        // waits only for the descriptors up to the nearest inclusive prefix)
         if (warp == 0) {
             uint64_t* mine = a.desc + tile;
             uint32_t excl = 0;
@@ -481,25 +727,35 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
                 int64_t hi = static_cast<int64_t>(tile) - 1;
                 for (;;) {
                     const int64_t t = hi - static_cast<int64_t>(lane);
-                    const uint64_t dd = t >= 0 ? wait_desc(a.desc + t, 1u) : pack_desc(1u, kPrefix, 0u);
-                    const uint32_t pm = __ballot_sync(kFull, desc_flag(dd) == kPrefix);
-                    if (pm) {
-                        const uint32_t first = __ffs(pm) - 1;
-                        excl += warp_sum(lane <= first ? desc_value(dd) : 0u);
-                        break;
+                    uint64_t dd = t >= 0 ? ld_relaxed(a.desc + t) : pack_desc(1u, kPrefix, 0u);
+                    bool done = false;
+                    for (;;) {
+                        const bool valid = desc_epoch(dd) == 1u && desc_flag(dd) != 0u;
+                        const uint32_t vm = __ballot_sync(kFull, valid);
+                        const uint32_t pm = __ballot_sync(kFull, valid && desc_flag(dd) == kPrefix);
+                        const uint32_t need = pm ? (((pm & (0u - pm)) << 1) - 1u) : kFull;
+                        if ((vm & need) == need) {
+                            excl += warp_sum(((need >> lane) & 1u) ? desc_value(dd) : 0u);
+                            done = pm != 0u;
+                            break;
+                        }
+                        if (!valid) {
+                            __nanosleep(20);
+                            dd = ld_relaxed(a.desc + t);
+                        }
                     }
-                    excl += warp_sum(desc_value(dd));
+                    if (done) break;
                     hi -= 32;
                 }
                 if (lane == 0) st_relaxed(mine, pack_desc(1u, kPrefix, excl + ttotal));
             }
-            if (lane == 0) s_misc[1] = excl;
+            if (lane == 0) s_misc[2] = excl;
         }
         __syncthreads();
-        const uint32_t tprefix = s_misc[1];
+        const uint32_t tprefix = s_misc[2];
         if (tid == 0 && tile == a.ntiles - 1) *a.count = static_cast<unsigned long long>(tprefix) + ttotal;
 
-        // ---- phase 2: new index per slot, map scatter, unique rows out
+        // ---- phase 2: new index per slot, bucketed pairs, unique rows out
         uint32_t running = tprefix + wexcl;
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
@@ -508,7 +764,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
                 const uint32_t* row = s_rows + static_cast<size_t>(p) * W;
                 const uint32_t nidx = running + __popc(bal[r] & lanemask_le()) - 1u;
                 const uint32_t org = row[D];
-                a.map[org] = nidx;
+                s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
                 const bool head = (bal[r] >> lane) & 1u;
                 if (head) {
                     uint32_t* dst = a.out_vtx + static_cast<size_t>(nidx) * D;
@@ -522,6 +778,31 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
             running += __popc(bal[r]);
         }
         __syncthreads();
+        // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
+        for (uint32_t q = tid; q < tile_n; q += kBlock) {
+            const uint2 pr = s_pairs[q];
+            pairs[s_bglob[pr.x >> bs] + q] = pr;
+        }
+        __syncthreads();
+    }
+}
+
+// K3b: map[org] = new_idx from the bucket-major pair array (streaming reads;
+// the stores of concurrently running CTAs fall in one or two buckets, i.e. an
+// L2-resident window of map, so partial sectors merge before write-back).
+__global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const uint32_t* rows0,
+                                                      const uint32_t* rows1, uint32_t* map, uint32_t n,
+                                                      const uint32_t* status) {
+    if (*status) return;
+    const uint4* pairs = reinterpret_cast<const uint4*>(plan[0] ? rows0 : rows1);
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
+    if (2 * i + 1 < n) {
+        const uint4 v = __ldcs(pairs + i);
+        map[v.x] = v.y;
+        map[v.z] = v.w;
+    } else if (2 * i < n) {
+        const uint2 v = reinterpret_cast<const uint2*>(pairs)[2 * i];
+        map[v.x] = v.y;
     }
 }
 

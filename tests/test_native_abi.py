@@ -35,7 +35,7 @@ def test_workspace_and_stage_queries():
     assert big > 2 * 157_500_000 * 16          # two row buffers of 16-byte rows
     assert lib.rmx_workspace_bytes(10, 0, 4, 3) == 0
     assert lib.rmx_workspace_bytes(10, 33, 4, 3) == 0
-    assert lib.rmx_stage_count(3) == 18
+    assert lib.rmx_stage_count(3) == 19
     assert lib.rmx_stage_name(3, 4) == b"sort_pass_0"
     assert lib.rmx_stage_name(3, 16) == b"unique"
 
