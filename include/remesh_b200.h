@@ -108,10 +108,14 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
 int rmx_stage_count(uint32_t dim);
 const char* rmx_stage_name(uint32_t dim, int k);
 
-/* Sort passes actually executed by the last call on this thread (digit
- * passes whose 8-bit digit is constant over all keys are skipped). Host-side
- * diagnostic: reads the device plan, so it synchronises `stream`. */
+/* Sort plan of the last call that used `workspace` (host-side diagnostic; it
+ * reads the device plan, so it synchronises `stream`).  Digit passes whose
+ * 8-bit digit is constant over all keys are skipped; when at most 64 key bits
+ * vary, the varying bits are packed into one u32/u64 key (order-preserving).
+ * rmx_last_executed_passes returns the executed sort passes;
+ * rmx_plan_info fills info[4] = {packed, key words, varying bits, passes}. */
 int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream);
+int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
 /*
  * Synthetic lattice soups of BASELINE.md section 3 (bench input generator;

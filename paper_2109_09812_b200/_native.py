@@ -25,7 +25,7 @@ RMX_MAX_DIM = 32
 EXPORTS = (
     "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex",
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name",
-    "rmx_last_executed_passes", "rmx_lattice_sizes", "rmx_gen_lattice_soup",
+    "rmx_last_executed_passes", "rmx_plan_info", "rmx_lattice_sizes", "rmx_gen_lattice_soup",
 )
 
 
@@ -58,6 +58,7 @@ _SIGNATURES = {
     "rmx_stage_count": (_int, [_u32]),
     "rmx_stage_name": (ctypes.c_char_p, [_u32, _int]),
     "rmx_last_executed_passes": (_int, [_vp, _u64, _u32, _vp]),
+    "rmx_plan_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
     "rmx_lattice_sizes": (_int, [_int, _u32, _u32, _u32, _u64,
                                  ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "rmx_gen_lattice_soup": (_int, [_int, _u32, _u32, _u32, _u64, _u64, _vp, _vp, _vp]),

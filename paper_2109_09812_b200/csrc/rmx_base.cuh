@@ -1,0 +1,34 @@
+// rmx_base.cuh -- launch geometry and the device plan layout shared by all kernels.
+#pragma once
+
+#include "../../include/remesh_b200.h"
+#include "rmx_common.cuh"
+
+namespace rmx {
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+
+// ---------------------------------------------------------------------------
+// Plan layout (uint32 words, lives in the workspace):
+//   [0] buffer holding the final sorted rows   [1] executed passes
+//   [2] first executed pass                    [3] first pass needs k_first_hist
+//   [4 + p]            pass p executes (digit not constant)
+//   [4 + P + p]        source buffer of pass p
+//   [4 + 2P + p]       next executed pass after p (P = none)
+//
+// Packed-key section, at word pk_base(P).  When at most 64 key bits vary over
+// the (cleaned) vertex set, the varying bits are gathered into one u32/u64
+// key -- an order-preserving compaction, since the dropped bits are equal in
+// every row -- and the sort runs over (packed key, origin) pairs instead:
+//   [0] mode (1 = packed)        [1] key words KW (1 | 2)   [2] varying bits B
+//   [3] packed passes ceil(B/8)  [4] number of runs         [5..7] reserved
+//   [8 + 4r ..] run r: component, source bit, length, destination bit
+// Runs are listed from component D-1 (least significant) to component 0,
+// low bits first, so destination bits grow monotonically.
+constexpr int kMaxRuns = 64;
+constexpr int kMaxPackedPasses = 8;
+__host__ __device__ inline size_t pk_base(int P) { return 4 + 3 * static_cast<size_t>(P); }
+__host__ __device__ inline size_t plan_words(int P) { return pk_base(P) + 8 + 4 * kMaxRuns; }
+
+}  // namespace rmx

@@ -31,101 +31,46 @@ int fail_cuda(cudaError_t e, const char* what) {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
-// Per-W kernel configurations.  W = dim + 1.  For the hot width (W = 4,
-// float3 keys) a menu of sort / unique variants is compiled in and one is
-// selected by RMX_SORT_CFG / RMX_UNIQ_CFG (tuning); other widths use one
-// configuration each.
-struct SortCfg { int ipt; bool reg; int pf; };
-struct UniqCfg { int ipt; };
+// Per-W tile sizes (rows per tile = 256 x IPT), chosen by measurement on B200.
+template <int W>
+struct SortIpt { static constexpr int v = W == 2 ? 16 : (W == 3 ? 16 : (W == 4 ? 12 : (W == 5 ? 10 : 2))); };
+template <int W>
+struct UniqIpt { static constexpr int v = W == 2 ? 16 : (W == 3 ? 12 : (W == 4 ? 8 : (W == 5 ? 8 : 2))); };
 
-#define RMX_SORT_MENU(X) \
-    X(0, 10, true, 1)    \
-    X(1, 8, false, 0)    \
-    X(2, 12, false, 1)   \
-    X(3, 8, true, 0)     \
-    X(4, 16, false, 0)   \
-    X(5, 6, false, 1)    \
-    X(6, 8, false, 1)    \
-    X(7, 10, false, 1)   \
-    X(8, 12, false, 0)
-#define RMX_UNIQ_MENU(X) \
-    X(0, 8)              \
-    X(1, 12)             \
-    X(2, 16)             \
-    X(3, 6)
-
-int env_choice(const char* name, int n, int dflt) {
-    const char* e = std::getenv(name);
-    if (!e || !*e) return dflt;
-    const int v = (*e >= 'A' && *e <= 'Z') ? *e - 'A' : ((*e >= 'a' && *e <= 'z') ? *e - 'a' : std::atoi(e));
-    return (v >= 0 && v < n) ? v : dflt;
-}
-int sort_choice() {
-    static int c = env_choice("RMX_SORT_CFG", 9, 8);
-    return c;
-}
-int uniq_choice() {
-    static int c = env_choice("RMX_UNIQ_CFG", 4, 0);
-    return c;
-}
-
-SortCfg sort_cfg(int W) {
-    if (W == 4) {
-        switch (sort_choice()) {
-#define X(id, ipt, reg, pf) case id: return SortCfg{ipt, reg, pf};
-            RMX_SORT_MENU(X)
-#undef X
-        }
-    }
+int sort_tile(int W) {
     switch (W) {
-        case 2: return SortCfg{16, true, 0};
-        case 3: return SortCfg{12, true, 0};
-        case 5: return SortCfg{8, true, 0};
-        default: return SortCfg{2, false, 0};
+        case 2: return kBlock * SortIpt<2>::v;
+        case 3: return kBlock * SortIpt<3>::v;
+        case 4: return kBlock * SortIpt<4>::v;
+        case 5: return kBlock * SortIpt<5>::v;
+        default: return kBlock * SortIpt<0>::v;
     }
 }
-UniqCfg uniq_cfg(int W) {
-    if (W == 4) {
-        switch (uniq_choice()) {
-#define X(id, ipt) case id: return UniqCfg{ipt};
-            RMX_UNIQ_MENU(X)
-#undef X
-        }
-    }
+int uniq_tile(int W) {
     switch (W) {
-        case 2: return UniqCfg{16};
-        case 3: return UniqCfg{12};
-        case 5: return UniqCfg{8};
-        default: return UniqCfg{2};
+        case 2: return kBlock * UniqIpt<2>::v;
+        case 3: return kBlock * UniqIpt<3>::v;
+        case 4: return kBlock * UniqIpt<4>::v;
+        case 5: return kBlock * UniqIpt<5>::v;
+        default: return kBlock * UniqIpt<0>::v;
     }
 }
-int sort_tile(int W) { return kBlock * sort_cfg(W).ipt; }
-int uniq_tile(int W) { return kBlock * uniq_cfg(W).ipt; }
 
-// tuning-only ablation switches (RMX_ABLATE bitmask; results are invalid when set)
-int ablate_bits() {
-    static int v = [] {
-        const char* e = std::getenv("RMX_ABLATE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
-// warp ranking variant (RMX_RANK=ballot selects the 8-ballot multi-split)
-int rank_mode() {
-    static int mode = [] {
-        const char* e = std::getenv("RMX_RANK");
-        return (e && std::strcmp(e, "ballot") == 0) ? kRankBallot : kRankMatch;
-    }();
-    return mode;
-}
+// packed-key path tiles
+constexpr int kPkSortIpt = 16;
+constexpr int kPkUniqIpt = 12;
+constexpr int kPkSortTile = kBlock * kPkSortIpt;
+constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
 
 struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, hist, vary, fill, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, hist, hist_pk, vary, fill, counters, desc, desc3, ctl_end;
     int bucket_shift;
+    uint32_t ntiles_pk, ntiles3_pk;
+    size_t vals_off;  // words: origins of the packed-key path inside a row buffer
+    size_t tile_counts;
     size_t total;
 };
 
@@ -136,13 +81,16 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.P = 4 * L.D;
     L.ntiles = static_cast<uint32_t>((V + sort_tile(L.W) - 1) / sort_tile(L.W));
     L.ntiles3 = static_cast<uint32_t>((V + uniq_tile(L.W) - 1) / uniq_tile(L.W));
+    L.ntiles_pk = static_cast<uint32_t>((V + kPkSortTile - 1) / kPkSortTile);
+    L.ntiles3_pk = static_cast<uint32_t>((V + kPkUniqTile - 1) / kPkUniqTile);
+    L.vals_off = (static_cast<size_t>(V) * (L.D >= 2 ? 2 : 1) + 3) & ~static_cast<size_t>(3);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t at = off;
         off = align_up(off + bytes);
         return at;
     };
-    const size_t row_bytes = static_cast<size_t>(V) * L.W * 4 + 16;  // +16: bulk copies round up
+    const size_t row_bytes = static_cast<size_t>(V) * L.W * 4 + 256;  // slack: bulk copies round up to 16 B
     L.flags = take(V);
     L.rows0 = take(row_bytes);
     L.rows1 = take(row_bytes);
@@ -150,14 +98,16 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.plan = take(plan_words(L.P) * 4);
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
+    L.hist_pk = take(static_cast<size_t>(kMaxPackedPasses) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
     L.fill = take(256 * 4);
     int bits = 0;
     while (bits < 40 && (1ull << bits) < V) ++bits;
     L.bucket_shift = bits > 8 ? bits - 8 : 0;
-    L.counters = take(static_cast<size_t>(L.P + 2) * 4);
-    L.desc = take(static_cast<size_t>(L.ntiles) * 256 * 8);
+    L.counters = take(static_cast<size_t>(L.P + 2 + kMaxPackedPasses + 1) * 4);
+    L.desc = take(static_cast<size_t>(L.ntiles > L.ntiles_pk ? L.ntiles : L.ntiles_pk) * 256 * 8);
     L.desc3 = take(static_cast<size_t>(L.ntiles3) * 8);
+    L.tile_counts = take(static_cast<size_t>(L.ntiles3_pk) * 4);
     L.ctl_end = off;
     L.total = off;
     return L;
@@ -208,10 +158,10 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     return RMX_OK;
 }
 
-template <int W_CT, int IPT, int RANK, bool REG, int PF>
+template <int W_CT, int IPT>
 int launch_pass(const SortArgs& a, cudaStream_t s) {
-    auto kern = k_sort_pass<W_CT, IPT, RANK, REG, PF>;
-    const size_t smem = SortTraits<W_CT, IPT, REG, PF>::smem_bytes(a.dim + 1);
+    auto kern = k_sort_pass<W_CT, IPT>;
+    const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
     int grid = 0;
     int rc = persistent_grid(kern, smem, a.ntiles, grid);
     if (rc) return rc;
@@ -232,6 +182,66 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
     return RMX_OK;
 }
 
+template <int D_CT>
+int launch_vary(const VaryArgs& a, cudaStream_t s) {
+    int grid = 0;
+    int rc = persistent_grid(k_vary<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
+    if (rc) return rc;
+    k_vary<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int dispatch_vary(const VaryArgs& a, cudaStream_t s) {
+    switch (a.dim) {
+        case 1: return launch_vary<1>(a, s);
+        case 2: return launch_vary<2>(a, s);
+        case 3: return launch_vary<3>(a, s);
+        case 4: return launch_vary<4>(a, s);
+        default: return launch_vary<0>(a, s);
+    }
+}
+
+template <int D_CT>
+int launch_pack(const PackArgs& a, cudaStream_t s) {
+    int grid = 0;
+    int rc = persistent_grid(k_pack<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
+    if (rc) return rc;
+    k_pack<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int dispatch_pack(const PackArgs& a, cudaStream_t s) {
+    switch (a.dim) {
+        case 1: return launch_pack<1>(a, s);
+        case 2: return launch_pack<2>(a, s);
+        case 3: return launch_pack<3>(a, s);
+        case 4: return launch_pack<4>(a, s);
+        default: return launch_pack<0>(a, s);
+    }
+}
+
+int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
+    const size_t smem = SortPkTraits<kPkSortIpt>::smem_bytes();
+    int grid = 0;
+    int rc = persistent_grid(k_sort_pk<kPkSortIpt>, smem, a.ntiles, grid);
+    if (rc) return rc;
+    k_sort_pk<kPkSortIpt><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
+    const size_t smem = UniquePkTraits<kPkUniqIpt>::smem_bytes();
+    int grid = 0;
+    int rc = persistent_grid(k_unique_pk<kPkUniqIpt>, smem, a.ntiles, grid);
+    if (rc) return rc;
+    k_unique_pk<kPkUniqIpt><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int dispatch_build(const BuildArgs& a, cudaStream_t s) {
     switch (a.dim) {
         case 1: return launch_build<1>(a, s);
@@ -242,40 +252,23 @@ int dispatch_build(const BuildArgs& a, cudaStream_t s) {
     }
 }
 
-template <int RANK>
-int dispatch_pass_r(const SortArgs& a, cudaStream_t s) {
-    switch (a.dim + 1) {
-        case 2: return launch_pass<2, 16, RANK, true, 0>(a, s);
-        case 3: return launch_pass<3, 12, RANK, true, 0>(a, s);
-        case 4:
-            switch (sort_choice()) {
-#define X(id, ipt, reg, pf) case id: return launch_pass<4, ipt, RANK, reg, pf>(a, s);
-                RMX_SORT_MENU(X)
-#undef X
-            }
-            return RMX_EINVAL;
-        case 5: return launch_pass<5, 8, RANK, true, 0>(a, s);
-        default: return launch_pass<0, 2, RANK, false, 0>(a, s);
-    }
-}
-
 int dispatch_pass(const SortArgs& a, cudaStream_t s) {
-    return rank_mode() == kRankBallot ? dispatch_pass_r<kRankBallot>(a, s) : dispatch_pass_r<kRankMatch>(a, s);
+    switch (a.dim + 1) {
+        case 2: return launch_pass<2, SortIpt<2>::v>(a, s);
+        case 3: return launch_pass<3, SortIpt<3>::v>(a, s);
+        case 4: return launch_pass<4, SortIpt<4>::v>(a, s);
+        case 5: return launch_pass<5, SortIpt<5>::v>(a, s);
+        default: return launch_pass<0, SortIpt<0>::v>(a, s);
+    }
 }
 
 int dispatch_unique(const UniqueArgs& a, cudaStream_t s) {
     switch (a.dim + 1) {
-        case 2: return launch_unique<2, 16>(a, s);
-        case 3: return launch_unique<3, 12>(a, s);
-        case 4:
-            switch (uniq_choice()) {
-#define X(id, ipt) case id: return launch_unique<4, ipt>(a, s);
-                RMX_UNIQ_MENU(X)
-#undef X
-            }
-            return RMX_EINVAL;
-        case 5: return launch_unique<5, 8>(a, s);
-        default: return launch_unique<0, 2>(a, s);
+        case 2: return launch_unique<2, UniqIpt<2>::v>(a, s);
+        case 3: return launch_unique<3, UniqIpt<3>::v>(a, s);
+        case 4: return launch_unique<4, UniqIpt<4>::v>(a, s);
+        case 5: return launch_unique<5, UniqIpt<5>::v>(a, s);
+        default: return launch_unique<0, UniqIpt<0>::v>(a, s);
     }
 }
 
@@ -372,15 +365,22 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (V == 0) {  // every index is out of range; status is set
         return RMX_OK;
     }
-    // K1b rows + histograms
+    // K1a varying bits of the cleaned vertex set, then the plan (packed or AoS)
+    const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
     {
-        BuildArgs a{vtx,     flags, idx, rows0, hist, vary, d_status, static_cast<uint32_t>(V), L.D,
-                    (aligned16(vtx) && aligned16(flags)) ? 1 : 0};
-        if ((rc = dispatch_build(a, s))) return rc;
+        VaryArgs a{vtx, flags, idx, vary, d_status, static_cast<uint32_t>(V), L.D, vec};
+        if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
     k_plan<<<1, 32, 0, s>>>(vary, plan, L.D, d_status);
     RMX_CHECK(cudaGetLastError());
+    if ((rc = rec.mark())) return rc;
+    // ---- AoS path (kernels exit at once in packed mode)
+    {
+        BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
+        if ((rc = dispatch_build(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
     {
         HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D};
         int grid = 0;
@@ -390,20 +390,49 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
-    // K2 onesweep passes, least significant digit first
-    for (int p = 0; p < L.P; ++p) {
-        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p,
-                   ablate_bits()};
+    for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
+        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p};
         if ((rc = dispatch_pass(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
-    // K3 unique + bucketed pairs, K3b map fill
+    // ---- packed-key path (kernels exit at once in AoS mode)
+    uint32_t* hist_pk = reinterpret_cast<uint32_t*>(base + L.hist_pk);
     {
-        UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, reinterpret_cast<uint32_t*>(base + L.fill), d_status,
+        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, hist_pk, d_status, static_cast<uint32_t>(V), L.D, vec};
+        if ((rc = dispatch_pack(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    for (int p = 0; p < kMaxPackedPasses; ++p) {
+        SortPkArgs a{rows0, rows1, L.vals_off, plan, hist_pk, desc, counters + L.P + 2, d_status,
+                     static_cast<uint32_t>(V), L.ntiles_pk, L.D, p};
+        if ((rc = launch_sort_pk(a, s))) return rc;
+        if ((rc = rec.mark())) return rc;
+    }
+    // ---- K3 unique + bucketed pairs (one of the two runs), K3b map fill
+    uint32_t* fill = reinterpret_cast<uint32_t*>(base + L.fill);
+    {
+        UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, fill, d_status,
                      out_vtx, reinterpret_cast<unsigned long long*>(d_count),
                      sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
                      sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D, L.bucket_shift};
         if ((rc = dispatch_unique(a, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    {
+        uint32_t* counts = reinterpret_cast<uint32_t*>(base + L.tile_counts);
+        HeadCountArgs h{rows0, rows1, plan, counts, d_status, static_cast<uint32_t>(V), L.ntiles3_pk,
+                        static_cast<uint32_t>(kPkUniqTile), L.D};
+        int grid = 0;
+        if ((rc = grid_for_stream(static_cast<uint64_t>(L.ntiles3_pk) * kBlock, grid))) return rc;
+        k_head_count_pk<<<grid, kBlock, 0, s>>>(h);
+        RMX_CHECK(cudaGetLastError());
+        k_tile_scan<<<1, 1024, 0, s>>>(counts, L.ntiles3_pk, plan, L.D, reinterpret_cast<unsigned long long*>(d_count),
+                                       d_status);
+        RMX_CHECK(cudaGetLastError());
+        UniquePkArgs a{rows0, rows1, L.vals_off, plan, vtx, idx, vary, counts, fill, d_status, out_vtx,
+                       sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
+                       sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
+        if ((rc = launch_unique_pk(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
     {
@@ -468,23 +497,45 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
                         n_events);
 }
 
-int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 7; }
+int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
     static thread_local char buf[32];
     const int P = static_cast<int>(4 * dim);
-    if (k == 0) return "start";
-    if (k == 1) return "mark";
-    if (k == 2) return "build_rows";
-    if (k == 3) return "plan";
-    if (k >= 4 && k < 4 + P) {
-        std::snprintf(buf, sizeof(buf), "sort_pass_%d", k - 4);
+    static const char* head[] = {"start", "mark", "vary", "plan", "build_rows", "first_hist"};
+    if (k >= 0 && k < 6) return head[k];
+    k -= 6;
+    if (k < P) {
+        std::snprintf(buf, sizeof(buf), "sort_pass_%d", k);
         return buf;
     }
-    if (k == 4 + P) return "unique";
-    if (k == 5 + P) return "map_fill";
-    if (k == 6 + P) return "remap";
+    k -= P;
+    if (k == 0) return "pack";
+    k -= 1;
+    if (k < kMaxPackedPasses) {
+        std::snprintf(buf, sizeof(buf), "pk_pass_%d", k);
+        return buf;
+    }
+    k -= kMaxPackedPasses;
+    static const char* tail[] = {"unique", "unique_pk", "map_fill", "remap"};
+    if (k >= 0 && k < 4) return tail[k];
     return "";
+}
+
+int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t h[8] = {0};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* plan = static_cast<char*>(workspace) + L.plan;
+    RMX_CHECK(cudaMemcpyAsync(h, plan, 8, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(h + 2, plan + pk_base(L.P) * 4, 16, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    info[0] = h[2];  // packed mode
+    info[1] = h[2] ? h[3] : 0u;  // key words
+    info[2] = h[2] ? h[4] : 0u;  // varying bits
+    info[3] = h[1];  // executed sort passes
+    return RMX_OK;
 }
 
 int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream) {

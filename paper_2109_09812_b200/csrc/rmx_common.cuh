@@ -116,6 +116,19 @@ __device__ __forceinline__ void stage_tile(void* dst, const void* src, uint32_t 
     }
 }
 
+// Two ranges staged onto one barrier (keys + values of a packed tile).
+__device__ __forceinline__ void stage_tile2(void* dst0, const void* src0, uint32_t bytes0, void* dst1, const void* src1,
+                                            uint32_t bytes1, uint64_t* bar) {
+    const uint32_t b0 = (bytes0 + 15u) & ~15u, b1 = (bytes1 + 15u) & ~15u;
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, b0 + b1);
+    constexpr uint32_t kChunk = 32768u;
+    for (uint32_t off = 0; off < b0; off += kChunk)
+        bulk_g2s(static_cast<char*>(dst0) + off, static_cast<const char*>(src0) + off, min(kChunk, b0 - off), bar);
+    for (uint32_t off = 0; off < b1; off += kChunk)
+        bulk_g2s(static_cast<char*>(dst1) + off, static_cast<const char*>(src1) + off, min(kChunk, b1 - off), bar);
+}
+
 // ---- block scan over one value per thread ----------------------------------
 // Exclusive scan of `v` across a block of NW warps; `s_warp` holds NW words and
 // must not be reused until a later __syncthreads.
@@ -140,6 +153,87 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     }
     total = all;
     return before + x - v;
+}
+
+// Ranking strategy per pass, from the digit's global histogram (`h` = this
+// thread's bin; 256-thread block): MATCH.ANY costs ~2 SM-cycles per DISTINCT
+// value in the warp (B200 measurement) and 8 ballots ~29, so match is used
+// when at most 16 bins are populated, the ballot multi-split otherwise.
+__device__ __forceinline__ bool prefer_match(uint32_t h) { return __syncthreads_count(h != 0u) <= 16; }
+
+// Stable warp ranking of IPT rounds of 8-bit digits (pk[r] = digit, 256 for
+// rows past the end of a partial tile).  wh = this warp's 256 digit counters
+// (zeroed).  On return pk[r] = digit << 16 | rank among this warp's earlier
+// rows with the same digit, and wh holds the warp's digit counts.
+// Peer masks of all rounds are formed first (independent instructions), then
+// only the short counter read-modify-write chain is serial.
+template <int IPT>
+__device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, bool use_match, bool partial) {
+    uint32_t pm[IPT];
+    if (use_match) {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) pm[r] = __match_any_sync(kFull, pk[r]);
+    } else {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t d = pk[r];
+            uint32_t peers = kFull;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t bb = __ballot_sync(kFull, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bb : ~bb;
+            }
+            pm[r] = peers;
+        }
+        if (partial) {
+#pragma unroll
+            for (int r = 0; r < IPT; ++r) pm[r] &= __ballot_sync(kFull, pk[r] < 256u);
+        }
+    }
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t d = pk[r];
+        const uint32_t peers = pm[r];
+        const bool valid = d < 256u;
+        const uint32_t before = valid ? wh[d] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) wh[d] = before + __popc(peers);
+        __syncwarp();
+        pk[r] = (d << 16) | (before + __popc(peers & lt));
+    }
+}
+
+// Decoupled look-back for one digit column of the [tile][256] descriptor
+// array: LB predecessors are read per round trip, and waiting on a
+// not-yet-published descriptor backs off exponentially (spinning threads
+// would otherwise steal issue slots from the CTAs doing real work).
+template <int LB>
+__device__ __forceinline__ uint32_t lookback_digit(const uint64_t* desc, uint32_t tile, uint32_t d, uint32_t epoch) {
+    uint32_t excl = 0;
+    int64_t t = static_cast<int64_t>(tile) - 1;
+    uint32_t backoff = 32;
+    for (;;) {
+        uint64_t v[LB];
+#pragma unroll
+        for (int j = 0; j < LB; ++j)
+            v[j] = (t - j >= 0) ? ld_relaxed(desc + static_cast<size_t>(t - j) * 256 + d) : pack_desc(epoch, kPrefix, 0u);
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < LB; ++j) {
+            if (!done) {
+                while (desc_epoch(v[j]) != epoch || desc_flag(v[j]) == 0u) {
+                    __nanosleep(backoff);
+                    backoff = min(backoff * 2u, 1024u);
+                    v[j] = ld_relaxed(desc + static_cast<size_t>(t - j) * 256 + d);
+                }
+                excl += desc_value(v[j]);
+                done = desc_flag(v[j]) == kPrefix;
+            }
+        }
+        if (done) return excl;
+        t -= LB;
+    }
 }
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {

@@ -1,0 +1,658 @@
+// rmx_packed.cuh -- the packed-key path.
+//
+// Mesh coordinates rarely use all 32 bits of every component: lattice or
+// quantised data leave exponent and low mantissa bits constant.  The plan
+// (rmx_prep.cuh:k_plan) gathers the bits that vary over the cleaned vertex
+// set into runs; when they total at most 64 bits the sort runs over
+// (packed key, origin) pairs instead of full (D key words, origin) rows:
+//
+//   K1a  k_vary       OR over used rows of (key ^ replacement key), per component
+//   K1b' k_pack       cleaned rows -> packed u32/u64 keys + origins (SoA), and the
+//                     histogram of packed digit 0 (overwrite_unused pipeline.py:54-63)
+//   K2'  k_sort_pk    onesweep LSD pass over packed keys (8-bit digits, ceil(B/8) passes)
+//   K3'  k_head_count_pk + k_tile_scan + k_unique_pk: reduce-then-scan of the
+//                     head flags on packed keys, unique rows unpacked back to D
+//                     words, bucketed (org, new_idx) pairs
+//
+// Order and equality are preserved exactly: bits dropped by the packing are
+// equal in every cleaned row (they equal the replacement key's bits), so the
+// first differing bit of two full keys is always a kept bit, kept bits keep
+// their relative significance, and unpacking restores the dropped bits from
+// the replacement key.
+#pragma once
+
+#include "rmx_prep.cuh"
+
+namespace rmx {
+
+template <int KW>
+struct PkKey;
+template <>
+struct PkKey<1> { using T = uint32_t; };
+template <>
+struct PkKey<2> { using T = uint64_t; };
+
+__device__ __forceinline__ uint32_t low_mask(uint32_t len) { return len >= 32u ? 0xFFFFFFFFu : ((1u << len) - 1u); }
+
+template <int D_CT>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&k)[D_CT], uint32_t c) {
+    uint32_t w = k[0];
+#pragma unroll
+    for (int i = 1; i < D_CT; ++i) w = (c == static_cast<uint32_t>(i)) ? k[i] : w;
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+// K1a: varying bits of the cleaned vertex set.
+struct VaryArgs {
+    const uint32_t* vtx;
+    const uint8_t* flags;
+    const uint32_t* idx;
+    uint32_t* vary;  // [D]
+    const uint32_t* status;
+    uint32_t n;
+    int dim;
+    int vec;  // vtx and flags 16-byte aligned
+};
+
+template <int D_CT>
+__global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
+    if (*a.status) return;  // uniform
+    const int D = D_CT > 0 ? D_CT : a.dim;
+    const uint32_t* repl = a.vtx + static_cast<size_t>(a.idx[0]) * D;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    if constexpr (D_CT > 0) {
+        uint32_t ref[D_CT], vor[D_CT];
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) {
+            ref[c] = __ldg(repl + c);
+            vor[c] = 0u;
+        }
+        uint64_t done = 0;
+        if constexpr (D_CT == 3) {
+            if (a.vec) {
+                const uint64_t ng = a.n >> 2;
+                const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
+                const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
+                for (uint64_t g = start; g < ng; g += stride) {
+                    const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
+                    const uint32_t f = __ldcs(f4 + g);
+                    const uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if ((f >> (8 * j)) & 255u) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) vor[c] |= k[j][c] ^ ref[c];
+                        }
+                    }
+                }
+                done = ng << 2;
+            }
+        }
+        for (uint64_t i = done + start; i < a.n; i += stride) {
+            if (a.flags[i]) {
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) vor[c] |= __ldg(a.vtx + i * D_CT + c) ^ ref[c];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) {
+            const uint32_t v = __reduce_or_sync(kFull, vor[c]);
+            if ((threadIdx.x & 31u) == 0u && v) atomicOr(a.vary + c, v);
+        }
+    } else {
+        __shared__ uint32_t s_vary[RMX_MAX_DIM];
+        if (threadIdx.x < RMX_MAX_DIM) s_vary[threadIdx.x] = 0u;
+        __syncthreads();
+        for (uint64_t i = start; i < a.n; i += stride) {
+            if (a.flags[i]) {
+                for (int c = 0; c < D; ++c) {
+                    const uint32_t x = __ldg(a.vtx + i * D + c) ^ __ldg(repl + c);
+                    if (x) atomicOr(s_vary + c, x);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < static_cast<unsigned>(D) && s_vary[threadIdx.x]) atomicOr(a.vary + threadIdx.x, s_vary[threadIdx.x]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1b': packed keys + origins, histogram of packed digit 0.
+struct PackArgs {
+    const uint32_t* vtx;
+    const uint8_t* flags;
+    const uint32_t* idx;
+    const uint32_t* plan;
+    uint32_t* buf0;   // keys at word 0, origins at word vals_off
+    size_t vals_off;  // words
+    uint32_t* hist;   // packed histograms [kMaxPackedPasses][256]
+    const uint32_t* status;
+    uint32_t n;
+    int dim;
+    int vec;
+};
+
+template <int D_CT>
+__global__ void __launch_bounds__(kBlock) k_pack(PackArgs a) {
+    const int D = D_CT > 0 ? D_CT : a.dim;
+    const uint32_t* pk = a.plan + pk_base(4 * D);
+    __shared__ uint32_t s_runs[4 * kMaxRuns];
+    __shared__ uint32_t s_h[256];
+    if (*a.status || pk[0] == 0u) return;  // uniform
+    const uint32_t nruns = pk[4];
+    const bool wide = pk[1] == 2u;
+    for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
+    s_h[threadIdx.x] = 0u;
+    __syncthreads();
+
+    const uint32_t r0 = a.idx[0];
+    const uint32_t* repl = a.vtx + static_cast<size_t>(r0) * D;
+    uint64_t* keys64 = reinterpret_cast<uint64_t*>(a.buf0);
+    uint32_t* keys32 = a.buf0;
+    uint32_t* vals = a.buf0 + a.vals_off;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    uint32_t rl = 0u;
+
+    auto put = [&](uint64_t i, uint64_t key) {
+        if (wide) keys64[i] = key;
+        else keys32[i] = static_cast<uint32_t>(key);
+        vals[i] = static_cast<uint32_t>(i);
+        rl_push(rl, static_cast<uint32_t>(key) & 255u, s_h);
+    };
+
+    if constexpr (D_CT > 0) {
+        uint32_t ref[D_CT];
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
+        // the first 8 runs live in registers (typical meshes need 1-2 per component)
+        constexpr int kRegRuns = 8;
+        uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
+#pragma unroll
+        for (int r = 0; r < kRegRuns; ++r) {
+            const bool on = static_cast<uint32_t>(r) < nruns;
+            rc[r] = on ? s_runs[4 * r] : 0u;
+            rs[r] = on ? s_runs[4 * r + 1] : 0u;
+            rm[r] = on ? low_mask(s_runs[4 * r + 2]) : 0u;
+            rd[r] = on ? s_runs[4 * r + 3] : 0u;
+        }
+        auto pack = [&](const uint32_t (&k)[D_CT]) {
+            uint64_t key = 0;
+#pragma unroll
+            for (int r = 0; r < kRegRuns; ++r)
+                key |= static_cast<uint64_t>((pick<D_CT>(k, rc[r]) >> rs[r]) & rm[r]) << rd[r];
+            for (uint32_t r = kRegRuns; r < nruns; ++r) {
+                const uint32_t* ru = s_runs + 4 * r;
+                key |= static_cast<uint64_t>((pick<D_CT>(k, ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
+            }
+            return key;
+        };
+        uint64_t done = 0;
+        if constexpr (D_CT == 3) {
+            if (a.vec) {
+                const uint64_t ng = a.n >> 2;
+                const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
+                const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
+                for (uint64_t g = start; g < ng; g += stride) {
+                    const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
+                    const uint32_t f = __ldcs(f4 + g);
+                    uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (((f >> (8 * j)) & 255u) == 0u) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
+                        }
+                        put(4 * g + j, pack(k[j]));
+                    }
+                }
+                done = ng << 2;
+            }
+        }
+        for (uint64_t i = done + start; i < a.n; i += stride) {
+            uint32_t k[D_CT];
+            const bool used = a.flags[i] != 0;
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) k[c] = used ? __ldg(a.vtx + i * D_CT + c) : ref[c];
+            put(i, pack(k));
+        }
+    } else {
+        for (uint64_t i = start; i < a.n; i += stride) {
+            const uint32_t* row = a.flags[i] ? a.vtx + i * D : repl;
+            uint64_t key = 0;
+            for (uint32_t r = 0; r < nruns; ++r) {
+                const uint32_t* ru = s_runs + 4 * r;
+                key |= static_cast<uint64_t>((__ldg(row + ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
+            }
+            put(i, key);
+        }
+    }
+    if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);
+    __syncthreads();
+    if (s_h[threadIdx.x]) atomicAdd(a.hist + threadIdx.x, s_h[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// K2': one onesweep LSD pass over (packed key, origin) pairs.  Same tile
+// machinery as k_sort_pass (TMA bulk staging of the key and origin ranges,
+// warp match ranking, windowed decoupled look-back, slot-index reorder).
+struct SortPkArgs {
+    uint32_t* buf0;
+    uint32_t* buf1;
+    size_t vals_off;       // words
+    const uint32_t* plan;
+    uint32_t* hist;        // [kMaxPackedPasses][256]
+    uint64_t* desc;        // [ntiles][256]
+    uint32_t* counters;    // [kMaxPackedPasses]
+    const uint32_t* status;
+    uint32_t n;
+    uint32_t ntiles;
+    int dim;
+    int pass;
+};
+
+template <int IPT>
+struct SortPkTraits {
+    static constexpr int kTile = kBlock * IPT;
+    static __host__ __device__ size_t smem_bytes() {
+        // keys sized for u64, origins, slot index, warp tables, digit tables, misc, barrier
+        return static_cast<size_t>(kTile) * (8 + 4 + 2) + (kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16;
+    }
+};
+
+template <int KW, int IPT>
+__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t npass, uint32_t* smem) {
+    using Key = typename PkKey<KW>::T;
+    constexpr int TILE = kBlock * IPT;
+    const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
+    uint32_t* ib = src ? a.buf1 : a.buf0;
+    uint32_t* ob = src ? a.buf0 : a.buf1;
+    const Key* __restrict__ in_k = reinterpret_cast<const Key*>(ib);
+    const uint32_t* __restrict__ in_v = ib + a.vals_off;
+    Key* __restrict__ out_k = reinterpret_cast<Key*>(ob);
+    uint32_t* __restrict__ out_v = ob + a.vals_off;
+    const int shift = 8 * a.pass;
+    const bool count_next = static_cast<uint32_t>(a.pass) + 1u < npass;
+    const int nshift = shift + 8;
+    const uint32_t epoch = static_cast<uint32_t>(a.pass) + 1u;
+    uint32_t* ctr = a.counters + a.pass;
+
+    Key* s_keys = reinterpret_cast<Key*>(smem);
+    uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;  // keys region sized for u64
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_vals + TILE);
+    uint32_t* s_whist = reinterpret_cast<uint32_t*>(s_src + TILE);
+    uint32_t* s_offs = s_whist + kWarps * 256;
+    uint32_t* s_gdst = s_offs + 256;
+    uint32_t* s_hnext = s_gdst + 256;
+    uint32_t* s_warp = s_hnext + 256;
+    uint32_t* s_misc = s_warp + kWarps;
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+    }
+    {
+        uint32_t tot;
+        s_offs[tid] = block_exclusive_scan<kWarps>(a.hist[a.pass * 256 + tid], s_warp, tot);
+        s_hnext[tid] = 0u;
+    }
+    const bool use_match = prefer_match(a.hist[a.pass * 256 + tid]);
+    for (uint32_t it = 0;; ++it) {
+        if (tid == 0) {
+            const uint32_t t = atomicAdd(ctr, 1u);
+            s_misc[0] = t;
+            if (t < a.ntiles) {
+                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
+                const size_t b = static_cast<size_t>(t) * TILE;
+                stage_tile2(s_keys, in_k + b, tn * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + b, tn * 4u, s_bar);
+            }
+        }
+        for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
+        __syncthreads();
+        const uint32_t tile = s_misc[0];
+        if (tile >= a.ntiles) break;
+        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - tile * static_cast<uint32_t>(TILE));
+        mbar_wait(s_bar, it & 1u);
+
+        // ---- ranking: digits (+ next pass's histogram), then stable warp ranks
+        uint32_t* wh = s_whist + warp * 256;
+        uint32_t pk[IPT];
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            uint32_t d = 256u;
+            if (p < tile_n) {
+                const Key key = s_keys[p];
+                d = static_cast<uint32_t>(key >> shift) & 255u;
+                if (count_next) atomicAdd(s_hnext + (static_cast<uint32_t>(key >> nshift) & 255u), 1u);
+            }
+            pk[r] = d;
+        }
+        warp_rank<IPT>(pk, wh, use_match, tile_n < static_cast<uint32_t>(TILE));
+        __syncthreads();
+
+        // ---- per digit: count, publish aggregate, tile-local start
+        const uint32_t d = tid;
+        uint32_t cnt = 0, start;
+        {
+            uint32_t wc[kWarps];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                wc[w] = s_whist[w * 256 + d];
+                cnt += wc[w];
+            }
+            st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d,
+                       pack_desc(epoch, tile == 0 ? kPrefix : kAggregate, cnt));
+            uint32_t tot;
+            start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+            uint32_t run = start;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                s_whist[w * 256 + d] = run;  // slot of this warp's first row with digit d
+                run += wc[w];
+            }
+        }
+        __syncthreads();
+        // ---- reorder (local only) while predecessors finish publishing
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            if (p < tile_n) s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
+        }
+        // ---- look-back: global start of this tile's run of digit d
+        {
+            uint32_t excl = 0;
+            if (tile > 0) {
+                excl = lookback_digit<16>(a.desc, tile, d, epoch);
+                st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d, pack_desc(epoch, kPrefix, excl + cnt));
+            }
+            s_gdst[d] = s_offs[d] + excl - start;
+        }
+        __syncthreads();
+
+        constexpr int U = 4;
+        for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
+            Key k[U];
+            uint32_t v[U], dst[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = q0 + u * kBlock;
+                if (q < tile_n) {
+                    const uint32_t p = s_src[q];
+                    k[u] = s_keys[p];
+                    v[u] = s_vals[p];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = q0 + u * kBlock;
+                if (q < tile_n) dst[u] = s_gdst[static_cast<uint32_t>(k[u] >> shift) & 255u] + q;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t q = q0 + u * kBlock;
+                if (q < tile_n) {
+                    out_k[dst[u]] = k[u];
+                    out_v[dst[u]] = v[u];
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (count_next && s_hnext[tid]) atomicAdd(a.hist + (a.pass + 1) * 256 + tid, s_hnext[tid]);
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kBlock, 3) k_sort_pk(SortPkArgs a) {
+    if (*a.status) return;
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    if (pk[0] == 0u || static_cast<uint32_t>(a.pass) >= pk[3]) return;
+    extern __shared__ __align__(128) uint32_t smem[];
+    if (pk[1] == 2u) sort_pk_body<2, IPT>(a, pk[3], smem);
+    else sort_pk_body<1, IPT>(a, pk[3], smem);
+}
+
+// ---------------------------------------------------------------------------
+// K3' as reduce-then-scan (no look-back chain):
+//   k_head_count_pk  heads per tile (reads keys only)
+//   k_tile_scan      exclusive scan of the per-tile counts, total -> new_count
+//   k_unique_pk      one tile per CTA: new index per slot, unique rows unpacked
+//                    to D words, bucketed (org, new_idx) pairs (see rmx_unique.cuh)
+struct HeadCountArgs {
+    uint32_t* buf0;
+    uint32_t* buf1;
+    const uint32_t* plan;
+    uint32_t* counts;  // [ntiles]
+    const uint32_t* status;
+    uint32_t n;
+    uint32_t ntiles;
+    uint32_t tile;     // rows per tile
+    int dim;
+};
+
+template <int KW>
+__device__ __forceinline__ void head_count_body(const HeadCountArgs& a) {
+    using Key = typename PkKey<KW>::T;
+    const Key* __restrict__ keys = reinterpret_cast<const Key*>(a.plan[0] ? a.buf1 : a.buf0);
+    __shared__ uint32_t s_red[kWarps];
+    for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const uint64_t base = static_cast<uint64_t>(t) * a.tile;
+        const uint64_t end = min(base + a.tile, static_cast<uint64_t>(a.n));
+        uint32_t cnt = 0;
+#pragma unroll 4
+        for (uint64_t g = base + threadIdx.x; g < end; g += kBlock)
+            cnt += (g == 0 || __ldg(keys + g) != __ldg(keys + g - 1)) ? 1u : 0u;
+        cnt = warp_sum(cnt);
+        if ((threadIdx.x & 31u) == 0u) s_red[threadIdx.x >> 5] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) tot += s_red[w];
+            a.counts[t] = tot;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
+    if (*a.status) return;
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    if (pk[0] == 0u) return;
+    if (pk[1] == 2u) head_count_body<2>(a);
+    else head_count_body<1>(a);
+}
+
+// Exclusive scan of per-tile counts in place (one CTA of 1024 threads);
+// the total is the output vertex count.
+__global__ void __launch_bounds__(1024) k_tile_scan(uint32_t* counts, uint32_t ntiles, const uint32_t* plan, int dim,
+                                                    unsigned long long* total_out, const uint32_t* status) {
+    if (*status || plan[pk_base(4 * dim)] == 0u) return;
+    __shared__ uint32_t s_warp[32];
+    const uint32_t per = (ntiles + 1023u) / 1024u;
+    const uint32_t lo = min(ntiles, threadIdx.x * per), hi = min(ntiles, lo + per);
+    uint32_t sum = 0;
+    for (uint32_t i = lo; i < hi; ++i) sum += counts[i];
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<32>(sum, s_warp, tot);
+    for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t c = counts[i];
+        counts[i] = run;
+        run += c;
+    }
+    if (threadIdx.x == 0) *total_out = tot;
+}
+
+struct UniquePkArgs {
+    uint32_t* buf0;
+    uint32_t* buf1;
+    size_t vals_off;
+    const uint32_t* plan;
+    const uint32_t* vtx;    // replacement key source (vtx[idx[0]])
+    const uint32_t* idx;
+    const uint32_t* vary;
+    const uint32_t* prefix; // [ntiles] exclusive head counts
+    uint32_t* fill;         // [256]
+    const uint32_t* status;
+    uint32_t* out_vtx;
+    uint32_t* sc_org;
+    uint8_t* sc_nodup;
+    uint32_t* sc_new;
+    uint32_t* sc_perm;
+    uint32_t n;
+    uint32_t ntiles;
+    int dim;
+    int bucket_shift;
+};
+
+template <int IPT>
+struct UniquePkTraits {
+    static constexpr int kTile = kBlock * IPT;
+    static __host__ __device__ size_t smem_bytes() {
+        return static_cast<size_t>(kTile) * (8 + 4 + 8) +
+               (4 * kMaxRuns + 3 * RMX_MAX_DIM + 3 * 256 + 2 * kWarps + 8 + 4) * 4 + 16;
+    }
+};
+
+template <int KW, int IPT>
+__device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* smem) {
+    using Key = typename PkKey<KW>::T;
+    constexpr int TILE = kBlock * IPT;
+    const int D = a.dim;
+    const uint32_t* pk = a.plan + pk_base(4 * D);
+    const uint32_t fin = a.plan[0];
+    const uint32_t* fb = fin ? a.buf1 : a.buf0;
+    const Key* __restrict__ keys = reinterpret_cast<const Key*>(fb);
+    const uint32_t* __restrict__ vals = fb + a.vals_off;
+    uint2* __restrict__ pairs = reinterpret_cast<uint2*>(fin ? a.buf0 : a.buf1);
+
+    Key* s_keys = reinterpret_cast<Key*>(smem);
+    uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;
+    uint2* s_pairs = reinterpret_cast<uint2*>(s_vals + TILE);
+    uint32_t* s_runs = reinterpret_cast<uint32_t*>(s_pairs + TILE);
+    uint32_t* s_const = s_runs + 4 * kMaxRuns;   // replacement bits outside the varying mask
+    uint32_t* s_rbeg = s_const + RMX_MAX_DIM;    // run range of each component
+    uint32_t* s_rend = s_rbeg + RMX_MAX_DIM;
+    uint32_t* s_bcnt = s_rend + RMX_MAX_DIM;
+    uint32_t* s_bcur = s_bcnt + 256;
+    uint32_t* s_bglob = s_bcur + 256;
+    uint32_t* s_warp = s_bglob + 256;
+    uint32_t* s_misc = s_warp + 2 * kWarps;
+    Key* s_prev = reinterpret_cast<Key*>(s_misc + 8);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 10);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const int bs = a.bucket_shift;
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+    }
+    const uint32_t nruns = pk[4];
+    for (uint32_t i = tid; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
+    if (tid < static_cast<uint32_t>(D)) {
+        s_const[tid] = a.vtx[static_cast<size_t>(a.idx[0]) * D + tid] & ~a.vary[tid];
+        uint32_t b = nruns, e = 0;
+        for (uint32_t r = 0; r < nruns; ++r)
+            if (pk[8 + 4 * r] == tid) {
+                b = min(b, r);
+                e = r + 1;
+            }
+        s_rbeg[tid] = b < e ? b : 0u;
+        s_rend[tid] = e;
+    }
+    // static tile striding: no cross-tile dependency remains (prefixes come from k_tile_scan)
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
+    const uint32_t base = tile * static_cast<uint32_t>(TILE);
+    const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
+    if (tid == 0) {
+        stage_tile2(s_keys, keys + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, vals + base, tile_n * 4u,
+                    s_bar);
+        if (tile > 0) *s_prev = keys[base - 1];
+    }
+    s_bcnt[tid] = 0u;
+    __syncthreads();
+    mbar_wait(s_bar, it & 1u);
+
+    // ---- phase 1: head flags (warp-striped rows), per-warp totals, bucket counts
+    uint32_t bal[IPT];
+    uint32_t wtotal = 0;
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        bool head = false;
+        if (p < tile_n) {
+            head = (base + p == 0u) || s_keys[p] != (p ? s_keys[p - 1] : *s_prev);
+            atomicAdd(s_bcnt + (s_vals[p] >> bs), 1u);
+        }
+        bal[r] = __ballot_sync(kFull, head);
+        wtotal += __popc(bal[r]);
+    }
+    if (lane == 0) s_warp[warp] = wtotal;
+    __syncthreads();
+    uint32_t wexcl = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) wexcl += (static_cast<uint32_t>(w) < warp) ? s_warp[w] : 0u;
+    {
+        const uint32_t cnt = s_bcnt[tid];
+        uint32_t tot;
+        const uint32_t start = block_exclusive_scan<kWarps>(cnt, s_warp + kWarps, tot);
+        s_bcur[tid] = start;
+        if (cnt) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, cnt) - start;
+    }
+    __syncthreads();
+
+    // ---- phase 2: new index per slot, bucketed pairs, unique rows out
+    uint32_t running = a.prefix[tile] + wexcl;
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        if (p < tile_n) {
+            const uint32_t nidx = running + __popc(bal[r] & lanemask_le()) - 1u;
+            const uint32_t org = s_vals[p];
+            s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
+            const bool head = (bal[r] >> lane) & 1u;
+            if (head) {
+                const uint64_t key = static_cast<uint64_t>(s_keys[p]);
+                uint32_t* dst = a.out_vtx + static_cast<size_t>(nidx) * D;
+                for (int c = 0; c < D; ++c) {
+                    uint32_t w = s_const[c];
+                    for (uint32_t q = s_rbeg[c]; q < s_rend[c]; ++q) {
+                        const uint32_t* ru = s_runs + 4 * q;
+                        w |= (static_cast<uint32_t>(key >> ru[3]) & low_mask(ru[2])) << ru[1];
+                    }
+                    dst[c] = w;
+                }
+            }
+            if (a.sc_org) a.sc_org[base + p] = org;
+            if (a.sc_nodup) a.sc_nodup[base + p] = head ? 1 : 0;
+            if (a.sc_new) a.sc_new[base + p] = nidx;
+            if (a.sc_perm) a.sc_perm[org] = base + p;
+        }
+        running += __popc(bal[r]);
+    }
+    __syncthreads();
+    // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
+    for (uint32_t q = tid; q < tile_n; q += kBlock) {
+        const uint2 pr = s_pairs[q];
+        pairs[s_bglob[pr.x >> bs] + q] = pr;
+    }
+    __syncthreads();
+    }
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(kBlock) k_unique_pk(UniquePkArgs a) {
+    if (*a.status) return;
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    if (pk[0] == 0u) return;
+    extern __shared__ __align__(128) uint32_t smem[];
+    if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
+    else unique_pk_body<1, IPT>(a, smem);
+}
+
+}  // namespace rmx

@@ -1,0 +1,261 @@
+// rmx_prep.cuh -- K1 mark, K1b row build, plan, first-pass histogram (AoS row path).
+#pragma once
+
+#include "rmx_base.cuh"
+
+namespace rmx {
+
+// ---------------------------------------------------------------------------
+// K1: mark used vertices; any index >= n_vtx sets the status bit.
+struct MarkArgs {
+    const uint32_t* idx;
+    uint64_t n_idx;
+    uint64_t n_vtx;
+    uint8_t* flags;
+    uint32_t* status;
+    int vec;  // idx 16-byte aligned
+};
+
+__global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    bool bad = false;
+    uint64_t done = 0;
+    if (a.vec) {
+        const uint64_t n4 = a.n_idx >> 2;
+        const uint4* i4 = reinterpret_cast<const uint4*>(a.idx);
+        for (uint64_t i = gtid; i < n4; i += stride) {
+            const uint4 v = __ldcs(i4 + i);
+            const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (x[k] < a.n_vtx) a.flags[x[k]] = 1;
+                else bad = true;
+            }
+        }
+        done = n4 << 2;
+    }
+    for (uint64_t i = done + gtid; i < a.n_idx; i += stride) {
+        const uint32_t x = __ldcs(a.idx + i);
+        if (x < a.n_vtx) a.flags[x] = 1;
+        else bad = true;
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31u) == 0u) atomicOr(a.status, RMX_STATUS_INDEX_OUT_OF_RANGE);
+}
+
+// ---------------------------------------------------------------------------
+// K1b (AoS mode): cleaned (key words, origin) rows and the digit histograms
+// of component D-1 (passes 0..3: the first executed pass is almost always
+// among them).
+struct BuildArgs {
+    const uint32_t* vtx;
+    const uint8_t* flags;
+    const uint32_t* idx;  // idx[0] is the replacement vertex (pipeline.py:148)
+    uint32_t* rows;
+    uint32_t* hist;       // [4D][256]; this kernel fills passes 0..3
+    const uint32_t* plan;
+    const uint32_t* status;
+    uint32_t n;
+    int dim;
+    int vec;              // vtx 16-byte aligned (4-row vector groups for D == 3)
+};
+
+// Run-length privatised histogram update: consecutive equal digits seen by a
+// thread are added with one shared atomic (low-entropy mesh coordinates have
+// long runs of identical bytes, which would otherwise serialise on one bank).
+__device__ __forceinline__ void rl_push(uint32_t& st, uint32_t d, uint32_t* bins) {
+    if ((st >> 8) != 0u && (st & 255u) == d) {
+        st += 256u;
+    } else {
+        if ((st >> 8) != 0u) atomicAdd(bins + (st & 255u), st >> 8);
+        st = 256u | d;
+    }
+}
+
+template <int D_CT>
+__global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
+    const int D = D_CT > 0 ? D_CT : a.dim;
+    const int W = D + 1;
+    __shared__ uint32_t s_hist[4 * 256];
+    for (int i = threadIdx.x; i < 4 * 256; i += kBlock) s_hist[i] = 0u;
+    __syncthreads();
+    if (*a.status || a.plan[pk_base(4 * D)] != 0u) return;  // uniform; packed mode builds no rows
+
+    const uint32_t r0 = a.idx[0];
+    const uint32_t* repl = a.vtx + static_cast<size_t>(r0) * D;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    uint32_t rl[4] = {0u, 0u, 0u, 0u};
+
+    if constexpr (D_CT > 0) {
+        uint32_t ref[D_CT];
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
+        auto emit = [&](uint64_t i, uint32_t (&k)[D_CT]) {
+            const uint32_t last = k[D_CT - 1];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) rl_push(rl[b], (last >> (8 * b)) & 255u, s_hist + b * 256);
+            if constexpr (D_CT == 3) {
+                reinterpret_cast<uint4*>(a.rows)[i] = make_uint4(k[0], k[1], k[2], static_cast<uint32_t>(i));
+            } else {
+                uint32_t* dst = a.rows + i * (D_CT + 1);
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) dst[c] = k[c];
+                dst[D_CT] = static_cast<uint32_t>(i);
+            }
+        };
+        uint64_t done = 0;
+        if constexpr (D_CT == 3) {
+            if (a.vec) {  // 4 rows = 3 x 16 B of vertex words + one 32-bit flag word
+                const uint64_t ng = a.n >> 2;
+                const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
+                const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
+                for (uint64_t g = start; g < ng; g += stride) {
+                    const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
+                    const uint32_t f = __ldcs(f4 + g);
+                    uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (((f >> (8 * j)) & 255u) == 0u) {
+#pragma unroll
+                            for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
+                        }
+                        emit(4 * g + j, k[j]);
+                    }
+                }
+                done = ng << 2;
+            }
+        }
+        for (uint64_t i = done + start; i < a.n; i += stride) {
+            const bool used = a.flags[i] != 0;
+            uint32_t k[D_CT];
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
+            if (!used) {
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) k[c] = ref[c];
+            }
+            emit(i, k);
+        }
+    } else {
+        for (uint64_t i = start; i < a.n; i += stride) {
+            const bool used = a.flags[i] != 0;
+            const uint32_t* srow = used ? a.vtx + i * D : repl;
+            uint32_t* dst = a.rows + i * W;
+            for (int c = 0; c < D; ++c) {
+                const uint32_t k = __ldg(srow + c);
+                dst[c] = k;
+                if (c == D - 1)
+                    for (int b = 0; b < 4; ++b) rl_push(rl[b], (k >> (8 * b)) & 255u, s_hist + b * 256);
+            }
+            dst[D] = static_cast<uint32_t>(i);
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+        if ((rl[b] >> 8) != 0u) atomicAdd(s_hist + b * 256 + (rl[b] & 255u), rl[b] >> 8);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4 * 256; i += kBlock)
+        if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
+}
+
+// ---------------------------------------------------------------------------
+// plan (one thread): from the per-component varying-bit masks decide between
+//  * packed mode -- at most 64 varying bits in at most kMaxRuns runs: the
+//    key is compacted to a u32/u64 and sorted in ceil(B/8) passes; and
+//  * AoS mode -- a byte pass executes iff its digit is not constant over all
+//    keys; passes chain to the next executed one, buffers ping-pong.
+__global__ void k_plan(const uint32_t* vary, uint32_t* plan, int D, const uint32_t* status) {
+    if (*status || threadIdx.x != 0) return;
+    const int P = 4 * D;
+    uint32_t* pk = plan + pk_base(P);
+    uint32_t bits = 0, runs = 0;
+    bool fits = true;
+    for (int c = D - 1; c >= 0 && fits; --c) {
+        uint32_t m = vary[c];
+        while (m) {
+            const uint32_t lo = __ffs(m) - 1u;
+            const uint32_t len = __ffs(~(m >> lo)) ? __ffs(~(m >> lo)) - 1u : 32u - lo;
+            if (runs == static_cast<uint32_t>(kMaxRuns) || bits + len > 64u) {
+                fits = false;
+                break;
+            }
+            pk[8 + 4 * runs + 0] = static_cast<uint32_t>(c);
+            pk[8 + 4 * runs + 1] = lo;
+            pk[8 + 4 * runs + 2] = len;
+            pk[8 + 4 * runs + 3] = bits;
+            ++runs;
+            bits += len;
+            m = len >= 32u ? 0u : (m & ~(((1u << len) - 1u) << lo));
+        }
+    }
+    if (fits) {
+        const uint32_t npass = (bits + 7u) / 8u;
+        pk[0] = 1u;
+        pk[1] = bits > 32u ? 2u : 1u;
+        pk[2] = bits;
+        pk[3] = npass;
+        pk[4] = runs;
+        for (int p = 0; p < P; ++p) {
+            plan[4 + p] = 0u;
+            plan[4 + P + p] = 0u;
+            plan[4 + 2 * P + p] = static_cast<uint32_t>(P);
+        }
+        plan[0] = npass & 1u;  // packed buffers ping-pong starting from buffer 0
+        plan[1] = npass;
+        plan[2] = 0u;
+        plan[3] = 0u;
+        return;
+    }
+    pk[0] = 0u;
+    uint32_t cur = 0, executed = 0, first = static_cast<uint32_t>(P), prev = static_cast<uint32_t>(P);
+    for (int p = 0; p < P; ++p) {
+        const int comp = D - 1 - (p >> 2);
+        const bool ex = ((vary[comp] >> (8 * (p & 3))) & 255u) != 0u;
+        plan[4 + p] = ex ? 1u : 0u;
+        plan[4 + P + p] = cur;
+        plan[4 + 2 * P + p] = static_cast<uint32_t>(P);
+        if (ex) {
+            if (first == static_cast<uint32_t>(P)) first = p;
+            if (prev != static_cast<uint32_t>(P)) plan[4 + 2 * P + prev] = p;
+            prev = p;
+            cur ^= 1u;
+            ++executed;
+        }
+    }
+    plan[0] = cur;
+    plan[1] = executed;
+    plan[2] = first;
+    plan[3] = (first < static_cast<uint32_t>(P) && first >= 4u) ? 1u : 0u;  // histogram not made by K1b
+}
+
+// Histogram of the first executed pass when it lies outside component D-1
+// (only then; exits immediately otherwise).
+struct HistArgs {
+    const uint32_t* rows;
+    uint32_t* hist;
+    const uint32_t* plan;
+    const uint32_t* status;
+    uint32_t n;
+    int dim;
+};
+
+__global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
+    if (*a.status || a.plan[3] == 0u || a.plan[pk_base(4 * a.dim)] != 0u) return;
+    __shared__ uint32_t s_h[256];
+    s_h[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint32_t p = a.plan[2];
+    const int comp = a.dim - 1 - static_cast<int>(p >> 2);
+    const int shift = 8 * static_cast<int>(p & 3u);
+    const int W = a.dim + 1;
+    uint32_t rl = 0u;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < a.n;
+         i += static_cast<uint64_t>(gridDim.x) * kBlock)
+        rl_push(rl, (__ldcs(a.rows + i * W + comp) >> shift) & 255u, s_h);
+    if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);
+    __syncthreads();
+    if (s_h[threadIdx.x]) atomicAdd(a.hist + p * 256 + threadIdx.x, s_h[threadIdx.x]);
+}
+
+}  // namespace rmx

@@ -1,0 +1,211 @@
+// rmx_sort.cuh -- K2 onesweep LSD pass over AoS (key words, origin) rows.
+#pragma once
+
+#include "rmx_base.cuh"
+
+namespace rmx {
+
+// ---------------------------------------------------------------------------
+// K2: one onesweep LSD pass.  Persistent CTAs take tile ids from an atomic
+// counter (forward progress for the look-back).  Tile data arrives by TMA
+// bulk copy.  PF = 1 double-buffers: the NEXT tile id is taken only after the
+// current tile has published its inclusive prefix (taking it earlier would
+// hold back that tile's aggregate and convoy the look-back of later tiles),
+// and its copy overlaps the reorder + write-out of the current tile.
+// REG = rows held in registers and reordered in place; otherwise a per-slot
+// source index (u16) drives the write-out straight from the staged tile.
+// Each pass also counts the digit of the next executed pass (>= 4), so the
+// global histogram of that pass is complete when it starts.
+struct SortArgs {
+    uint32_t* rows0;
+    uint32_t* rows1;
+    const uint32_t* plan;
+    uint32_t* hist;      // [P][256]
+    uint64_t* desc;      // [ntiles][256] look-back descriptors (shared by all passes, epoch-tagged)
+    uint32_t* counters;  // [P] tile-id counters
+    const uint32_t* status;
+    uint32_t n;
+    uint32_t ntiles;
+    int dim;
+    int pass;
+};
+
+template <int W_CT, int IPT>
+struct SortTraits {
+    static constexpr int kTile = kBlock * IPT;
+    static __host__ __device__ size_t smem_bytes(int W) {
+        return static_cast<size_t>(kTile) * W * 4 + static_cast<size_t>(kTile) * 2 +
+               (kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16;
+    }
+};
+
+template <int W_CT>
+__device__ __forceinline__ uint32_t pick_word(const uint4& v, int comp) {
+    return comp == 0 ? v.x : (comp == 1 ? v.y : v.z);
+}
+
+template <int W_CT, int IPT>
+__global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
+    using T = SortTraits<W_CT, IPT>;
+    constexpr int TILE = T::kTile;
+    const int W = W_CT > 0 ? W_CT : a.dim + 1;
+    const int P = 4 * a.dim;
+    if (*a.status) return;
+    const uint32_t* plan = a.plan;
+    if (plan[4 + a.pass] == 0u) return;  // constant digit (or packed mode): nothing moves
+    const uint32_t src = plan[4 + P + a.pass];
+    const uint32_t* __restrict__ in = src ? a.rows1 : a.rows0;
+    uint32_t* __restrict__ out = src ? a.rows0 : a.rows1;
+    const int comp = a.dim - 1 - (a.pass >> 2);
+    const int shift = 8 * (a.pass & 3);
+    const uint32_t epoch = static_cast<uint32_t>(a.pass) + 1u;
+    const int nxt = static_cast<int>(plan[4 + 2 * P + a.pass]);
+    // passes 0..3 are counted by K1b; later ones by the pass before them
+    const bool count_next = nxt < P && nxt >= 4;
+    const int ncomp = count_next ? a.dim - 1 - (nxt >> 2) : 0;
+    const int nshift = 8 * (nxt & 3);
+    uint32_t* ctr = a.counters + a.pass;
+
+    extern __shared__ __align__(128) uint32_t smem[];
+    const size_t tw = static_cast<size_t>(TILE) * W;
+    uint32_t* s_rows = smem;                          // [TILE * W]
+    uint32_t* s_whist = smem + tw;                    // [warp][256]
+    uint32_t* s_offs = s_whist + kWarps * 256;        // global exclusive digit starts
+    uint32_t* s_gdst = s_offs + 256;                  // global row of tile slot 0, per digit
+    uint32_t* s_hnext = s_gdst + 256;                 // histogram of the next executed pass
+    uint32_t* s_warp = s_hnext + 256;
+    uint32_t* s_misc = s_warp + kWarps;
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
+    uint16_t* s_src = reinterpret_cast<uint16_t*>(s_bar + 2);  // slot -> row of the staged tile
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+    }
+    const uint32_t h = a.hist[a.pass * 256 + tid];
+    {
+        uint32_t tot;
+        s_offs[tid] = block_exclusive_scan<kWarps>(h, s_warp, tot);
+        s_hnext[tid] = 0u;
+    }
+    const bool use_match = prefer_match(h);
+    for (uint32_t it = 0;; ++it) {
+        if (tid == 0) {
+            const uint32_t t = atomicAdd(ctr, 1u);
+            s_misc[0] = t;
+            if (t < a.ntiles) {
+                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
+                stage_tile(s_rows, in + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
+            }
+        }
+        for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
+        __syncthreads();
+        const uint32_t tile = s_misc[0];
+        if (tile >= a.ntiles) break;
+        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - tile * static_cast<uint32_t>(TILE));
+        mbar_wait(s_bar, it & 1u);
+
+        // ---- digits (+ next pass's histogram), stable warp ranks
+        uint32_t pk[IPT];
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            uint32_t d = 256u;
+            if (p < tile_n) {
+                uint32_t key, nkey = 0;
+                if constexpr (W_CT == 4) {
+                    const uint4 v = reinterpret_cast<const uint4*>(s_rows)[p];
+                    key = pick_word<4>(v, comp);
+                    if (count_next) nkey = pick_word<4>(v, ncomp);
+                } else {
+                    key = s_rows[static_cast<size_t>(p) * W + comp];
+                    if (count_next) nkey = s_rows[static_cast<size_t>(p) * W + ncomp];
+                }
+                d = (key >> shift) & 255u;
+                if (count_next) atomicAdd(s_hnext + ((nkey >> nshift) & 255u), 1u);
+            }
+            pk[r] = d;
+        }
+        warp_rank<IPT>(pk, s_whist + warp * 256, use_match, tile_n < static_cast<uint32_t>(TILE));
+        __syncthreads();
+
+        // ---- per digit: count, publish aggregate, tile-local start
+        const uint32_t d = tid;
+        uint32_t cnt = 0, start;
+        {
+            uint32_t wc[kWarps];
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                wc[w] = s_whist[w * 256 + d];
+                cnt += wc[w];
+            }
+            st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d,
+                       pack_desc(epoch, tile == 0 ? kPrefix : kAggregate, cnt));
+            uint32_t tot;
+            start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+            uint32_t run = start;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                s_whist[w * 256 + d] = run;
+                run += wc[w];
+            }
+        }
+        __syncthreads();
+        // ---- reorder (local) while predecessors finish publishing
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            if (p < tile_n) s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
+        }
+        // ---- look-back: global start of this tile's run of digit d
+        {
+            uint32_t excl = 0;
+            if (tile > 0) {
+                excl = lookback_digit<16>(a.desc, tile, d, epoch);
+                st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d, pack_desc(epoch, kPrefix, excl + cnt));
+            }
+            s_gdst[d] = s_offs[d] + excl - start;  // mod 2^32; + tile slot gives the global row
+        }
+        __syncthreads();
+
+        // ---- coalesced write-out: consecutive slots of one digit are consecutive rows
+        if constexpr (W_CT == 4) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(s_rows);
+            uint4* o4 = reinterpret_cast<uint4*>(out);
+            constexpr int U = 4;
+            for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
+                uint4 v[U];
+                uint32_t dst[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) v[u] = s4[s_src[q]];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) dst[u] = s_gdst[(pick_word<4>(v[u], comp) >> shift) & 255u] + q;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t q = q0 + u * kBlock;
+                    if (q < tile_n) o4[dst[u]] = v[u];
+                }
+            }
+        } else {
+            const uint32_t nw = tile_n * W;
+            for (uint32_t q = tid; q < nw; q += kBlock) {
+                const uint32_t slot = q / W;
+                const uint32_t c = q - slot * W;
+                const size_t p = s_src[slot];
+                const uint32_t dd = (s_rows[p * W + comp] >> shift) & 255u;
+                out[static_cast<size_t>(s_gdst[dd] + slot) * W + c] = s_rows[p * W + c];
+            }
+        }
+        __syncthreads();
+    }
+    if (count_next && s_hnext[tid]) atomicAdd(a.hist + nxt * 256 + tid, s_hnext[tid]);
+}
+
+}  // namespace rmx
