@@ -117,6 +117,10 @@ const char* rmx_stage_name(uint32_t dim, int k);
 int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream);
 int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
+/* Tuning diagnostic: look-back statistics {windows, spins, look-backs, 0} of
+ * the AoS sort passes when built with -DRMX_PHASES (otherwise zeros; returns 0). */
+int rmx_debug_phase_cycles(unsigned long long* out, int n, int reset);
+
 /*
  * Synthetic lattice soups of BASELINE.md section 3 (bench input generator;
  * not part of the reference interface).  kind 0 = triangles (dim 3, arity 3,

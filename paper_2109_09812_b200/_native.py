@@ -15,7 +15,8 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_NAME = "librmx_b200.so"
-LIB_PATH = os.path.join(_HERE, LIB_NAME)
+# RMX_LIB overrides the library file (tuning builds, e.g. the -DRMX_PHASES variant)
+LIB_PATH = os.environ.get("RMX_LIB") or os.path.join(_HERE, LIB_NAME)
 
 RMX_OK, RMX_EINVAL, RMX_ERANGE, RMX_ECUDA, RMX_ENOSPC = 0, 1, 2, 3, 4
 RMX_STATUS_INDEX_OUT_OF_RANGE = 1
@@ -25,7 +26,8 @@ RMX_MAX_DIM = 32
 EXPORTS = (
     "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex",
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name",
-    "rmx_last_executed_passes", "rmx_plan_info", "rmx_lattice_sizes", "rmx_gen_lattice_soup",
+    "rmx_last_executed_passes", "rmx_plan_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
+    "rmx_gen_lattice_soup",
 )
 
 
@@ -59,6 +61,7 @@ _SIGNATURES = {
     "rmx_stage_name": (ctypes.c_char_p, [_u32, _int]),
     "rmx_last_executed_passes": (_int, [_vp, _u64, _u32, _vp]),
     "rmx_plan_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
+    "rmx_debug_phase_cycles": (_int, [ctypes.POINTER(ctypes.c_ulonglong), _int, _int]),
     "rmx_lattice_sizes": (_int, [_int, _u32, _u32, _u32, _u64,
                                  ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "rmx_gen_lattice_soup": (_int, [_int, _u32, _u32, _u32, _u64, _u64, _vp, _vp, _vp]),

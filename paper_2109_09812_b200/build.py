@@ -5,6 +5,7 @@
 """
 from __future__ import annotations
 
+import glob
 import os
 import shutil
 import subprocess
@@ -12,8 +13,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "rmx_capi.cu")]
-DEPENDS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("rmx_common.cuh", "rmx_kernels.cuh")] + [
-    os.path.join(ROOT, "include", "remesh_b200.h")]
+DEPENDS = SOURCES + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu*"))) + [
+    os.path.join(ROOT, "include", "remesh_b200.h"), os.path.abspath(__file__)]
 OUTPUT = os.path.join(HERE, "librmx_b200.so")
 
 NVCC_FLAGS = [
@@ -38,11 +39,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in DEPENDS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), output: str | None = None) -> str:
+    """Compile the library; ``defines`` (e.g. ("RMX_PHASES",)) build a tuning variant into ``output``."""
+    out = output or OUTPUT
+    if not force and not defines and out == OUTPUT and up_to_date():
         return OUTPUT
-    tmp = OUTPUT + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    tmp = out + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -50,10 +53,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")
     if verbose:
         print(res.stderr)
-    os.replace(tmp, OUTPUT)
-    return OUTPUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
     import sys
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--phases" in sys.argv:
+        print(build(defines=("RMX_PHASES",), output=os.path.join(HERE, "librmx_b200_phases.so")))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

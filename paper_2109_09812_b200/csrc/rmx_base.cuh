@@ -6,6 +6,10 @@
 
 namespace rmx {
 
+#ifndef RMX_LB
+#define RMX_LB 16  // look-back window (predecessor tiles read per round trip)
+#endif
+
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 

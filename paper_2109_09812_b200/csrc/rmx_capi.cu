@@ -56,11 +56,31 @@ int uniq_tile(int W) {
     }
 }
 
-// packed-key path tiles
-constexpr int kPkSortIpt = 16;
+// warp multi-split override for tuning (RMX_RANK = match | ballot | atomic)
+int rank_force() {
+    static int v = [] {
+        const char* e = std::getenv("RMX_RANK");
+        if (!e) return -1;
+        if (!std::strcmp(e, "match")) return kRankMatch;
+        if (!std::strcmp(e, "ballot")) return kRankBallot;
+        if (!std::strcmp(e, "atomic")) return kRankAtomic;
+        return -1;
+    }();
+    return v;
+}
+
+// packed-key path tiles (RMX_PK_IPT = 8 | 12 | 16 selects the sort tile, tuning)
 constexpr int kPkUniqIpt = 12;
-constexpr int kPkSortTile = kBlock * kPkSortIpt;
 constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
+int pk_sort_ipt() {
+    static int v = [] {
+        const char* e = std::getenv("RMX_PK_IPT");
+        const int x = e ? std::atoi(e) : 12;
+        return (x == 8 || x == 12 || x == 16) ? x : 12;
+    }();
+    return v;
+}
+int pk_sort_tile() { return kBlock * pk_sort_ipt(); }
 
 struct Layout {
     int D, W, P;
@@ -71,6 +91,7 @@ struct Layout {
     uint32_t ntiles_pk, ntiles3_pk;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
     size_t tile_counts;
+    size_t pk_counts, pk_totals;  // packed passes: [256][ntiles_pk] tile counts / column scans, [256] totals
     size_t total;
 };
 
@@ -81,7 +102,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.P = 4 * L.D;
     L.ntiles = static_cast<uint32_t>((V + sort_tile(L.W) - 1) / sort_tile(L.W));
     L.ntiles3 = static_cast<uint32_t>((V + uniq_tile(L.W) - 1) / uniq_tile(L.W));
-    L.ntiles_pk = static_cast<uint32_t>((V + kPkSortTile - 1) / kPkSortTile);
+    L.ntiles_pk = static_cast<uint32_t>((V + pk_sort_tile() - 1) / pk_sort_tile());
     L.ntiles3_pk = static_cast<uint32_t>((V + kPkUniqTile - 1) / kPkUniqTile);
     L.vals_off = (static_cast<size_t>(V) * (L.D >= 2 ? 2 : 1) + 3) & ~static_cast<size_t>(3);
     size_t off = 0;
@@ -96,6 +117,8 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.rows1 = take(row_bytes);
     L.map = take(static_cast<size_t>(V) * 4);
     L.plan = take(plan_words(L.P) * 4);
+    L.pk_counts = take(static_cast<size_t>(L.ntiles_pk) * 256 * 4);
+    L.pk_totals = take(256 * 4);
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.hist_pk = take(static_cast<size_t>(kMaxPackedPasses) * 256 * 4);
@@ -145,6 +168,8 @@ int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
     grid = static_cast<int>(g < 1 ? 1 : g);
     return RMX_OK;
 }
+
+int grid_for_stream(uint64_t items, int& grid);
 
 // ---- kernel dispatch by compile-time width --------------------------------
 template <int D_CT>
@@ -222,14 +247,35 @@ int dispatch_pack(const PackArgs& a, cudaStream_t s) {
     }
 }
 
-int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
-    const size_t smem = SortPkTraits<kPkSortIpt>::smem_bytes();
-    int grid = 0;
-    int rc = persistent_grid(k_sort_pk<kPkSortIpt>, smem, a.ntiles, grid);
-    if (rc) return rc;
-    k_sort_pk<kPkSortIpt><<<grid, kBlock, smem, s>>>(a);
+template <int IPT>
+int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
+    const size_t smem = SortPkTraits<IPT>::smem_bytes();
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    RMX_CHECK(cudaGetDevice(&dev));
+    if (attr_dev != dev) {
+        RMX_CHECK(cudaFuncSetAttribute(k_pk_downsweep<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+        attr_dev = dev;
+    }
+    k_pk_downsweep<IPT><<<a.ntiles, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
+}
+
+int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
+    int grid = 0;
+    int rc = grid_for_stream(static_cast<uint64_t>(a.ntiles) * kBlock, grid);
+    if (rc) return rc;
+    k_pk_upsweep<<<grid, kBlock, 0, s>>>(a, static_cast<uint32_t>(pk_sort_tile()));
+    RMX_CHECK(cudaGetLastError());
+    k_pk_colscan<<<256, 1024, 0, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    switch (pk_sort_ipt()) {
+        case 8: return launch_downsweep<8>(a, s);
+        case 12: return launch_downsweep<12>(a, s);
+        default: return launch_downsweep<16>(a, s);
+    }
 }
 
 int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
@@ -391,7 +437,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
-        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p};
+        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p,
+                   rank_force()};
         if ((rc = dispatch_pass(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
@@ -403,8 +450,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
-        SortPkArgs a{rows0, rows1, L.vals_off, plan, hist_pk, desc, counters + L.P + 2, d_status,
-                     static_cast<uint32_t>(V), L.ntiles_pk, L.D, p};
+        SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
+                     reinterpret_cast<uint32_t*>(base + L.pk_totals), d_status, static_cast<uint32_t>(V), L.ntiles_pk,
+                     L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
@@ -547,6 +595,23 @@ int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim,
         return -1;
     if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
     return static_cast<int>(v);
+}
+
+int rmx_debug_phase_cycles(unsigned long long* out, int n, int reset) {
+#ifdef RMX_PHASES
+    unsigned long long h[4] = {0};
+    RMX_CHECK(cudaMemcpyFromSymbol(h, g_lb_stats, sizeof(h)));
+    for (int i = 0; i < n && i < 4; ++i) out[i] = h[i];
+    if (reset) {
+        unsigned long long z[4] = {0};
+        RMX_CHECK(cudaMemcpyToSymbol(g_lb_stats, z, sizeof(z)));
+    }
+    return 4;
+#else
+    for (int i = 0; i < n; ++i) out[i] = 0;
+    (void)reset;
+    return 0;
+#endif
 }
 
 int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n_elem_take, uint64_t* n_elements,

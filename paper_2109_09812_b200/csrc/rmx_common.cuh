@@ -155,25 +155,36 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     return before + x - v;
 }
 
-// Ranking strategy per pass, from the digit's global histogram (`h` = this
-// thread's bin; 256-thread block): MATCH.ANY costs ~2 SM-cycles per DISTINCT
-// value in the warp (B200 measurement) and 8 ballots ~29, so match is used
-// when at most 16 bins are populated, the ballot multi-split otherwise.
-__device__ __forceinline__ bool prefer_match(uint32_t h) { return __syncthreads_count(h != 0u) <= 16; }
+// Warp multi-split strategies (per pass, uniform):
+//   kRankMatch  -- MATCH.ANY: ~2 SM-cycles per DISTINCT value in the warp on B200;
+//   kRankBallot -- 8 ballots: ~29 SM-cycles per warp round regardless of entropy;
+//   kRankAtomic -- OR lane bits into a per-warp smem mask per digit, read back.
+// prefer: match when at most 16 digit bins are populated (from the global
+// histogram, `h` = this thread's bin of a 256-thread block), ballot otherwise.
+constexpr int kRankMatch = 0, kRankBallot = 1, kRankAtomic = 2;
+__device__ __forceinline__ int choose_rank(uint32_t h, int forced) {
+    const int populated = __syncthreads_count(h != 0u);
+    if (forced >= 0) return forced;
+    return populated <= 16 ? kRankMatch : kRankBallot;
+}
 
 // Stable warp ranking of IPT rounds of 8-bit digits (pk[r] = digit, 256 for
-// rows past the end of a partial tile).  wh = this warp's 256 digit counters
-// (zeroed).  On return pk[r] = digit << 16 | rank among this warp's earlier
-// rows with the same digit, and wh holds the warp's digit counts.
-// Peer masks of all rounds are formed first (independent instructions), then
+// rows past the end of a partial tile).  wh = this warp's 256 digit counters,
+// wm = its 256 peer masks (kRankAtomic only); both zero on entry, wm zero on
+// exit.  On return pk[r] = digit << 16 | rank among this warp's earlier rows
+// with the same digit, and wh holds the warp's digit counts.  Peer masks of
+// all rounds are formed first where possible (independent instructions);
 // only the short counter read-modify-write chain is serial.
 template <int IPT>
-__device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, bool use_match, bool partial) {
+__device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uint32_t* wm, int mode, bool partial) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t bit = 1u << lane;
+    const uint32_t lt = bit - 1u;
     uint32_t pm[IPT];
-    if (use_match) {
+    if (mode == kRankMatch) {
 #pragma unroll
         for (int r = 0; r < IPT; ++r) pm[r] = __match_any_sync(kFull, pk[r]);
-    } else {
+    } else if (mode == kRankBallot) {
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t d = pk[r];
@@ -189,8 +200,19 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, boo
 #pragma unroll
             for (int r = 0; r < IPT; ++r) pm[r] &= __ballot_sync(kFull, pk[r] < 256u);
         }
+    } else {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t d = pk[r];
+            const bool valid = d < 256u;
+            if (valid) atomicOr(wm + d, bit);
+            __syncwarp();
+            pm[r] = valid ? wm[d] : 0u;
+            __syncwarp();
+            if (valid && (pm[r] & lt) == 0u) wm[d] = 0u;
+            __syncwarp();
+        }
     }
-    const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < IPT; ++r) {
         const uint32_t d = pk[r];
@@ -208,12 +230,22 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, boo
 // array: LB predecessors are read per round trip, and waiting on a
 // not-yet-published descriptor backs off exponentially (spinning threads
 // would otherwise steal issue slots from the CTAs doing real work).
+#ifdef RMX_PHASES
+__device__ unsigned long long g_lb_stats[4];  // windows, spins, look-backs, distance
+#endif
+
 template <int LB>
 __device__ __forceinline__ uint32_t lookback_digit(const uint64_t* desc, uint32_t tile, uint32_t d, uint32_t epoch) {
     uint32_t excl = 0;
     int64_t t = static_cast<int64_t>(tile) - 1;
     uint32_t backoff = 32;
+#ifdef RMX_PHASES
+    uint32_t st_w = 0, st_s = 0;
+#endif
     for (;;) {
+#ifdef RMX_PHASES
+        ++st_w;
+#endif
         uint64_t v[LB];
 #pragma unroll
         for (int j = 0; j < LB; ++j)
@@ -223,6 +255,9 @@ __device__ __forceinline__ uint32_t lookback_digit(const uint64_t* desc, uint32_
         for (int j = 0; j < LB; ++j) {
             if (!done) {
                 while (desc_epoch(v[j]) != epoch || desc_flag(v[j]) == 0u) {
+#ifdef RMX_PHASES
+                    ++st_s;
+#endif
                     __nanosleep(backoff);
                     backoff = min(backoff * 2u, 1024u);
                     v[j] = ld_relaxed(desc + static_cast<size_t>(t - j) * 256 + d);
@@ -231,7 +266,16 @@ __device__ __forceinline__ uint32_t lookback_digit(const uint64_t* desc, uint32_
                 done = desc_flag(v[j]) == kPrefix;
             }
         }
-        if (done) return excl;
+        if (done) {
+#ifdef RMX_PHASES
+            if (d == 0) {
+                atomicAdd(g_lb_stats + 0, st_w);
+                atomicAdd(g_lb_stats + 1, st_s);
+                atomicAdd(g_lb_stats + 2, 1ull);
+            }
+#endif
+            return excl;
+        }
         t -= LB;
     }
 }

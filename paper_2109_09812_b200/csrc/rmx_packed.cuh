@@ -9,7 +9,8 @@
 //   K1a  k_vary       OR over used rows of (key ^ replacement key), per component
 //   K1b' k_pack       cleaned rows -> packed u32/u64 keys + origins (SoA), and the
 //                     histogram of packed digit 0 (overwrite_unused pipeline.py:54-63)
-//   K2'  k_sort_pk    onesweep LSD pass over packed keys (8-bit digits, ceil(B/8) passes)
+//   K2'  k_pk_upsweep + k_pk_colscan + k_pk_downsweep: one LSD pass over packed
+//                     keys as reduce-then-scan (8-bit digits, ceil(B/8) passes)
 //   K3'  k_head_count_pk + k_tile_scan + k_unique_pk: reduce-then-scan of the
 //                     head flags on packed keys, unique rows unpacked back to D
 //                     words, bucketed (org, new_idx) pairs
@@ -235,35 +236,105 @@ __global__ void __launch_bounds__(kBlock) k_pack(PackArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K2': one onesweep LSD pass over (packed key, origin) pairs.  Same tile
-// machinery as k_sort_pass (TMA bulk staging of the key and origin ranges,
-// warp match ranking, windowed decoupled look-back, slot-index reorder).
+// K2': one LSD pass over (packed key, origin) pairs, as reduce-then-scan:
+//   k_pk_upsweep   per-tile digit counts, reading the keys only
+//                  (counts stored digit-major: counts[d][tile])
+//   k_pk_colscan   one CTA per digit: exclusive scan of counts[d][*] in place,
+//                  totals[d]; with the exclusive scan of totals this gives the
+//                  global output row of every (digit, tile) run
+//   k_pk_downsweep one tile per CTA, no cross-tile dependency: TMA bulk
+//                  staging of keys + origins, stable warp multi-split ranking,
+//                  slot-index reorder, coalesced write-out
+// Measured on B200 the single-kernel onesweep variant spent ~20% of every
+// tile in decoupled look-back round trips (L2 latency under full HBM load);
+// the extra key-only read of the upsweep (4-8 B/row) is cheaper.
 struct SortPkArgs {
     uint32_t* buf0;
     uint32_t* buf1;
     size_t vals_off;       // words
     const uint32_t* plan;
-    uint32_t* hist;        // [kMaxPackedPasses][256]
-    uint64_t* desc;        // [ntiles][256]
-    uint32_t* counters;    // [kMaxPackedPasses]
+    uint32_t* counts;      // [256][ntiles] per-tile digit counts -> exclusive column scans
+    uint32_t* totals;      // [256] digit totals of this pass
     const uint32_t* status;
     uint32_t n;
     uint32_t ntiles;
     int dim;
     int pass;
+    int rank_force;        // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
 };
+
+// true when this packed pass runs (packed mode, pass < number of packed passes)
+__device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    return pk[0] != 0u && static_cast<uint32_t>(a.pass) < pk[3];
+}
+
+template <int KW>
+__device__ __forceinline__ void pk_upsweep_body(const SortPkArgs& a, uint32_t tile_rows) {
+    using Key = typename PkKey<KW>::T;
+    const uint32_t* ib = (static_cast<uint32_t>(a.pass) & 1u) ? a.buf1 : a.buf0;
+    const Key* __restrict__ keys = reinterpret_cast<const Key*>(ib);
+    const int shift = 8 * a.pass;
+    __shared__ uint32_t s_h[256];
+    for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        s_h[threadIdx.x] = 0u;
+        __syncthreads();
+        const uint64_t base = static_cast<uint64_t>(t) * tile_rows;
+        const uint64_t end = min(base + tile_rows, static_cast<uint64_t>(a.n));
+#pragma unroll 4
+        for (uint64_t g = base + threadIdx.x; g < end; g += kBlock)
+            atomicAdd(s_h + (static_cast<uint32_t>(__ldcs(keys + g) >> shift) & 255u), 1u);
+        __syncthreads();
+        a.counts[static_cast<size_t>(threadIdx.x) * a.ntiles + t] = s_h[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
+    if (*a.status || !pk_pass_active(a)) return;
+    if (a.plan[pk_base(4 * a.dim) + 1] == 2u) pk_upsweep_body<2>(a, tile_rows);
+    else pk_upsweep_body<1>(a, tile_rows);
+}
+
+// One CTA per digit: exclusive scan of counts[d][0 .. ntiles) in place,
+// totals[d].  Chunks of 4096 values: each thread scans 4 consecutive values
+// (one coalesced 16-byte access), a block scan joins the threads, a running
+// carry joins the chunks.
+__global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a) {
+    if (*a.status || !pk_pass_active(a)) return;
+    __shared__ uint32_t s_warp[32];
+    uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.ntiles;
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < a.ntiles; c0 += 4096u) {
+        const uint32_t i = c0 + 4u * threadIdx.x;
+        uint32_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = (i + k < a.ntiles) ? row[i + k] : 0u;
+        const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+        uint32_t tot;
+        uint32_t run = carry + block_exclusive_scan<32>(sum, s_warp, tot);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i + k < a.ntiles) row[i + k] = run;
+            run += v[k];
+        }
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.totals[blockIdx.x] = carry;
+}
 
 template <int IPT>
 struct SortPkTraits {
     static constexpr int kTile = kBlock * IPT;
     static __host__ __device__ size_t smem_bytes() {
-        // keys sized for u64, origins, slot index, warp tables, digit tables, misc, barrier
-        return static_cast<size_t>(kTile) * (8 + 4 + 2) + (kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16;
+        // keys sized for u64, origins, slot index, warp counters + peer masks, digit tables, misc, barrier
+        return static_cast<size_t>(kTile) * (8 + 4 + 2) + (2 * kWarps * 256 + 256 + kWarps + 8) * 4 + 16;
     }
 };
 
 template <int KW, int IPT>
-__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t npass, uint32_t* smem) {
+__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
     const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
@@ -274,146 +345,110 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t npass
     Key* __restrict__ out_k = reinterpret_cast<Key*>(ob);
     uint32_t* __restrict__ out_v = ob + a.vals_off;
     const int shift = 8 * a.pass;
-    const bool count_next = static_cast<uint32_t>(a.pass) + 1u < npass;
-    const int nshift = shift + 8;
-    const uint32_t epoch = static_cast<uint32_t>(a.pass) + 1u;
-    uint32_t* ctr = a.counters + a.pass;
 
     Key* s_keys = reinterpret_cast<Key*>(smem);
     uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;  // keys region sized for u64
     uint16_t* s_src = reinterpret_cast<uint16_t*>(s_vals + TILE);
     uint32_t* s_whist = reinterpret_cast<uint32_t*>(s_src + TILE);
-    uint32_t* s_offs = s_whist + kWarps * 256;
-    uint32_t* s_gdst = s_offs + 256;
-    uint32_t* s_hnext = s_gdst + 256;
-    uint32_t* s_warp = s_hnext + 256;
+    uint32_t* s_wmask = s_whist + kWarps * 256;
+    uint32_t* s_gdst = s_wmask + kWarps * 256;
+    uint32_t* s_warp = s_gdst + 256;
     uint32_t* s_misc = s_warp + kWarps;
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t tile = blockIdx.x;
+    const uint32_t base = tile * static_cast<uint32_t>(TILE);
+    const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
     if (tid == 0) {
         mbar_init(s_bar, 1);
         fence_mbar_init();
+        stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + base, tile_n * 4u,
+                    s_bar);
     }
+    // global row of this tile's digit-d run = (rows with smaller digits) + (digit-d rows of earlier tiles)
+    const uint32_t tot_d = a.totals[tid];
+    const int rank_mode = choose_rank(tot_d, a.rank_force);
+    uint32_t dummy;
+    const uint32_t run_base = block_exclusive_scan<kWarps>(tot_d, s_warp, dummy) +
+                              a.counts[static_cast<size_t>(tid) * a.ntiles + tile];
+    for (int i = tid; i < kWarps * 256; i += kBlock) {
+        s_whist[i] = 0u;
+        if (rank_mode == kRankAtomic) s_wmask[i] = 0u;
+    }
+    __syncthreads();
+    mbar_wait(s_bar, 0u);
+
+    uint32_t pk[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        pk[r] = p < tile_n ? (static_cast<uint32_t>(s_keys[p] >> shift) & 255u) : 256u;
+    }
+    warp_rank<IPT>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, tile_n < static_cast<uint32_t>(TILE));
+    __syncthreads();
     {
-        uint32_t tot;
-        s_offs[tid] = block_exclusive_scan<kWarps>(a.hist[a.pass * 256 + tid], s_warp, tot);
-        s_hnext[tid] = 0u;
-    }
-    const bool use_match = prefer_match(a.hist[a.pass * 256 + tid]);
-    for (uint32_t it = 0;; ++it) {
-        if (tid == 0) {
-            const uint32_t t = atomicAdd(ctr, 1u);
-            s_misc[0] = t;
-            if (t < a.ntiles) {
-                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
-                const size_t b = static_cast<size_t>(t) * TILE;
-                stage_tile2(s_keys, in_k + b, tn * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + b, tn * 4u, s_bar);
-            }
-        }
-        for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
-        __syncthreads();
-        const uint32_t tile = s_misc[0];
-        if (tile >= a.ntiles) break;
-        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - tile * static_cast<uint32_t>(TILE));
-        mbar_wait(s_bar, it & 1u);
-
-        // ---- ranking: digits (+ next pass's histogram), then stable warp ranks
-        uint32_t* wh = s_whist + warp * 256;
-        uint32_t pk[IPT];
-#pragma unroll
-        for (int r = 0; r < IPT; ++r) {
-            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
-            uint32_t d = 256u;
-            if (p < tile_n) {
-                const Key key = s_keys[p];
-                d = static_cast<uint32_t>(key >> shift) & 255u;
-                if (count_next) atomicAdd(s_hnext + (static_cast<uint32_t>(key >> nshift) & 255u), 1u);
-            }
-            pk[r] = d;
-        }
-        warp_rank<IPT>(pk, wh, use_match, tile_n < static_cast<uint32_t>(TILE));
-        __syncthreads();
-
-        // ---- per digit: count, publish aggregate, tile-local start
         const uint32_t d = tid;
-        uint32_t cnt = 0, start;
-        {
-            uint32_t wc[kWarps];
+        uint32_t wc[kWarps];
+        uint32_t cnt = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                wc[w] = s_whist[w * 256 + d];
-                cnt += wc[w];
-            }
-            st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d,
-                       pack_desc(epoch, tile == 0 ? kPrefix : kAggregate, cnt));
-            uint32_t tot;
-            start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
-            uint32_t run = start;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
-                s_whist[w * 256 + d] = run;  // slot of this warp's first row with digit d
-                run += wc[w];
-            }
+        for (int w = 0; w < kWarps; ++w) {
+            wc[w] = s_whist[w * 256 + d];
+            cnt += wc[w];
         }
-        __syncthreads();
-        // ---- reorder (local only) while predecessors finish publishing
+        uint32_t tot;
+        const uint32_t start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+        uint32_t run = start;
 #pragma unroll
-        for (int r = 0; r < IPT; ++r) {
-            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
-            if (p < tile_n) s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
+        for (int w = 0; w < kWarps; ++w) {
+            s_whist[w * 256 + d] = run;  // slot of this warp's first row with digit d
+            run += wc[w];
         }
-        // ---- look-back: global start of this tile's run of digit d
-        {
-            uint32_t excl = 0;
-            if (tile > 0) {
-                excl = lookback_digit<16>(a.desc, tile, d, epoch);
-                st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d, pack_desc(epoch, kPrefix, excl + cnt));
-            }
-            s_gdst[d] = s_offs[d] + excl - start;
-        }
-        __syncthreads();
-
-        constexpr int U = 4;
-        for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
-            Key k[U];
-            uint32_t v[U], dst[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t q = q0 + u * kBlock;
-                if (q < tile_n) {
-                    const uint32_t p = s_src[q];
-                    k[u] = s_keys[p];
-                    v[u] = s_vals[p];
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t q = q0 + u * kBlock;
-                if (q < tile_n) dst[u] = s_gdst[static_cast<uint32_t>(k[u] >> shift) & 255u] + q;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t q = q0 + u * kBlock;
-                if (q < tile_n) {
-                    out_k[dst[u]] = k[u];
-                    out_v[dst[u]] = v[u];
-                }
-            }
-        }
-        __syncthreads();
+        s_gdst[d] = run_base - start;  // mod 2^32; + tile slot gives the global row
     }
-    if (count_next && s_hnext[tid]) atomicAdd(a.hist + (a.pass + 1) * 256 + tid, s_hnext[tid]);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        if (p < tile_n) s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
+    }
+    __syncthreads();
+
+    constexpr int U = 4;
+    for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
+        Key k[U];
+        uint32_t v[U], dst[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * kBlock;
+            if (q < tile_n) {
+                const uint32_t p = s_src[q];
+                k[u] = s_keys[p];
+                v[u] = s_vals[p];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * kBlock;
+            if (q < tile_n) dst[u] = s_gdst[static_cast<uint32_t>(k[u] >> shift) & 255u] + q;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = q0 + u * kBlock;
+            if (q < tile_n) {
+                out_k[dst[u]] = k[u];
+                out_v[dst[u]] = v[u];
+            }
+        }
+    }
 }
 
 template <int IPT>
-__global__ void __launch_bounds__(kBlock, 3) k_sort_pk(SortPkArgs a) {
-    if (*a.status) return;
-    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    if (pk[0] == 0u || static_cast<uint32_t>(a.pass) >= pk[3]) return;
+__global__ void __launch_bounds__(kBlock, IPT <= 8 ? 4 : 3) k_pk_downsweep(SortPkArgs a) {
+    if (*a.status || !pk_pass_active(a)) return;
     extern __shared__ __align__(128) uint32_t smem[];
-    if (pk[1] == 2u) sort_pk_body<2, IPT>(a, pk[3], smem);
-    else sort_pk_body<1, IPT>(a, pk[3], smem);
+    if (a.plan[pk_base(4 * a.dim) + 1] == 2u) sort_pk_body<2, IPT>(a, smem);
+    else sort_pk_body<1, IPT>(a, smem);
 }
 
 // ---------------------------------------------------------------------------

@@ -28,6 +28,7 @@ struct SortArgs {
     uint32_t ntiles;
     int dim;
     int pass;
+    int rank_force;  // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
 };
 
 template <int W_CT, int IPT>
@@ -35,7 +36,7 @@ struct SortTraits {
     static constexpr int kTile = kBlock * IPT;
     static __host__ __device__ size_t smem_bytes(int W) {
         return static_cast<size_t>(kTile) * W * 4 + static_cast<size_t>(kTile) * 2 +
-               (kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16;
+               (2 * kWarps * 256 + 256 * 3 + kWarps + 8) * 4 + 16;
     }
 };
 
@@ -69,8 +70,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
     extern __shared__ __align__(128) uint32_t smem[];
     const size_t tw = static_cast<size_t>(TILE) * W;
     uint32_t* s_rows = smem;                          // [TILE * W]
-    uint32_t* s_whist = smem + tw;                    // [warp][256]
-    uint32_t* s_offs = s_whist + kWarps * 256;        // global exclusive digit starts
+    uint32_t* s_whist = smem + tw;                    // [warp][256] digit counters
+    uint32_t* s_wmask = s_whist + kWarps * 256;       // [warp][256] peer masks (zero between rounds)
+    uint32_t* s_offs = s_wmask + kWarps * 256;        // global exclusive digit starts
     uint32_t* s_gdst = s_offs + 256;                  // global row of tile slot 0, per digit
     uint32_t* s_hnext = s_gdst + 256;                 // histogram of the next executed pass
     uint32_t* s_warp = s_hnext + 256;
@@ -88,8 +90,9 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
         uint32_t tot;
         s_offs[tid] = block_exclusive_scan<kWarps>(h, s_warp, tot);
         s_hnext[tid] = 0u;
+        for (int i = tid; i < kWarps * 256; i += kBlock) s_wmask[i] = 0u;
     }
-    const bool use_match = prefer_match(h);
+    const int rank_mode = choose_rank(a.hist[a.pass * 256 + tid], a.rank_force);
     for (uint32_t it = 0;; ++it) {
         if (tid == 0) {
             const uint32_t t = atomicAdd(ctr, 1u);
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
             }
             pk[r] = d;
         }
-        warp_rank<IPT>(pk, s_whist + warp * 256, use_match, tile_n < static_cast<uint32_t>(TILE));
+        warp_rank<IPT>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, tile_n < static_cast<uint32_t>(TILE));
         __syncthreads();
 
         // ---- per digit: count, publish aggregate, tile-local start
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
         {
             uint32_t excl = 0;
             if (tile > 0) {
-                excl = lookback_digit<16>(a.desc, tile, d, epoch);
+                excl = lookback_digit<RMX_LB>(a.desc, tile, d, epoch);
                 st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d, pack_desc(epoch, kPrefix, excl + cnt));
             }
             s_gdst[d] = s_offs[d] + excl - start;  // mod 2^32; + tile slot gives the global row

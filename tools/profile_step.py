@@ -51,6 +51,9 @@ def main():
         tot += ms
         print(f"{names[k]:>14s} {ms:8.3f} ms")
     print(f"{'total':>14s} {tot:8.3f} ms")
+    ph = (ctypes.c_ulonglong * 4)()
+    if lib.rmx_debug_phase_cycles(ph, 4, 1) and ph[2]:
+        print(f"  look-back (digit 0): {ph[0] / ph[2]:.2f} windows, {ph[1] / ph[2]:.2f} spins per tile")
 
 
 if __name__ == "__main__":
