@@ -210,9 +210,9 @@ def run_b200(args):
     count, status = (int(x) for x in info.cpu())
     expect_u = (cells[0] + 1) * (cells[1] + 1) * ((cells[2] + 1) if kind == "tet" else 1)
     assert status == 0 and count == expect_u, (count, status, expect_u)
-    info = (ctypes.c_uint32 * 4)()
-    _native.check(lib.rmx_plan_info(ws.data_ptr(), V, D, stream.cuda_stream, info))
-    packed, key_words, vbits, executed = (int(x) for x in info)
+    pinfo = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_plan_info(ws.data_ptr(), V, D, stream.cuda_stream, pinfo))
+    packed, key_words, vbits, executed = (int(x) for x in pinfo)
 
     # per-stage CUDA events for every timed step (recorded on the launching stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
@@ -295,7 +295,7 @@ def run_b200(args):
             try:
                 with open(tp) as f:
                     tj = json.load(f)
-                traffic = tj.get(args.config, {}).get("sort_pass_bytes_per_launch")
+                traffic = tj.get(args.config, {}).get("pass_dram_bytes_per_launch")
             except Exception:
                 traffic = None
         line = {
@@ -309,7 +309,8 @@ def run_b200(args):
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": ("k_sort_pk" if packed else "k_sort_pass") + " (one onesweep LSD pass)",
+                         "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
+                                    else "one onesweep LSD pass: k_sort_pass"),
                          "key": (f"packed {vbits} varying bits in {key_words} x u32" if packed
                                  else f"{D} x u32 words"),
                          "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
@@ -320,7 +321,7 @@ def run_b200(args):
             "stage_ms": stage_ms,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": (n_ev - 1) * args.steps,
+            "gpu_launches": lib.rmx_kernel_launches(D) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -108,6 +108,11 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
 int rmx_stage_count(uint32_t dim);
 const char* rmx_stage_name(uint32_t dim, int k);
 
+/* Kernels one rmx_reindex call launches (n_elements > 0).  The plan is made on
+ * the device, so the kernels of the path not taken (AoS rows vs packed keys,
+ * constant digits) are still launched and return at once. */
+int rmx_kernel_launches(uint32_t dim);
+
 /* Sort plan of the last call that used `workspace` (host-side diagnostic; it
  * reads the device plan, so it synchronises `stream`).  Digit passes whose
  * 8-bit digit is constant over all keys are skipped; when at most 64 key bits

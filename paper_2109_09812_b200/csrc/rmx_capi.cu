@@ -545,6 +545,13 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
                         n_events);
 }
 
+int rmx_kernel_launches(uint32_t dim) {
+    // mark, vary, plan, build_rows, first_hist, 4*dim AoS passes, pack,
+    // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
+    // head_count + tile_scan + unique_pk, map_fill, remap
+    return 5 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 3 + 2;
+}
+
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
