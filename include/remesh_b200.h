@@ -127,6 +127,20 @@ int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
 int rmx_debug_phase_cycles(unsigned long long* out, int n, int reset);
 
 /*
+ * Steps of the multi-GPU path (paper_2109_09812_b200/dist.py).
+ * rmx_gather_u32: out[i] = table[idx[i]] -- the remap of remap_elements
+ *   (pipeline.py:116-130) with a caller-supplied table; an index >= n_table
+ *   sets RMX_STATUS_INDEX_OUT_OF_RANGE in *d_status and leaves out[i] unwritten.
+ * rmx_lower_bound_rows: for each query row, the first position in the sorted
+ *   rows[0..n) whose row is >= the query in the reference's bitwise order
+ *   (component 0 most significant, raw unsigned words; primitives.py:23-27).
+ */
+int rmx_gather_u32(const uint32_t* table, uint64_t n_table, const uint32_t* idx, uint64_t n,
+                   uint32_t* out, uint32_t* d_status, void* stream);
+int rmx_lower_bound_rows(const uint32_t* rows, uint64_t n, uint32_t dim, const uint32_t* queries,
+                         uint64_t n_queries, uint64_t* out_positions, void* stream);
+
+/*
  * Synthetic lattice soups of BASELINE.md section 3 (bench input generator;
  * not part of the reference interface).  kind 0 = triangles (dim 3, arity 3,
  * cells nx*ny), kind 1 = Kuhn tetrahedra (dim 4, arity 4, cells nx*ny*nz).
@@ -139,6 +153,13 @@ int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz,
 int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed,
                          uint64_t n_elem_take, uint32_t* out_vtx_bits, uint32_t* out_idx,
                          void* stream);
+/* Elements [e_begin, e_end) of the same soup with the vertex slots they own
+ * (up to the next element), indices relative to the first written slot: one
+ * rank's shard of a soup partitioned across GPUs.  Slot count of a range =
+ * rmx_lattice_sizes(e_end) - rmx_lattice_sizes(e_begin). */
+int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed,
+                               uint64_t e_begin, uint64_t e_end, uint32_t* out_vtx_bits,
+                               uint32_t* out_idx, void* stream);
 
 #ifdef __cplusplus
 }

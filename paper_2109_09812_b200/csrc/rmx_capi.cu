@@ -621,6 +621,31 @@ int rmx_debug_phase_cycles(unsigned long long* out, int n, int reset) {
 #endif
 }
 
+int rmx_gather_u32(const uint32_t* table, uint64_t n_table, const uint32_t* idx, uint64_t n, uint32_t* out,
+                   uint32_t* d_status, void* stream) {
+    g_err[0] = '\0';
+    if (n == 0) return RMX_OK;
+    if (!table || !idx || !out || !d_status) return RMX_EINVAL;
+    int grid = 0;
+    int rc = grid_for_stream(n, grid);
+    if (rc) return rc;
+    k_gather<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(table, n_table, idx, n, out, d_status);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int rmx_lower_bound_rows(const uint32_t* rows, uint64_t n, uint32_t dim, const uint32_t* queries, uint64_t n_queries,
+                         uint64_t* out_positions, void* stream) {
+    g_err[0] = '\0';
+    if (n_queries == 0) return RMX_OK;
+    if (dim < 1 || !queries || !out_positions || (n && !rows)) return RMX_EINVAL;
+    const unsigned grid = static_cast<unsigned>((n_queries + 127) / 128);
+    k_lower_bound<<<grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        rows, n, static_cast<int>(dim), queries, n_queries, reinterpret_cast<unsigned long long*>(out_positions));
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t n_elem_take, uint64_t* n_elements,
                       uint64_t* n_vertices) {
     if (kind != 0 && kind != 1) return RMX_EINVAL;
@@ -633,8 +658,8 @@ int rmx_lattice_sizes(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t 
     return RMX_OK;
 }
 
-int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed, uint64_t n_elem_take,
-                         uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream) {
+int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed, uint64_t e_begin,
+                               uint64_t e_end, uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream) {
     if (kind != 0 && kind != 1) return RMX_EINVAL;
     GenArgs g{};
     g.kind = kind;
@@ -643,9 +668,11 @@ int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64
     g.nz = nz;
     const uint64_t K = kind == 0 ? 3 : 4;
     g.n_elem = kind == 0 ? 2ull * nx * ny : 6ull * nx * ny * nz;
-    g.take = n_elem_take < g.n_elem ? n_elem_take : g.n_elem;
+    g.take = e_end < g.n_elem ? e_end : g.n_elem;
+    g.e0 = e_begin < g.take ? e_begin : g.take;
     g.n_unused = (g.n_elem * K) / 20;
-    if (g.take == 0) return RMX_OK;
+    g.v0 = g.e0 * K + (g.n_elem ? (g.e0 * g.n_unused) / g.n_elem : 0);
+    if (g.take == g.e0) return RMX_OK;
     int bits = 0;
     while ((1ull << bits) < g.n_elem) ++bits;  // bit length of n-1
     if (bits < 2) bits = 2;
@@ -657,11 +684,16 @@ int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64
     g.vtx = out_vtx_bits;
     g.idx = out_idx;
     int grid = 0;
-    int rc = grid_for_stream(g.take, grid);
+    int rc = grid_for_stream(g.take - g.e0, grid);
     if (rc) return rc;
     k_gen_lattice<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(g);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
+}
+
+int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64_t seed, uint64_t n_elem_take,
+                         uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream) {
+    return rmx_gen_lattice_soup_range(kind, nx, ny, nz, seed, 0, n_elem_take, out_vtx_bits, out_idx, stream);
 }
 
 }  // extern "C"

@@ -18,7 +18,9 @@ struct GenArgs {
     int kind;  // 0 tri, 1 tet
     uint32_t nx, ny, nz;
     uint64_t n_elem;  // total lattice elements (permutation domain)
-    uint64_t take;    // elements written
+    uint64_t e0;      // first element written (element range [e0, take))
+    uint64_t v0;      // its first vertex slot; written slots and indices are relative to it
+    uint64_t take;    // end of the element range
     uint64_t n_unused;
     uint32_t half;
     uint64_t mask;
@@ -44,12 +46,12 @@ __global__ void __launch_bounds__(kBlock) k_gen_lattice(GenArgs g) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const int K = g.kind == 0 ? 3 : 4;
     const int D = K;
-    for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; e < g.take; e += stride) {
+    for (uint64_t e = g.e0 + static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; e < g.take; e += stride) {
         uint64_t t = feistel(e, g);
         while (t >= g.n_elem) t = feistel(t, g);
         const uint64_t u0 = (e * g.n_unused) / g.n_elem;
         const uint64_t u1 = ((e + 1) * g.n_unused) / g.n_elem;
-        const uint64_t base = e * K + u0;
+        const uint64_t base = e * K + u0 - g.v0;
         int pts[4][3];
         if (g.kind == 0) {
             const uint64_t q = t >> 1;
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(kBlock) k_gen_lattice(GenArgs g) {
                 row[2] = __float_as_uint(__fmul_rn(static_cast<float>(k), 0.5f));
                 row[3] = __float_as_uint(__fmul_rn(static_cast<float>((3 * i + 5 * j + 7 * k) % 97), 0.125f));
             }
-            g.idx[e * K + s] = static_cast<uint32_t>(base + s);
+            g.idx[(e - g.e0) * K + s] = static_cast<uint32_t>(base + s);
         }
         for (uint64_t o = u0; o < u1; ++o) {
             uint32_t* row = g.vtx + (base + K + (o - u0)) * D;

@@ -32,3 +32,4 @@
 #include "rmx_unique.cuh"
 #include "rmx_packed.cuh"
 #include "rmx_gen.cuh"
+#include "rmx_steps.cuh"

@@ -136,7 +136,7 @@ struct PackArgs {
 };
 
 template <int D_CT>
-__global__ void __launch_bounds__(kBlock) k_pack(PackArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
@@ -168,8 +168,8 @@ __global__ void __launch_bounds__(kBlock) k_pack(PackArgs a) {
         uint32_t ref[D_CT];
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
-        // the first 8 runs live in registers (typical meshes need 1-2 per component)
-        constexpr int kRegRuns = 8;
+        // the first 4 runs live in registers (typical meshes need 1 per component)
+        constexpr int kRegRuns = 4;
         uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
 #pragma unroll
         for (int r = 0; r < kRegRuns; ++r) {

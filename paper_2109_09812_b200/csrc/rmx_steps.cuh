@@ -1,0 +1,46 @@
+// rmx_steps.cuh -- small device steps of the multi-GPU path:
+//   k_gather      out[i] = table[idx[i]]         (the K4 remap with a caller table)
+//   k_lower_bound first row >= query, rows in the reference's bitwise order
+#pragma once
+
+#include "rmx_base.cuh"
+
+namespace rmx {
+
+__global__ void __launch_bounds__(kBlock) k_gather(const uint32_t* table, uint64_t n_table, const uint32_t* idx,
+                                                   uint64_t n, uint32_t* out, uint32_t* status) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    bool bad = false;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < n; i += stride) {
+        const uint32_t j = __ldcs(idx + i);
+        if (j < n_table) out[i] = __ldg(table + j);
+        else bad = true;
+    }
+    if (__any_sync(kFull, bad) && (threadIdx.x & 31u) == 0u) atomicOr(status, RMX_STATUS_INDEX_OUT_OF_RANGE);
+}
+
+// Lexicographic compare of D-word rows, component 0 most significant, raw
+// unsigned words (primitives.py:23-27).
+__device__ __forceinline__ int row_cmp(const uint32_t* a, const uint32_t* b, int D) {
+    for (int c = 0; c < D; ++c) {
+        if (a[c] != b[c]) return a[c] < b[c] ? -1 : 1;
+    }
+    return 0;
+}
+
+// One thread per query: first position in rows[0..n) (sorted) whose row >= query.
+__global__ void k_lower_bound(const uint32_t* rows, uint64_t n, int D, const uint32_t* queries, uint64_t nq,
+                              unsigned long long* out) {
+    const uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint32_t* key = queries + q * D;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (row_cmp(rows + mid * D, key, D) < 0) lo = mid + 1;
+        else hi = mid;
+    }
+    out[q] = lo;
+}
+
+}  // namespace rmx

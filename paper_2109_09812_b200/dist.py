@@ -1,0 +1,286 @@
+"""Multi-GPU re-indexing: one mesh partitioned across the GPUs of one box.
+
+Semantics: the G ranks together hold ONE mesh -- rank r owns a contiguous block
+of vertices and the elements that reference them (local indices) -- exactly
+like ``remeshx.merge`` (ops.py:10-35) concatenates meshes: the result equals
+``reindex(merge([shard_0, ..., shard_{G-1}]))`` bit for bit.  Every rank gets
+its slice of the global (bitwise-sorted) unique vertex array, the slice's
+global offset, the global count, and its elements remapped to global indices.
+
+Algorithm (a sample sort on deduplicated keys):
+
+1. local re-index on each GPU (the full single-GPU CUDA pipeline): duplicates
+   inside a shard disappear before anything crosses NVLink (a soup shrinks ~6x);
+2. regular samples of the local sorted unique keys -> AllGather -> G-1 splitters
+   (key-only splitters are balanced here: after step 1 a key occurs at most
+   once per rank, so no heavy hitter survives);
+3. ``rmx_lower_bound_rows`` partitions each sorted key array into G contiguous
+   ranges -> all-to-all of the keys (counts first, then data);
+4. each rank re-indexes what it received (identity elements): sorted unique
+   keys of its range plus the local rank of every received key.  All copies of a
+   key go to the same rank, so there are no boundary duplicates;
+5. AllGather of the per-rank unique counts -> global offsets;
+6. reverse all-to-all of the global ids, in the order the keys arrived: each
+   sender gets the global id of every local unique key back in its own sorted
+   order, i.e. its old->new map, with no scatter;
+7. ``rmx_gather_u32`` remaps the local elements.
+
+Collectives go through a small ``Comm`` interface: :class:`TorchComm`
+(torch.distributed -- NCCL over NVLink on GPUs, gloo on CPU) or
+:class:`ThreadComm` (G ranks as threads of one process, for tests on one GPU
+or on CPU).  The local steps go through a backend: :class:`CudaBackend` is the
+product; tests may inject a CPU backend.
+"""
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+from .mesh import MeshError
+
+
+# ---------------------------------------------------------------------------
+# collectives
+class Comm:
+    rank: int
+    size: int
+
+    def all_gather_int(self, x: int) -> list[int]:
+        raise NotImplementedError
+
+    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        raise NotImplementedError
+
+    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        raise NotImplementedError
+
+
+class TorchComm(Comm):
+    """torch.distributed collectives (NCCL for CUDA tensors, gloo for CPU tensors)."""
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self.device = device or torch.device("cpu")
+
+    def all_gather_int(self, x: int) -> list[int]:
+        t = torch.tensor([int(x)], dtype=torch.int64, device=self.device)
+        out = [torch.empty_like(t) for _ in range(self.size)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(o.item()) for o in out]
+
+    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        sizes = self.all_gather_int(t.shape[0])
+        cap = max(sizes) if sizes else 0
+        if cap == 0:
+            return t.new_empty((0,) + tuple(t.shape[1:]))
+        pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
+        pad[: t.shape[0]] = t
+        out = [torch.empty_like(pad) for _ in range(self.size)]
+        self.dist.all_gather(out, pad, group=self.group)
+        return torch.cat([o[:n] for o, n in zip(out, sizes)])
+
+    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=self.device)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        recv_counts = [int(x) for x in rc.tolist()]
+        out = t.new_empty((sum(recv_counts),) + tuple(t.shape[1:]))
+        self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=recv_counts,
+                                    input_split_sizes=list(send_counts), group=self.group)
+        return out, recv_counts
+
+
+class ThreadHub:
+    """Shared state of G in-process ranks (see :class:`ThreadComm`)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.slots: list = [None] * size
+        self.barrier = threading.Barrier(size)
+
+
+class ThreadComm(Comm):
+    """G ranks as threads of one process: collectives are hand-offs through a hub.
+
+    Used to run the multi-rank host logic on one GPU (each thread drives the
+    same device) or on CPU; no rank ever waits on another inside a kernel.
+    """
+
+    def __init__(self, hub: ThreadHub, rank: int):
+        self.hub = hub
+        self.rank = rank
+        self.size = hub.size
+
+    def _exchange(self, obj):
+        self.hub.slots[self.rank] = obj
+        self.hub.barrier.wait()
+        out = list(self.hub.slots)
+        self.hub.barrier.wait()
+        return out
+
+    def all_gather_int(self, x: int) -> list[int]:
+        return [int(v) for v in self._exchange(int(x))]
+
+    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+        parts = self._exchange(t)
+        return torch.cat([p.to(t.device) for p in parts])
+
+    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        parts = self._exchange((t, list(send_counts)))
+        chunks, recv_counts = [], []
+        for src, counts in parts:
+            start = sum(counts[: self.rank])
+            n = counts[self.rank]
+            chunks.append(src[start:start + n].to(t.device))
+            recv_counts.append(n)
+        out = torch.cat(chunks) if chunks else t.new_empty((0,) + tuple(t.shape[1:]))
+        return out, recv_counts
+
+
+# ---------------------------------------------------------------------------
+# local steps
+class CudaBackend:
+    """Local steps on this rank's GPU through the C-ABI."""
+
+    def __init__(self, device: torch.device | None = None):
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.lib = _native.lib()
+
+    def reindex(self, vertex_bits: torch.Tensor, elements: torch.Tensor):
+        from .pipeline import reindex_tensors
+        res = reindex_tensors(vertex_bits, elements)
+        return res.vertices, res.elements
+
+    def lower_bound(self, rows: torch.Tensor, queries: torch.Tensor) -> list[int]:
+        q = queries.shape[0]
+        if q == 0:
+            return []
+        out = torch.empty(q, dtype=torch.int64, device=self.device)
+        rows = rows.contiguous()
+        queries = queries.contiguous()
+        _native.check(self.lib.rmx_lower_bound_rows(
+            rows.data_ptr() if rows.numel() else None, rows.shape[0], rows.shape[1], queries.data_ptr(), q,
+            out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+        return [int(x) for x in out.cpu().tolist()]
+
+    def gather(self, table: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        n = idx.numel()
+        out = torch.empty(n, dtype=torch.int32, device=self.device)
+        if n == 0:
+            return out
+        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        _native.check(self.lib.rmx_gather_u32(
+            table.data_ptr() if table.numel() else None, table.numel(), idx.contiguous().data_ptr(), n,
+            out.data_ptr(), status.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+        if int(status.item()):
+            raise MeshError("remap table index out of range (internal)")
+        return out
+
+
+@dataclass
+class DistResult:
+    """This rank's part of the distributed result.
+
+    ``vertices``: (u_r, D) int32 bit view, the slice [offset, offset + u_r) of the
+    global sorted unique vertex array; ``elements``: this rank's elements with
+    GLOBAL new indices; ``total``: the global unique count.
+    """
+
+    vertices: torch.Tensor
+    offset: int
+    total: int
+    elements: torch.Tensor
+
+
+def reindex_distributed(vertex_bits: torch.Tensor, elements: torch.Tensor, comm: Comm, backend=None,
+                        samples_per_rank: int = 1024) -> DistResult:
+    """Re-index the mesh whose rank-r shard is (vertex_bits, elements); see module doc."""
+    backend = backend or CudaBackend(vertex_bits.device)
+    if vertex_bits.dim() != 2 or elements.dim() != 2:
+        raise MeshError("vertex_bits must be (V, D) and elements (E, K)")
+    D = vertex_bits.shape[1]
+    G = comm.size
+    dims = comm.all_gather_int(D)
+    if any(d != D for d in dims):
+        raise MeshError(f"all shards must share dim, got {dims}")
+    # 1. local dedup: sorted unique keys + local old->new indices
+    uniq, local_out = backend.reindex(vertex_bits, elements)
+    u = uniq.shape[0]
+    if G == 1:
+        return DistResult(uniq, 0, u, local_out)
+    # 2. splitters from regular samples
+    s = min(samples_per_rank, u)
+    pos = (torch.arange(s, dtype=torch.int64) * u) // max(s, 1)
+    samples = uniq[pos.to(uniq.device)] if s else uniq[:0]
+    every = comm.all_gather_rows(samples)
+    m_all = every.shape[0]
+    if m_all:
+        ident = torch.arange(m_all, dtype=torch.int32, device=every.device).view(m_all, 1)
+        sorted_samples, _ = backend.reindex(every, ident)
+        m = sorted_samples.shape[0]
+        pick = (torch.arange(1, G, dtype=torch.int64) * m) // G
+        splitters = sorted_samples[pick.to(sorted_samples.device)]
+    else:
+        splitters = uniq.new_empty((0, D))
+    # 3. partition the sorted keys into G contiguous ranges and exchange them
+    if splitters.shape[0]:
+        bounds = [0] + backend.lower_bound(uniq, splitters) + [u]
+    else:
+        bounds = [0] + [u] * (G - 1) + [u]
+    send_counts = [bounds[g + 1] - bounds[g] for g in range(G)]
+    recv_keys, recv_counts = comm.all_to_all(uniq, send_counts)
+    # 4. merge what arrived: sorted unique keys of this range + local rank of each key
+    n_recv = recv_keys.shape[0]
+    if n_recv:
+        ident = torch.arange(n_recv, dtype=torch.int32, device=recv_keys.device).view(n_recv, 1)
+        mine, rank_of = backend.reindex(recv_keys, ident)
+    else:
+        mine, rank_of = recv_keys.new_empty((0, D)), recv_keys.new_empty((0, 1))
+    # 5. global offsets
+    sizes = comm.all_gather_int(mine.shape[0])
+    offset = sum(sizes[: comm.rank])
+    total = sum(sizes)
+    if total >= 1 << 32:
+        raise MeshError(f"global unique count {total} exceeds 32-bit index range")
+    gid = (rank_of.reshape(-1).to(torch.int64) + offset).to(torch.int32)
+    # 6. reverse exchange: global id of every local unique key, in local order
+    new_of_local, _ = comm.all_to_all(gid, recv_counts)
+    # 7. remap this rank's elements
+    out = backend.gather(new_of_local, local_out.reshape(-1)).view(local_out.shape)
+    return DistResult(mine, offset, total, out)
+
+
+def run_threads(shards, backend_factory, samples_per_rank: int = 1024) -> list[DistResult]:
+    """Run reindex_distributed over G in-process ranks (one thread each)."""
+    G = len(shards)
+    hub = ThreadHub(G)
+    results: list = [None] * G
+    errors: list = []
+
+    def body(r):
+        try:
+            v, e = shards[r]
+            results[r] = reindex_distributed(v, e, ThreadComm(hub, r), backend_factory(r), samples_per_rank)
+        except BaseException as exc:  # noqa: BLE001 - surfaced below
+            errors.append(exc)
+            hub.barrier.abort()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
+__all__ = ["Comm", "TorchComm", "ThreadComm", "ThreadHub", "CudaBackend", "DistResult",
+           "reindex_distributed", "run_threads"]

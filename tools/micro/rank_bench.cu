@@ -39,6 +39,32 @@ __global__ void k_rank(uint32_t* out, int iters) {
                         peers &= ((d >> b) & 1) ? bb : ~bb;
                     }
                 }
+            } else if (MODE == 4) {
+                // ballots via redux.sync OR of lane bits
+                peers = 0xffffffffu;
+                const uint32_t lb = 1u << lane;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const uint32_t bb = __reduce_or_sync(0xffffffffu, ((d >> b) & 1) ? lb : 0u);
+                    peers &= ((d >> b) & 1) ? bb : ~bb;
+                }
+            } else if (MODE == 5) {
+                // half ballots, half redux (two different units)
+                peers = 0xffffffffu;
+                const uint32_t lb = 1u << lane;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1);
+                    peers &= ((d >> b) & 1) ? bb : ~bb;
+                }
+#pragma unroll
+                for (int b = 4; b < 8; ++b) {
+                    const uint32_t bb = __reduce_or_sync(0xffffffffu, ((d >> b) & 1) ? lb : 0u);
+                    peers &= ((d >> b) & 1) ? bb : ~bb;
+                }
+            } else if (MODE == 6) {
+                // nibble matches: peers = match(low nibble) & match(high nibble)... (exact: match on d>>4 and d&15)
+                peers = __match_any_sync(0xffffffffu, d & 15u) & __match_any_sync(0xffffffffu, d >> 4);
             } else {
                 // bitonic sort of (d<<5|lane) across the warp, then peers from neighbours
                 uint32_t k = (d << 5) | lane;
@@ -108,6 +134,9 @@ int main() {
     run("uniform+ballot8 256", k_rank<2, 256>);
     run("uniform+ballot8 1", k_rank<2, 1>);
     run("bitonic32 256", k_rank<3, 256>);
+    run("redux8 256", k_rank<4, 256>);
+    run("ballot4+redux4 256", k_rank<5, 256>);
+    run("match nibbles 256", k_rank<6, 256>);
     uint32_t* o; cudaMalloc(&o, 4); cudaMemset(o, 0, 4);
     k_atom_order<<<148, 256>>>(o);
     uint32_t bad; cudaMemcpy(&bad, o, 4, cudaMemcpyDeviceToHost);
