@@ -1,0 +1,86 @@
+"""Composition ops: host-side argument checks (CPU) and GPU parity with the
+reference remeshx.merge / soup_to_mesh / subset golden vectors."""
+import numpy as np
+import pytest
+
+from conftest import load_group
+
+
+def test_merge_argument_errors_cpu():
+    import paper_2109_09812_b200 as rmx
+    with pytest.raises(rmx.MeshError):
+        rmx.merge([])
+    tri = rmx.Mesh(np.zeros((3, 2), np.float32), np.array([(0, 1, 2)], np.uint32))
+    quad = rmx.Mesh(np.zeros((4, 2), np.float32), np.array([(0, 1, 2, 3)], np.uint32))
+    with pytest.raises(rmx.MeshError):
+        rmx.merge([tri, quad])
+    bad = rmx.Mesh(np.zeros((1, 2), np.float32), np.array([(0, 0, 5)], np.uint32))
+    with pytest.raises(rmx.InvalidMeshError):
+        rmx.merge([bad])
+
+
+def test_subset_selector_errors_cpu():
+    import paper_2109_09812_b200 as rmx
+    m = rmx.Mesh(np.zeros((3, 2), np.float32), np.array([(0, 1, 2)] * 4, np.uint32))
+    for keep in ([0, 9], [2, 1], np.array([True, False]), [0.5]):
+        with pytest.raises(rmx.MeshError):
+            rmx.subset(m, keep)
+
+
+def test_soup_errors_cpu():
+    import paper_2109_09812_b200 as rmx
+    with pytest.raises(rmx.MeshError):
+        rmx.soup_to_mesh([[[0, 0], [1, 1], [2, 2]], [[0, 0], [1, 1]]])
+    with pytest.raises(rmx.MeshError):
+        rmx.soup_to_mesh(np.zeros((3, 3), np.float32))
+    e = rmx.soup_to_mesh(np.empty((0, 3, 2), np.float32))
+    assert e.n_vertices == 0 and e.arity == 3 and e.dim == 2
+
+
+def _cases(prefix):
+    g = load_group("ops")
+    return sorted((k, v) for k, v in g.items() if k.startswith(prefix))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,case", _cases("merge"), ids=[c[0] for c in _cases("merge")])
+def test_merge_matches_reference(cuda_ok, name, case):
+    import paper_2109_09812_b200 as rmx
+    parts = [rmx.Mesh(case[f"piece_vtx_{k}"].view(np.float32), case[f"piece_idx_{k}"])
+             for k in range(int(case["n_pieces"]))]
+    out = rmx.merge(parts)
+    assert np.array_equal(out.vertices.view(np.uint32), case["out_vtx"])
+    assert np.array_equal(out.elements, case["out_idx"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,case", _cases("soup"), ids=[c[0] for c in _cases("soup")])
+def test_soup_to_mesh_matches_reference(cuda_ok, name, case):
+    import paper_2109_09812_b200 as rmx
+    out = rmx.soup_to_mesh(case["soup"].view(np.float32))
+    assert np.array_equal(out.vertices.view(np.uint32), case["out_vtx"])
+    assert np.array_equal(out.elements, case["out_idx"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,case", _cases("subset"), ids=[c[0] for c in _cases("subset")])
+def test_subset_matches_reference(cuda_ok, name, case):
+    import paper_2109_09812_b200 as rmx
+    m = rmx.Mesh(case["in_vtx"].view(np.float32), case["in_idx"])
+    keep = case["keep"]
+    out = rmx.subset(m, keep)
+    assert np.array_equal(out.vertices.view(np.uint32), case["out_vtx"])
+    assert np.array_equal(out.elements, case["out_idx"])
+    mask = np.zeros(m.n_elements, bool)
+    mask[keep] = True
+    assert rmx.bitwise_equal(rmx.subset(m, mask), out)
+
+
+@pytest.mark.gpu
+def test_merge_empties_and_single(cuda_ok):
+    import paper_2109_09812_b200 as rmx
+    e = rmx.merge([rmx.Mesh.empty(), rmx.Mesh.empty()])
+    assert e.n_vertices == 0 and e.n_elements == 0
+    c = load_group("worked")["worked"]
+    w = rmx.Mesh(c["in_vtx"].view(np.float32), c["in_idx"])
+    assert rmx.bitwise_equal(rmx.merge([w]), rmx.reindex(w)[0])

@@ -158,10 +158,46 @@ def lattices(cases):
             record(cases, name, v, e)
 
 
+def record_mesh(cases, name, mesh):
+    cases[f"{name}/out_vtx"] = np.asarray(mesh.vertices).view(np.uint32)
+    cases[f"{name}/out_idx"] = np.asarray(mesh.elements)
+
+
+def ops(cases):
+    """remeshx.merge / soup_to_mesh / subset (ops.py:10-87) on seeded inputs."""
+    for seed in range(12):
+        arity = [3, 4][seed % 2]
+        parts = [remeshx.random_mesh(remeshx.RandomMeshSpec(seed=seed * 10 + k, arity=arity,
+                                                            dim=[2, 3][(seed // 2) % 2])) for k in range(1 + seed % 4)]
+        name = f"merge_{seed:02d}"
+        for k, p in enumerate(parts):
+            cases[f"{name}/piece_vtx_{k}"] = p.vertices.view(np.uint32)
+            cases[f"{name}/piece_idx_{k}"] = p.elements
+        cases[f"{name}/n_pieces"] = np.array(len(parts))
+        record_mesh(cases, name, remeshx.merge(parts))
+        soup = remeshx.dereference(parts[0])
+        cases[f"soup_{seed:02d}/soup"] = soup.view(np.uint32)
+        record_mesh(cases, f"soup_{seed:02d}", remeshx.soup_to_mesh(soup))
+        m = parts[-1]
+        keep = [e for e in range(m.n_elements) if (e + seed) % 3]
+        cases[f"subset_{seed:02d}/in_vtx"] = m.vertices.view(np.uint32)
+        cases[f"subset_{seed:02d}/in_idx"] = m.elements
+        cases[f"subset_{seed:02d}/keep"] = np.array(keep, np.int64)
+        record_mesh(cases, f"subset_{seed:02d}", remeshx.subset(m, keep))
+    q = lambda x0, y0: remeshx.Mesh(np.array([(x0, y0), (x0 + 1, y0), (x0 + 1, y0 + 1), (x0, y0 + 1)], np.float32),
+                                    np.array([(0, 1, 2, 3)], np.uint32))
+    parts = [q(0, 0), q(1, 0)]
+    for k, p in enumerate(parts):
+        cases[f"merge_quads/piece_vtx_{k}"] = p.vertices.view(np.uint32)
+        cases[f"merge_quads/piece_idx_{k}"] = p.elements
+    cases["merge_quads/n_pieces"] = np.array(2)
+    record_mesh(cases, "merge_quads", remeshx.merge(parts))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     groups = {"worked": worked, "reftests": reftests, "torture": torture, "random": random_meshes,
-              "grid": grids, "lattice": lattices}
+              "grid": grids, "lattice": lattices, "ops": ops}
     for gname, fn in groups.items():
         cases: dict = {}
         fn(cases)
