@@ -278,14 +278,25 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     }
 }
 
-int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
+template <int D_CT>
+int launch_unique_pk_d(const UniquePkArgs& a, cudaStream_t s) {
     const size_t smem = UniquePkTraits<kPkUniqIpt>::smem_bytes();
     int grid = 0;
-    int rc = persistent_grid(k_unique_pk<kPkUniqIpt>, smem, a.ntiles, grid);
+    int rc = persistent_grid(k_unique_pk<kPkUniqIpt, D_CT>, smem, a.ntiles, grid);
     if (rc) return rc;
-    k_unique_pk<kPkUniqIpt><<<grid, kBlock, smem, s>>>(a);
+    k_unique_pk<kPkUniqIpt, D_CT><<<grid, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
+}
+
+int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
+    switch (a.dim) {
+        case 1: return launch_unique_pk_d<1>(a, s);
+        case 2: return launch_unique_pk_d<2>(a, s);
+        case 3: return launch_unique_pk_d<3>(a, s);
+        case 4: return launch_unique_pk_d<4>(a, s);
+        default: return launch_unique_pk_d<0>(a, s);
+    }
 }
 
 int dispatch_build(const BuildArgs& a, cudaStream_t s) {

@@ -175,7 +175,20 @@ __device__ __forceinline__ int choose_rank(uint32_t h, int forced) {
 // with the same digit, and wh holds the warp's digit counts.  Peer masks of
 // all rounds are formed first where possible (independent instructions);
 // only the short counter read-modify-write chain is serial.
-template <int IPT>
+// peers &= { lanes whose (digit & mask) agrees with mine }
+__device__ __forceinline__ void bit_plane_and(uint32_t& peers, uint32_t d, uint32_t mask) {
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t, bb, m;\n\t"
+        "and.b32 t, %1, %2;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "vote.sync.ballot.b32 bb, p, 0xffffffff;\n\t"
+        "selp.b32 m, 0, 0xffffffff, p;\n\t"
+        "xor.b32 bb, bb, m;\n\t"
+        "and.b32 %0, %0, bb;\n\t}"
+        : "+r"(peers)
+        : "r"(d), "r"(mask));
+}
+
+template <int IPT, bool PARTIAL = true>
 __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uint32_t* wm, int mode, bool partial) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t bit = 1u << lane;
@@ -185,21 +198,18 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uin
 #pragma unroll
         for (int r = 0; r < IPT; ++r) pm[r] = __match_any_sync(kFull, pk[r]);
     } else if (mode == kRankBallot) {
-        // bit-plane masks via redux.sync OR of lane bits: 20.7 SM-cycles per warp
-        // round on B200 versus 28.7 for __ballot_sync
+        // 8 bit planes; per bit one LOP3.P (test), VOTE, SEL and a 3-input LOP3
+        // (peers &= ballot ^ ~mine): written in PTX so ptxas does not re-derive
+        // the predicate or spill it into a register bitmask.
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t d = pk[r];
-            uint32_t miss = 0u;
+            uint32_t peers = kFull;
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const uint32_t on = (d >> b) & 1u;
-                const uint32_t bb = __reduce_or_sync(kFull, on ? bit : 0u);
-                miss |= bb ^ (0u - on);  // lanes whose bit b differs from mine
-            }
-            pm[r] = ~miss;
+            for (int b = 0; b < 8; ++b) bit_plane_and(peers, d, 1u << b);
+            pm[r] = peers;
         }
-        if (partial) {
+        if (PARTIAL && partial) {
 #pragma unroll
             for (int r = 0; r < IPT; ++r) pm[r] &= __ballot_sync(kFull, pk[r] < 256u);
         }
@@ -207,7 +217,7 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uin
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t d = pk[r];
-            const bool valid = d < 256u;
+            const bool valid = !PARTIAL || d < 256u;
             if (valid) atomicOr(wm + d, bit);
             __syncwarp();
             pm[r] = valid ? wm[d] : 0u;
@@ -220,10 +230,10 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uin
     for (int r = 0; r < IPT; ++r) {
         const uint32_t d = pk[r];
         const uint32_t peers = pm[r];
-        const bool valid = d < 256u;
-        const uint32_t before = valid ? wh[d] : 0u;
+        const bool valid = !PARTIAL || d < 256u;
+        const uint32_t before = valid ? wh[d & 255u] : 0u;
         __syncwarp();
-        if (valid && (peers & lt) == 0u) wh[d] = before + __popc(peers);
+        if (valid && (peers & lt) == 0u) wh[d & 255u] = before + __popc(peers);
         __syncwarp();
         pk[r] = (d << 16) | (before + __popc(peers & lt));
     }

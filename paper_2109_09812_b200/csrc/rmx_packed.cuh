@@ -43,6 +43,43 @@ __device__ __forceinline__ uint32_t pick(const uint32_t (&k)[D_CT], uint32_t c) 
     return w;
 }
 
+__device__ __forceinline__ uint32_t shfl_up_key(uint32_t k) { return __shfl_up_sync(kFull, k, 1); }
+__device__ __forceinline__ uint64_t shfl_up_key(uint64_t k) {
+    const uint32_t lo = __shfl_up_sync(kFull, static_cast<uint32_t>(k), 1);
+    const uint32_t hi = __shfl_up_sync(kFull, static_cast<uint32_t>(k >> 32), 1);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// Packed key -> D words: replacement bits outside the varying mask, varying
+// bits deposited back from their runs (inverse of k_pack).
+template <int D_CT>
+__device__ __forceinline__ void unpack_row(uint64_t key, uint32_t* dst, int D, const uint32_t* s_const,
+                                           const uint32_t* s_runs, uint32_t nruns, const uint32_t* s_rbeg,
+                                           const uint32_t* s_rend) {
+    if constexpr (D_CT > 0) {
+        uint32_t w[D_CT];
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) w[c] = s_const[c];
+        for (uint32_t q = 0; q < nruns; ++q) {
+            const uint32_t* ru = s_runs + 4 * q;
+            const uint32_t bits = (static_cast<uint32_t>(key >> ru[3]) & low_mask(ru[2])) << ru[1];
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) w[c] |= (ru[0] == static_cast<uint32_t>(c)) ? bits : 0u;
+        }
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) dst[c] = w[c];
+    } else {
+        for (int c = 0; c < D; ++c) {
+            uint32_t w = s_const[c];
+            for (uint32_t q = s_rbeg[c]; q < s_rend[c]; ++q) {
+                const uint32_t* ru = s_runs + 4 * q;
+                w |= (static_cast<uint32_t>(key >> ru[3]) & low_mask(ru[2])) << ru[1];
+            }
+            dst[c] = w;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K1a: varying bits of the cleaned vertex set.
 struct VaryArgs {
@@ -380,12 +417,19 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     mbar_wait(s_bar, 0u);
 
     uint32_t pk[IPT];
+    if (tile_n == static_cast<uint32_t>(TILE)) {  // full tile: no validity tests
 #pragma unroll
-    for (int r = 0; r < IPT; ++r) {
-        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
-        pk[r] = p < tile_n ? (static_cast<uint32_t>(s_keys[p] >> shift) & 255u) : 256u;
+        for (int r = 0; r < IPT; ++r)
+            pk[r] = static_cast<uint32_t>(s_keys[warp * (32u * IPT) + r * 32u + lane] >> shift) & 255u;
+        warp_rank<IPT, false>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, false);
+    } else {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            pk[r] = p < tile_n ? (static_cast<uint32_t>(s_keys[p] >> shift) & 255u) : 256u;
+        }
+        warp_rank<IPT, true>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, true);
     }
-    warp_rank<IPT>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, tile_n < static_cast<uint32_t>(TILE));
     __syncthreads();
     {
         const uint32_t d = tid;
@@ -553,7 +597,7 @@ struct UniquePkTraits {
     }
 };
 
-template <int KW, int IPT>
+template <int KW, int IPT, int D_CT>
 __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* smem) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
@@ -613,17 +657,30 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     __syncthreads();
     mbar_wait(s_bar, it & 1u);
 
-    // ---- phase 1: head flags (warp-striped rows), per-warp totals, bucket counts
+    // ---- phase 1: head flags (warp-striped rows; the previous key comes from the
+    // neighbouring lane), per-warp totals, bucket counts.  Keys and origins stay
+    // in registers for phase 2.
     uint32_t bal[IPT];
+    Key kreg[IPT];
+    uint32_t vreg[IPT];
     uint32_t wtotal = 0;
 #pragma unroll
     for (int r = 0; r < IPT; ++r) {
         const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        const bool valid = p < tile_n;
+        const Key key = valid ? s_keys[p] : Key(0);
+        Key prev = shfl_up_key(key);
+        if (lane == 0 && valid && p > 0) prev = s_keys[p - 1];
+        if (lane == 0 && p == 0 && base > 0) prev = *s_prev;
         bool head = false;
-        if (p < tile_n) {
-            head = (base + p == 0u) || s_keys[p] != (p ? s_keys[p - 1] : *s_prev);
-            atomicAdd(s_bcnt + (s_vals[p] >> bs), 1u);
+        uint32_t org = 0;
+        if (valid) {
+            head = (base + p == 0u) || key != prev;
+            org = s_vals[p];
+            atomicAdd(s_bcnt + (org >> bs), 1u);
         }
+        kreg[r] = key;
+        vreg[r] = org;
         bal[r] = __ballot_sync(kFull, head);
         wtotal += __popc(bal[r]);
     }
@@ -648,21 +705,11 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
         const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
         if (p < tile_n) {
             const uint32_t nidx = running + __popc(bal[r] & lanemask_le()) - 1u;
-            const uint32_t org = s_vals[p];
+            const uint32_t org = vreg[r];
             s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
             const bool head = (bal[r] >> lane) & 1u;
-            if (head) {
-                const uint64_t key = static_cast<uint64_t>(s_keys[p]);
-                uint32_t* dst = a.out_vtx + static_cast<size_t>(nidx) * D;
-                for (int c = 0; c < D; ++c) {
-                    uint32_t w = s_const[c];
-                    for (uint32_t q = s_rbeg[c]; q < s_rend[c]; ++q) {
-                        const uint32_t* ru = s_runs + 4 * q;
-                        w |= (static_cast<uint32_t>(key >> ru[3]) & low_mask(ru[2])) << ru[1];
-                    }
-                    dst[c] = w;
-                }
-            }
+            if (head) unpack_row<D_CT>(static_cast<uint64_t>(kreg[r]), a.out_vtx + static_cast<size_t>(nidx) * D, D,
+                                       s_const, s_runs, nruns, s_rbeg, s_rend);
             if (a.sc_org) a.sc_org[base + p] = org;
             if (a.sc_nodup) a.sc_nodup[base + p] = head ? 1 : 0;
             if (a.sc_new) a.sc_new[base + p] = nidx;
@@ -680,14 +727,14 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     }
 }
 
-template <int IPT>
-__global__ void __launch_bounds__(kBlock) k_unique_pk(UniquePkArgs a) {
+template <int IPT, int D_CT>
+__global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
     extern __shared__ __align__(128) uint32_t smem[];
-    if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
-    else unique_pk_body<1, IPT>(a, smem);
+    if (pk[1] == 2u) unique_pk_body<2, IPT, D_CT>(a, smem);
+    else unique_pk_body<1, IPT, D_CT>(a, smem);
 }
 
 }  // namespace rmx
