@@ -86,12 +86,13 @@ struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, hist, hist_pk, vary, fill, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, hist, vary, fill, counters, desc, desc3, ctl_end;
     int bucket_shift;
     uint32_t ntiles_pk, ntiles3_pk;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
     size_t tile_counts;
     size_t pk_counts, pk_totals;  // packed passes: [256][ntiles_pk] tile counts / column scans, [256] totals
+    size_t pk_digits;             // packed passes: [V] digit byte of the current pass per row
     size_t total;
 };
 
@@ -119,9 +120,9 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.plan = take(plan_words(L.P) * 4);
     L.pk_counts = take(static_cast<size_t>(L.ntiles_pk) * 256 * 4);
     L.pk_totals = take(256 * 4);
+    L.pk_digits = take(static_cast<size_t>(V) + 16);
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
-    L.hist_pk = take(static_cast<size_t>(kMaxPackedPasses) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
     L.fill = take(256 * 4);
     int bits = 0;
@@ -454,16 +455,16 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = rec.mark())) return rc;
     }
     // ---- packed-key path (kernels exit at once in AoS mode)
-    uint32_t* hist_pk = reinterpret_cast<uint32_t*>(base + L.hist_pk);
     {
-        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, hist_pk, d_status, static_cast<uint32_t>(V), L.D, vec};
+        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), d_status,
+                   static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
-                     reinterpret_cast<uint32_t*>(base + L.pk_totals), d_status, static_cast<uint32_t>(V), L.ntiles_pk,
-                     L.D, p, rank_force()};
+                     reinterpret_cast<uint32_t*>(base + L.pk_totals), reinterpret_cast<uint8_t*>(base + L.pk_digits),
+                     d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }

@@ -165,7 +165,7 @@ struct PackArgs {
     const uint32_t* plan;
     uint32_t* buf0;   // keys at word 0, origins at word vals_off
     size_t vals_off;  // words
-    uint32_t* hist;   // packed histograms [kMaxPackedPasses][256]
+    uint8_t* digits;  // [n] packed digit 0 per row (read by the first upsweep)
     const uint32_t* status;
     uint32_t n;
     int dim;
@@ -177,12 +177,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
-    __shared__ uint32_t s_h[256];
     if (*a.status || pk[0] == 0u) return;  // uniform
     const uint32_t nruns = pk[4];
     const bool wide = pk[1] == 2u;
     for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
-    s_h[threadIdx.x] = 0u;
     __syncthreads();
 
     const uint32_t r0 = a.idx[0];
@@ -192,13 +190,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     uint32_t* vals = a.buf0 + a.vals_off;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    uint32_t rl = 0u;
 
     auto put = [&](uint64_t i, uint64_t key) {
         if (wide) keys64[i] = key;
         else keys32[i] = static_cast<uint32_t>(key);
         vals[i] = static_cast<uint32_t>(i);
-        rl_push(rl, static_cast<uint32_t>(key) & 255u, s_h);
+        a.digits[i] = static_cast<uint8_t>(key);
     };
 
     if constexpr (D_CT > 0) {
@@ -237,14 +234,30 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
                     const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
                     const uint32_t f = __ldcs(f4 + g);
                     uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
+                    uint64_t key[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         if (((f >> (8 * j)) & 255u) == 0u) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
                         }
-                        put(4 * g + j, pack(k[j]));
+                        key[j] = pack(k[j]);
                     }
+                    // 16-byte stores of 4 consecutive rows (vals_off is a multiple of 4 words)
+                    if (wide) {
+                        ulonglong2* k2 = reinterpret_cast<ulonglong2*>(keys64 + 4 * g);
+                        __stcs(k2, make_ulonglong2(key[0], key[1]));
+                        __stcs(k2 + 1, make_ulonglong2(key[2], key[3]));
+                    } else {
+                        __stcs(reinterpret_cast<uint4*>(keys32 + 4 * g),
+                               make_uint4(static_cast<uint32_t>(key[0]), static_cast<uint32_t>(key[1]),
+                                          static_cast<uint32_t>(key[2]), static_cast<uint32_t>(key[3])));
+                    }
+                    const uint32_t i0 = static_cast<uint32_t>(4 * g);
+                    __stcs(reinterpret_cast<uint4*>(vals + 4 * g), make_uint4(i0, i0 + 1, i0 + 2, i0 + 3));
+                    reinterpret_cast<uint32_t*>(a.digits)[g] =
+                        (static_cast<uint32_t>(key[0]) & 255u) | ((static_cast<uint32_t>(key[1]) & 255u) << 8) |
+                        ((static_cast<uint32_t>(key[2]) & 255u) << 16) | (static_cast<uint32_t>(key[3]) << 24);
                 }
                 done = ng << 2;
             }
@@ -267,9 +280,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
             put(i, key);
         }
     }
-    if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);
-    __syncthreads();
-    if (s_h[threadIdx.x]) atomicAdd(a.hist + threadIdx.x, s_h[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
@@ -292,6 +302,7 @@ struct SortPkArgs {
     const uint32_t* plan;
     uint32_t* counts;      // [256][ntiles] per-tile digit counts -> exclusive column scans
     uint32_t* totals;      // [256] digit totals of this pass
+    uint8_t* digits;       // [n] this pass's digit per row (written by k_pack / the previous downsweep)
     const uint32_t* status;
     uint32_t n;
     uint32_t ntiles;
@@ -306,31 +317,30 @@ __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
     return pk[0] != 0u && static_cast<uint32_t>(a.pass) < pk[3];
 }
 
-template <int KW>
-__device__ __forceinline__ void pk_upsweep_body(const SortPkArgs& a, uint32_t tile_rows) {
-    using Key = typename PkKey<KW>::T;
-    const uint32_t* ib = (static_cast<uint32_t>(a.pass) & 1u) ? a.buf1 : a.buf0;
-    const Key* __restrict__ keys = reinterpret_cast<const Key*>(ib);
-    const int shift = 8 * a.pass;
+// Per-tile digit counts from the digit-byte array (1 B/row instead of the 4-8 B
+// key: k_pack and every downsweep also emit the next pass's digit per row).
+__global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
+    if (*a.status || !pk_pass_active(a)) return;
     __shared__ uint32_t s_h[256];
+    const uint32_t* d4 = reinterpret_cast<const uint32_t*>(a.digits);  // tile_rows is a multiple of 4
     for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         s_h[threadIdx.x] = 0u;
         __syncthreads();
         const uint64_t base = static_cast<uint64_t>(t) * tile_rows;
         const uint64_t end = min(base + tile_rows, static_cast<uint64_t>(a.n));
-#pragma unroll 4
-        for (uint64_t g = base + threadIdx.x; g < end; g += kBlock)
-            atomicAdd(s_h + (static_cast<uint32_t>(__ldcs(keys + g) >> shift) & 255u), 1u);
+        const uint64_t end4 = base + ((end - base) & ~3ull);
+        for (uint64_t g = base + 4u * threadIdx.x; g < end4; g += 4u * kBlock) {
+            const uint32_t w = __ldcs(d4 + (g >> 2));
+            atomicAdd(s_h + (w & 255u), 1u);
+            atomicAdd(s_h + ((w >> 8) & 255u), 1u);
+            atomicAdd(s_h + ((w >> 16) & 255u), 1u);
+            atomicAdd(s_h + (w >> 24), 1u);
+        }
+        for (uint64_t g = end4 + threadIdx.x; g < end; g += kBlock) atomicAdd(s_h + a.digits[g], 1u);
         __syncthreads();
         a.counts[static_cast<size_t>(threadIdx.x) * a.ntiles + t] = s_h[threadIdx.x];
         __syncthreads();
     }
-}
-
-__global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
-    if (*a.status || !pk_pass_active(a)) return;
-    if (a.plan[pk_base(4 * a.dim) + 1] == 2u) pk_upsweep_body<2>(a, tile_rows);
-    else pk_upsweep_body<1>(a, tile_rows);
 }
 
 // One CTA per digit: exclusive scan of counts[d][0 .. ntiles) in place,
@@ -382,6 +392,8 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     Key* __restrict__ out_k = reinterpret_cast<Key*>(ob);
     uint32_t* __restrict__ out_v = ob + a.vals_off;
     const int shift = 8 * a.pass;
+    // the next pass (if any) reads its digits from the byte array
+    const bool emit_next = static_cast<uint32_t>(a.pass) + 1u < a.plan[pk_base(4 * a.dim) + 3];
 
     Key* s_keys = reinterpret_cast<Key*>(smem);
     uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;  // keys region sized for u64
@@ -482,6 +494,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
             if (q < tile_n) {
                 out_k[dst[u]] = k[u];
                 out_v[dst[u]] = v[u];
+                if (emit_next) a.digits[dst[u]] = static_cast<uint8_t>(k[u] >> (shift + 8));
             }
         }
     }
