@@ -8,13 +8,13 @@ behind the C-ABI in include/remesh_b200.h.
 from .mesh import (InvalidMeshError, Issue, Mesh, MeshError, bitwise_equal, dereference,
                    require_valid, soups_equal, validate, vertex_bits)
 from .ops import merge, soup_to_mesh, subset
-from .pipeline import (DeviceResult, ReindexScratch, Reindexer, reindex, reindex_tensors,
+from .pipeline import (DeviceResult, ReindexScratch, Reindexer, ReindexStream, reindex, reindex_tensors,
                        workspace_bytes)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Mesh", "Issue", "MeshError", "InvalidMeshError", "ReindexScratch", "DeviceResult",
-    "Reindexer", "reindex", "reindex_tensors", "workspace_bytes", "merge", "soup_to_mesh", "subset",
+    "Reindexer", "ReindexStream", "reindex", "reindex_tensors", "workspace_bytes", "merge", "soup_to_mesh", "subset",
     "validate", "require_valid", "dereference", "soups_equal", "bitwise_equal", "vertex_bits",
 ]

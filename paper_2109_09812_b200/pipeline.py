@@ -334,3 +334,132 @@ class Reindexer:
             s.synchronize()
         self.last_count = count
         return (self.host_v[:count].numpy().view(np.float32), self.host_e.numpy().view(np.uint32))
+
+
+class _Slot:
+    """Device + pinned host buffers of one in-flight mesh of a :class:`ReindexStream`."""
+
+    def __init__(self, V: int, D: int, E: int, K: int, dev: torch.device):
+        self.vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
+        self.idx_d = torch.empty((E, K), dtype=torch.int32, device=dev)
+        self.out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
+        self.out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
+        self.info = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.host_v = torch.empty((V, D), dtype=torch.int32, pin_memory=True)
+        self.host_e = torch.empty((E, K), dtype=torch.int32, pin_memory=True)
+        self.host_info = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.h2d_done = torch.cuda.Event()
+        self.comp_done = torch.cuda.Event()
+        self.d2h_done = torch.cuda.Event()
+        self.used = False
+        self.inputs = None
+        self.shape = (0, 0)
+
+
+class ReindexStream:
+    """Pipelined host-to-host re-indexing of a sequence of meshes.
+
+    The three engines of the GPU work on different meshes at once: while mesh
+    k is re-indexed on the compute stream, mesh k+1's vertices and elements
+    cross PCIe host->device on one copy stream and mesh k-1's result comes
+    back device->host on the other (the link is full duplex).  The kernels
+    share one workspace (compute is serialised on one stream); inputs and
+    results are double-buffered.
+
+    ``run(batches)`` takes an iterable of pinned ``(vertices int32 (V, D),
+    elements int32 (E, K))`` tensors with V, E within the capacity given at
+    construction and yields ``(vertices (U, D) float32, elements (E, K)
+    uint32)`` numpy views in input order.  A yielded result stays valid until
+    the generator is advanced again (copy it to keep it).  An out-of-range
+    index raises :class:`InvalidMeshError` for that mesh, like :func:`reindex`.
+    """
+
+    def __init__(self, max_vertices: int, dim: int, max_elements: int, arity: int, device=None, depth: int = 2):
+        self.device = _device(device)
+        self.V, self.D, self.E, self.K = int(max_vertices), int(dim), int(max_elements), int(arity)
+        if depth < 2:
+            raise ValueError("depth must be >= 2")
+        dev = self.device
+        with torch.cuda.device(dev):
+            self.slots = [_Slot(self.V, self.D, self.E, self.K, dev) for _ in range(depth)]
+            self.ws = torch.empty(max(1, workspace_bytes(self.V, self.D, self.E, self.K)), dtype=torch.uint8,
+                                  device=dev)
+            self.h2d = torch.cuda.Stream(dev)
+            self.comp = torch.cuda.Stream(dev)
+            self.d2h = torch.cuda.Stream(dev)
+        self.last_counts: list[int] = []
+
+    def bytes_per_mesh(self, n_vertices: int, n_elements: int, count: int) -> tuple[int, int]:
+        h2d = n_vertices * self.D * 4 + n_elements * self.K * 4
+        d2h = 16 + count * self.D * 4 + n_elements * self.K * 4
+        return h2d, d2h
+
+    def _submit(self, slot: _Slot, vertices: torch.Tensor, elements: torch.Tensor) -> None:
+        V, E = vertices.shape[0], elements.shape[0]
+        if vertices.shape[1:] != (self.D,) or elements.shape[1:] != (self.K,):
+            raise MeshError(f"mesh shapes {tuple(vertices.shape)} / {tuple(elements.shape)} do not match "
+                            f"dim={self.D} arity={self.K}")
+        if V > self.V or E > self.E:
+            raise MeshError(f"mesh ({V} vertices, {E} elements) exceeds the stream capacity ({self.V}, {self.E})")
+        if slot.used:  # the previous mesh of this slot must be off its buffers
+            self.h2d.wait_event(slot.comp_done)
+        with torch.cuda.stream(self.h2d):
+            slot.vtx_d[:V].copy_(vertices, non_blocking=True)
+            slot.idx_d[:E].copy_(elements, non_blocking=True)
+            slot.h2d_done.record(self.h2d)
+        self.comp.wait_event(slot.h2d_done)
+        if slot.used:
+            self.comp.wait_event(slot.d2h_done)
+        with torch.cuda.stream(self.comp):
+            if E:
+                launch(slot.vtx_d, V, self.D, slot.idx_d, E, self.K, slot.out_v, slot.out_e, slot.info, self.ws,
+                       None, self.comp)
+            else:
+                slot.info.zero_()
+            slot.host_info.copy_(slot.info, non_blocking=True)
+            slot.comp_done.record(self.comp)
+        slot.used = True
+        slot.inputs = (vertices, elements)
+        slot.shape = (V, E)
+
+    def _finish(self, slot: _Slot):
+        V, E = slot.shape
+        # the element result has a known size: start it before the host learns the count.
+        # (Enqueued here, not at submit: the copy stream must not queue behind the next mesh.)
+        self.d2h.wait_event(slot.comp_done)
+        with torch.cuda.stream(self.d2h):
+            if E:
+                slot.host_e[:E].copy_(slot.out_e[:E], non_blocking=True)
+        slot.comp_done.synchronize()
+        count, status = (int(x) for x in slot.host_info)
+        if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+            self.synchronize()
+            hv, he = slot.inputs
+            raise InvalidMeshError(validate(_Arrays(hv.numpy().view(np.float32), he.numpy().view(np.uint32))))
+        with torch.cuda.stream(self.d2h):
+            if count:
+                slot.host_v[:count].copy_(slot.out_v[:count], non_blocking=True)
+            slot.d2h_done.record(self.d2h)
+        slot.d2h_done.synchronize()
+        slot.inputs = None
+        self.last_counts.append(count)
+        return (slot.host_v[:count].numpy().view(np.float32), slot.host_e[:E].numpy().view(np.uint32))
+
+    def run(self, batches):
+        depth = len(self.slots)
+        pending: list[_Slot] = []
+        k = 0
+        with torch.cuda.device(self.device):
+            for vertices, elements in batches:
+                slot = self.slots[k % depth]
+                self._submit(slot, vertices, elements)
+                pending.append(slot)
+                k += 1
+                if len(pending) == depth:
+                    yield self._finish(pending.pop(0))
+            while pending:
+                yield self._finish(pending.pop(0))
+
+    def synchronize(self) -> None:
+        for s in (self.h2d, self.comp, self.d2h):
+            s.synchronize()

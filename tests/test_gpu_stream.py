@@ -1,0 +1,101 @@
+"""GPU: the host-to-host entry points (Reindexer, ReindexStream) against the oracle.
+
+Both wrap the same ``rmx_reindex`` call as :func:`reindex`; these tests pin the
+buffer handling around it -- pinned copies, capacity slicing, double-buffered
+slots, the count-dependent vertex read-back, errors in the middle of a stream.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import remesh_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rmx(cuda_ok):
+    import paper_2109_09812_b200 as p
+    return p
+
+
+def random_mesh(seed, V, D, E, K, pool=64):
+    rng = np.random.default_rng(seed)
+    vals = rng.integers(0, 1 << 32, size=pool, dtype=np.uint64).astype(np.uint32)
+    v = vals[rng.integers(0, pool, size=(V, D))]
+    # leave the tail unused, repeat rows so duplicates exist
+    v[V // 2:] = v[rng.integers(0, max(1, V // 2), size=V - V // 2)]
+    e = rng.integers(0, max(1, (V * 9) // 10), size=(E, K)).astype(np.uint32)
+    return v, e
+
+
+def pinned(v, e):
+    hv = torch.from_numpy(np.ascontiguousarray(v).view(np.int32)).pin_memory()
+    he = torch.from_numpy(np.ascontiguousarray(e).view(np.int32)).pin_memory()
+    return hv, he
+
+
+def expect(v, e):
+    r = O.reindex(v.view(np.float32), e)
+    return np.asarray(r["vertices"]).view(np.uint32), np.asarray(r["elements"])
+
+
+def test_reindexer_repeated_calls(rmx):
+    v, e = random_mesh(1, 5000, 3, 3000, 3)
+    rx = rmx.Reindexer(5000, 3, 3000, 3)
+    hv, he = pinned(v, e)
+    ev, ee = expect(v, e)
+    for _ in range(3):
+        gv, ge = rx.run(hv, he)
+        assert np.array_equal(gv.view(np.uint32), ev)
+        assert np.array_equal(ge, ee)
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_stream_matches_oracle_in_order(rmx, depth):
+    shapes = [(5000, 3000), (1, 4), (777, 50), (5000, 3000), (4096, 2999), (300, 0), (2, 1), (4999, 1234)]
+    meshes = [random_mesh(10 + i, V, 3, E, 4) for i, (V, E) in enumerate(shapes)]
+    rs = rmx.ReindexStream(5000, 3, 3000, 4, depth=depth)
+    got = [(gv.copy(), ge.copy()) for gv, ge in rs.run(pinned(v, e) for v, e in meshes)]
+    assert len(got) == len(meshes)
+    for (v, e), (gv, ge) in zip(meshes, got):
+        if e.shape[0] == 0:
+            assert gv.shape == (0, 3) and ge.shape == (0, 4)
+            continue
+        ev, ee = expect(v, e)
+        assert np.array_equal(gv.view(np.uint32), ev)
+        assert np.array_equal(ge, ee)
+    assert rs.last_counts[0] == expect(*meshes[0])[0].shape[0]
+
+
+def test_stream_views_valid_until_next(rmx):
+    meshes = [random_mesh(40 + i, 2000, 2, 1500, 3, pool=16) for i in range(5)]
+    rs = rmx.ReindexStream(2000, 2, 1500, 3)
+    for (v, e), (gv, ge) in zip(meshes, rs.run(pinned(v, e) for v, e in meshes)):
+        ev, ee = expect(v, e)
+        assert np.array_equal(gv.view(np.uint32), ev)
+        assert np.array_equal(ge, ee)
+
+
+def test_stream_out_of_range_raises(rmx):
+    good = random_mesh(3, 100, 3, 80, 3)
+    bad_v, bad_e = random_mesh(4, 100, 3, 80, 3)
+    bad_e = bad_e.copy()
+    bad_e[7, 1] = 100
+    rs = rmx.ReindexStream(100, 3, 80, 3)
+    it = rs.run(pinned(v, e) for v, e in [good, (bad_v, bad_e), good])
+    gv, ge = next(it)
+    assert np.array_equal(ge, expect(*good)[1])
+    with pytest.raises(rmx.InvalidMeshError) as ei:
+        next(it)
+    assert ei.value.issues[0] == rmx.Issue(7, 1, 100)
+
+
+def test_stream_capacity_and_shape_errors(rmx):
+    rs = rmx.ReindexStream(100, 3, 80, 3)
+    v, e = random_mesh(5, 101, 3, 80, 3)
+    with pytest.raises(rmx.MeshError):
+        list(rs.run([pinned(v, e)]))
+    v, e = random_mesh(5, 50, 2, 40, 3)
+    with pytest.raises(rmx.MeshError):
+        list(rs.run([pinned(v, e)]))
