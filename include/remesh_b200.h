@@ -161,6 +161,15 @@ int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, 
                                uint64_t e_begin, uint64_t e_end, uint32_t* out_vtx_bits,
                                uint32_t* out_idx, void* stream);
 
+/*
+ * grid_quads(n) of the paper's Table 1 on the device (reference
+ * pkg/src/remeshx/bench.py:42-68): 5*n*n float2 rows (4 corners + an unused
+ * centre per quad) into out_vtx_bits (10*n*n words) and n*n quads
+ * (5q, 5q+1, 5q+2, 5q+3) into out_idx (4*n*n words); bit-identical to the
+ * reference generator.  RMX_ERANGE when 5*n*n >= 2^32.
+ */
+int rmx_gen_grid_quads(uint32_t n, uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

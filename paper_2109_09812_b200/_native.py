@@ -27,7 +27,7 @@ EXPORTS = (
     "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex",
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches",
     "rmx_last_executed_passes", "rmx_plan_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
-    "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gather_u32", "rmx_lower_bound_rows",
+    "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
 )
 
 
@@ -67,6 +67,7 @@ _SIGNATURES = {
                                  ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "rmx_gen_lattice_soup": (_int, [_int, _u32, _u32, _u32, _u64, _u64, _vp, _vp, _vp]),
     "rmx_gen_lattice_soup_range": (_int, [_int, _u32, _u32, _u32, _u64, _u64, _u64, _vp, _vp, _vp]),
+    "rmx_gen_grid_quads": (_int, [_u32, _vp, _vp, _vp]),
     "rmx_gather_u32": (_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
     "rmx_lower_bound_rows": (_int, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
 }

@@ -708,4 +708,17 @@ int rmx_gen_lattice_soup(int kind, uint32_t nx, uint32_t ny, uint32_t nz, uint64
     return rmx_gen_lattice_soup_range(kind, nx, ny, nz, seed, 0, n_elem_take, out_vtx_bits, out_idx, stream);
 }
 
+int rmx_gen_grid_quads(uint32_t n, uint32_t* out_vtx_bits, uint32_t* out_idx, void* stream) {
+    if (n < 1) return RMX_EINVAL;
+    const uint64_t quads = static_cast<uint64_t>(n) * n;
+    if (quads * 5u >= (1ull << 32)) return RMX_ERANGE;
+    if (!out_vtx_bits || !out_idx) return RMX_EINVAL;
+    int grid = 0;
+    int rc = grid_for_stream(quads * 10u, grid);
+    if (rc) return rc;
+    k_gen_grid_quads<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(n, quads, out_vtx_bits, out_idx);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 }  // extern "C"

@@ -102,4 +102,37 @@ __global__ void __launch_bounds__(kBlock) k_gen_lattice(GenArgs g) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// grid_quads(n) of the paper's Table 1 (reference bench.py:42-68): quad q has
+// qi = q mod n, qj = q div n and owns 5 float2 rows -- corners (qi,qj),
+// (qi+1,qj), (qi+1,qj+1), (qi,qj+1) and the unused centre (qi+.5,qj+.5) --
+// and the element (5q, 5q+1, 5q+2, 5q+3) (uint32 arithmetic, like the
+// reference's uint32 arange).  One thread per output word: both arrays are
+// written fully coalesced.
+__global__ void __launch_bounds__(kBlock) k_gen_grid_quads(uint32_t n, uint64_t quads, uint32_t* vtx,
+                                                           uint32_t* idx) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    for (uint64_t w = t0; w < quads * 10u; w += stride) {
+        const uint64_t q = w / 10u;
+        const uint32_t r = static_cast<uint32_t>(w - q * 10u);
+        const float qi = static_cast<float>(q % n), qj = static_cast<float>(q / n);
+        const uint32_t row = r >> 1, c = r & 1u;
+        const float base = c ? qj : qi;
+        float v;
+        if (row == 4u) {
+            v = __fadd_rn(base, 0.5f);
+        } else {
+            // corners: x + 1 for rows 1, 2; y + 1 for rows 2, 3
+            const bool plus = c ? (row >= 2u) : (row == 1u || row == 2u);
+            v = plus ? __fadd_rn(base, 1.0f) : base;
+        }
+        vtx[w] = __float_as_uint(v);
+    }
+    for (uint64_t w = t0; w < quads * 4u; w += stride) {
+        const uint64_t q = w >> 2;
+        idx[w] = static_cast<uint32_t>(q) * 5u + static_cast<uint32_t>(w & 3u);
+    }
+}
+
 }  // namespace rmx

@@ -19,6 +19,8 @@ Cases:
   random      -- remeshx.random_mesh seeds sweeping dup/unused fraction, arity
   grid        -- remeshx.grid_quads(N) for N = 1, 2, 8, 64 (paper Table 1 counts)
   lattice     -- small oracle/lattice.py soups (pins the lattice closed form)
+  ops         -- merge / soup_to_mesh / subset results
+  rmx1/*.rmx  -- RMX1 files written by the reference write_bin
 """
 from __future__ import annotations
 
@@ -194,8 +196,28 @@ def ops(cases):
     record_mesh(cases, "merge_quads", remeshx.merge(parts))
 
 
+def files():
+    """RMX1 containers written by the reference write_bin (fileio.py:125-133)."""
+    d = os.path.join(OUT, "rmx1")
+    os.makedirs(d, exist_ok=True)
+    A, B, C, D, E, F = (0, 0), (0, 1), (0, 2), (0, 3), (0, 4), (0, 5)
+    X, Y = (9, 9), (8, 8)
+    meshes = {
+        "worked": remeshx.Mesh(np.array([A, B, C, X, D, C, E, F, Y, D], np.float32),
+                               np.array([(0, 1, 2), (0, 2, 4), (5, 6, 7), (5, 7, 9)], np.uint32)),
+        "empty": remeshx.Mesh.empty(),
+        "nan_bits": remeshx.Mesh(np.array([(np.uint32(0x7FC00123).view(np.float32), -0.0)], np.float32),
+                                 np.array([(0, 0, 0)], np.uint32)),
+        "random_quads3d": remeshx.random_mesh(remeshx.RandomMeshSpec(seed=5, arity=4, dim=3)),
+    }
+    for name, m in meshes.items():
+        remeshx.write_bin(m, os.path.join(d, f"{name}.rmx"))
+        print(f"{d}/{name}.rmx")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    files()
     groups = {"worked": worked, "reftests": reftests, "torture": torture, "random": random_meshes,
               "grid": grids, "lattice": lattices, "ops": ops}
     for gname, fn in groups.items():
