@@ -188,6 +188,17 @@ __device__ __forceinline__ void bit_plane_and(uint32_t& peers, uint32_t d, uint3
         : "r"(d), "r"(mask));
 }
 
+// Swizzled slot of digit d in a 256-entry per-warp counter table.  Digits of
+// real keys are structured (float mantissas of lattice-like data keep their
+// low bits constant while high bits vary), so the lanes of a warp touching
+// distinct digits d = h*32 + c would all hit bank c; folding the high bits
+// into the bank spreads them.  A bijection on [0, 256).
+__device__ __forceinline__ uint32_t hsw(uint32_t d) { return d ^ (d >> 5); }
+
+// Rank the IPT digits (pk[r] < 256, or 256 = invalid when PARTIAL) of this
+// lane within the warp.  On return pk[r] = (hsw(d) << 16) | (rows of this warp
+// with digit d before this one, counted on top of wh[hsw(d)]); wh[hsw(d)] has
+// grown by the warp's count of digit d.
 template <int IPT, bool PARTIAL = true>
 __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uint32_t* wm, int mode, bool partial) {
     const uint32_t lane = threadIdx.x & 31u;
@@ -218,11 +229,12 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uin
         for (int r = 0; r < IPT; ++r) {
             const uint32_t d = pk[r];
             const bool valid = !PARTIAL || d < 256u;
-            if (valid) atomicOr(wm + d, bit);
+            const uint32_t ds = hsw(d & 255u);
+            if (valid) atomicOr(wm + ds, bit);
             __syncwarp();
-            pm[r] = valid ? wm[d] : 0u;
+            pm[r] = valid ? wm[ds] : 0u;
             __syncwarp();
-            if (valid && (pm[r] & lt) == 0u) wm[d] = 0u;
+            if (valid && (pm[r] & lt) == 0u) wm[ds] = 0u;
             __syncwarp();
         }
     }
@@ -231,11 +243,12 @@ __device__ __forceinline__ void warp_rank(uint32_t (&pk)[IPT], uint32_t* wh, uin
         const uint32_t d = pk[r];
         const uint32_t peers = pm[r];
         const bool valid = !PARTIAL || d < 256u;
-        const uint32_t before = valid ? wh[d & 255u] : 0u;
+        const uint32_t ds = hsw(d & 255u);
+        const uint32_t before = valid ? wh[ds] : 0u;
         __syncwarp();
-        if (valid && (peers & lt) == 0u) wh[d & 255u] = before + __popc(peers);
+        if (valid && (peers & lt) == 0u) wh[ds] = before + __popc(peers);
         __syncwarp();
-        pk[r] = (d << 16) | (before + __popc(peers & lt));
+        pk[r] = (ds << 16) | (before + __popc(peers & lt));
     }
 }
 

@@ -449,7 +449,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
         uint32_t cnt = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            wc[w] = s_whist[w * 256 + d];
+            wc[w] = s_whist[w * 256 + hsw(d)];
             cnt += wc[w];
         }
         uint32_t tot;
@@ -457,7 +457,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
         uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            s_whist[w * 256 + d] = run;  // slot of this warp's first row with digit d
+            s_whist[w * 256 + hsw(d)] = run;  // slot of this warp's first row with digit d
             run += wc[w];
         }
         s_gdst[d] = run_base - start;  // mod 2^32; + tile slot gives the global row
@@ -656,16 +656,20 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
         s_rbeg[tid] = b < e ? b : 0u;
         s_rend[tid] = e;
     }
-    // static tile striding: no cross-tile dependency remains (prefixes come from k_tile_scan)
+    // static tile striding: no cross-tile dependency remains (prefixes come from k_tile_scan).
+    // The staging buffers are free once phase 1 has moved a tile into registers, so the
+    // next tile's bulk copy is issued there and overlaps phase 2 and the pair write-out.
+    auto issue = [&](uint32_t t) {
+        const uint32_t b = t * static_cast<uint32_t>(TILE);
+        const uint32_t n = min(static_cast<uint32_t>(TILE), a.n - b);
+        stage_tile2(s_keys, keys + b, n * static_cast<uint32_t>(sizeof(Key)), s_vals, vals + b, n * 4u, s_bar);
+        if (t > 0) *s_prev = keys[b - 1];
+    };
+    if (tid == 0 && blockIdx.x < a.ntiles) issue(blockIdx.x);
     uint32_t it = 0;
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
     const uint32_t base = tile * static_cast<uint32_t>(TILE);
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
-    if (tid == 0) {
-        stage_tile2(s_keys, keys + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, vals + base, tile_n * 4u,
-                    s_bar);
-        if (tile > 0) *s_prev = keys[base - 1];
-    }
     s_bcnt[tid] = 0u;
     __syncthreads();
     mbar_wait(s_bar, it & 1u);
@@ -699,6 +703,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     }
     if (lane == 0) s_warp[warp] = wtotal;
     __syncthreads();
+    if (tid == 0 && tile + gridDim.x < a.ntiles) issue(tile + gridDim.x);
     uint32_t wexcl = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wexcl += (static_cast<uint32_t>(w) < warp) ? s_warp[w] : 0u;

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
             uint32_t wc[kWarps];
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-                wc[w] = s_whist[w * 256 + d];
+                wc[w] = s_whist[w * 256 + hsw(d)];
                 cnt += wc[w];
             }
             st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d,
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_sort_pass(SortArgs a) {
             uint32_t run = start;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-                s_whist[w * 256 + d] = run;
+                s_whist[w * 256 + hsw(d)] = run;
                 run += wc[w];
             }
         }
