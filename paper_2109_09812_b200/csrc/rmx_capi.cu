@@ -88,7 +88,7 @@ struct Layout {
     size_t flags, rows0, rows1, map, plan;
     size_t ctl_begin, hist, vary, fill, counters, desc, desc3, ctl_end;
     int bucket_shift;
-    uint32_t ntiles_pk, ntiles3_pk;
+    uint32_t ntiles_pk, ntiles3_pk, pk_cstride;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
     size_t tile_counts;
     size_t pk_counts, pk_totals;  // packed passes: [256][ntiles_pk] tile counts / column scans, [256] totals
@@ -118,7 +118,8 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.rows1 = take(row_bytes);
     L.map = take(static_cast<size_t>(V) * 4);
     L.plan = take(plan_words(L.P) * 4);
-    L.pk_counts = take(static_cast<size_t>(L.ntiles_pk) * 256 * 4);
+    L.pk_cstride = (L.ntiles_pk + kUpGroup - 1) / kUpGroup * kUpGroup;
+    L.pk_counts = take(static_cast<size_t>(L.pk_cstride) * 256 * 4);
     L.pk_totals = take(256 * 4);
     L.pk_digits = take(static_cast<size_t>(V) + 16);
     L.ctl_begin = off;
@@ -266,7 +267,7 @@ int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
 
 int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     int grid = 0;
-    int rc = grid_for_stream(static_cast<uint64_t>(a.ntiles) * kBlock, grid);
+    int rc = grid_for_stream(static_cast<uint64_t>((a.ntiles + kUpGroup - 1) / kUpGroup) * kBlock, grid);
     if (rc) return rc;
     k_pk_upsweep<<<grid, kBlock, 0, s>>>(a, static_cast<uint32_t>(pk_sort_tile()));
     RMX_CHECK(cudaGetLastError());
@@ -464,7 +465,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     for (int p = 0; p < kMaxPackedPasses; ++p) {
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), reinterpret_cast<uint8_t*>(base + L.pk_digits),
-                     d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.D, p, rank_force()};
+                     d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride, L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }

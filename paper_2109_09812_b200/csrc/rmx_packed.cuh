@@ -156,6 +156,40 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
     }
 }
 
+// Cleaned row (D_CT words) -> packed key with the plan's runs (run r takes
+// len bits of component comp from bit src and puts them at bit dst).  The first
+// kRegRuns runs live in registers (typical meshes need one per component).
+template <int D_CT>
+struct RowPacker {
+    static constexpr int kRegRuns = 4;
+    uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
+    const uint32_t* s_runs;
+    uint32_t nruns;
+
+    __device__ __forceinline__ RowPacker(const uint32_t* runs, uint32_t n) : s_runs(runs), nruns(n) {
+#pragma unroll
+        for (int r = 0; r < kRegRuns; ++r) {
+            const bool on = static_cast<uint32_t>(r) < n;
+            rc[r] = on ? runs[4 * r] : 0u;
+            rs[r] = on ? runs[4 * r + 1] : 0u;
+            rm[r] = on ? low_mask(runs[4 * r + 2]) : 0u;
+            rd[r] = on ? runs[4 * r + 3] : 0u;
+        }
+    }
+
+    __device__ __forceinline__ uint64_t operator()(const uint32_t (&k)[D_CT]) const {
+        uint64_t key = 0;
+#pragma unroll
+        for (int r = 0; r < kRegRuns; ++r)
+            key |= static_cast<uint64_t>((pick<D_CT>(k, rc[r]) >> rs[r]) & rm[r]) << rd[r];
+        for (uint32_t r = kRegRuns; r < nruns; ++r) {
+            const uint32_t* ru = s_runs + 4 * r;
+            key |= static_cast<uint64_t>((pick<D_CT>(k, ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
+        }
+        return key;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // K1b': packed keys + origins, histogram of packed digit 0.
 struct PackArgs {
@@ -202,28 +236,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
         uint32_t ref[D_CT];
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
-        // the first 4 runs live in registers (typical meshes need 1 per component)
-        constexpr int kRegRuns = 4;
-        uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
-#pragma unroll
-        for (int r = 0; r < kRegRuns; ++r) {
-            const bool on = static_cast<uint32_t>(r) < nruns;
-            rc[r] = on ? s_runs[4 * r] : 0u;
-            rs[r] = on ? s_runs[4 * r + 1] : 0u;
-            rm[r] = on ? low_mask(s_runs[4 * r + 2]) : 0u;
-            rd[r] = on ? s_runs[4 * r + 3] : 0u;
-        }
-        auto pack = [&](const uint32_t (&k)[D_CT]) {
-            uint64_t key = 0;
-#pragma unroll
-            for (int r = 0; r < kRegRuns; ++r)
-                key |= static_cast<uint64_t>((pick<D_CT>(k, rc[r]) >> rs[r]) & rm[r]) << rd[r];
-            for (uint32_t r = kRegRuns; r < nruns; ++r) {
-                const uint32_t* ru = s_runs + 4 * r;
-                key |= static_cast<uint64_t>((pick<D_CT>(k, ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
-            }
-            return key;
-        };
+        const RowPacker<D_CT> pack(s_runs, nruns);
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
             if (a.vec) {
@@ -306,10 +319,15 @@ struct SortPkArgs {
     const uint32_t* status;
     uint32_t n;
     uint32_t ntiles;
+    uint32_t cstride;      // row stride of counts: ntiles rounded up to kUpGroup
     int dim;
     int pass;
     int rank_force;        // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
 };
+
+// The upsweep counts kUpGroup consecutive tiles per CTA iteration so every digit's
+// counts of the group leave as one 32-byte sector (digit-major layout).
+constexpr uint32_t kUpGroup = 8;
 
 // true when this packed pass runs (packed mode, pass < number of packed passes)
 __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
@@ -318,27 +336,40 @@ __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
 }
 
 // Per-tile digit counts from the digit-byte array (1 B/row instead of the 4-8 B
-// key: k_pack and every downsweep also emit the next pass's digit per row).
+// key: k_pack and every downsweep also emit the next pass's digit per row),
+// 16 digits per 16-byte load, kUpGroup tiles per CTA iteration.
 __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
     if (*a.status || !pk_pass_active(a)) return;
-    __shared__ uint32_t s_h[256];
-    const uint32_t* d4 = reinterpret_cast<const uint32_t*>(a.digits);  // tile_rows is a multiple of 4
-    for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        s_h[threadIdx.x] = 0u;
+    __shared__ uint32_t s_h[kUpGroup * 256];
+    const uint32_t ngroups = (a.ntiles + kUpGroup - 1u) / kUpGroup;
+    const uint4* d16 = reinterpret_cast<const uint4*>(a.digits);  // tile_rows is a multiple of 16
+    for (uint32_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        for (uint32_t i = threadIdx.x; i < kUpGroup * 256u; i += kBlock) s_h[i] = 0u;
         __syncthreads();
-        const uint64_t base = static_cast<uint64_t>(t) * tile_rows;
-        const uint64_t end = min(base + tile_rows, static_cast<uint64_t>(a.n));
-        const uint64_t end4 = base + ((end - base) & ~3ull);
-        for (uint64_t g = base + 4u * threadIdx.x; g < end4; g += 4u * kBlock) {
-            const uint32_t w = __ldcs(d4 + (g >> 2));
-            atomicAdd(s_h + (w & 255u), 1u);
-            atomicAdd(s_h + ((w >> 8) & 255u), 1u);
-            atomicAdd(s_h + ((w >> 16) & 255u), 1u);
-            atomicAdd(s_h + (w >> 24), 1u);
+        const uint64_t base = static_cast<uint64_t>(g) * kUpGroup * tile_rows;
+        const uint32_t span = static_cast<uint32_t>(min(static_cast<uint64_t>(kUpGroup) * tile_rows,
+                                                        static_cast<uint64_t>(a.n) - base));
+        const uint32_t span16 = span & ~15u;
+#pragma unroll 2
+        for (uint32_t r = 16u * threadIdx.x; r < span16; r += 16u * kBlock) {
+            const uint4 w = __ldcs(d16 + ((base + r) >> 4));
+            uint32_t* h = s_h + (r / tile_rows) * 256u;  // the 16 rows share a tile
+            const uint32_t q[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                atomicAdd(h + (q[k] & 255u), 1u);
+                atomicAdd(h + ((q[k] >> 8) & 255u), 1u);
+                atomicAdd(h + ((q[k] >> 16) & 255u), 1u);
+                atomicAdd(h + (q[k] >> 24), 1u);
+            }
         }
-        for (uint64_t g = end4 + threadIdx.x; g < end; g += kBlock) atomicAdd(s_h + a.digits[g], 1u);
+        for (uint32_t r = span16 + threadIdx.x; r < span; r += kBlock)
+            atomicAdd(s_h + (r / tile_rows) * 256u + a.digits[base + r], 1u);
         __syncthreads();
-        a.counts[static_cast<size_t>(threadIdx.x) * a.ntiles + t] = s_h[threadIdx.x];
+        const uint32_t d = threadIdx.x;
+        uint4* dst = reinterpret_cast<uint4*>(a.counts + static_cast<size_t>(d) * a.cstride + g * kUpGroup);
+        dst[0] = make_uint4(s_h[d], s_h[256 + d], s_h[512 + d], s_h[768 + d]);
+        dst[1] = make_uint4(s_h[1024 + d], s_h[1280 + d], s_h[1536 + d], s_h[1792 + d]);
         __syncthreads();
     }
 }
@@ -350,7 +381,7 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t ti
 __global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a) {
     if (*a.status || !pk_pass_active(a)) return;
     __shared__ uint32_t s_warp[32];
-    uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.ntiles;
+    uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.cstride;
     uint32_t carry = 0;
     for (uint32_t c0 = 0; c0 < a.ntiles; c0 += 4096u) {
         const uint32_t i = c0 + 4u * threadIdx.x;
@@ -420,7 +451,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const int rank_mode = choose_rank(tot_d, a.rank_force);
     uint32_t dummy;
     const uint32_t run_base = block_exclusive_scan<kWarps>(tot_d, s_warp, dummy) +
-                              a.counts[static_cast<size_t>(tid) * a.ntiles + tile];
+                              a.counts[static_cast<size_t>(tid) * a.cstride + tile];
     for (int i = tid; i < kWarps * 256; i += kBlock) {
         s_whist[i] = 0u;
         if (rank_mode == kRankAtomic) s_wmask[i] = 0u;
