@@ -93,6 +93,7 @@ struct Layout {
     size_t tile_counts;
     size_t pk_counts, pk_totals;  // packed passes: [256][ntiles_pk] tile counts / column scans, [256] totals
     size_t pk_digits;             // packed passes: [V] digit byte of the current pass per row
+    size_t ukeys;                 // packed key of every unique row (K3' -> unpack)
     size_t total;
 };
 
@@ -122,6 +123,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.pk_counts = take(static_cast<size_t>(L.pk_cstride) * 256 * 4);
     L.pk_totals = take(256 * 4);
     L.pk_digits = take(static_cast<size_t>(V) + 16);
+    L.ukeys = take(static_cast<size_t>(V) * 8);
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
@@ -280,24 +282,33 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     }
 }
 
-template <int D_CT>
-int launch_unique_pk_d(const UniquePkArgs& a, cudaStream_t s) {
+int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
     const size_t smem = UniquePkTraits<kPkUniqIpt>::smem_bytes();
     int grid = 0;
-    int rc = persistent_grid(k_unique_pk<kPkUniqIpt, D_CT>, smem, a.ntiles, grid);
+    int rc = persistent_grid(k_unique_pk<kPkUniqIpt>, smem, a.ntiles, grid);
     if (rc) return rc;
-    k_unique_pk<kPkUniqIpt, D_CT><<<grid, kBlock, smem, s>>>(a);
+    k_unique_pk<kPkUniqIpt><<<grid, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
 
-int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
+template <int D_CT>
+int launch_unpack_pk_d(const UnpackPkArgs& a, uint64_t max_rows, cudaStream_t s) {
+    int grid = 0;
+    int rc = grid_for_stream(max_rows, grid);
+    if (rc) return rc;
+    k_unpack_pk<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int launch_unpack_pk(const UnpackPkArgs& a, uint64_t max_rows, cudaStream_t s) {
     switch (a.dim) {
-        case 1: return launch_unique_pk_d<1>(a, s);
-        case 2: return launch_unique_pk_d<2>(a, s);
-        case 3: return launch_unique_pk_d<3>(a, s);
-        case 4: return launch_unique_pk_d<4>(a, s);
-        default: return launch_unique_pk_d<0>(a, s);
+        case 1: return launch_unpack_pk_d<1>(a, max_rows, s);
+        case 2: return launch_unpack_pk_d<2>(a, max_rows, s);
+        case 3: return launch_unpack_pk_d<3>(a, max_rows, s);
+        case 4: return launch_unpack_pk_d<4>(a, max_rows, s);
+        default: return launch_unpack_pk_d<0>(a, max_rows, s);
     }
 }
 
@@ -490,10 +501,14 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         k_tile_scan<<<1, 1024, 0, s>>>(counts, L.ntiles3_pk, plan, L.D, reinterpret_cast<unsigned long long*>(d_count),
                                        d_status);
         RMX_CHECK(cudaGetLastError());
-        UniquePkArgs a{rows0, rows1, L.vals_off, plan, vtx, idx, vary, counts, fill, d_status, out_vtx,
+        void* ukeys = base + L.ukeys;
+        UniquePkArgs a{rows0, rows1, L.vals_off, plan, counts, fill, d_status, ukeys,
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
                        sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
         if ((rc = launch_unique_pk(a, s))) return rc;
+        UnpackPkArgs u{plan, vtx, idx, vary, ukeys, out_vtx, reinterpret_cast<unsigned long long*>(d_count), d_status,
+                       L.D};
+        if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
     {
@@ -561,8 +576,8 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
 int rmx_kernel_launches(uint32_t dim) {
     // mark, vary, plan, build_rows, first_hist, 4*dim AoS passes, pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
-    // head_count + tile_scan + unique_pk, map_fill, remap
-    return 5 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 3 + 2;
+    // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
+    return 5 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
 }
 
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }

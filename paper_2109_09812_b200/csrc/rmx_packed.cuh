@@ -615,13 +615,10 @@ struct UniquePkArgs {
     uint32_t* buf1;
     size_t vals_off;
     const uint32_t* plan;
-    const uint32_t* vtx;    // replacement key source (vtx[idx[0]])
-    const uint32_t* idx;
-    const uint32_t* vary;
     const uint32_t* prefix; // [ntiles] exclusive head counts
     uint32_t* fill;         // [256]
     const uint32_t* status;
-    uint32_t* out_vtx;
+    void* ukeys;            // [U] packed key of every unique row (unpacked by k_unpack_pk)
     uint32_t* sc_org;
     uint8_t* sc_nodup;
     uint32_t* sc_new;
@@ -636,17 +633,14 @@ template <int IPT>
 struct UniquePkTraits {
     static constexpr int kTile = kBlock * IPT;
     static __host__ __device__ size_t smem_bytes() {
-        return static_cast<size_t>(kTile) * (8 + 4 + 8) +
-               (4 * kMaxRuns + 3 * RMX_MAX_DIM + 3 * 256 + 2 * kWarps + 8 + 4) * 4 + 16;
+        return static_cast<size_t>(kTile) * (8 + 4 + 8) + (3 * 256 + 2 * kWarps + 8 + 4) * 4 + 16;
     }
 };
 
-template <int KW, int IPT, int D_CT>
+template <int KW, int IPT>
 __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* smem) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
-    const int D = a.dim;
-    const uint32_t* pk = a.plan + pk_base(4 * D);
     const uint32_t fin = a.plan[0];
     const uint32_t* fb = fin ? a.buf1 : a.buf0;
     const Key* __restrict__ keys = reinterpret_cast<const Key*>(fb);
@@ -656,11 +650,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     Key* s_keys = reinterpret_cast<Key*>(smem);
     uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;
     uint2* s_pairs = reinterpret_cast<uint2*>(s_vals + TILE);
-    uint32_t* s_runs = reinterpret_cast<uint32_t*>(s_pairs + TILE);
-    uint32_t* s_const = s_runs + 4 * kMaxRuns;   // replacement bits outside the varying mask
-    uint32_t* s_rbeg = s_const + RMX_MAX_DIM;    // run range of each component
-    uint32_t* s_rend = s_rbeg + RMX_MAX_DIM;
-    uint32_t* s_bcnt = s_rend + RMX_MAX_DIM;
+    uint32_t* s_bcnt = reinterpret_cast<uint32_t*>(s_pairs + TILE);
     uint32_t* s_bcur = s_bcnt + 256;
     uint32_t* s_bglob = s_bcur + 256;
     uint32_t* s_warp = s_bglob + 256;
@@ -674,19 +664,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
         mbar_init(s_bar, 1);
         fence_mbar_init();
     }
-    const uint32_t nruns = pk[4];
-    for (uint32_t i = tid; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
-    if (tid < static_cast<uint32_t>(D)) {
-        s_const[tid] = a.vtx[static_cast<size_t>(a.idx[0]) * D + tid] & ~a.vary[tid];
-        uint32_t b = nruns, e = 0;
-        for (uint32_t r = 0; r < nruns; ++r)
-            if (pk[8 + 4 * r] == tid) {
-                b = min(b, r);
-                e = r + 1;
-            }
-        s_rbeg[tid] = b < e ? b : 0u;
-        s_rend[tid] = e;
-    }
+    Key* __restrict__ ukeys = static_cast<Key*>(a.ukeys);
     // static tile striding: no cross-tile dependency remains (prefixes come from k_tile_scan).
     // The staging buffers are free once phase 1 has moved a tile into registers, so the
     // next tile's bulk copy is issued there and overlaps phase 2 and the pair write-out.
@@ -701,6 +679,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {
     const uint32_t base = tile * static_cast<uint32_t>(TILE);
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
+    const uint32_t tile_prefix = a.prefix[tile];  // consumed in phase 2: the load overlaps phase 1
     s_bcnt[tid] = 0u;
     __syncthreads();
     mbar_wait(s_bar, it & 1u);
@@ -738,17 +717,19 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     uint32_t wexcl = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) wexcl += (static_cast<uint32_t>(w) < warp) ? s_warp[w] : 0u;
+    // bucket space of this tile's pairs: the reservation's round trip overlaps phase 2
+    const uint32_t bcnt = s_bcnt[tid];
+    uint32_t bstart, bfill = 0u;
     {
-        const uint32_t cnt = s_bcnt[tid];
         uint32_t tot;
-        const uint32_t start = block_exclusive_scan<kWarps>(cnt, s_warp + kWarps, tot);
-        s_bcur[tid] = start;
-        if (cnt) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, cnt) - start;
+        bstart = block_exclusive_scan<kWarps>(bcnt, s_warp + kWarps, tot);
+        s_bcur[tid] = bstart;
+        if (bcnt) bfill = atomicAdd(a.fill + tid, bcnt);
     }
     __syncthreads();
 
     // ---- phase 2: new index per slot, bucketed pairs, unique rows out
-    uint32_t running = a.prefix[tile] + wexcl;
+    uint32_t running = tile_prefix + wexcl;
 #pragma unroll
     for (int r = 0; r < IPT; ++r) {
         const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
@@ -757,8 +738,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
             const uint32_t org = vreg[r];
             s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
             const bool head = (bal[r] >> lane) & 1u;
-            if (head) unpack_row<D_CT>(static_cast<uint64_t>(kreg[r]), a.out_vtx + static_cast<size_t>(nidx) * D, D,
-                                       s_const, s_runs, nruns, s_rbeg, s_rend);
+            if (head) ukeys[nidx] = kreg[r];
             if (a.sc_org) a.sc_org[base + p] = org;
             if (a.sc_nodup) a.sc_nodup[base + p] = head ? 1 : 0;
             if (a.sc_new) a.sc_new[base + p] = nidx;
@@ -766,6 +746,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
         }
         running += __popc(bal[r]);
     }
+    if (bcnt) s_bglob[tid] = (tid << bs) + bfill - bstart;
     __syncthreads();
     // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
@@ -776,14 +757,64 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     }
 }
 
-template <int IPT, int D_CT>
+template <int IPT>
 __global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
     extern __shared__ __align__(128) uint32_t smem[];
-    if (pk[1] == 2u) unique_pk_body<2, IPT, D_CT>(a, smem);
-    else unique_pk_body<1, IPT, D_CT>(a, smem);
+    if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
+    else unique_pk_body<1, IPT>(a, smem);
+}
+
+// Unique rows out: packed key -> D words (dense, one row per thread; the
+// unique kernel only stores the packed key of each head).
+struct UnpackPkArgs {
+    const uint32_t* plan;
+    const uint32_t* vtx;    // replacement key source (vtx[idx[0]])
+    const uint32_t* idx;
+    const uint32_t* vary;
+    const void* ukeys;
+    uint32_t* out_vtx;
+    const unsigned long long* count;
+    const uint32_t* status;
+    int dim;
+};
+
+template <int D_CT>
+__global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
+    if (*a.status) return;
+    const int D = D_CT > 0 ? D_CT : a.dim;
+    const uint32_t* pk = a.plan + pk_base(4 * D);
+    if (pk[0] == 0u) return;
+    __shared__ uint32_t s_runs[4 * kMaxRuns];
+    __shared__ uint32_t s_const[RMX_MAX_DIM];  // replacement bits outside the varying mask
+    __shared__ uint32_t s_rbeg[RMX_MAX_DIM];   // run range of each component
+    __shared__ uint32_t s_rend[RMX_MAX_DIM];
+    const uint32_t nruns = pk[4];
+    for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
+    if (threadIdx.x < static_cast<uint32_t>(D)) {
+        const uint32_t c = threadIdx.x;
+        s_const[c] = a.vtx[static_cast<size_t>(a.idx[0]) * D + c] & ~a.vary[c];
+        uint32_t b = nruns, e = 0;
+        for (uint32_t r = 0; r < nruns; ++r)
+            if (pk[8 + 4 * r] == c) {
+                b = min(b, r);
+                e = r + 1;
+            }
+        s_rbeg[c] = b < e ? b : 0u;
+        s_rend[c] = e;
+    }
+    __syncthreads();
+    const uint64_t U = *a.count;
+    const bool wide = pk[1] == 2u;
+    const uint64_t* k64 = static_cast<const uint64_t*>(a.ukeys);
+    const uint32_t* k32 = static_cast<const uint32_t*>(a.ukeys);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < U; i += stride) {
+        const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+        unpack_row<D_CT>(key, a.out_vtx + i * D, D, s_const, s_runs, nruns, s_rbeg, s_rend);
+    }
 }
 
 }  // namespace rmx
