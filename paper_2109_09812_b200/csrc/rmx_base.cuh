@@ -28,11 +28,27 @@ constexpr int kWarps = kBlock / 32;
 //   [0] mode (1 = packed)        [1] key words KW (1 | 2)   [2] varying bits B
 //   [3] packed passes ceil(B/8)  [4] number of runs         [5..7] reserved
 //   [8 + 4r ..] run r: component, source bit, length, destination bit
+//   [8 + 4 kMaxRuns + c] field rank of component c: 0 = none, else
+//                        (1 << 31) | (rank bits << 16) | destination bit
 // Runs are listed from component D-1 (least significant) to component 0,
 // low bits first, so destination bits grow monotonically.
+//
+// Field ranks (D <= kMaxRankDim): the sign+exponent field (bits 23..31) of a
+// float word takes few distinct values in real geometry (coordinates span a few
+// binades) but its varying bits are spread over the whole field.  When
+// ceil(log2(#distinct fields)) < #varying field bits, the field is replaced in
+// the key by its rank among the fields that occur -- monotone and injective on
+// them, so order and equality of the words are unchanged -- and the mantissa
+// bits keep their runs.  K1a records the occurring fields in a 512-bit set per
+// component; pack / unpack build rank / inverse tables from it.
 constexpr int kMaxRuns = 64;
 constexpr int kMaxPackedPasses = 8;
+constexpr int kFieldLo = 23;            // sign + exponent = bits 23..31
+constexpr int kFieldValues = 512;
+constexpr int kFieldWords = kFieldValues / 32;
+constexpr int kMaxRankDim = 4;
 __host__ __device__ inline size_t pk_base(int P) { return 4 + 3 * static_cast<size_t>(P); }
-__host__ __device__ inline size_t plan_words(int P) { return pk_base(P) + 8 + 4 * kMaxRuns; }
+__host__ __device__ inline size_t pk_rank_base(int P) { return pk_base(P) + 8 + 4 * kMaxRuns; }
+__host__ __device__ inline size_t plan_words(int P) { return pk_rank_base(P) + RMX_MAX_DIM; }
 
 }  // namespace rmx

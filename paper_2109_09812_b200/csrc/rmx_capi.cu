@@ -86,7 +86,7 @@ struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, hist, vary, fill, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, hist, vary, fields, fill, counters, desc, desc3, ctl_end;
     int bucket_shift;
     uint32_t ntiles_pk, ntiles3_pk, pk_cstride;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
@@ -127,6 +127,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.ctl_begin = off;
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
+    L.fields = take(static_cast<size_t>(L.D) * kFieldWords * 4);
     L.fill = take(256 * 4);
     int bits = 0;
     while (bits < 40 && (1ull << bits) < V) ++bits;
@@ -415,6 +416,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint32_t* plan = reinterpret_cast<uint32_t*>(base + L.plan);
     uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
     uint32_t* vary = reinterpret_cast<uint32_t*>(base + L.vary);
+    uint32_t* fields = reinterpret_cast<uint32_t*>(base + L.fields);
     uint32_t* counters = reinterpret_cast<uint32_t*>(base + L.counters);
     uint64_t* desc = reinterpret_cast<uint64_t*>(base + L.desc);
     uint64_t* desc3 = reinterpret_cast<uint64_t*>(base + L.desc3);
@@ -438,11 +440,11 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // K1a varying bits of the cleaned vertex set, then the plan (packed or AoS)
     const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
     {
-        VaryArgs a{vtx, flags, idx, vary, d_status, static_cast<uint32_t>(V), L.D, vec};
+        VaryArgs a{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    k_plan<<<1, 32, 0, s>>>(vary, plan, L.D, d_status);
+    k_plan<<<1, 32, 0, s>>>(vary, fields, plan, L.D, d_status);
     RMX_CHECK(cudaGetLastError());
     if ((rc = rec.mark())) return rc;
     // ---- AoS path (kernels exit at once in packed mode)
@@ -468,8 +470,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     // ---- packed-key path (kernels exit at once in AoS mode)
     {
-        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), d_status,
-                   static_cast<uint32_t>(V), L.D, vec};
+        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), fields,
+                   d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
@@ -506,8 +508,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
                        sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
         if ((rc = launch_unique_pk(a, s))) return rc;
-        UnpackPkArgs u{plan, vtx, idx, vary, ukeys, out_vtx, reinterpret_cast<unsigned long long*>(d_count), d_status,
-                       L.D};
+        UnpackPkArgs u{plan, vtx, idx, vary, fields, ukeys, out_vtx, reinterpret_cast<unsigned long long*>(d_count),
+                       d_status, L.D};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;

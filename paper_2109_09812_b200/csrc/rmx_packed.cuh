@@ -50,12 +50,33 @@ __device__ __forceinline__ uint64_t shfl_up_key(uint64_t k) {
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
+// Field-rank tables (rmx_base.cuh) built in shared memory from the K1a field
+// sets: rank of every occurring field (pack) or field of every rank (unpack).
+__device__ __forceinline__ uint32_t field_rank(const uint32_t* set, uint32_t v) {
+    uint32_t r = 0;
+    for (uint32_t w = 0; w < (v >> 5); ++w) r += __popc(set[w]);
+    return r + __popc(set[v >> 5] & ((1u << (v & 31u)) - 1u));
+}
+
+__device__ __forceinline__ void build_field_tables(const uint32_t* fields, const uint32_t* rk, int D, uint16_t* s_rank,
+                                                   uint16_t* s_value) {
+    for (int c = 0; c < D; ++c) {
+        if (!(rk[c] >> 31)) continue;
+        const uint32_t* set = fields + c * kFieldWords;
+        for (uint32_t v = threadIdx.x; v < static_cast<uint32_t>(kFieldValues); v += blockDim.x) {
+            const uint32_t r = field_rank(set, v);
+            if (s_rank) s_rank[c * kFieldValues + v] = static_cast<uint16_t>(r);
+            if (s_value && ((set[v >> 5] >> (v & 31u)) & 1u)) s_value[c * kFieldValues + r] = static_cast<uint16_t>(v);
+        }
+    }
+}
+
 // Packed key -> D words: replacement bits outside the varying mask, varying
-// bits deposited back from their runs (inverse of k_pack).
+// bits deposited back from their runs, ranked fields looked up (inverse of k_pack).
 template <int D_CT>
 __device__ __forceinline__ void unpack_row(uint64_t key, uint32_t* dst, int D, const uint32_t* s_const,
                                            const uint32_t* s_runs, uint32_t nruns, const uint32_t* s_rbeg,
-                                           const uint32_t* s_rend) {
+                                           const uint32_t* s_rend, const uint32_t* s_rk, const uint16_t* s_value) {
     if constexpr (D_CT > 0) {
         uint32_t w[D_CT];
 #pragma unroll
@@ -65,6 +86,16 @@ __device__ __forceinline__ void unpack_row(uint64_t key, uint32_t* dst, int D, c
             const uint32_t bits = (static_cast<uint32_t>(key >> ru[3]) & low_mask(ru[2])) << ru[1];
 #pragma unroll
             for (int c = 0; c < D_CT; ++c) w[c] |= (ru[0] == static_cast<uint32_t>(c)) ? bits : 0u;
+        }
+        if constexpr (D_CT <= kMaxRankDim) {
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) {
+                const uint32_t rk = s_rk[c];
+                if (rk >> 31) {
+                    const uint32_t r = static_cast<uint32_t>(key >> (rk & 0xFFFFu)) & low_mask((rk >> 16) & 0xFFu);
+                    w[c] |= static_cast<uint32_t>(s_value[c * kFieldValues + r]) << kFieldLo;
+                }
+            }
         }
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) dst[c] = w[c];
@@ -87,10 +118,46 @@ struct VaryArgs {
     const uint8_t* flags;
     const uint32_t* idx;
     uint32_t* vary;  // [D]
+    uint32_t* fields;  // [D][kFieldWords] set of occurring sign+exponent fields (D <= kMaxRankDim)
     const uint32_t* status;
     uint32_t n;
     int dim;
     int vec;  // vtx and flags 16-byte aligned
+};
+
+// Occurring sign+exponent fields of one component: a per-thread window of 32
+// exponents around the replacement row's (one register per sign) catches
+// real geometry; anything outside goes to the block's shared set.
+struct FieldSet {
+    uint32_t win[2];
+    uint32_t lo;  // first exponent of the window
+    __device__ __forceinline__ void init(uint32_t ref_word) {
+        win[0] = win[1] = 0u;
+        const uint32_t e = (ref_word >> kFieldLo) & 255u;
+        lo = e > 16u ? min(e - 16u, 224u) : 0u;
+    }
+    __device__ __forceinline__ void add(uint32_t word, uint32_t* s_set) {
+        const uint32_t f = word >> kFieldLo;
+        const uint32_t x = (f & 255u) - lo;
+        if (x < 32u) {
+            if (f >> 8) win[1] |= 1u << x;
+            else win[0] |= 1u << x;
+        } else {
+            atomicOr(s_set + (f >> 5), 1u << (f & 31u));
+        }
+    }
+    // OR this thread's windows into the shared set (words may straddle)
+    __device__ __forceinline__ void flush(uint32_t* s_set) const {
+#pragma unroll
+        for (int sg = 0; sg < 2; ++sg) {
+            const uint32_t w = win[sg];
+            if (!w) continue;
+            const uint32_t f0 = (static_cast<uint32_t>(sg) << 8) + lo;  // field of bit 0
+            const uint32_t sh = f0 & 31u;
+            atomicOr(s_set + (f0 >> 5), w << sh);
+            if (sh) atomicOr(s_set + (f0 >> 5) + 1, w >> (32u - sh));
+        }
+    }
 };
 
 template <int D_CT>
@@ -101,12 +168,24 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     if constexpr (D_CT > 0) {
+        constexpr int kSets = D_CT <= kMaxRankDim ? D_CT : 1;
+        __shared__ uint32_t s_fields[kSets * kFieldWords];
         uint32_t ref[D_CT], vor[D_CT];
+        FieldSet fs[kSets];
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) {
             ref[c] = __ldg(repl + c);
             vor[c] = 0u;
+            if (c < kSets) fs[c].init(ref[c]);
         }
+        for (uint32_t i = threadIdx.x; i < kSets * kFieldWords; i += kBlock) s_fields[i] = 0u;
+        __syncthreads();
+        auto note = [&](const uint32_t* k) {
+            if constexpr (D_CT <= kMaxRankDim) {
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) fs[c].add(k[c], s_fields + c * kFieldWords);
+            }
+        };
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
             if (a.vec) {
@@ -122,6 +201,7 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
                         if ((f >> (8 * j)) & 255u) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) vor[c] |= k[j][c] ^ ref[c];
+                            note(k[j]);
                         }
                     }
                 }
@@ -130,14 +210,26 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
         }
         for (uint64_t i = done + start; i < a.n; i += stride) {
             if (a.flags[i]) {
+                uint32_t k[D_CT];
 #pragma unroll
-                for (int c = 0; c < D_CT; ++c) vor[c] |= __ldg(a.vtx + i * D_CT + c) ^ ref[c];
+                for (int c = 0; c < D_CT; ++c) {
+                    k[c] = __ldg(a.vtx + i * D_CT + c);
+                    vor[c] |= k[c] ^ ref[c];
+                }
+                note(k);
             }
         }
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) {
             const uint32_t v = __reduce_or_sync(kFull, vor[c]);
             if ((threadIdx.x & 31u) == 0u && v) atomicOr(a.vary + c, v);
+        }
+        if constexpr (D_CT <= kMaxRankDim) {
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) fs[c].flush(s_fields + c * kFieldWords);
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < D_CT * kFieldWords; i += kBlock)
+                if (s_fields[i]) atomicOr(a.fields + i, s_fields[i]);
         }
     } else {
         __shared__ uint32_t s_vary[RMX_MAX_DIM];
@@ -162,11 +254,15 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
 template <int D_CT>
 struct RowPacker {
     static constexpr int kRegRuns = 4;
+    static constexpr int kRanked = D_CT <= kMaxRankDim ? D_CT : 0;
     uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
+    uint32_t fd[kRanked > 0 ? kRanked : 1];  // destination bit of a ranked field, 64 = none
     const uint32_t* s_runs;
+    const uint16_t* s_rank;                  // [D_CT][kFieldValues]
     uint32_t nruns;
 
-    __device__ __forceinline__ RowPacker(const uint32_t* runs, uint32_t n) : s_runs(runs), nruns(n) {
+    __device__ __forceinline__ RowPacker(const uint32_t* runs, uint32_t n, const uint32_t* rk, const uint16_t* ranks)
+        : s_runs(runs), s_rank(ranks), nruns(n) {
 #pragma unroll
         for (int r = 0; r < kRegRuns; ++r) {
             const bool on = static_cast<uint32_t>(r) < n;
@@ -175,6 +271,8 @@ struct RowPacker {
             rm[r] = on ? low_mask(runs[4 * r + 2]) : 0u;
             rd[r] = on ? runs[4 * r + 3] : 0u;
         }
+#pragma unroll
+        for (int c = 0; c < kRanked; ++c) fd[c] = (rk[c] >> 31) ? (rk[c] & 0xFFFFu) : 64u;
     }
 
     __device__ __forceinline__ uint64_t operator()(const uint32_t (&k)[D_CT]) const {
@@ -186,6 +284,9 @@ struct RowPacker {
             const uint32_t* ru = s_runs + 4 * r;
             key |= static_cast<uint64_t>((pick<D_CT>(k, ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
         }
+#pragma unroll
+        for (int c = 0; c < kRanked; ++c)
+            if (fd[c] < 64u) key |= static_cast<uint64_t>(s_rank[c * kFieldValues + (k[c] >> kFieldLo)]) << fd[c];
         return key;
     }
 };
@@ -200,6 +301,7 @@ struct PackArgs {
     uint32_t* buf0;   // keys at word 0, origins at word vals_off
     size_t vals_off;  // words
     uint8_t* digits;  // [n] packed digit 0 per row (read by the first upsweep)
+    const uint32_t* fields;  // [D][kFieldWords] occurring sign+exponent fields (K1a)
     const uint32_t* status;
     uint32_t n;
     int dim;
@@ -211,10 +313,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
+    constexpr int kLut = (D_CT > 0 && D_CT <= kMaxRankDim) ? D_CT * kFieldValues : 1;
+    __shared__ uint16_t s_rank[kLut];
     if (*a.status || pk[0] == 0u) return;  // uniform
     const uint32_t nruns = pk[4];
     const bool wide = pk[1] == 2u;
+    const uint32_t* rk = a.plan + pk_rank_base(4 * D);
     for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
+    if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(a.fields, rk, D_CT, s_rank, nullptr);
     __syncthreads();
 
     const uint32_t r0 = a.idx[0];
@@ -236,7 +342,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
         uint32_t ref[D_CT];
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
-        const RowPacker<D_CT> pack(s_runs, nruns);
+        const RowPacker<D_CT> pack(s_runs, nruns, rk, s_rank);
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
             if (a.vec) {
@@ -774,6 +880,7 @@ struct UnpackPkArgs {
     const uint32_t* vtx;    // replacement key source (vtx[idx[0]])
     const uint32_t* idx;
     const uint32_t* vary;
+    const uint32_t* fields;
     const void* ukeys;
     uint32_t* out_vtx;
     const unsigned long long* count;
@@ -791,11 +898,19 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
     __shared__ uint32_t s_const[RMX_MAX_DIM];  // replacement bits outside the varying mask
     __shared__ uint32_t s_rbeg[RMX_MAX_DIM];   // run range of each component
     __shared__ uint32_t s_rend[RMX_MAX_DIM];
+    __shared__ uint32_t s_rk[RMX_MAX_DIM];
+    constexpr int kLut = (D_CT > 0 && D_CT <= kMaxRankDim) ? D_CT * kFieldValues : 1;
+    __shared__ uint16_t s_value[kLut];
     const uint32_t nruns = pk[4];
+    const uint32_t* rk = a.plan + pk_rank_base(4 * D);
     for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
+    if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(a.fields, rk, D_CT, nullptr, s_value);
     if (threadIdx.x < static_cast<uint32_t>(D)) {
         const uint32_t c = threadIdx.x;
-        s_const[c] = a.vtx[static_cast<size_t>(a.idx[0]) * D + c] & ~a.vary[c];
+        s_rk[c] = rk[c];
+        // a ranked field comes back from the value table, not from the replacement row
+        const uint32_t keep = (rk[c] >> 31) ? ~(a.vary[c] | ~((1u << kFieldLo) - 1u)) : ~a.vary[c];
+        s_const[c] = a.vtx[static_cast<size_t>(a.idx[0]) * D + c] & keep;
         uint32_t b = nruns, e = 0;
         for (uint32_t r = 0; r < nruns; ++r)
             if (pk[8 + 4 * r] == c) {
@@ -813,7 +928,7 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < U; i += stride) {
         const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
-        unpack_row<D_CT>(key, a.out_vtx + i * D, D, s_const, s_runs, nruns, s_rbeg, s_rend);
+        unpack_row<D_CT>(key, a.out_vtx + i * D, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
     }
 }
 

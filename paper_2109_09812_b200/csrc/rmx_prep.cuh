@@ -165,14 +165,26 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
 //    key is compacted to a u32/u64 and sorted in ceil(B/8) passes; and
 //  * AoS mode -- a byte pass executes iff its digit is not constant over all
 //    keys; passes chain to the next executed one, buffers ping-pong.
-__global__ void k_plan(const uint32_t* vary, uint32_t* plan, int D, const uint32_t* status) {
+__global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status) {
     if (*status || threadIdx.x != 0) return;
     const int P = 4 * D;
     uint32_t* pk = plan + pk_base(P);
+    uint32_t* rk = plan + pk_rank_base(P);
     uint32_t bits = 0, runs = 0;
     bool fits = true;
     for (int c = D - 1; c >= 0 && fits; --c) {
         uint32_t m = vary[c];
+        // field rank (see rmx_base.cuh) when it needs fewer bits than the varying field bits
+        uint32_t rank_bits = 0;
+        bool ranked = false;
+        if (D <= kMaxRankDim) {
+            uint32_t distinct = 0;
+            for (int w = 0; w < kFieldWords; ++w) distinct += __popc(fields[c * kFieldWords + w]);
+            while ((1u << rank_bits) < distinct) ++rank_bits;
+            ranked = rank_bits < static_cast<uint32_t>(__popc(m >> kFieldLo));
+        }
+        rk[c] = 0u;
+        if (ranked) m &= (1u << kFieldLo) - 1u;
         while (m) {
             const uint32_t lo = __ffs(m) - 1u;
             const uint32_t len = __ffs(~(m >> lo)) ? __ffs(~(m >> lo)) - 1u : 32u - lo;
@@ -187,6 +199,14 @@ __global__ void k_plan(const uint32_t* vary, uint32_t* plan, int D, const uint32
             ++runs;
             bits += len;
             m = len >= 32u ? 0u : (m & ~(((1u << len) - 1u) << lo));
+        }
+        if (ranked && fits) {
+            if (bits + rank_bits > 64u) {
+                fits = false;
+            } else {
+                rk[c] = (1u << 31) | (rank_bits << 16) | bits;
+                bits += rank_bits;
+            }
         }
     }
     if (fits) {
