@@ -1,0 +1,69 @@
+"""profiles/traffic.json from an ncu launch list of one C2 step.
+
+    ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+        --clock-control none --csv --log-file gpurun_out/launches.csv \
+        python tools/profile_step.py --config C2 --steps 1
+    python tools/traffic.py gpurun_out/launches.csv C2 <executed packed passes> <V> <key words>
+
+Per executed packed pass: DRAM bytes of upsweep + colscan + downsweep, averaged
+over the executed passes (launches whose downsweep moved data).
+"""
+import csv
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def load(path):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ix = {h: i for i, h in enumerate(hdr)}
+    agg, order = {}, []
+    for r in rows[start + 1:]:
+        if len(r) < len(hdr):
+            continue
+        k = (int(r[ix["ID"]]), r[ix["Kernel Name"]])
+        if k not in agg:
+            agg[k] = {}
+            order.append(k)
+        agg[k][r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "") or 0)
+    return [(k[1], agg[k]) for k in order]
+
+
+def main():
+    path, cfg, npass, V, kw = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+    launches = load(path)
+    per_pass = []
+    cur = 0.0
+    for name, m in launches:
+        b = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+        if "k_pk_upsweep" in name:
+            cur = b
+        elif "k_pk_colscan" in name:
+            cur += b
+        elif "k_pk_downsweep" in name:
+            cur += b
+            per_pass.append(cur)
+    executed = per_pass[:npass]
+    algo = (2 * (4 * kw + 4) + 2) * V
+    out_path = os.path.join(ROOT, "profiles", "traffic.json")
+    data = json.load(open(out_path)) if os.path.exists(out_path) else {}
+    data[cfg] = {
+        "pass_dram_bytes_per_launch": sum(executed) / len(executed),
+        "algorithmic_bytes_per_launch": algo,
+        "executed_passes": npass,
+        "source": f"{os.path.basename(path)} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, one step of "
+                  f"tools/profile_step.py --config {cfg}), mean over the executed packed passes of "
+                  "upsweep + colscan + downsweep",
+        "note": "algorithmic = keys + origins read and written (2 x (4 KW + 4) B/row) + the next-digit byte "
+                "written by the downsweep and read by the next upsweep (2 B/row)",
+    }
+    json.dump(data, open(out_path, "w"), indent=1)
+    print(json.dumps(data[cfg], indent=1))
+
+
+if __name__ == "__main__":
+    main()
