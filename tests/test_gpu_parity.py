@@ -204,6 +204,23 @@ def test_full_size_configs(rmx, cfg):
     torch.cuda.empty_cache()
 
 
+def test_c5_shard_full_size(rmx):
+    """One GPU's shard of C5 at 8 GPUs (first 1/8 of the 1B-triangle soup, 393.75M vertex slots):
+    index arithmetic past 2^28 rows, 128K+ tiles per pass, output determined by properties."""
+    import torch
+    from paper_2109_09812_b200 import gen
+    kind, cells = lattice.CONFIGS["C5"]
+    E_all, _ = gen.lattice_sizes(kind, cells)
+    vtx, idx = gen.lattice_soup_tensors(kind, cells, seed=0, n_elem_take=E_all // 8)
+    assert vtx.shape[0] == 393_750_000
+    res = rmx.reindex_tensors(vtx, idx)
+    U = res.vertices.shape[0]
+    assert 0 < U < vtx.shape[0]
+    check_determining_properties(vtx, idx, res.vertices, res.elements, U)
+    del res, vtx, idx
+    torch.cuda.empty_cache()
+
+
 def test_native_library_is_the_loaded_code(rmx):
     rmx.reindex(rmx.Mesh(np.zeros((2, 2), np.float32), np.array([(0, 1)], np.uint32)))
     maps = open("/proc/self/maps").read()
