@@ -103,6 +103,28 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
                          const rmx_scratch* scratch, void* stream,
                          void* const* events, int n_events);
 
+/*
+ * Graph launch path: the whole rmx_reindex call for these exact buffers and
+ * sizes, captured once into a CUDA graph.  The sections that only some inputs
+ * need (AoS rows vs packed keys, every sort pass) are IF conditional nodes the
+ * plan kernel switches on the device, so no kernel of a path not taken is
+ * launched.  Replaces repeated rmx_reindex calls on fixed buffers (the
+ * reference's bench loop, pkg/src/remeshx/bench.py:71-94, calls reindex on the
+ * same mesh repeatedly); results are identical to rmx_reindex.
+ *   rmx_graph_create   builds and instantiates (host-side, no stream work);
+ *   rmx_graph_launch   enqueues one re-index on `stream`;
+ *   rmx_graph_destroy  frees it.
+ */
+typedef struct rmx_graph rmx_graph;
+int rmx_graph_create(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim,
+                     const uint32_t* idx, uint64_t n_elements, uint32_t arity,
+                     uint32_t* out_vtx_bits, uint32_t* out_idx,
+                     uint64_t* d_new_count, uint32_t* d_status,
+                     void* workspace, size_t workspace_bytes,
+                     const rmx_scratch* scratch, rmx_graph** out);
+int rmx_graph_launch(rmx_graph* graph, void* stream);
+void rmx_graph_destroy(rmx_graph* graph);
+
 /* Number of stage-boundary events rmx_reindex_profiled records for `dim`, and
  * the name of the kernel that runs between event k-1 and event k. */
 int rmx_stage_count(uint32_t dim);

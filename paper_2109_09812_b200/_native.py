@@ -28,6 +28,7 @@ EXPORTS = (
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches",
     "rmx_last_executed_passes", "rmx_plan_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
+    "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy",
 )
 
 
@@ -70,6 +71,10 @@ _SIGNATURES = {
     "rmx_gen_grid_quads": (_int, [_u32, _vp, _vp, _vp]),
     "rmx_gather_u32": (_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
     "rmx_lower_bound_rows": (_int, [_vp, _u64, _u32, _vp, _u64, _vp, _vp]),
+    "rmx_graph_create": (_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _sz,
+                                ctypes.POINTER(Scratch), ctypes.POINTER(_vp)]),
+    "rmx_graph_launch": (_int, [_vp, _vp]),
+    "rmx_graph_destroy": (None, [_vp]),
 }
 
 

@@ -368,9 +368,54 @@ struct Recorder {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// ---- graph launch path ------------------------------------------------------
+// run_pipeline emits its launches onto a capturing stream; each section that
+// may be a no-op for the data at hand (AoS vs packed, each sort pass) becomes
+// the body of an IF conditional node whose value k_plan sets on the device.
+constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
+
+struct GraphCtx {
+    cudaGraph_t g = nullptr;
+    cudaStream_t s = nullptr;
+    GraphHandles gh{};
+    cudaGraphNode_t cond = nullptr;
+};
+
+// Close the current capture segment and open the body of IF(slot).
+int cond_begin(GraphCtx* gc, int slot) {
+    if (!gc) return RMX_OK;
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    RMX_CHECK(cudaStreamGetCaptureInfo(gc->s, &st, nullptr, nullptr, &deps, &nd));
+    cudaGraphNode_t dv[16];
+    if (nd > 16) return RMX_ECUDA;
+    for (size_t i = 0; i < nd; ++i) dv[i] = deps[i];
+    cudaGraph_t g = nullptr;
+    RMX_CHECK(cudaStreamEndCapture(gc->s, &g));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = gc->gh.h[slot];
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    RMX_CHECK(cudaGraphAddNode(&gc->cond, gc->g, dv, nd, &cp));
+    RMX_CHECK(cudaStreamBeginCaptureToGraph(gc->s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0, kCaptureMode));
+    return RMX_OK;
+}
+
+// Close the IF body and continue the main graph after the conditional node.
+int cond_end(GraphCtx* gc) {
+    if (!gc) return RMX_OK;
+    cudaGraph_t body = nullptr;
+    RMX_CHECK(cudaStreamEndCapture(gc->s, &body));
+    RMX_CHECK(cudaStreamBeginCaptureToGraph(gc->s, gc->g, &gc->cond, nullptr, 1, kCaptureMode));
+    return RMX_OK;
+}
+
 int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* idx, uint64_t E, uint32_t K,
                  uint32_t* out_vtx, uint32_t* out_idx, uint64_t* d_count, uint32_t* d_status, void* ws,
-                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events) {
+                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events,
+                 GraphCtx* gc = nullptr) {
     g_err[0] = '\0';
     if (D < 1 || K < 1) {
         std::snprintf(g_err, sizeof(g_err), "dim and arity must be >= 1 (got %u, %u)", D, K);
@@ -444,10 +489,11 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    k_plan<<<1, 32, 0, s>>>(vary, fields, plan, L.D, d_status);
+    k_plan<<<1, 32, 0, s>>>(vary, fields, plan, L.D, d_status, gc ? gc->gh : GraphHandles{});
     RMX_CHECK(cudaGetLastError());
     if ((rc = rec.mark())) return rc;
     // ---- AoS path (kernels exit at once in packed mode)
+    if ((rc = cond_begin(gc, kSlotAosA))) return rc;
     {
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
@@ -461,29 +507,37 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         k_first_hist<<<grid, kBlock, 0, s>>>(a);
         RMX_CHECK(cudaGetLastError());
     }
+    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
+        if ((rc = cond_begin(gc, kSlotAosPass + p))) return rc;
         SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p,
                    rank_force()};
         if ((rc = dispatch_pass(a, s))) return rc;
+        if ((rc = cond_end(gc))) return rc;
         if ((rc = rec.mark())) return rc;
     }
     // ---- packed-key path (kernels exit at once in AoS mode)
+    if ((rc = cond_begin(gc, kSlotPkA))) return rc;
     {
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), fields,
                    d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
+    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
+        if ((rc = cond_begin(gc, slot_pk_pass(L.P, p)))) return rc;
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), reinterpret_cast<uint8_t*>(base + L.pk_digits),
                      d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride, L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
+        if ((rc = cond_end(gc))) return rc;
         if ((rc = rec.mark())) return rc;
     }
     // ---- K3 unique + bucketed pairs (one of the two runs), K3b map fill
     uint32_t* fill = reinterpret_cast<uint32_t*>(base + L.fill);
+    if ((rc = cond_begin(gc, kSlotAosB))) return rc;
     {
         UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, fill, d_status,
                      out_vtx, reinterpret_cast<unsigned long long*>(d_count),
@@ -491,7 +545,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                      sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D, L.bucket_shift};
         if ((rc = dispatch_unique(a, s))) return rc;
     }
+    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
+    if ((rc = cond_begin(gc, kSlotPkB))) return rc;
     {
         uint32_t* counts = reinterpret_cast<uint32_t*>(base + L.tile_counts);
         HeadCountArgs h{rows0, rows1, plan, counts, d_status, static_cast<uint32_t>(V), L.ntiles3_pk,
@@ -512,6 +568,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        d_status, L.D};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
+    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
     {
         const uint64_t threads = (V + 1) / 2;
@@ -573,6 +630,71 @@ int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t
     return run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
                         d_status, workspace, workspace_bytes, scratch, static_cast<cudaStream_t>(stream), events,
                         n_events);
+}
+
+struct rmx_graph {
+    cudaGraphExec_t exec;
+};
+
+int rmx_graph_create(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,
+                     uint64_t n_elements, uint32_t arity, uint32_t* out_vtx_bits, uint32_t* out_idx,
+                     uint64_t* d_new_count, uint32_t* d_status, void* workspace, size_t workspace_bytes,
+                     const rmx_scratch* scratch, rmx_graph** out) {
+    if (!out) return RMX_EINVAL;
+    *out = nullptr;
+    if (dim < 1 || dim > RMX_MAX_DIM) {
+        std::snprintf(g_err, sizeof(g_err), "dim %u outside [1, %d]", dim, RMX_MAX_DIM);
+        return RMX_EINVAL;
+    }
+    GraphCtx gc;
+    RMX_CHECK(cudaStreamCreateWithFlags(&gc.s, cudaStreamNonBlocking));
+    int rc = RMX_OK;
+    if (cudaGraphCreate(&gc.g, 0) != cudaSuccess) rc = RMX_ECUDA;
+    const int P = 4 * static_cast<int>(dim);
+    gc.gh.n = kSlotAosPass + P + kMaxPackedPasses;
+    for (int i = 0; i < gc.gh.n && rc == RMX_OK; ++i)
+        if (cudaGraphConditionalHandleCreate(&gc.gh.h[i], gc.g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
+            rc = RMX_ECUDA;
+    bool capturing = false;
+    if (rc == RMX_OK) {
+        if (cudaStreamBeginCaptureToGraph(gc.s, gc.g, nullptr, nullptr, 0, kCaptureMode) == cudaSuccess) {
+            capturing = true;
+            rc = run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
+                              d_status, workspace, workspace_bytes, scratch, gc.s, nullptr, 0, &gc);
+        } else {
+            rc = RMX_ECUDA;
+        }
+    }
+    if (capturing) {
+        cudaGraph_t g = nullptr;
+        if (cudaStreamEndCapture(gc.s, &g) != cudaSuccess && rc == RMX_OK) rc = RMX_ECUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (rc == RMX_OK) {
+        const cudaError_t e = cudaGraphInstantiate(&exec, gc.g, 0);
+        if (e != cudaSuccess) {
+            std::snprintf(g_err, sizeof(g_err), "graph instantiate: %s", cudaGetErrorString(e));
+            rc = RMX_ECUDA;
+        }
+    }
+    (void)cudaGetLastError();
+    if (gc.g) cudaGraphDestroy(gc.g);
+    cudaStreamDestroy(gc.s);
+    if (rc != RMX_OK) return rc;
+    *out = new rmx_graph{exec};
+    return RMX_OK;
+}
+
+int rmx_graph_launch(rmx_graph* graph, void* stream) {
+    if (!graph) return RMX_EINVAL;
+    RMX_CHECK(cudaGraphLaunch(graph->exec, static_cast<cudaStream_t>(stream)));
+    return RMX_OK;
+}
+
+void rmx_graph_destroy(rmx_graph* graph) {
+    if (!graph) return;
+    cudaGraphExecDestroy(graph->exec);
+    delete graph;
 }
 
 int rmx_kernel_launches(uint32_t dim) {

@@ -165,8 +165,17 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
 //    key is compacted to a u32/u64 and sorted in ceil(B/8) passes; and
 //  * AoS mode -- a byte pass executes iff its digit is not constant over all
 //    keys; passes chain to the next executed one, buffers ping-pong.
-__global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status) {
-    if (*status || threadIdx.x != 0) return;
+// Conditional-node handles of the graph launch path (rmx_graph_*): k_plan
+// switches on exactly the sections that do work; n = 0 for direct launches
+// (there every kernel checks the plan and exits at once instead).
+enum GraphSlot { kSlotAosA = 0, kSlotAosB = 1, kSlotPkA = 2, kSlotPkB = 3, kSlotAosPass = 4 };
+__host__ __device__ inline int slot_pk_pass(int P, int p) { return kSlotAosPass + P + p; }
+struct GraphHandles {
+    unsigned long long h[kSlotAosPass + 4 * RMX_MAX_DIM + kMaxPackedPasses];
+    int n;
+};
+
+__device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D) {
     const int P = 4 * D;
     uint32_t* pk = plan + pk_base(P);
     uint32_t* rk = plan + pk_rank_base(P);
@@ -247,6 +256,25 @@ __global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* p
     plan[1] = executed;
     plan[2] = first;
     plan[3] = (first < static_cast<uint32_t>(P) && first >= 4u) ? 1u : 0u;  // histogram not made by K1b
+}
+
+__global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status,
+                       GraphHandles gh) {
+    if (*status || threadIdx.x != 0) return;  // graph: every conditional keeps its default 0
+    plan_body(vary, fields, plan, D);
+    if (gh.n) {
+        const int P = 4 * D;
+        const uint32_t* pk = plan + pk_base(P);
+        const bool packed = pk[0] != 0u;
+        cudaGraphSetConditional(gh.h[kSlotAosA], packed ? 0u : 1u);
+        cudaGraphSetConditional(gh.h[kSlotAosB], packed ? 0u : 1u);
+        cudaGraphSetConditional(gh.h[kSlotPkA], packed ? 1u : 0u);
+        cudaGraphSetConditional(gh.h[kSlotPkB], packed ? 1u : 0u);
+        for (int p = 0; p < P; ++p)
+            cudaGraphSetConditional(gh.h[kSlotAosPass + p], (!packed && plan[4 + p]) ? 1u : 0u);
+        for (int p = 0; p < kMaxPackedPasses; ++p)
+            cudaGraphSetConditional(gh.h[slot_pk_pass(P, p)], (packed && static_cast<uint32_t>(p) < pk[3]) ? 1u : 0u);
+    }
 }
 
 // Histogram of the first executed pass when it lies outside component D-1

@@ -103,6 +103,46 @@ def launch(vtx: torch.Tensor, n_vertices: int, dim: int, idx: torch.Tensor, n_el
     _raise_for(rc)
 
 
+class PipelineGraph:
+    """``rmx_reindex`` for fixed buffers and sizes captured once as a CUDA graph.
+
+    Sections a given input does not need (AoS rows vs packed keys, each sort
+    pass) are conditional nodes the plan kernel switches on the device, so
+    a launch runs only the kernels that do work, and the whole pipeline is one
+    host call (for embedding in a caller's graph, or host-bound loops).  The
+    tensors are kept alive by the object; results land in ``out_vtx`` /
+    ``out_idx`` / ``info`` like :func:`launch`.  Measured on B200 the device
+    time equals direct launches within a few percent (C2 8.87 vs 8.94 ms): a
+    skipped conditional node costs about what a no-op kernel did.
+    """
+
+    def __init__(self, vtx, n_vertices, dim, idx, n_elements, arity, out_vtx, out_idx, info, workspace):
+        lib = _native.lib()
+        self._keep = (vtx, idx, out_vtx, out_idx, info, workspace)
+        base = info.data_ptr()
+        h = ctypes.c_void_p()
+        rc = lib.rmx_graph_create(_ptr(vtx), n_vertices, dim, _ptr(idx), n_elements, arity, _ptr(out_vtx),
+                                  _ptr(out_idx), base, base + 8, workspace.data_ptr(), workspace.numel(), None,
+                                  ctypes.byref(h))
+        _raise_for(rc)
+        self._h = h
+
+    def launch(self, stream: torch.cuda.Stream) -> None:
+        _raise_for(_native.lib().rmx_graph_launch(self._h, stream.cuda_stream))
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _native.lib().rmx_graph_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the module globals may be gone
+            pass
+
+
 def _alloc_scratch(n_vertices: int, device) -> dict:
     return dict(is_used=torch.empty(n_vertices, dtype=torch.uint8, device=device),
                 org_id=torch.empty(n_vertices, dtype=torch.int32, device=device),

@@ -99,3 +99,61 @@ def test_stream_capacity_and_shape_errors(rmx):
     v, e = random_mesh(5, 50, 2, 40, 3)
     with pytest.raises(rmx.MeshError):
         list(rs.run([pinned(v, e)]))
+
+
+def _graph_run(rmx, g, bufs, v, e, expect_ok=True):
+    vt, it, ov, oe, info = bufs
+    vt.copy_(torch.from_numpy(np.ascontiguousarray(v).view(np.int32)))
+    it.copy_(torch.from_numpy(np.ascontiguousarray(e).view(np.int32)))
+    s = torch.cuda.current_stream()
+    g.launch(s)
+    s.synchronize()
+    count, status = (int(x) for x in info.cpu())
+    return count, status, ov[:count].cpu().numpy().view(np.uint32), oe.cpu().numpy().view(np.uint32)
+
+
+@pytest.mark.parametrize("D,K", [(1, 2), (2, 4), (3, 3), (4, 4), (7, 3)])
+def test_graph_switches_paths_per_launch(rmx, D, K):
+    """One captured graph, relaunched on packed-key data, then AoS data (> 64 varying bits), then
+    packed again: the conditional nodes follow each input's plan; every result matches the oracle."""
+    from paper_2109_09812_b200 import pipeline
+    V, E = 20_000, 9_000
+    dev = torch.device("cuda")
+    vt = torch.empty((V, D), dtype=torch.int32, device=dev)
+    it = torch.empty((E, K), dtype=torch.int32, device=dev)
+    ov, oe = torch.empty_like(vt), torch.empty_like(it)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(pipeline.workspace_bytes(V, D, E, K), dtype=torch.uint8, device=dev)
+    g = pipeline.PipelineGraph(vt, V, D, it, E, K, ov, oe, info, ws)
+    rng = np.random.default_rng(D)
+    for mode in ("pool", "raw", "pool", "raw"):
+        if mode == "pool":
+            v = rng.integers(0, 40, size=(V, D)).astype(np.uint32) * np.uint32(0x00010001)
+        else:
+            v = rng.integers(0, 1 << 32, size=(V, D), dtype=np.uint64).astype(np.uint32)
+        e = rng.integers(0, V - 100, size=(E, K)).astype(np.uint32)
+        count, status, gv, ge = _graph_run(rmx, g, (vt, it, ov, oe, info), v, e)
+        ev, ee = expect(v, e)
+        assert status == 0 and count == ev.shape[0]
+        assert np.array_equal(gv, ev)
+        assert np.array_equal(ge, ee)
+
+
+def test_graph_out_of_range_status(rmx):
+    from paper_2109_09812_b200 import pipeline
+    V, D, E, K = 1000, 3, 500, 3
+    dev = torch.device("cuda")
+    vt = torch.empty((V, D), dtype=torch.int32, device=dev)
+    it = torch.empty((E, K), dtype=torch.int32, device=dev)
+    ov, oe = torch.empty_like(vt), torch.empty_like(it)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(pipeline.workspace_bytes(V, D, E, K), dtype=torch.uint8, device=dev)
+    g = pipeline.PipelineGraph(vt, V, D, it, E, K, ov, oe, info, ws)
+    v, e = random_mesh(9, V, D, E, K)
+    bad = e.copy()
+    bad[3, 2] = V + 5
+    _, status, _, _ = _graph_run(rmx, g, (vt, it, ov, oe, info), v, bad)
+    assert status & 1
+    count, status, gv, ge = _graph_run(rmx, g, (vt, it, ov, oe, info), v, e)   # status resets per launch
+    ev, ee = expect(v, e)
+    assert status == 0 and np.array_equal(gv, ev) and np.array_equal(ge, ee)

@@ -51,6 +51,19 @@ def main():
         tot += ms
         print(f"{names[k]:>14s} {ms:8.3f} ms")
     print(f"{'total':>14s} {tot:8.3f} ms")
+    # whole-step time: direct launches vs the captured graph (conditional nodes)
+    g = pipeline.PipelineGraph(vtx, V, D, idx, E, D, out_v, out_e, info, ws)
+    for name, fn in (("direct", lambda: pipeline.launch(vtx, V, D, idx, E, D, out_v, out_e, info, ws, None, s)),
+                     ("graph", lambda: g.launch(s))):
+        fn()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record(s)
+        for _ in range(a.steps):
+            fn()
+        t1.record(s)
+        torch.cuda.synchronize()
+        print(f"{name + ' step':>14s} {t0.elapsed_time(t1) / a.steps:8.3f} ms   count {int(info[0])}")
     ph = (ctypes.c_ulonglong * 4)()
     if lib.rmx_debug_phase_cycles(ph, 4, 1) and ph[2]:
         print(f"  look-back (digit 0): {ph[0] / ph[2]:.2f} windows, {ph[1] / ph[2]:.2f} spins per tile")
