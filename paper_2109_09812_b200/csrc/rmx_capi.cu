@@ -74,7 +74,7 @@ constexpr int kPkUniqIpt = 12;
 constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
 int pk_sort_ipt() {
     static int v = [] {
-        const char* e = std::getenv("RMX_PK_IPT");
+        const char* e = std::getenv("RMX_PK_CFG");
         const int x = e ? std::atoi(e) : 12;
         return (x == 8 || x == 12 || x == 16) ? x : 12;
     }();
@@ -252,20 +252,30 @@ int dispatch_pack(const PackArgs& a, cudaStream_t s) {
     }
 }
 
-template <int IPT>
+template <int IPT, int MINB>
 int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     const size_t smem = SortPkTraits<IPT>::smem_bytes();
     static thread_local int attr_dev = -1;
     int dev = 0;
     RMX_CHECK(cudaGetDevice(&dev));
     if (attr_dev != dev) {
-        RMX_CHECK(cudaFuncSetAttribute(k_pk_downsweep<IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RMX_CHECK(cudaFuncSetAttribute(k_pk_downsweep<IPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
         attr_dev = dev;
     }
-    k_pk_downsweep<IPT><<<a.ntiles, kBlock, smem, s>>>(a);
+    k_pk_downsweep<IPT, MINB><<<a.ntiles, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
+}
+
+// RMX_PK_CFG = "<rows per thread>x<CTAs per SM>" (tuning aid; default 12x3)
+int pk_minb() {
+    static int v = [] {
+        const char* e = std::getenv("RMX_PK_CFG");
+        const char* x = e ? std::strchr(e, 'x') : nullptr;
+        return x ? std::atoi(x + 1) : 3;
+    }();
+    return v;
 }
 
 int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
@@ -276,10 +286,13 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     RMX_CHECK(cudaGetLastError());
     k_pk_colscan<<<256, 1024, 0, s>>>(a);
     RMX_CHECK(cudaGetLastError());
-    switch (pk_sort_ipt()) {
-        case 8: return launch_downsweep<8>(a, s);
-        case 12: return launch_downsweep<12>(a, s);
-        default: return launch_downsweep<16>(a, s);
+    const int cfg = pk_sort_ipt() * 10 + pk_minb();
+    switch (cfg) {
+        case 84: return launch_downsweep<8, 4>(a, s);
+        case 124: return launch_downsweep<12, 4>(a, s);
+        case 162: return launch_downsweep<16, 2>(a, s);
+        case 163: return launch_downsweep<16, 3>(a, s);
+        default: return launch_downsweep<12, 3>(a, s);
     }
 }
 

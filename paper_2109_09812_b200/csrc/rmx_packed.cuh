@@ -513,7 +513,8 @@ struct SortPkTraits {
     static constexpr int kTile = kBlock * IPT;
     static __host__ __device__ size_t smem_bytes() {
         // keys sized for u64, origins, slot index, warp counters + peer masks, digit tables, misc, barrier
-        return static_cast<size_t>(kTile) * (8 + 4 + 2) + (2 * kWarps * 256 + 256 + kWarps + 8) * 4 + 16;
+        // (no peer-mask table: packed passes rank with match or ballots only)
+        return static_cast<size_t>(kTile) * (8 + 4 + 2) + (kWarps * 256 + 256 + kWarps + 8) * 4 + 16;
     }
 };
 
@@ -536,8 +537,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;  // keys region sized for u64
     uint16_t* s_src = reinterpret_cast<uint16_t*>(s_vals + TILE);
     uint32_t* s_whist = reinterpret_cast<uint32_t*>(s_src + TILE);
-    uint32_t* s_wmask = s_whist + kWarps * 256;
-    uint32_t* s_gdst = s_wmask + kWarps * 256;
+    uint32_t* s_gdst = s_whist + kWarps * 256;
     uint32_t* s_warp = s_gdst + 256;
     uint32_t* s_misc = s_warp + kWarps;
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
@@ -554,13 +554,12 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     }
     // global row of this tile's digit-d run = (rows with smaller digits) + (digit-d rows of earlier tiles)
     const uint32_t tot_d = a.totals[tid];
-    const int rank_mode = choose_rank(tot_d, a.rank_force);
+    const int rank_mode = choose_rank(tot_d, a.rank_force == kRankAtomic ? kRankBallot : a.rank_force);
     uint32_t dummy;
     const uint32_t run_base = block_exclusive_scan<kWarps>(tot_d, s_warp, dummy) +
                               a.counts[static_cast<size_t>(tid) * a.cstride + tile];
     for (int i = tid; i < kWarps * 256; i += kBlock) {
         s_whist[i] = 0u;
-        if (rank_mode == kRankAtomic) s_wmask[i] = 0u;
     }
     __syncthreads();
     mbar_wait(s_bar, 0u);
@@ -570,14 +569,14 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
 #pragma unroll
         for (int r = 0; r < IPT; ++r)
             pk[r] = static_cast<uint32_t>(s_keys[warp * (32u * IPT) + r * 32u + lane] >> shift) & 255u;
-        warp_rank<IPT, false>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, false);
+        warp_rank<IPT, false>(pk, s_whist + warp * 256, nullptr, rank_mode, false);
     } else {
 #pragma unroll
         for (int r = 0; r < IPT; ++r) {
             const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
             pk[r] = p < tile_n ? (static_cast<uint32_t>(s_keys[p] >> shift) & 255u) : 256u;
         }
-        warp_rank<IPT, true>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, true);
+        warp_rank<IPT, true>(pk, s_whist + warp * 256, nullptr, rank_mode, true);
     }
     __syncthreads();
     {
@@ -637,8 +636,8 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     }
 }
 
-template <int IPT>
-__global__ void __launch_bounds__(kBlock, IPT <= 8 ? 4 : 3) k_pk_downsweep(SortPkArgs a) {
+template <int IPT, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a) {
     if (*a.status || !pk_pass_active(a)) return;
     extern __shared__ __align__(128) uint32_t smem[];
     if (a.plan[pk_base(4 * a.dim) + 1] == 2u) sort_pk_body<2, IPT>(a, smem);
