@@ -331,10 +331,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
 
+    // origins are the row numbers: the first pass makes them itself, so they are
+    // only stored when no pass runs (all keys equal)
+    const bool want_vals = pk[3] == 0u;
     auto put = [&](uint64_t i, uint64_t key) {
         if (wide) keys64[i] = key;
         else keys32[i] = static_cast<uint32_t>(key);
-        vals[i] = static_cast<uint32_t>(i);
+        if (want_vals) vals[i] = static_cast<uint32_t>(i);
         a.digits[i] = static_cast<uint8_t>(key);
     };
 
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
                                           static_cast<uint32_t>(key[2]), static_cast<uint32_t>(key[3])));
                     }
                     const uint32_t i0 = static_cast<uint32_t>(4 * g);
-                    __stcs(reinterpret_cast<uint4*>(vals + 4 * g), make_uint4(i0, i0 + 1, i0 + 2, i0 + 3));
+                    if (want_vals) __stcs(reinterpret_cast<uint4*>(vals + 4 * g), make_uint4(i0, i0 + 1, i0 + 2, i0 + 3));
                     reinterpret_cast<uint32_t*>(a.digits)[g] =
                         (static_cast<uint32_t>(key[0]) & 255u) | ((static_cast<uint32_t>(key[1]) & 255u) << 8) |
                         ((static_cast<uint32_t>(key[2]) & 255u) << 16) | (static_cast<uint32_t>(key[3]) << 24);
@@ -546,11 +549,16 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const uint32_t tile = blockIdx.x;
     const uint32_t base = tile * static_cast<uint32_t>(TILE);
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
+    // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none)
+    const bool iota = a.pass == 0;
     if (tid == 0) {
         mbar_init(s_bar, 1);
         fence_mbar_init();
-        stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + base, tile_n * 4u,
-                    s_bar);
+        if (iota)
+            stage_tile(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_bar);
+        else
+            stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + base,
+                        tile_n * 4u, s_bar);
     }
     // global row of this tile's digit-d run = (rows with smaller digits) + (digit-d rows of earlier tiles)
     const uint32_t tot_d = a.totals[tid];
@@ -616,7 +624,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
             if (q < tile_n) {
                 const uint32_t p = s_src[q];
                 k[u] = s_keys[p];
-                v[u] = s_vals[p];
+                v[u] = iota ? base + p : s_vals[p];
             }
         }
 #pragma unroll
