@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from .mesh import MAX_VERTICES, Mesh, MeshError, require_valid
-from .pipeline import _device, reindex, reindex_tensors
+from .pipeline import _device, host_tensor, reindex, reindex_tensors
 
 
 def _to_mesh(res) -> Mesh:
@@ -52,9 +52,9 @@ def merge(meshes, device=None) -> Mesh:
         for m in meshes:
             nv, ne = m.n_vertices, m.n_elements
             if nv:
-                vtx[v0:v0 + nv].copy_(torch.from_numpy(np.ascontiguousarray(m.vertices).view(np.int32)))
+                vtx[v0:v0 + nv].copy_(host_tensor(np.ascontiguousarray(m.vertices).view(np.int32)))
             if ne:
-                seg = torch.from_numpy(np.ascontiguousarray(m.elements).view(np.int32)).to(dev)
+                seg = host_tensor(np.ascontiguousarray(m.elements).view(np.int32)).to(dev)
                 idx[e0:e0 + ne] = (seg.to(torch.int64) & 0xFFFFFFFF) + v0
             v0 += nv
             e0 += ne
@@ -84,7 +84,7 @@ def soup_to_mesh(soup, device=None) -> Mesh:
         raise MeshError(f"soup has {n} vertices, exceeds 32-bit index range")
     dev = _device(device)
     with torch.cuda.device(dev):
-        vtx = torch.from_numpy(np.ascontiguousarray(arr.reshape(n, dim)).view(np.int32)).to(dev)
+        vtx = host_tensor(np.ascontiguousarray(arr.reshape(n, dim)).view(np.int32)).to(dev)
         idx = torch.arange(n, dtype=torch.int64, device=dev).view(m, arity)
         res = reindex_tensors(vtx, idx.to(torch.int32) if n < (1 << 31) else _narrow_u32(idx))
     return _to_mesh(res)

@@ -25,6 +25,7 @@ library.  There is no CPU fallback: a missing library raises.
 from __future__ import annotations
 
 import ctypes
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -55,6 +56,16 @@ def _raise_for(rc: int) -> None:
     if rc in (_native.RMX_EINVAL, _native.RMX_ERANGE):
         raise MeshError(msg)
     raise RuntimeError(f"CUDA re-indexing failed ({rc}): {msg}")
+
+
+def host_tensor(a: np.ndarray) -> torch.Tensor:
+    """Zero-copy torch view of a host array that is only read (copied to the device).
+
+    Mesh arrays are read-only; torch warns on wrapping them although nothing writes.
+    """
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a)
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -219,8 +230,8 @@ class ReindexScratch:
             E, K = elements.shape
             dev = self._device
             with torch.cuda.device(dev):
-                vtx_d = torch.from_numpy(np.ascontiguousarray(vertices).view(np.int32).reshape(V, D)).to(dev)
-                idx_d = torch.from_numpy(np.ascontiguousarray(elements).view(np.int32).reshape(E, K)).to(dev)
+                vtx_d = host_tensor(np.ascontiguousarray(vertices).view(np.int32).reshape(V, D)).to(dev)
+                idx_d = host_tensor(np.ascontiguousarray(elements).view(np.int32).reshape(E, K)).to(dev)
                 res = reindex_tensors(vtx_d, idx_d, scratch=True)
                 sc = res.scratch
                 n = V if E else 0
@@ -292,8 +303,8 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
         stream = torch.cuda.current_stream(dev)
         vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
         idx_d = torch.empty((E, K), dtype=torch.int32, device=dev)
-        vtx_d.copy_(torch.from_numpy(vertices.view(np.int32)))
-        idx_d.copy_(torch.from_numpy(elements.view(np.int32)))
+        vtx_d.copy_(host_tensor(vertices.view(np.int32)))
+        idx_d.copy_(host_tensor(elements.view(np.int32)))
         out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
         out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
         info = torch.zeros(2, dtype=torch.int64, device=dev)
