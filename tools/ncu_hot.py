@@ -1,6 +1,8 @@
 """Print the hottest SASS instructions (by warp-stall samples) of an ncu report.
 
-    python tools/ncu_hot.py gpurun_out/prof.ncu-rep [top]
+    python tools/ncu_hot.py gpurun_out/prof.ncu-rep [top] [kernel-regex]
+
+With a kernel regex, the first matching launch of a multi-kernel report.
 """
 import csv
 import io
@@ -11,13 +13,18 @@ import sys
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
+    filt = ["-k", f"regex:{sys.argv[3]}", "-c", "1"] if len(sys.argv) > 3 else []
+    out = subprocess.run(["ncu", "-i", rep, *filt, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
     lines = out.splitlines()
     rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
     hdr = rows[0]
     ix = {h: i for i, h in enumerate(hdr)}
-    body = rows[1:]
+    body, seen = [], set()
+    for r in rows[1:]:  # the SASS listing can repeat (one copy per view); keep each address once
+        if len(r) == len(hdr) and r[ix["Address"]] not in seen:
+            seen.add(r[ix["Address"]])
+            body.append(r)
     samp = ix["Warp Stall Sampling (All Samples)"]
     stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 
