@@ -184,6 +184,24 @@ int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, 
                                uint32_t* out_idx, void* stream);
 
 /*
+ * merge (reference pkg/src/remeshx/ops.py:29-34) on the device: out[i] =
+ * idx[i] + offset (mod 2^32), the index array of one piece shifted by the
+ * vertex count of the pieces before it in the concatenation.
+ */
+int rmx_offset_indices(const uint32_t* idx, uint64_t n, uint32_t offset, uint32_t* out, void* stream);
+
+/*
+ * Welded (indexed) tile of the C4 merge workload:
+ * the triangulated n x n quad grid whose lattice rows start at row0, every
+ * point stored once, 5 % unused rows; points and triangles row-major, or
+ * with shuffle != 0 at seeded positions / in seeded order (the random-access
+ * case); bit-identical to oracle/lattice.py:welded_tile.
+ */
+int rmx_welded_tile_sizes(uint32_t n, uint64_t* n_vertices, uint64_t* n_elements);
+int rmx_gen_welded_tile(uint32_t n, uint32_t row0, uint64_t seed, int shuffle, uint32_t* out_vtx_bits,
+                        uint32_t* out_idx, void* stream);
+
+/*
  * grid_quads(n) of the paper's Table 1 on the device (reference
  * pkg/src/remeshx/bench.py:42-68): 5*n*n float2 rows (4 corners + an unused
  * centre per quad) into out_vtx_bits (10*n*n words) and n*n quads

@@ -223,3 +223,77 @@ def lattice_expected(kind: str, cells, seed: int = 0, n_elem_take: int | None = 
         p = np.stack([used // ((ny + 1) * (nz + 1)), (used // (nz + 1)) % (ny + 1), used % (nz + 1)], -1)
     out_v = point_coords(kind, cells, p)
     return out_v, inv.reshape(ranks.shape).astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
+# C4: welded (indexed) tiles for merge (BASELINE configs[3]):
+# tile k = the triangulated n x n quad grid whose lattice rows start at
+# ``row0`` (C4: n = 5000, row0 = 4500 k -> 500 shared rows between
+# neighbours), every lattice point stored ONCE (welded), + 5 % unused rows.
+#
+# * point p = i (n+1) + j (local, 0 <= i, j <= n) sits at position
+#   q = p (row-major, like a grid generator writes it) or, with shuffle,
+#   q = permute(p, n_pts, seed); position q owns slot q + u(q) with
+#   u(q) = q n_unused // n_pts, and the u(q+1) - u(q) following slots hold
+#   unused rows (ordinals u(q) ..), like the soup generator;
+# * coordinates are those of the global lattice point (row0 + i, j);
+# * element e = triangle e of the grid (row-major quads, same split as the
+#   soup) or, with shuffle, triangle permute(e, E, seed + 1); indices = slots
+#   of its corner points.  C4 uses the row-major tiles (SURVEY 8(d) models
+#   mark/remap as streams); shuffled tiles are the random-access stress case.
+#
+# Merging tiles k = 0..T-1 (concatenated, indices offset) re-indexes to the
+# closed form: the (row0_max + n + 1) x (n + 1) lattice points row-major.
+COLS_C4 = 5000
+ROW_STEP_C4 = 4500
+TILES_C4 = 8
+
+
+def welded_sizes(n: int) -> dict:
+    n_pts = (n + 1) * (n + 1)
+    n_unused = n_pts // 20
+    return dict(n_points=n_pts, n_unused=n_unused, n_vertices=n_pts + n_unused, n_elem=2 * n * n)
+
+
+def welded_tile(n: int, row0: int, seed: int = 0, shuffle: bool = False):
+    """(vertices float32 (V, 3), elements uint32 (2 n^2, 3)) of one welded tile."""
+    s = welded_sizes(n)
+    n_pts, n_unused, V, E = s["n_points"], s["n_unused"], s["n_vertices"], s["n_elem"]
+    p = np.arange(n_pts, dtype=np.int64)
+    q = permute(p.astype(np.uint64), n_pts, seed).astype(np.int64) if shuffle else p
+    uq = (q.astype(np.uint64) * np.uint64(n_unused) // np.uint64(n_pts)).astype(np.int64)
+    slot_of_point = q + uq
+    verts = np.empty((V, 3), dtype=np.uint32)
+    pts = np.stack([row0 + p // (n + 1), p % (n + 1)], -1)
+    verts[slot_of_point] = point_coords("tri", None, pts).view(np.uint32)
+    # unused rows: after position q's slot, ordinals u(q) .. u(q+1)-1
+    qa = np.arange(n_pts + 1, dtype=np.uint64)
+    u = (qa * np.uint64(n_unused) // np.uint64(n_pts)).astype(np.int64)
+    cnt = u[1:] - u[:-1]
+    owners = np.repeat(np.arange(n_pts, dtype=np.int64), cnt)
+    ords = np.arange(int(u[-1]), dtype=np.int64)
+    if ords.size:
+        verts[owners + u[owners] + 1 + (ords - u[owners])] = unused_words(seed, ords, 3)
+    t = np.arange(E, dtype=np.int64)
+    if shuffle:
+        t = permute(t.astype(np.uint64), E, seed + 1).astype(np.int64)
+    corners = element_points("tri", (n, n), t)                     # local (i, j)
+    cp = corners[..., 0] * (n + 1) + corners[..., 1]
+    elements = slot_of_point[cp].astype(np.uint32)
+    return verts.view(np.float32), elements
+
+
+def welded_merge_expected(n: int, row0s, seed: int = 0, shuffle: bool = False):
+    """Closed-form merge + re-index of welded tiles at ``row0s`` (each with ``seed + k``)."""
+    rows = max(row0s) + n + 1
+    grid = np.stack(np.meshgrid(np.arange(rows), np.arange(n + 1), indexing="ij"), -1).reshape(-1, 2)
+    out_v = point_coords("tri", None, grid)
+    idx = []
+    for k, r0 in enumerate(row0s):
+        E = 2 * n * n
+        t = np.arange(E, dtype=np.int64)
+        if shuffle:
+            t = permute(t.astype(np.uint64), E, seed + k + 1).astype(np.int64)
+        corners = element_points("tri", (n, n), t)
+        idx.append(((corners[..., 0] + r0) * (n + 1) + corners[..., 1]).astype(np.uint32))
+    return out_v, np.concatenate(idx)

@@ -28,7 +28,8 @@ EXPORTS = (
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches",
     "rmx_last_executed_passes", "rmx_plan_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
-    "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy",
+    "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy", "rmx_offset_indices",
+    "rmx_welded_tile_sizes", "rmx_gen_welded_tile",
 )
 
 
@@ -75,6 +76,9 @@ _SIGNATURES = {
                                 ctypes.POINTER(Scratch), ctypes.POINTER(_vp)]),
     "rmx_graph_launch": (_int, [_vp, _vp]),
     "rmx_graph_destroy": (None, [_vp]),
+    "rmx_offset_indices": (_int, [_vp, _u64, _u32, _vp, _vp]),
+    "rmx_welded_tile_sizes": (_int, [_u32, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "rmx_gen_welded_tile": (_int, [_u32, _u32, _u64, _int, _vp, _vp, _vp]),
 }
 
 

@@ -799,6 +799,51 @@ int rmx_gather_u32(const uint32_t* table, uint64_t n_table, const uint32_t* idx,
     return RMX_OK;
 }
 
+int rmx_offset_indices(const uint32_t* idx, uint64_t n, uint32_t offset, uint32_t* out, void* stream) {
+    g_err[0] = '\0';
+    if (n == 0) return RMX_OK;
+    if (!idx || !out) return RMX_EINVAL;
+    const int vec = (aligned16(idx) && aligned16(out)) ? 1 : 0;
+    int grid = 0;
+    int rc = grid_for_stream(vec ? (n + 3) / 4 : n, grid);
+    if (rc) return rc;
+    k_offset_indices<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(idx, n, offset, out, vec);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int rmx_welded_tile_sizes(uint32_t n, uint64_t* n_vertices, uint64_t* n_elements) {
+    if (n < 1) return RMX_EINVAL;
+    const uint64_t pts = static_cast<uint64_t>(n + 1) * (n + 1);
+    if (n_vertices) *n_vertices = pts + pts / 20;
+    if (n_elements) *n_elements = 2ull * n * n;
+    return RMX_OK;
+}
+
+int rmx_gen_welded_tile(uint32_t n, uint32_t row0, uint64_t seed, int shuffle, uint32_t* out_vtx_bits,
+                        uint32_t* out_idx, void* stream) {
+    if (n < 1 || !out_vtx_bits || !out_idx) return RMX_EINVAL;
+    TileArgs a{};
+    a.n = n;
+    a.row0 = row0;
+    a.shuffle = shuffle ? 1 : 0;
+    a.n_pts = static_cast<uint64_t>(n + 1) * (n + 1);
+    a.n_unused = a.n_pts / 20;
+    a.n_elem = 2ull * n * n;
+    if (a.n_pts + a.n_unused >= (1ull << 32)) return RMX_ERANGE;
+    a.pts = make_perm(a.n_pts, seed);
+    a.elems = make_perm(a.n_elem, seed + 1);
+    a.useed = splitmix64(seed + 0x5555);
+    a.vtx = out_vtx_bits;
+    a.idx = out_idx;
+    int grid = 0;
+    int rc = grid_for_stream(a.n_elem, grid);
+    if (rc) return rc;
+    k_gen_welded_tile<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int rmx_lower_bound_rows(const uint32_t* rows, uint64_t n, uint32_t dim, const uint32_t* queries, uint64_t n_queries,
                          uint64_t* out_positions, void* stream) {
     g_err[0] = '\0';

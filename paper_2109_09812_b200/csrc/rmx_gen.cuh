@@ -135,4 +135,98 @@ __global__ void __launch_bounds__(kBlock) k_gen_grid_quads(uint32_t n, uint64_t 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Welded (indexed) tiles of the C4 merge workload (bit-identical to
+// oracle/lattice.py:welded_tile): n x n quads whose lattice rows start at
+// row0, each point stored once with 5 % unused rows interleaved; points and
+// triangles row-major, or (shuffle) at seeded positions / in seeded order.
+struct Perm {
+    uint64_t n;
+    uint32_t half;
+    uint64_t mask;
+    uint64_t keys[4];
+};
+
+inline Perm make_perm(uint64_t n, uint64_t seed) {
+    Perm f{};
+    f.n = n;
+    int bits = 0;
+    while ((1ull << bits) < n) ++bits;  // bit length of n-1
+    if (bits < 2) bits = 2;
+    bits += bits & 1;
+    f.half = static_cast<uint32_t>(bits / 2);
+    f.mask = (1ull << f.half) - 1;
+    for (int r = 0; r < 4; ++r) f.keys[r] = splitmix64(static_cast<uint64_t>(r) + seed * 4 + 1);
+    return f;
+}
+
+__device__ __forceinline__ uint64_t perm_apply(uint64_t v, const Perm& f) {
+    do {
+        uint64_t left = v >> f.half, right = v & f.mask;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint64_t g = (splitmix64(right ^ f.keys[r]) >> 7) & f.mask;
+            const uint64_t nl = right;
+            right = left ^ g;
+            left = nl;
+        }
+        v = (left << f.half) | right;
+    } while (v >= f.n);  // cycle walking
+    return v;
+}
+
+struct TileArgs {
+    uint32_t n;        // quads per side
+    uint32_t row0;     // global lattice row of local row 0
+    int shuffle;       // 0: row-major points and triangles; 1: seeded positions and order
+    uint64_t n_pts, n_unused, n_elem;
+    Perm pts, elems;
+    uint64_t useed;
+    uint32_t* vtx;
+    uint32_t* idx;
+};
+
+__device__ __forceinline__ uint64_t tile_slot(uint64_t q, const TileArgs& a) {
+    return q + (q * a.n_unused) / a.n_pts;
+}
+
+__global__ void __launch_bounds__(kBlock) k_gen_welded_tile(TileArgs a) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint32_t cols = a.n + 1;
+    // points at their positions, unused rows after each position
+    for (uint64_t p = t0; p < a.n_pts; p += stride) {
+        const uint64_t q = a.shuffle ? perm_apply(p, a.pts) : p;
+        const int i = static_cast<int>(a.row0 + p / cols), j = static_cast<int>(p % cols);
+        uint32_t* row = a.vtx + tile_slot(q, a) * 3;
+        row[0] = __float_as_uint(__fmul_rn(static_cast<float>(i), 0.5f));
+        row[1] = __float_as_uint(__fmul_rn(static_cast<float>(j), 0.5f));
+        row[2] = __float_as_uint(__fmul_rn(static_cast<float>((7 * i + 13 * j) % 64), 0.25f));
+    }
+    for (uint64_t q = t0; q < a.n_pts; q += stride) {
+        const uint64_t u0 = (q * a.n_unused) / a.n_pts, u1 = ((q + 1) * a.n_unused) / a.n_pts;
+        for (uint64_t o = u0; o < u1; ++o) {
+            uint32_t* row = a.vtx + (q + u0 + 1 + (o - u0)) * 3;
+            for (int c = 0; c < 3; ++c) {
+                const uint64_t h = splitmix64((o * 3 + c) ^ a.useed);
+                const uint64_t expo = (0x7Full + ((h >> 32) % 10ull)) << 23;
+                row[c] = static_cast<uint32_t>((h & 0x807FFFFFull) | expo);
+            }
+        }
+    }
+    // triangles: corner points -> their slots
+    for (uint64_t e = t0; e < a.n_elem; e += stride) {
+        const uint64_t t = a.shuffle ? perm_apply(e, a.elems) : e;
+        const uint64_t qd = t >> 1;
+        const int h = static_cast<int>(t & 1);
+        const uint32_t qi = static_cast<uint32_t>(qd / a.n), qj = static_cast<uint32_t>(qd % a.n);
+        const uint32_t ci[3] = {qi, qi + 1, h ? qi : qi + 1};
+        const uint32_t cj[3] = {qj, h ? qj + 1 : qj, qj + 1};
+        for (int s = 0; s < 3; ++s) {
+            const uint64_t p = static_cast<uint64_t>(ci[s]) * cols + cj[s];
+            a.idx[e * 3 + s] = static_cast<uint32_t>(tile_slot(a.shuffle ? perm_apply(p, a.pts) : p, a));
+        }
+    }
+}
+
 }  // namespace rmx

@@ -126,14 +126,15 @@ struct VaryArgs {
 };
 
 // Occurring sign+exponent fields of one component: a per-thread window of 32
-// exponents around the replacement row's (one register per sign) catches
-// real geometry; anything outside goes to the block's shared set.
+// exponents (one register per sign) centred on a sample word -- the thread's
+// first row, or the replacement row when that is zero -- catches real
+// geometry; anything outside goes to the block's shared set.
 struct FieldSet {
     uint32_t win[2];
     uint32_t lo;  // first exponent of the window
-    __device__ __forceinline__ void init(uint32_t ref_word) {
+    __device__ __forceinline__ void init(uint32_t sample_word) {
         win[0] = win[1] = 0u;
-        const uint32_t e = (ref_word >> kFieldLo) & 255u;
+        const uint32_t e = (sample_word >> kFieldLo) & 255u;
         lo = e > 16u ? min(e - 16u, 224u) : 0u;
     }
     __device__ __forceinline__ void add(uint32_t word, uint32_t* s_set) {
@@ -176,7 +177,10 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
         for (int c = 0; c < D_CT; ++c) {
             ref[c] = __ldg(repl + c);
             vor[c] = 0u;
-            if (c < kSets) fs[c].init(ref[c]);
+            if (c < kSets) {
+                const uint32_t w = start < a.n ? __ldg(a.vtx + start * D_CT + c) : 0u;
+                fs[c].init((w & 0x7F800000u) ? w : ref[c]);
+            }
         }
         for (uint32_t i = threadIdx.x; i < kSets * kFieldWords; i += kBlock) s_fields[i] = 0u;
         __syncthreads();

@@ -43,4 +43,24 @@ __global__ void k_lower_bound(const uint32_t* rows, uint64_t n, int D, const uin
     out[q] = lo;
 }
 
+// merge (reference ops.py:29-34): a piece's indices shifted by the vertex
+// count of the pieces before it, written into the concatenated index array.
+__global__ void __launch_bounds__(kBlock) k_offset_indices(const uint32_t* __restrict__ idx, uint64_t n,
+                                                           uint32_t offset, uint32_t* __restrict__ out, int vec) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t n4 = n >> 2;
+        const uint4* i4 = reinterpret_cast<const uint4*>(idx);
+        uint4* o4 = reinterpret_cast<uint4*>(out);
+        for (uint64_t i = t0; i < n4; i += stride) {
+            const uint4 v = __ldcs(i4 + i);
+            __stcs(o4 + i, make_uint4(v.x + offset, v.y + offset, v.z + offset, v.w + offset));
+        }
+        done = n4 << 2;
+    }
+    for (uint64_t i = done + t0; i < n; i += stride) out[i] = idx[i] + offset;
+}
+
 }  // namespace rmx

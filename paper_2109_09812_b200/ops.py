@@ -63,6 +63,44 @@ def merge(meshes, device=None) -> Mesh:
     return _to_mesh(res)
 
 
+def merge_tensors(pieces, device=None):
+    """Device-resident merge (ops.py:10-35): concatenate the pieces' vertex bits,
+    shift each piece's indices by the vertices before it (``rmx_offset_indices``),
+    re-index.  ``pieces`` = [(vertex bits int32 (V_k, D), elements int32 (E_k, K))]
+    on one device; returns the :class:`~paper_2109_09812_b200.DeviceResult`.
+    """
+    from . import _native
+    pieces = list(pieces)
+    if not pieces:
+        raise MeshError("merge needs at least one mesh")
+    D, K = pieces[0][0].shape[1], pieces[0][1].shape[1]
+    for k, (v, e) in enumerate(pieces):
+        if v.dim() != 2 or e.dim() != 2 or v.shape[1] != D or e.shape[1] != K:
+            raise MeshError(f"piece {k} has shapes {tuple(v.shape)} / {tuple(e.shape)}, expected (*, {D}) / (*, {K})")
+    total = sum(v.shape[0] for v, _ in pieces)
+    if total >= MAX_VERTICES:
+        raise MeshError(f"merged vertex count {total} exceeds 32-bit index range")
+    n_elem = sum(e.shape[0] for _, e in pieces)
+    dev = pieces[0][0].device if device is None else torch.device(device)
+    lib = _native.lib()
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        vtx = torch.empty((total, D), dtype=torch.int32, device=dev)
+        idx = torch.empty((n_elem, K), dtype=torch.int32, device=dev)
+        v0 = e0 = 0
+        for v, e in pieces:
+            nv, ne = v.shape[0], e.shape[0]
+            if nv:
+                vtx[v0:v0 + nv].copy_(v, non_blocking=True)
+            if ne:
+                src = e.contiguous()
+                _native.check(lib.rmx_offset_indices(src.data_ptr(), ne * K, v0, idx[e0:e0 + ne].data_ptr(),
+                                                     stream.cuda_stream))
+            v0 += nv
+            e0 += ne
+        return reindex_tensors(vtx, idx)
+
+
 def _narrow_u32(x: torch.Tensor) -> torch.Tensor:
     """int64 values in [0, 2**32) -> int32 tensor with the same low 32 bits."""
     return (x - ((x >> 31) << 32)).to(torch.int32)

@@ -225,3 +225,29 @@ def test_native_library_is_the_loaded_code(rmx):
     rmx.reindex(rmx.Mesh(np.zeros((2, 2), np.float32), np.array([(0, 1)], np.uint32)))
     maps = open("/proc/self/maps").read()
     assert "librmx_b200.so" in maps
+
+
+def test_c4_merge_full_size(rmx):
+    """BASELINE configs[3] at one GPU: 8 welded 5000 x 5000 tiles (500 shared rows) merged on the
+    device -- 210,084,008 vertex slots in, 182,541,501 out; determining properties + closed-form
+    ranks of sampled elements of every tile."""
+    import torch
+    C, S, T = lattice.COLS_C4, lattice.ROW_STEP_C4, lattice.TILES_C4
+    pieces = [rmx.gen.welded_tile_tensors(C, S * k, k) for k in range(T)]
+    vtx = torch.cat([p[0] for p in pieces])
+    offs = np.cumsum([0] + [p[0].shape[0] for p in pieces])[:-1]
+    res = rmx.merge_tensors(pieces)
+    assert vtx.shape[0] == 210_084_008
+    assert res.vertices.shape[0] == 182_541_501
+    E = 2 * C * C
+    for k in (0, 3, T - 1):
+        t = np.arange(E - 500, E, dtype=np.int64)
+        corners = lattice.element_points("tri", (C, C), t)
+        want = ((corners[..., 0] + S * k) * (C + 1) + corners[..., 1]).astype(np.uint32)
+        got = res.elements[k * E + E - 500:(k + 1) * E].cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, want)
+    idx = torch.cat([(p[1].to(torch.int64) + int(o)).to(torch.int32) for p, o in zip(pieces, offs)])
+    del pieces
+    check_determining_properties(vtx, idx, res.vertices, res.elements, 182_541_501)
+    del res, vtx, idx
+    torch.cuda.empty_cache()

@@ -84,3 +84,63 @@ def test_merge_empties_and_single(cuda_ok):
     c = load_group("worked")["worked"]
     w = rmx.Mesh(c["in_vtx"].view(np.float32), c["in_idx"])
     assert rmx.bitwise_equal(rmx.merge([w]), rmx.reindex(w)[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,case", _cases("merge"), ids=[c[0] for c in _cases("merge")])
+def test_merge_tensors_matches_reference(cuda_ok, name, case):
+    """The device-resident merge (offset kernel + re-index) against the reference merge."""
+    import torch
+
+    import paper_2109_09812_b200 as rmx
+    pieces = []
+    for k in range(int(case["n_pieces"])):
+        v = torch.from_numpy(case[f"piece_vtx_{k}"].view(np.int32).copy()).cuda()
+        e = torch.from_numpy(case[f"piece_idx_{k}"].view(np.int32).copy()).cuda()
+        pieces.append((v, e))
+    res = rmx.merge_tensors(pieces)
+    assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), case["out_vtx"])
+    assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), case["out_idx"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,row0,seed,shuffle", [(1, 0, 0, False), (6, 4, 1, True), (13, 100, 7, False),
+                                                  (40, 36, 3, True), (17, 9, 2, True)])
+def test_welded_tile_generator_matches_oracle(cuda_ok, n, row0, seed, shuffle):
+    from oracle import lattice
+
+    from paper_2109_09812_b200 import gen
+    vtx, idx = gen.welded_tile_tensors(n, row0, seed, shuffle)
+    v, e = lattice.welded_tile(n, row0, seed, shuffle)
+    assert np.array_equal(vtx.cpu().numpy().view(np.uint32), v.view(np.uint32))
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), e)
+
+
+@pytest.mark.gpu
+def test_merge_tensors_welded_tiles_closed_form(cuda_ok):
+    from oracle import lattice
+
+    import paper_2109_09812_b200 as rmx
+    n, row0s = 30, [0, 25, 50, 75]
+    for shuffle in (False, True):
+        pieces = [rmx.gen.welded_tile_tensors(n, r0, k, shuffle) for k, r0 in enumerate(row0s)]
+        res = rmx.merge_tensors(pieces)
+        ev, ei = lattice.welded_merge_expected(n, row0s, shuffle=shuffle)
+        assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), ev.view(np.uint32))
+        assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), ei)
+    ev, ei = lattice.welded_merge_expected(n, row0s, shuffle=True)
+    assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), ev.view(np.uint32))
+    assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), ei)
+
+
+@pytest.mark.gpu
+def test_merge_tensors_errors(cuda_ok):
+    import torch
+
+    import paper_2109_09812_b200 as rmx
+    with pytest.raises(rmx.MeshError):
+        rmx.merge_tensors([])
+    a = (torch.zeros((3, 2), dtype=torch.int32, device="cuda"), torch.zeros((1, 3), dtype=torch.int32, device="cuda"))
+    b = (torch.zeros((3, 3), dtype=torch.int32, device="cuda"), torch.zeros((1, 3), dtype=torch.int32, device="cuda"))
+    with pytest.raises(rmx.MeshError):
+        rmx.merge_tensors([a, b])

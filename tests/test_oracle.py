@@ -81,3 +81,26 @@ def test_permutation_is_bijection():
     for n in (1, 2, 3, 17, 1000, 4097):
         p = lattice.permute(np.arange(n, dtype=np.uint64), n, seed=9)
         assert sorted(p.tolist()) == list(range(n))
+
+
+@pytest.mark.parametrize("n,row0s,shuffle", [(6, [0, 4, 8], False), (5, [0], True), (9, [0, 3, 6, 9, 12], True),
+                                             (4, [0, 4], False), (7, [0, 5, 10], True)])
+def test_welded_merge_closed_form_matches_oracle(n, row0s, shuffle):
+    """C4 recipe: merging welded tiles (overlapping rows) re-indexes to the lattice closed form."""
+    tiles = [lattice.welded_tile(n, r0, seed=k, shuffle=shuffle) for k, r0 in enumerate(row0s)]
+    offs = np.cumsum([0] + [t[0].shape[0] for t in tiles])[:-1]
+    v = np.concatenate([t[0] for t in tiles])
+    e = np.concatenate([t[1] + np.uint32(o) for t, o in zip(tiles, offs)])
+    ref = O.reindex(v, e)
+    ev, ei = lattice.welded_merge_expected(n, row0s, shuffle=shuffle)
+    assert np.array_equal(ref["vertices"].view(np.uint32), ev.view(np.uint32))
+    assert np.array_equal(ref["elements"], ei)
+    s = lattice.welded_sizes(n)
+    assert tiles[0][0].shape[0] == s["n_vertices"] and tiles[0][1].shape[0] == s["n_elem"]
+
+
+def test_c4_counts():
+    s = lattice.welded_sizes(lattice.COLS_C4)
+    assert lattice.TILES_C4 * s["n_vertices"] == 210_084_008
+    rows = lattice.ROW_STEP_C4 * (lattice.TILES_C4 - 1) + lattice.COLS_C4 + 1
+    assert rows * (lattice.COLS_C4 + 1) == 182_541_501

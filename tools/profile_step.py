@@ -22,16 +22,31 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--steps", type=int, default=2)
     a = ap.parse_args()
-    kid, nx, ny, nz, D = CFG[a.config]
     lib = _native.lib()
-    E, V = ctypes.c_uint64(), ctypes.c_uint64()
-    lib.rmx_lattice_sizes(kid, nx, ny, nz, 1 << 63, ctypes.byref(E), ctypes.byref(V))
-    E, V = E.value, V.value
     dev = torch.device("cuda", 0)
     s = torch.cuda.current_stream(dev)
-    vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
-    idx = torch.empty((E, D), dtype=torch.int32, device=dev)
-    _native.check(lib.rmx_gen_lattice_soup(kid, nx, ny, nz, 0, 1 << 63, vtx.data_ptr(), idx.data_ptr(), s.cuda_stream))
+    if a.config == "C4":  # 8 welded tiles concatenated with index offsets (the merge input)
+        from paper_2109_09812_b200 import gen
+        pieces = [gen.welded_tile_tensors(5000, 4500 * k, k) for k in range(8)]
+        D = 3
+        V = sum(p[0].shape[0] for p in pieces)
+        E = sum(p[1].shape[0] for p in pieces)
+        vtx = torch.cat([p[0] for p in pieces])
+        offs, o = [], 0
+        for p in pieces:
+            offs.append(o)
+            o += p[0].shape[0]
+        idx = torch.cat([(p[1].to(torch.int64) + off).to(torch.int32) for p, off in zip(pieces, offs)])
+        del pieces
+    else:
+        kid, nx, ny, nz, D = CFG[a.config]
+        E, V = ctypes.c_uint64(), ctypes.c_uint64()
+        lib.rmx_lattice_sizes(kid, nx, ny, nz, 1 << 63, ctypes.byref(E), ctypes.byref(V))
+        E, V = E.value, V.value
+        vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
+        idx = torch.empty((E, D), dtype=torch.int32, device=dev)
+        _native.check(lib.rmx_gen_lattice_soup(kid, nx, ny, nz, 0, 1 << 63, vtx.data_ptr(), idx.data_ptr(),
+                                               s.cuda_stream))
     out_v = torch.empty_like(vtx)
     out_e = torch.empty_like(idx)
     info = torch.zeros(2, dtype=torch.int64, device=dev)
