@@ -86,7 +86,7 @@ struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, hist, vary, fields, fill, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, markbits, hist, vary, fields, fill, counters, desc, desc3, ctl_end;
     int bucket_shift;
     uint32_t ntiles_pk, ntiles3_pk, pk_cstride;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
@@ -125,6 +125,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.pk_digits = take(static_cast<size_t>(V) + 16);
     L.ukeys = take(static_cast<size_t>(V) * 8);
     L.ctl_begin = off;
+    L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
     L.fields = take(static_cast<size_t>(L.D) * kFieldWords * 4);
@@ -482,14 +483,21 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     RMX_CHECK(cudaMemsetAsync(base + L.ctl_begin, 0, L.ctl_end - L.ctl_begin, s));
     if (V) RMX_CHECK(cudaMemsetAsync(flags, 0, V, s));
 
-    // K1 mark
+    // K1 mark (byte flags for in-order indices, a bit set for scattered ones), then merge them
     {
-        MarkArgs a{idx, I, V, flags, d_status, aligned16(idx) ? 1 : 0};
+        uint32_t* bits = reinterpret_cast<uint32_t*>(base + L.markbits);
+        MarkArgs a{idx, I, V, flags, bits, d_status, aligned16(idx) ? 1 : 0};
         int grid = 0;
         rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
         if (rc) return rc;
         k_mark<<<grid, kBlock, 0, s>>>(a);
         RMX_CHECK(cudaGetLastError());
+        if (V) {
+            rc = grid_for_stream((V + 31) / 32, grid);
+            if (rc) return rc;
+            k_expand_marks<<<grid, kBlock, 0, s>>>(bits, V, flags);
+            RMX_CHECK(cudaGetLastError());
+        }
     }
     if ((rc = rec.mark())) return rc;
     if (V == 0) {  // every index is out of range; status is set
@@ -711,10 +719,10 @@ void rmx_graph_destroy(rmx_graph* graph) {
 }
 
 int rmx_kernel_launches(uint32_t dim) {
-    // mark, vary, plan, build_rows, first_hist, 4*dim AoS passes, pack,
+    // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes, pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
-    return 5 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
+    return 6 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
 }
 
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }

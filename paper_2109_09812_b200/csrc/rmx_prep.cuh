@@ -7,30 +7,66 @@ namespace rmx {
 
 // ---------------------------------------------------------------------------
 // K1: mark used vertices; any index >= n_vtx sets the status bit.
+// Each warp looks at its first 128 indices: when they fall in a window of
+// kMarkWindow vertices (soups, grid meshes: indices in or near element order)
+// it writes the byte flags directly -- the window's sectors merge in L2.
+// Otherwise (shuffled indexed meshes) it sets bits in a bit set instead (V/8
+// bytes, L2-resident up to ~10^9 vertices) with atomicOr: a direct byte store
+// there costs a DRAM read-modify-write per index.  Either choice is correct
+// for any index order.  k_expand_marks ORs the bit set into the byte flags.
+constexpr uint32_t kMarkWindow = 1u << 16;
+
 struct MarkArgs {
     const uint32_t* idx;
     uint64_t n_idx;
     uint64_t n_vtx;
-    uint8_t* flags;
+    uint8_t* flags;   // [n_vtx] zeroed
+    uint32_t* bits;   // [ceil(n_vtx / 32)] zeroed
     uint32_t* status;
-    int vec;  // idx 16-byte aligned
+    int vec;          // idx 16-byte aligned
 };
 
 __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
     bool bad = false;
     uint64_t done = 0;
     if (a.vec) {
         const uint64_t n4 = a.n_idx >> 2;
         const uint4* i4 = reinterpret_cast<const uint4*>(a.idx);
-        for (uint64_t i = gtid; i < n4; i += stride) {
-            const uint4 v = __ldcs(i4 + i);
-            const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+        const uint64_t wbase = gtid - lane;  // warp-uniform trip count for the vote below
+        int local = -1;                      // decided on the warp's first group of indices
+        for (uint64_t i0 = wbase; i0 < n4; i0 += stride) {
+            const uint64_t i = i0 + lane;
+            uint32_t x[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+            if (i < n4) {
+                const uint4 v = __ldcs(i4 + i);
+                x[0] = v.x;
+                x[1] = v.y;
+                x[2] = v.z;
+                x[3] = v.w;
+            }
+            uint32_t lo = 0xFFFFFFFFu, hi = 0u;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (x[k] < a.n_vtx) a.flags[x[k]] = 1;
-                else bad = true;
+                if (x[k] < a.n_vtx) {
+                    lo = min(lo, x[k]);
+                    hi = max(hi, x[k]);
+                } else if (i < n4) {
+                    bad = true;
+                }
+            }
+            if (local < 0) {
+                const uint32_t wlo = __reduce_min_sync(kFull, lo), whi = __reduce_max_sync(kFull, hi);
+                local = (wlo == 0xFFFFFFFFu || whi - wlo < kMarkWindow) ? 1 : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (x[k] < a.n_vtx) {
+                    if (local) a.flags[x[k]] = 1;
+                    else atomicOr(a.bits + (x[k] >> 5), 1u << (x[k] & 31u));
+                }
             }
         }
         done = n4 << 2;
@@ -40,7 +76,22 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
         if (x < a.n_vtx) a.flags[x] = 1;
         else bad = true;
     }
-    if (__any_sync(kFull, bad) && (threadIdx.x & 31u) == 0u) atomicOr(a.status, RMX_STATUS_INDEX_OUT_OF_RANGE);
+    if (__any_sync(kFull, bad) && lane == 0u) atomicOr(a.status, RMX_STATUS_INDEX_OUT_OF_RANGE);
+}
+
+// flags |= bit set (one word of 32 vertices per thread; words with no bit
+// set -- all of them when no warp took the scattered path -- cost one load).
+__global__ void __launch_bounds__(kBlock) k_expand_marks(const uint32_t* bits, uint64_t n_vtx, uint8_t* flags) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t nw = (n_vtx + 31) >> 5;
+    for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; w < nw; w += stride) {
+        uint32_t b = __ldcs(bits + w);
+        while (b) {
+            const uint32_t t = __ffs(b) - 1u;
+            flags[(w << 5) + t] = 1;
+            b &= b - 1u;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

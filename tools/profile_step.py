@@ -25,9 +25,9 @@ def main():
     lib = _native.lib()
     dev = torch.device("cuda", 0)
     s = torch.cuda.current_stream(dev)
-    if a.config == "C4":  # 8 welded tiles concatenated with index offsets (the merge input)
+    if a.config in ("C4", "C4S"):  # 8 welded tiles concatenated with index offsets (the merge input)
         from paper_2109_09812_b200 import gen
-        pieces = [gen.welded_tile_tensors(5000, 4500 * k, k) for k in range(8)]
+        pieces = [gen.welded_tile_tensors(5000, 4500 * k, k, a.config == "C4S") for k in range(8)]
         D = 3
         V = sum(p[0].shape[0] for p in pieces)
         E = sum(p[1].shape[0] for p in pieces)
