@@ -251,3 +251,33 @@ def test_c4_merge_full_size(rmx):
     check_determining_properties(vtx, idx, res.vertices, res.elements, 182_541_501)
     del res, vtx, idx
     torch.cuda.empty_cache()
+
+
+def test_more_than_2_31_vertices(rmx):
+    """V = 2^31 + 4099 one-word vertices, every row used once (arity 1): indices and positions past
+    the int32 range, 700K tiles per pass.  Output checked by the determining properties, chunked."""
+    import torch
+    V = (1 << 31) + 4099
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120 * (1 << 30):
+        pytest.skip(f"needs ~120 GB free device memory, have {free / 2**30:.0f} GB")
+    dev = torch.device("cuda")
+    ar = torch.arange(V, dtype=torch.int64, device=dev)
+    # 2^30 distinct values (x * odd constant mod 2^30), bit 31 set on half of them
+    vals = ((ar * 2654435761) & ((1 << 30) - 1)) | ((ar & 1) << 31)
+    vtx = torch.where(vals >= 2**31, vals - 2**32, vals).to(torch.int32).view(V, 1)
+    idx = torch.where(ar >= 2**31, ar - 2**32, ar).to(torch.int32).view(V, 1)
+    del ar, vals
+    res = rmx.reindex_tensors(vtx, idx)
+    out_v, out_e = res.vertices, res.elements
+    U = out_v.shape[0]
+    assert 0 < U <= V
+    chunk = 1 << 27
+    for s in range(0, U - 1, chunk):
+        a = out_v[s:s + chunk + 1].view(-1).to(torch.int64) & 0xFFFFFFFF
+        assert bool((a[1:] > a[:-1]).all())
+    for s in range(0, V, chunk):
+        e = out_e[s:s + chunk].view(-1).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(out_v.view(-1)[e], vtx.view(-1)[s:s + chunk])
+    del res, out_v, out_e, vtx, idx
+    torch.cuda.empty_cache()
