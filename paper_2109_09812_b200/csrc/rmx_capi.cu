@@ -586,7 +586,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
         if ((rc = launch_unique_pk(a, s))) return rc;
         UnpackPkArgs u{plan, vtx, idx, vary, fields, ukeys, out_vtx, reinterpret_cast<unsigned long long*>(d_count),
-                       d_status, L.D};
+                       d_status, L.D, aligned16(out_vtx) ? 1 : 0};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
     if ((rc = cond_end(gc))) return rc;

@@ -897,6 +897,7 @@ struct UnpackPkArgs {
     const unsigned long long* count;
     const uint32_t* status;
     int dim;
+    int vec;  // out_vtx 16-byte aligned
 };
 
 template <int D_CT>
@@ -937,7 +938,28 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
     const uint64_t* k64 = static_cast<const uint64_t*>(a.ukeys);
     const uint32_t* k32 = static_cast<const uint32_t*>(a.ukeys);
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < U; i += stride) {
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    uint64_t done = 0;
+    if constexpr (D_CT == 3 || D_CT == 4) {
+        if (a.vec) {  // 4 rows per thread, written as D_CT 16-byte stores
+            uint32_t w[4 * D_CT];
+            const uint64_t ng = U >> 2;
+            for (uint64_t g = t0; g < ng; g += stride) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint64_t i = 4 * g + r;
+                    const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+                    unpack_row<D_CT>(key, w + r * D_CT, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
+                }
+                uint4* dst = reinterpret_cast<uint4*>(a.out_vtx + 4 * g * D_CT);
+#pragma unroll
+                for (int q = 0; q < D_CT; ++q)
+                    __stcs(dst + q, make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+            }
+            done = ng << 2;
+        }
+    }
+    for (uint64_t i = done + t0; i < U; i += stride) {
         const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
         unpack_row<D_CT>(key, a.out_vtx + i * D, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
     }
