@@ -382,6 +382,13 @@ struct Recorder {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// small meshes take the one-CTA path (RMX_SMALL=0 forces the large-mesh pipeline, for tests)
+bool small_path(uint64_t V, uint32_t D, uint64_t I) {
+    if (V < 1 || V > kSmallV || D > kSmallD || I > kSmallI) return false;
+    const char* e = std::getenv("RMX_SMALL");  // read per call: tests switch it at run time
+    return !(e && e[0] == '0');
+}
+
 // ---- graph launch path ------------------------------------------------------
 // run_pipeline emits its launches onto a capturing stream; each section that
 // may be a no-op for the data at hand (AoS vs packed, each sort pass) becomes
@@ -466,6 +473,18 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (!ws || ws_bytes < L.total) {
         std::snprintf(g_err, sizeof(g_err), "workspace %zu bytes < required %zu", ws_bytes, L.total);
         return RMX_ENOSPC;
+    }
+    if (small_path(V, D, I)) {  // one CTA does it all (rmx_small.cuh)
+        const size_t smem = small_smem_bytes(static_cast<uint32_t>(V), D);
+        RMX_CHECK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        SmallArgs a{vtx, static_cast<uint32_t>(V), D, idx, I, out_vtx, out_idx,
+                    reinterpret_cast<unsigned long long*>(d_count), d_status, sc ? *sc : rmx_scratch{}};
+        k_small<<<1, kSmallThreads, smem, s>>>(a);
+        RMX_CHECK(cudaGetLastError());
+        while (rec.k < rec.n) {  // stage events of a profiled call: all at the end
+            if ((rc = rec.mark())) return rc;
+        }
+        return RMX_OK;
     }
     char* base = static_cast<char*>(ws);
     uint8_t* flags = (sc && sc->is_used) ? sc->is_used : reinterpret_cast<uint8_t*>(base + L.flags);
@@ -672,7 +691,9 @@ int rmx_graph_create(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim
     int rc = RMX_OK;
     if (cudaGraphCreate(&gc.g, 0) != cudaSuccess) rc = RMX_ECUDA;
     const int P = 4 * static_cast<int>(dim);
-    gc.gh.n = kSlotAosPass + P + kMaxPackedPasses;
+    // the one-CTA small-mesh path and the zero-element case have no conditional sections
+    const bool plain = n_elements == 0 || small_path(n_vertices, dim, n_elements * arity);
+    gc.gh.n = plain ? 0 : kSlotAosPass + P + kMaxPackedPasses;
     for (int i = 0; i < gc.gh.n && rc == RMX_OK; ++i)
         if (cudaGraphConditionalHandleCreate(&gc.gh.h[i], gc.g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
             rc = RMX_ECUDA;

@@ -17,6 +17,7 @@
 //                       (pipeline.py:72-113, primitives.py:43-69)
 //   K3b  k_map_fill     map[org] = new_idx from the bucket-major pairs
 //   K4   k_remap        out_idx = map[idx] (remap_elements pipeline.py:116-130)
+//   small k_small       the whole pipeline in one CTA for small meshes (rmx_small.cuh)
 //   gen  k_gen_lattice  synthetic bench input (oracle/lattice.py recipe)
 //
 // Data layout in HBM: a row is W = D+1 uint32 words -- the D key words of the
@@ -33,3 +34,4 @@
 #include "rmx_packed.cuh"
 #include "rmx_gen.cuh"
 #include "rmx_steps.cuh"
+#include "rmx_small.cuh"

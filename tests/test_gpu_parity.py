@@ -29,8 +29,15 @@ def as_mesh(p, in_vtx, in_idx):
     return p.Mesh(np.asarray(in_vtx, np.uint32).view(np.float32), in_idx)
 
 
+@pytest.fixture(params=["small", "large"])
+def mesh_path(request, monkeypatch):
+    """Run a test through the one-CTA small-mesh path and through the large-mesh pipeline."""
+    monkeypatch.setenv("RMX_SMALL", "1" if request.param == "small" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("name,case", CASES, ids=[c[0] for c in CASES])
-def test_reindex_matches_reference_golden(rmx, name, case):
+def test_reindex_matches_reference_golden(rmx, name, case, mesh_path):
     out, sc = rmx.reindex(as_mesh(rmx, case["in_vtx"], case["in_idx"]))
     assert np.array_equal(out.vertices.view(np.uint32), case["out_vtx"])
     assert np.array_equal(out.elements, case["out_idx"])
@@ -59,7 +66,7 @@ def test_worked_example_criterion_1(rmx):
     assert best < 1e-3, best
 
 
-def test_out_of_range_raises_with_issue_list(rmx):
+def test_out_of_range_raises_with_issue_list(rmx, mesh_path):
     with pytest.raises(rmx.InvalidMeshError) as err:
         rmx.reindex(rmx.Mesh(np.array([(0, 0), (1, 1)], np.float32), np.array([(0, 1, 2)], np.uint32)))
     assert err.value.issues == [rmx.Issue(element=0, slot=2, index=2)]
@@ -83,7 +90,7 @@ def test_dim_limit_is_a_mesh_error(rmx):
         rmx.reindex(rmx.Mesh(np.zeros((2, 33), np.float32), np.array([(0, 1)], np.uint32)))
 
 
-def test_idempotent_and_tensor_api(rmx):
+def test_idempotent_and_tensor_api(rmx, mesh_path):
     import torch
     c = load_group("random")["random_big"]
     mesh = as_mesh(rmx, c["in_vtx"], c["in_idx"])
@@ -281,3 +288,18 @@ def test_more_than_2_31_vertices(rmx):
         assert torch.equal(out_v.view(-1)[e], vtx.view(-1)[s:s + chunk])
     del res, out_v, out_e, vtx, idx
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("V,D,E,K", [(1, 1, 1, 1), (2048, 8, 3000, 3), (2048, 3, 40_000, 4), (1000, 5, 1, 2),
+                                     (2047, 1, 5000, 1), (1500, 2, 32_768, 4)])
+def test_small_path_limits_vs_oracle(rmx, V, D, E, K, mesh_path):
+    """Edges of the one-CTA path (V = 2048, D = 8, I = 2^17) and just inside, both paths."""
+    rng = np.random.default_rng(V + D + E)
+    words = rng.integers(0, 8, size=(V, D)).astype(np.uint32) * np.uint32(0x9E3779B1)
+    idx = rng.integers(0, V, size=(E, K)).astype(np.uint32)
+    ref = O.reindex(words, idx)
+    out, sc = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
