@@ -384,7 +384,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // small meshes take the one-CTA path (RMX_SMALL=0 forces the large-mesh pipeline, for tests)
 bool small_path(uint64_t V, uint32_t D, uint64_t I) {
-    if (V < 1 || V > kSmallV || D > kSmallD || I > kSmallI) return false;
+    if (V < 1 || V > kSmallV || D > kSmallD || V * D > kSmallWords || I > kSmallI) return false;
     const char* e = std::getenv("RMX_SMALL");  // read per call: tests switch it at run time
     return !(e && e[0] == '0');
 }

@@ -1,8 +1,8 @@
 // rmx_small.cuh -- the whole re-index of a small mesh in one CTA.
 //
-// For V <= kSmallV vertices (D <= kSmallD words each, I <= kSmallI index
-// slots) the ~50 launches of the large-mesh pipeline cost far more than the
-// work.  One 1024-thread CTA runs every step in shared memory with the same
+// For V <= kSmallV vertices (D <= kSmallD words each, V * D <= kSmallWords,
+// I <= kSmallI index slots) the ~50 launches of the large-mesh pipeline cost
+// far more than the work.  One 1024-thread CTA runs every step in shared memory with the same
 // semantics (pipeline.py:133-157):
 //   mark (pipeline.py:41-51) -> replace unused rows (54-63) -> stable
 //   lexicographic sort of (key words, row) by a bitonic network on row ids
@@ -16,9 +16,11 @@
 namespace rmx {
 
 constexpr int kSmallThreads = 1024;
-constexpr uint32_t kSmallV = 2048;            // bitonic network of <= 2048 ids: one pair per thread per step
+constexpr uint32_t kSmallV = 8192;            // bitonic network of <= 8192 row ids (<= 4 pairs per thread per step)
 constexpr uint32_t kSmallD = 8;
-constexpr uint64_t kSmallI = 1ull << 17;
+constexpr uint32_t kSmallWords = 24576;       // V * D key words in shared memory (96 KB)
+constexpr uint64_t kSmallI = 1ull << 18;
+constexpr int kSmallSlots = kSmallV / kSmallThreads;  // sorted slots per thread in the head scan
 
 __host__ __device__ inline size_t small_smem_bytes(uint32_t V, uint32_t D) {
     // keys, sorted ids (u16), map (u32), flags (u8), scan scratch
@@ -102,12 +104,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a) {
             __syncthreads();
         }
     }
-    // ---- head flags (reuse s_flag) and their inclusive scan -> new index per slot
-    uint32_t local[2] = {0, 0};
+    // ---- head flags and their inclusive scan -> new index per slot
+    uint32_t local[kSmallSlots];
     uint32_t sum = 0;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const uint32_t p = 2 * tid + r;
+    for (int r = 0; r < kSmallSlots; ++r) {
+        const uint32_t p = kSmallSlots * tid + r;
         uint32_t h = 0;
         if (p < V) {
             if (p == 0) {
@@ -130,8 +132,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a) {
     __syncthreads();
     uint32_t run = excl;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-        const uint32_t p = 2 * tid + r;
+    for (int r = 0; r < kSmallSlots; ++r) {
+        const uint32_t p = kSmallSlots * tid + r;
         run += local[r];
         if (p < V) {
             const uint32_t row = s_ord[p];

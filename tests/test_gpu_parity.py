@@ -290,10 +290,11 @@ def test_more_than_2_31_vertices(rmx):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("V,D,E,K", [(1, 1, 1, 1), (2048, 8, 3000, 3), (2048, 3, 40_000, 4), (1000, 5, 1, 2),
-                                     (2047, 1, 5000, 1), (1500, 2, 32_768, 4)])
+@pytest.mark.parametrize("V,D,E,K", [(1, 1, 1, 1), (3072, 8, 3000, 3), (8192, 3, 65_536, 4), (1000, 5, 1, 2),
+                                     (8191, 1, 5000, 1), (4500, 2, 32_768, 4), (2049, 7, 999, 3),
+                                     (8192, 3, 70_000, 4)])
 def test_small_path_limits_vs_oracle(rmx, V, D, E, K, mesh_path):
-    """Edges of the one-CTA path (V = 2048, D = 8, I = 2^17) and just inside, both paths."""
+    """Edges of the one-CTA path (V = 8192, V D = 24576, I = 2^18) and just past them, both paths."""
     rng = np.random.default_rng(V + D + E)
     words = rng.integers(0, 8, size=(V, D)).astype(np.uint32) * np.uint32(0x9E3779B1)
     idx = rng.integers(0, V, size=(E, K)).astype(np.uint32)
