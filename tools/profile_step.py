@@ -38,6 +38,12 @@ def main():
             o += p[0].shape[0]
         idx = torch.cat([(p[1].to(torch.int64) + off).to(torch.int32) for p, off in zip(pieces, offs)])
         del pieces
+    elif a.config == "C5s":  # one GPU's shard of C5 at 8 GPUs: the first 1/8 of the 1B-triangle soup
+        from paper_2109_09812_b200 import gen
+        E_all, _ = gen.lattice_sizes("tri", (20000, 25000))
+        vtx, idx = gen.lattice_soup_tensors("tri", (20000, 25000), seed=0, n_elem_take=E_all // 8)
+        V, D = vtx.shape
+        E = idx.shape[0]
     else:
         kid, nx, ny, nz, D = CFG[a.config]
         E, V = ctypes.c_uint64(), ctypes.c_uint64()
