@@ -170,7 +170,7 @@ def run_reference(args):
         "cpu_baseline": {"value": rate, "unit": "verts/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": rate, "unit": "verts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def executed_model(V, I, U, D, KW, npass):
@@ -363,7 +363,7 @@ def run_b200(args):
             "clocks": clk.summary(),
             "gpu_launches": lib.rmx_kernel_launches(D) * args.steps,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -411,7 +411,15 @@ def run_b200_dist(args):
     idx = torch.empty((E, K), dtype=torch.int32, device=dev)
     _native.check(lib.rmx_gen_lattice_soup_range(0, nx, ny, 0, 0, e0, e1, vtx.data_ptr(), idx.data_ptr(),
                                                  torch.cuda.current_stream(dev).cuda_stream))
-    comm = rdist.TorchComm(device=dev)
+    # data exchange over peer memory (symmetric buffers + rmx_scatter_rows); NCCL all-to-all only if
+    # the symmetric-memory rendezvous is not available on this box
+    try:
+        comm = rdist.SymmComm(device=dev)
+        comm._ensure(1 << 16)
+        exchange = "peer-memory stores (rmx_scatter_rows into symmetric buffers over NVLink)"
+    except Exception as exc:  # noqa: BLE001 - recorded in the JSON line
+        comm = rdist.TorchComm(device=dev)
+        exchange = f"NCCL all_to_all (symmetric memory unavailable: {type(exc).__name__}: {exc})"[:200]
     backend = rdist.CudaBackend(dev)
     expect_u = (nx + 1) * (ny + 1)
 
@@ -502,7 +510,8 @@ def run_b200_dist(args):
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": f"C2 per GPU: one shuffled float3 lattice soup of {nx}x{ny} quads "
                                    f"({E_all:,} triangles, {V_all:,} vertex slots), element ranges per rank",
-                       "n_vertices": V_all, "unique": expect_u, "parallelism": f"dp{world} sample sort (NCCL)",
+                       "n_vertices": V_all, "unique": expect_u, "parallelism": f"dp{world} sample sort",
+                       "exchange": exchange,
                        "l2": "inputs 2.5 GB per GPU > 126 MB L2, no flush needed"},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -515,12 +524,26 @@ def run_b200_dist(args):
             # per step: local re-index, sample sort/dedup, merge re-index (3 pipeline calls) + lower bound + gather
             "gpu_launches": (3 * lib.rmx_kernel_launches(D) + 2) * args.steps,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     tdist.barrier()
     tdist.destroy_process_group()
 
 
+_JSON_OUT = None  # the real stdout: libraries (NCCL prints its version banner) get stderr instead
+
+
+def emit(line: dict) -> None:
+    """The one JSON line of this run, on the original stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)  # anything else written to fd 1 (C libraries included) goes to stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

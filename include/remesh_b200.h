@@ -191,6 +191,18 @@ int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, 
 int rmx_offset_indices(const uint32_t* idx, uint64_t n, uint32_t offset, uint32_t* out, void* stream);
 
 /*
+ * Distributed exchange over peer memory:
+ * rows [bounds[g], bounds[g+1]) of src (n rows of `words` u32, sorted by
+ * destination) are stored into the buffer at dst_ptrs[g] (a peer GPU's
+ * symmetric receive buffer, reached over NVLink) starting at row dst_off[g].
+ * bounds (groups+1 entries), dst_ptrs and dst_off (groups entries) are
+ * DEVICE arrays.  Replaces the send staging + NCCL all-to-all of
+ * dist.py's exchange; the caller orders it with a barrier on the receivers.
+ */
+int rmx_scatter_rows(const uint32_t* src, uint64_t n, uint32_t words, const uint64_t* bounds, uint32_t groups,
+                     const uint64_t* dst_ptrs, const uint64_t* dst_off, void* stream);
+
+/*
  * Welded (indexed) tile of the C4 merge workload:
  * the triangulated n x n quad grid whose lattice rows start at row0, every
  * point stored once, 5 % unused rows; points and triangles row-major, or

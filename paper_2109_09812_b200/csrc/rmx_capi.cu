@@ -841,6 +841,20 @@ int rmx_offset_indices(const uint32_t* idx, uint64_t n, uint32_t offset, uint32_
     return RMX_OK;
 }
 
+int rmx_scatter_rows(const uint32_t* src, uint64_t n, uint32_t words, const uint64_t* bounds, uint32_t groups,
+                     const uint64_t* dst_ptrs, const uint64_t* dst_off, void* stream) {
+    g_err[0] = '\0';
+    if (n == 0) return RMX_OK;
+    if (!src || !bounds || !dst_ptrs || !dst_off || words < 1 || groups < 1) return RMX_EINVAL;
+    int grid = 0;
+    int rc = grid_for_stream(n * words, grid);
+    if (rc) return rc;
+    k_scatter_rows<<<grid, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(src, n, words, bounds, groups, dst_ptrs,
+                                                                           dst_off);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int rmx_welded_tile_sizes(uint32_t n, uint64_t* n_vertices, uint64_t* n_elements) {
     if (n < 1) return RMX_EINVAL;
     const uint64_t pts = static_cast<uint64_t>(n + 1) * (n + 1);

@@ -63,4 +63,29 @@ __global__ void __launch_bounds__(kBlock) k_offset_indices(const uint32_t* __res
     for (uint64_t i = done + t0; i < n; i += stride) out[i] = idx[i] + offset;
 }
 
+// Distributed exchange over peer memory (dist.SymmComm): rows [bounds[g],
+// bounds[g+1]) of the sorted local array go straight into peer g's symmetric
+// receive buffer at row dst_off[g] -- the partition and the NVLink transfer in
+// one kernel, no send staging, no NCCL kernel.  One thread per output word:
+// reads are coalesced, and so are the stores inside each destination range.
+__global__ void __launch_bounds__(kBlock) k_scatter_rows(const uint32_t* __restrict__ src, uint64_t n, uint32_t words,
+                                                         const uint64_t* __restrict__ bounds, uint32_t G,
+                                                         const uint64_t* __restrict__ dst_ptrs,
+                                                         const uint64_t* __restrict__ dst_off) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    const uint64_t total = n * words;
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; t < total; t += stride) {
+        const uint64_t row = t / words;
+        const uint32_t w = static_cast<uint32_t>(t - row * words);
+        uint32_t lo = 0, hi = G;  // last g with bounds[g] <= row
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (bounds[mid] <= row) lo = mid;
+            else hi = mid;
+        }
+        uint32_t* dst = reinterpret_cast<uint32_t*>(dst_ptrs[lo]);
+        dst[(dst_off[lo] + row - bounds[lo]) * words + w] = src[t];
+    }
+}
+
 }  // namespace rmx

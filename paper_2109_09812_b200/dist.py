@@ -25,10 +25,11 @@ Algorithm (a sample sort on deduplicated keys):
    order, i.e. its old->new map, with no scatter;
 7. ``rmx_gather_u32`` remaps the local elements.
 
-Collectives go through a small ``Comm`` interface: :class:`TorchComm`
-(torch.distributed -- NCCL over NVLink on GPUs, gloo on CPU) or
-:class:`ThreadComm` (G ranks as threads of one process, for tests on one GPU
-or on CPU).  The local steps go through a backend: :class:`CudaBackend` is the
+Collectives go through a small ``Comm`` interface: :class:`SymmComm` (GPUs:
+the data exchange as ``rmx_scatter_rows`` stores into the peers' symmetric
+buffers over NVLink, the small collectives on NCCL), :class:`TorchComm`
+(torch.distributed all-to-all -- NCCL, or gloo on CPU) or :class:`ThreadComm`
+(G ranks as threads of one process, for tests on one GPU or on CPU).  The local steps go through a backend: :class:`CudaBackend` is the
 product; tests may inject a CPU backend.
 """
 from __future__ import annotations
@@ -94,6 +95,71 @@ class TorchComm(Comm):
         out = t.new_empty((sum(recv_counts),) + tuple(t.shape[1:]))
         self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=recv_counts,
                                     input_split_sizes=list(send_counts), group=self.group)
+        return out, recv_counts
+
+
+class SymmComm(TorchComm):
+    """TorchComm whose all-to-all moves the rows over peer memory.
+
+    Small collectives (counts, samples, sizes) stay on torch.distributed
+    (NCCL).  The data exchange writes each rank's partition straight into the
+    receivers' symmetric buffers (``torch.distributed._symmetric_memory``,
+    CUDA IPC over NVLink) with ``rmx_scatter_rows``: the partition and the
+    transfer are one kernel, with no send staging and no NCCL kernel
+    ("B200-native fused variant").  Two device-side
+    barriers per exchange order it: one before writing (every receiver has
+    copied the previous exchange out), one after (all writes have landed).
+    """
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        super().__init__(group, device)
+        import torch.distributed._symmetric_memory as symm
+        self.symm = symm
+        self.group_name = (group if group is not None else self.dist.group.WORLD).group_name
+        self.lib = _native.lib()
+        self._buf = None
+        self._handle = None
+        self._cap = 0  # int32 words
+
+    def _ensure(self, words: int) -> None:
+        """Collective: every rank calls it with the same ``words``."""
+        if words <= self._cap:
+            return
+        cap = max(words, int(self._cap * 1.5), 1 << 16)
+        buf = self.symm.empty(cap, dtype=torch.int32, device=self.device)
+        self._handle = self.symm.rendezvous(buf, self.group_name)
+        self._buf = buf
+        self._cap = cap
+
+    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+        G, me = self.size, self.rank
+        if t.dtype != torch.int32:
+            raise MeshError("SymmComm exchanges int32 rows")
+        words = 1
+        for x in t.shape[1:]:
+            words *= int(x)
+        sc = torch.tensor(send_counts, dtype=torch.int64, device=self.device)
+        allc = torch.empty(G * G, dtype=torch.int64, device=self.device)
+        self.dist.all_gather_into_tensor(allc, sc, group=self.group)
+        C = [[int(v) for v in row] for row in allc.view(G, G).tolist()]  # C[s][g]: rows s sends to g
+        recv_counts = [C[s][me] for s in range(G)]
+        recv_total = sum(recv_counts)
+        self._ensure(max(sum(C[s][g] for s in range(G)) for g in range(G)) * words)
+        bounds = [0]
+        for c in send_counts:
+            bounds.append(bounds[-1] + c)
+        dst_off = [sum(C[s][g] for s in range(me)) for g in range(G)]
+        meta = torch.tensor(bounds + dst_off, dtype=torch.int64, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self._handle.barrier(channel=0)
+        n = t.shape[0]
+        if n:
+            src = t.contiguous()
+            _native.check(self.lib.rmx_scatter_rows(src.data_ptr(), n, words, meta.data_ptr(), G,
+                                                    self._handle.buffer_ptrs_dev, meta.data_ptr() + 8 * (G + 1),
+                                                    stream))
+        self._handle.barrier(channel=0)
+        out = self._buf[:recv_total * words].view((recv_total,) + tuple(t.shape[1:])).clone()
         return out, recv_counts
 
 
@@ -282,5 +348,5 @@ def run_threads(shards, backend_factory, samples_per_rank: int = 1024) -> list[D
     return results
 
 
-__all__ = ["Comm", "TorchComm", "ThreadComm", "ThreadHub", "CudaBackend", "DistResult",
+__all__ = ["Comm", "TorchComm", "SymmComm", "ThreadComm", "ThreadHub", "CudaBackend", "DistResult",
            "reindex_distributed", "run_threads"]

@@ -75,3 +75,57 @@ def test_range_generator_is_a_shard_of_the_soup(cuda_ok, e0, e1):
     if e1 > e0:
         assert np.array_equal(dv[: s1 - s0].cpu().numpy().view(np.uint32), bits[s0:s1])
         assert np.array_equal(de[: e1 - e0].cpu().numpy().view(np.uint32), (e[e0:e1] - s0).astype(np.uint32))
+
+
+@pytest.mark.parametrize("G,words", [(1, 3), (2, 1), (5, 4), (8, 3), (16, 2)])
+def test_scatter_rows_into_peer_buffers(cuda_ok, G, words):
+    """rmx_scatter_rows with G 'peer' buffers on one GPU: rows [bounds[g], bounds[g+1]) land in
+    buffer g from row dst_off[g] (the layout SymmComm relies on)."""
+    from paper_2109_09812_b200 import _native
+    rng = np.random.default_rng(G * 10 + words)
+    counts = rng.integers(0, 500, size=G)
+    counts[G // 2] = 0
+    n = int(counts.sum())
+    src = torch.from_numpy(rng.integers(-2**31, 2**31 - 1, size=(n, words), dtype=np.int64).astype(np.int32)).cuda()
+    offs = rng.integers(0, 300, size=G)
+    peers = [torch.full((int(offs[g] + counts[g] + 10), words), -1, dtype=torch.int32, device="cuda")
+             for g in range(G)]
+    bounds = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    meta = torch.tensor(np.concatenate([bounds, offs]).astype(np.int64), device="cuda")
+    ptrs = torch.tensor([p.data_ptr() for p in peers], dtype=torch.int64, device="cuda")
+    _native.check(_native.lib().rmx_scatter_rows(src.data_ptr(), n, words, meta.data_ptr(), G, ptrs.data_ptr(),
+                                                 meta.data_ptr() + 8 * (G + 1),
+                                                 torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for g in range(G):
+        got = peers[g].cpu()
+        assert torch.equal(got[offs[g]:offs[g] + counts[g]], src[bounds[g]:bounds[g + 1]].cpu())
+        assert bool((got[:offs[g]] == -1).all()) and bool((got[offs[g] + counts[g]:] == -1).all())
+
+
+def test_symm_comm_world_of_one(cuda_ok):
+    """SymmComm (symmetric memory + rmx_scatter_rows) in a one-rank NCCL group: the exchange is the
+    identity, and reindex_distributed through it equals the single-GPU re-index."""
+    import socket
+
+    import torch.distributed as tdist
+
+    import paper_2109_09812_b200 as rmx
+    from paper_2109_09812_b200.dist import CudaBackend, SymmComm, reindex_distributed
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dev = torch.device("cuda", 0)
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1, device_id=dev)
+    try:
+        comm = SymmComm(device=dev)
+        rows = torch.randint(-2**31, 2**31 - 1, (12345, 3), dtype=torch.int32, device=dev)
+        out, rc = comm.all_to_all(rows, [12345])
+        assert rc == [12345] and torch.equal(out, rows)
+        shards = random_shards(3, 1)
+        (v, e), = as_tensors(shards, "cuda")
+        res = reindex_distributed(v, e, comm, CudaBackend(dev))
+        ref = rmx.reindex_tensors(v, e)
+        assert torch.equal(res.vertices, ref.vertices) and torch.equal(res.elements, ref.elements)
+    finally:
+        tdist.destroy_process_group()
