@@ -260,9 +260,15 @@ def run_b200(args):
     active = sorted((stage_ms[n] for n in pass_names), reverse=True)[:executed]
     pass_ms = sum(active) / max(1, len(active))
     row_bytes = (4 * key_words + 4) if packed else (4 * D + 4)
-    # packed pass: keys + origins in and out, plus the next-digit byte written here and read by
-    # the next upsweep; AoS pass: rows in and out
-    pass_bytes = (2 * row_bytes + 2) * V if packed else 2 * row_bytes * V
+    # packed pass: keys + origins in and out, the digit byte read by its upsweep and the next
+    # pass's digit byte written (pass 0 reads no origins: they are the row numbers; the last pass
+    # writes no next digit) -- mean over the executed passes; AoS pass: rows in and out
+    if packed:
+        per_pass = [8 * key_words + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < executed else 0)
+                    for p in range(executed)]
+        pass_bytes = sum(per_pass) / len(per_pass) * V
+    else:
+        pass_bytes = 2 * row_bytes * V
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     nominal = (32 * D * D + 44 * D + 15) * V + 16 * E * K + 4 * D * expect_u

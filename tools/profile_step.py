@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--no-compare", action="store_true", help="skip the direct-vs-graph timing (ncu launch lists)")
     a = ap.parse_args()
     lib = _native.lib()
     dev = torch.device("cuda", 0)
@@ -73,8 +74,8 @@ def main():
         print(f"{names[k]:>14s} {ms:8.3f} ms")
     print(f"{'total':>14s} {tot:8.3f} ms")
     # whole-step time: direct launches vs the captured graph (conditional nodes)
-    g = pipeline.PipelineGraph(vtx, V, D, idx, E, D, out_v, out_e, info, ws)
-    for name, fn in (("direct", lambda: pipeline.launch(vtx, V, D, idx, E, D, out_v, out_e, info, ws, None, s)),
+    g = pipeline.PipelineGraph(vtx, V, D, idx, E, D, out_v, out_e, info, ws) if not a.no_compare else None
+    for name, fn in [] if a.no_compare else (("direct", lambda: pipeline.launch(vtx, V, D, idx, E, D, out_v, out_e, info, ws, None, s)),
                      ("graph", lambda: g.launch(s))):
         fn()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

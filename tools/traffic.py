@@ -48,7 +48,8 @@ def main():
             cur += b
             per_pass.append(cur)
     executed = per_pass[:npass]
-    algo = (2 * (4 * kw + 4) + 2) * V
+    per_pass = [8 * kw + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass)]
+    algo = sum(per_pass) / npass * V
     out_path = os.path.join(ROOT, "profiles", "traffic.json")
     data = json.load(open(out_path)) if os.path.exists(out_path) else {}
     data[cfg] = {
@@ -58,8 +59,9 @@ def main():
         "source": f"{os.path.basename(path)} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, one step of "
                   f"tools/profile_step.py --config {cfg}), mean over the executed packed passes of "
                   "upsweep + colscan + downsweep",
-        "note": "algorithmic = keys + origins read and written (2 x (4 KW + 4) B/row) + the next-digit byte "
-                "written by the downsweep and read by the next upsweep (2 B/row)",
+        "note": "algorithmic, mean over the executed passes = keys + origins read and written (pass 0 reads no "
+                "origins), the pass's digit byte read by its upsweep, the next pass's digit byte written "
+                "(not by the last pass)",
     }
     json.dump(data, open(out_path, "w"), indent=1)
     print(json.dumps(data[cfg], indent=1))
