@@ -175,9 +175,16 @@ def run_reference(args):
 
 def executed_model(V, I, U, D, KW, npass):
     """Algorithmic HBM bytes of one packed-path step (the kernels that ran)."""
-    return int((4 * I + 2 * V) + (4 * D + 1) * V + (4 * D + 1) * V + (4 * KW + 5) * V
-               + npass * (8 * KW + 10) * V + 4 * KW * V + (4 * KW + 12) * V + 4 * KW * U
-               + (4 * KW + 4 * D) * U + 12 * V + 12 * I)
+    passes = sum(8 * KW + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass))
+    return int((4 * I + 2 * V)                       # mark: indices in, flags cleared + set
+               + (4 * D + 1) * V                     # vary: rows + flags
+               + (4 * D + 1) * V + (4 * KW + 1) * V  # pack: rows + flags in, keys + digit 0 out
+               + passes * V                          # LSD passes
+               + 4 * KW * V                          # head count
+               + (4 * KW + 12) * V + 4 * KW * U      # unique: keys + origins in, pairs + unique keys out
+               + (4 * KW + 4 * D) * U                # unpack
+               + 12 * V                              # map fill: pairs in, map out
+               + 12 * I)                             # remap: indices + map in, indices out
 
 
 def run_b200(args):
@@ -359,7 +366,7 @@ def run_b200(args):
                 "achieved_gbs": executed_bytes / (ms * 1e-3) / 1e9 if executed_bytes else None,
                 "frac": executed_bytes / (ms * 1e-3) / 1e9 / hbm if executed_bytes else None,
                 "note": "algorithmic bytes of the kernels that ran (DESIGN.md (d)): mark 4I+2V, vary (4D+1)V, "
-                        "pack (4D+1)V+(4KW+5)V, per pass (8KW+10)V, head count 4KW V, unique (4KW+12)V+4KW U, "
+                        "pack (4D+1)V+(4KW+1)V, per pass <= (8KW+10)V, head count 4KW V, unique (4KW+12)V+4KW U, "
                         "unpack (4KW+4D)U, map fill 12V, remap 12I",
                 "survey_nominal_bytes": nominal,
                 "survey_note": "SURVEY 8(d) nominal model (32D^2+44D+15)V+16I+4DU counts 4D byte passes of 16 B "
