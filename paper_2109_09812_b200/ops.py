@@ -18,14 +18,15 @@ from __future__ import annotations
 import numpy as np
 import torch
 
+from . import hostio
 from .mesh import MAX_VERTICES, Mesh, MeshError, require_valid
 from .pipeline import _device, host_tensor, reindex, reindex_tensors
 
 
 def _to_mesh(res) -> Mesh:
-    v = res.vertices.cpu().numpy().view(np.float32)
-    e = res.elements.cpu().numpy().view(np.uint32)
-    return Mesh._adopt(np.ascontiguousarray(v), np.ascontiguousarray(e))
+    v = hostio.to_host(res.vertices).view(np.float32)
+    e = hostio.to_host(res.elements).view(np.uint32)
+    return Mesh._adopt(v, e)
 
 
 def merge(meshes, device=None) -> Mesh:

@@ -31,7 +31,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _native
+from . import _native, hostio
 from .mesh import InvalidMeshError, Mesh, MeshError, validate
 
 _SCRATCH_FIELDS = ("is_used", "org_id", "nodup", "new_idx", "perm")
@@ -230,17 +230,19 @@ class ReindexScratch:
             E, K = elements.shape
             dev = self._device
             with torch.cuda.device(dev):
-                vtx_d = host_tensor(np.ascontiguousarray(vertices).view(np.int32).reshape(V, D)).to(dev)
-                idx_d = host_tensor(np.ascontiguousarray(elements).view(np.int32).reshape(E, K)).to(dev)
+                vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
+                idx_d = torch.empty((E, K), dtype=torch.int32, device=dev)
+                hostio.to_device(np.ascontiguousarray(vertices), vtx_d)
+                hostio.to_device(np.ascontiguousarray(elements), idx_d)
                 res = reindex_tensors(vtx_d, idx_d, scratch=True)
                 sc = res.scratch
                 n = V if E else 0
                 arrays = dict(
-                    is_used=sc["is_used"].cpu().numpy().astype(bool),
-                    org_id=sc["org_id"][:n].cpu().numpy().view(np.uint32),
-                    nodup=sc["nodup"][:n].cpu().numpy().astype(bool),
-                    new_idx=sc["new_idx"][:n].cpu().numpy().view(np.uint32),
-                    perm=sc["perm"][:n].cpu().numpy().view(np.uint32))
+                    is_used=hostio.to_host(sc["is_used"]).view(bool),
+                    org_id=hostio.to_host(sc["org_id"][:n]).view(np.uint32),
+                    nodup=hostio.to_host(sc["nodup"][:n]).view(bool),
+                    new_idx=hostio.to_host(sc["new_idx"][:n]).view(np.uint32),
+                    perm=hostio.to_host(sc["perm"][:n]).view(np.uint32))
             for a in arrays.values():
                 a.flags.writeable = False
             object.__setattr__(self, "_arrays", arrays)
@@ -303,8 +305,8 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
         stream = torch.cuda.current_stream(dev)
         vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
         idx_d = torch.empty((E, K), dtype=torch.int32, device=dev)
-        vtx_d.copy_(host_tensor(vertices.view(np.int32)))
-        idx_d.copy_(host_tensor(elements.view(np.int32)))
+        hostio.to_device(vertices, vtx_d)
+        hostio.to_device(elements, idx_d)
         out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
         out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
         info = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -313,8 +315,8 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
         count, status = (int(x) for x in info.cpu())
         if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
             raise InvalidMeshError(validate(_Arrays(vertices, elements)))
-        host_v = out_v[:count].cpu().numpy().view(np.float32)
-        host_e = out_e.cpu().numpy().view(np.uint32)
+        host_v = hostio.to_host(out_v[:count]).view(np.float32)
+        host_e = hostio.to_host(out_e).view(np.uint32)
     return Mesh._adopt(host_v, host_e), ReindexScratch(vertices, elements, count, dev)
 
 
