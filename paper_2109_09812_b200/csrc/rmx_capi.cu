@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/remesh_b200.h"
 #include "rmx_kernels.cuh"
@@ -159,13 +160,46 @@ int device_sms(int& sms) {
     return RMX_OK;
 }
 
+// Opt a kernel in to `smem` bytes of dynamic shared memory on the current
+// device.  The attribute only ever grows: calls on other threads with a
+// smaller need (another dim, a smaller mesh) must not shrink it under a
+// launch that is about to use more.
+std::mutex g_attr_mu;
+struct SmemAttr {
+    const void* fn;
+    int dev;
+    size_t bytes;
+};
+std::vector<SmemAttr> g_attr;
+
+template <typename K>
+int ensure_smem(K kernel, size_t smem) {
+    if (smem <= 48 * 1024) return RMX_OK;
+    int dev = 0;
+    RMX_CHECK(cudaGetDevice(&dev));
+    const void* fn = reinterpret_cast<const void*>(kernel);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    for (SmemAttr& e : g_attr) {
+        if (e.fn == fn && e.dev == dev) {
+            if (e.bytes < smem) {
+                RMX_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                e.bytes = smem;
+            }
+            return RMX_OK;
+        }
+    }
+    RMX_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    g_attr.push_back(SmemAttr{fn, dev, smem});
+    return RMX_OK;
+}
+
 // Persistent grid size for a kernel: resident CTAs per SM x SMs.
 template <typename K>
 int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
     int sms = 0;
     int rc = device_sms(sms);
     if (rc) return rc;
-    if (smem > 48 * 1024) RMX_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if ((rc = ensure_smem(kernel, smem))) return rc;
     int per_sm = 0;
     RMX_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
     if (per_sm < 1) per_sm = 1;
@@ -256,14 +290,8 @@ int dispatch_pack(const PackArgs& a, cudaStream_t s) {
 template <int IPT, int MINB>
 int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     const size_t smem = SortPkTraits<IPT>::smem_bytes();
-    static thread_local int attr_dev = -1;
-    int dev = 0;
-    RMX_CHECK(cudaGetDevice(&dev));
-    if (attr_dev != dev) {
-        RMX_CHECK(cudaFuncSetAttribute(k_pk_downsweep<IPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
-        attr_dev = dev;
-    }
+    int rc = ensure_smem(k_pk_downsweep<IPT, MINB>, smem);
+    if (rc) return rc;
     k_pk_downsweep<IPT, MINB><<<a.ntiles, kBlock, smem, s>>>(a);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
@@ -476,7 +504,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     if (small_path(V, D, I)) {  // one CTA does it all (rmx_small.cuh)
         const size_t smem = small_smem_bytes(static_cast<uint32_t>(V), D);
-        RMX_CHECK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        if ((rc = ensure_smem(k_small, smem))) return rc;
         SmallArgs a{vtx, static_cast<uint32_t>(V), D, idx, I, out_vtx, out_idx,
                     reinterpret_cast<unsigned long long*>(d_count), d_status, sc ? *sc : rmx_scratch{}};
         k_small<<<1, kSmallThreads, smem, s>>>(a);

@@ -157,3 +157,38 @@ def test_graph_out_of_range_status(rmx):
     count, status, gv, ge = _graph_run(rmx, g, (vt, it, ov, oe, info), v, e)   # status resets per launch
     ev, ee = expect(v, e)
     assert status == 0 and np.array_equal(gv, ev) and np.array_equal(ge, ee)
+
+
+def test_concurrent_calls_from_threads(rmx):
+    """The C-ABI is reentrant: 8 host threads re-index meshes of different sizes and dims at once
+    (small-mesh and large-mesh paths, different shared-memory needs) on one device."""
+    import threading
+    jobs = []
+    for t in range(8):
+        D = 1 + t % 4
+        V = [300, 5000, 8000, 40_000][t % 4]
+        jobs.append(random_mesh(100 + t, V, D, V // 2, 3, pool=50))
+    results, errors = [None] * len(jobs), []
+
+    def run(k):
+        try:
+            out = []
+            for _ in range(4):
+                v, e = jobs[k]
+                res = rmx.reindex_tensors(torch.from_numpy(v.view(np.int32)).cuda(),
+                                          torch.from_numpy(e.view(np.int32)).cuda())
+                out.append((res.vertices.cpu().numpy().view(np.uint32), res.elements.cpu().numpy().view(np.uint32)))
+            results[k] = out
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(len(jobs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[0]
+    for (v, e), outs in zip(jobs, results):
+        ev, ee = expect(v, e)
+        for gv, ge in outs:
+            assert np.array_equal(gv, ev) and np.array_equal(ge, ee)
