@@ -287,12 +287,17 @@ int dispatch_pack(const PackArgs& a, cudaStream_t s) {
     }
 }
 
+constexpr int kCommonPasses = 5;
+
 template <int IPT, int MINB>
 int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     const size_t smem = SortPkTraits<IPT>::smem_bytes();
     int rc = ensure_smem(k_pk_downsweep<IPT, MINB>, smem);
     if (rc) return rc;
-    k_pk_downsweep<IPT, MINB><<<a.ntiles, kBlock, smem, s>>>(a);
+    // passes past kCommonPasses run only for > 40-bit keys: 4 tiles per CTA there, so that when
+    // they do not run (the common case) the exiting grid is a quarter the size
+    const uint32_t tpc = a.pass >= kCommonPasses ? 4u : 1u;
+    k_pk_downsweep<IPT, MINB><<<(a.ntiles + tpc - 1) / tpc, kBlock, smem, s>>>(a, tpc);
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }

@@ -526,7 +526,7 @@ struct SortPkTraits {
 };
 
 template <int KW, int IPT>
-__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem) {
+__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
     const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
@@ -550,14 +550,15 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_misc + 8);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
-    const uint32_t tile = blockIdx.x;
     const uint32_t base = tile * static_cast<uint32_t>(TILE);
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
     // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none)
     const bool iota = a.pass == 0;
     if (tid == 0) {
-        mbar_init(s_bar, 1);
-        fence_mbar_init();
+        if (it == 0) {
+            mbar_init(s_bar, 1);
+            fence_mbar_init();
+        }
         if (iota)
             stage_tile(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_bar);
         else
@@ -574,7 +575,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
         s_whist[i] = 0u;
     }
     __syncthreads();
-    mbar_wait(s_bar, 0u);
+    mbar_wait(s_bar, it & 1u);
 
     uint32_t pk[IPT];
     if (tile_n == static_cast<uint32_t>(TILE)) {  // full tile: no validity tests
@@ -648,12 +649,20 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     }
 }
 
+// One tile per CTA, or (tiles_per_cta > 1: the passes that few keys reach, so
+// that a pass which does not run costs a small grid) consecutive tiles.
 template <int IPT, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a) {
+__global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a, uint32_t tiles_per_cta) {
     if (*a.status || !pk_pass_active(a)) return;
     extern __shared__ __align__(128) uint32_t smem[];
-    if (a.plan[pk_base(4 * a.dim) + 1] == 2u) sort_pk_body<2, IPT>(a, smem);
-    else sort_pk_body<1, IPT>(a, smem);
+    const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
+    for (uint32_t j = 0; j < tiles_per_cta; ++j) {
+        const uint32_t tile = blockIdx.x * tiles_per_cta + j;
+        if (tile >= a.ntiles) break;
+        if (j) __syncthreads();  // the next tile's bulk copy overwrites the staging buffers
+        if (wide) sort_pk_body<2, IPT>(a, smem, tile, j);
+        else sort_pk_body<1, IPT>(a, smem, tile, j);
+    }
 }
 
 // ---------------------------------------------------------------------------
