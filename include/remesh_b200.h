@@ -203,6 +203,20 @@ int rmx_scatter_rows(const uint32_t* src, uint64_t n, uint32_t words, const uint
                      const uint64_t* dst_ptrs, const uint64_t* dst_off, void* stream);
 
 /*
+ * Multi-GPU step 4 (dist.py): keys (n_rows x key_words u32) are n_runs runs,
+ * run r = rows [run_starts[r], run_starts[r+1]) (host array), each sorted
+ * lexicographically (word 0 most significant) and duplicate-free.  Writes the
+ * sorted unique keys to out_keys (capacity n_rows x key_words), the index in
+ * out_keys of every input row to rank_of[n_rows], and their count to
+ * *d_new_count (device).  Pairwise merge-path rounds, then one compaction.
+ * key_words <= 8.
+ */
+size_t rmx_merge_workspace_bytes(uint64_t n_rows, uint32_t key_words);
+int rmx_merge_unique_runs(const uint32_t* keys, uint64_t n_rows, uint32_t key_words, const uint64_t* run_starts,
+                          uint32_t n_runs, uint32_t* out_keys, uint32_t* rank_of, uint64_t* d_new_count,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * Welded (indexed) tile of the C4 merge workload:
  * the triangulated n x n quad grid whose lattice rows start at row0, every
  * point stored once, 5 % unused rows; points and triangles row-major, or

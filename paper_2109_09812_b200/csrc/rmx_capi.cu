@@ -888,6 +888,78 @@ int rmx_scatter_rows(const uint32_t* src, uint64_t n, uint32_t words, const uint
     return RMX_OK;
 }
 
+size_t rmx_merge_workspace_bytes(uint64_t n_rows, uint32_t key_words) {
+    const uint64_t W = static_cast<uint64_t>(key_words) + 1;
+    const uint64_t tiles = (n_rows + kMergeTile - 1) / kMergeTile;
+    return static_cast<size_t>(2 * n_rows * W * 4 + 256 + tiles * 4 + 256 + (tiles + 1) * 8 + 256);
+}
+
+int rmx_merge_unique_runs(const uint32_t* keys, uint64_t n_rows, uint32_t key_words, const uint64_t* run_starts,
+                          uint32_t n_runs, uint32_t* out_keys, uint32_t* rank_of, uint64_t* d_count,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+    g_err[0] = '\0';
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!d_count) return RMX_EINVAL;
+    RMX_CHECK(cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s));
+    if (n_rows == 0) return RMX_OK;
+    const uint32_t D = key_words, W = key_words + 1;
+    if (!keys || !run_starts || !out_keys || !rank_of || D < 1 || W > kMergeMaxW || n_runs < 1 ||
+        n_rows >= (1ull << 32)) {
+        std::snprintf(g_err, sizeof(g_err), "merge: bad arguments (key words %u, runs %u)", key_words, n_runs);
+        return RMX_EINVAL;
+    }
+    if (!workspace || workspace_bytes < rmx_merge_workspace_bytes(n_rows, key_words)) return RMX_ENOSPC;
+    uint32_t* buf[2] = {static_cast<uint32_t*>(workspace),
+                        static_cast<uint32_t*>(workspace) + n_rows * W + 64};
+    uint32_t* counts = buf[1] + n_rows * W + 64;
+    const uint64_t max_tiles = (n_rows + kMergeTile - 1) / kMergeTile;
+    uint64_t* splits = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(counts + max_tiles + 64) + 7) & ~static_cast<uintptr_t>(7));
+    int grid = 0;
+    int rc = grid_for_stream(n_rows * W, grid);
+    if (rc) return rc;
+    k_merge_rows_init<<<grid, kBlock, 0, s>>>(keys, n_rows, D, buf[0]);
+    RMX_CHECK(cudaGetLastError());
+    // pairwise rounds: runs (0,1), (2,3), ... until one run is left
+    std::vector<uint64_t> starts(run_starts, run_starts + n_runs);
+    starts.push_back(n_rows);
+    const size_t smem = 2 * (static_cast<size_t>(kMergeTile) * W + kMergeTile / 8 + 1) * 4;  // padded in + out
+    if ((rc = ensure_smem(k_merge_path, smem))) return rc;
+    int cur = 0;
+    while (starts.size() > 2) {
+        std::vector<uint64_t> next;
+        for (size_t r = 0; r + 1 < starts.size(); r += 2) {
+            const uint64_t a0 = starts[r], a1 = starts[r + 1];
+            const uint64_t b1 = (r + 2 < starts.size()) ? starts[r + 2] : a1;
+            next.push_back(a0);
+            const uint64_t n = b1 - a0;
+            if (r + 2 >= starts.size() || n == 0) {  // odd run out: copy through
+                if (n) RMX_CHECK(cudaMemcpyAsync(buf[cur ^ 1] + a0 * W, buf[cur] + a0 * W, n * W * 4,
+                                                 cudaMemcpyDeviceToDevice, s));
+                continue;
+            }
+            const unsigned blocks = static_cast<unsigned>((n + kMergeTile - 1) / kMergeTile);
+            k_merge_splits<<<(blocks + 1 + kBlock - 1) / kBlock, kBlock, 0, s>>>(
+                buf[cur] + a0 * W, a1 - a0, buf[cur] + a1 * W, b1 - a1, W, D, splits, blocks + 1);
+            RMX_CHECK(cudaGetLastError());
+            k_merge_path<<<blocks, kBlock, smem, s>>>(buf[cur] + a0 * W, a1 - a0, buf[cur] + a1 * W, b1 - a1, W, D,
+                                                      splits, buf[cur ^ 1] + a0 * W);
+            RMX_CHECK(cudaGetLastError());
+        }
+        next.push_back(n_rows);
+        starts.swap(next);
+        cur ^= 1;
+    }
+    const uint32_t tiles = static_cast<uint32_t>((n_rows + kMergeTile - 1) / kMergeTile);
+    k_rows_heads<<<tiles, kBlock, 0, s>>>(buf[cur], n_rows, W, D, counts);
+    RMX_CHECK(cudaGetLastError());
+    k_rows_scan<<<1, 1024, 0, s>>>(counts, tiles, reinterpret_cast<unsigned long long*>(d_count));
+    RMX_CHECK(cudaGetLastError());
+    k_rows_unique<<<tiles, kBlock, 0, s>>>(buf[cur], n_rows, W, D, counts, out_keys, rank_of);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int rmx_welded_tile_sizes(uint32_t n, uint64_t* n_vertices, uint64_t* n_elements) {
     if (n < 1) return RMX_EINVAL;
     const uint64_t pts = static_cast<uint64_t>(n + 1) * (n + 1);

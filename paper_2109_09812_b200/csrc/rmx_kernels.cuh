@@ -18,6 +18,7 @@
 //   K3b  k_map_fill     map[org] = new_idx from the bucket-major pairs
 //   K4   k_remap        out_idx = map[idx] (remap_elements pipeline.py:116-130)
 //   small k_small       the whole pipeline in one CTA for small meshes (rmx_small.cuh)
+//   merge k_merge_path  sorted-run merge + unique of the multi-GPU exchange (rmx_merge.cuh)
 //   gen  k_gen_lattice  synthetic bench input (oracle/lattice.py recipe)
 //
 // Data layout in HBM: a row is W = D+1 uint32 words -- the D key words of the
@@ -35,3 +36,4 @@
 #include "rmx_gen.cuh"
 #include "rmx_steps.cuh"
 #include "rmx_small.cuh"
+#include "rmx_merge.cuh"

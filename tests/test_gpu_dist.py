@@ -129,3 +129,31 @@ def test_symm_comm_world_of_one(cuda_ok):
         assert torch.equal(res.vertices, ref.vertices) and torch.equal(res.elements, ref.elements)
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G,D,n", [(1, 3, 5000), (2, 1, 100_000), (3, 4, 7777), (8, 3, 300_000), (5, 8, 20_000),
+                                   (16, 2, 60_000)])
+def test_merge_unique_runs_vs_numpy(cuda_ok, G, D, n):
+    """rmx_merge_unique_runs: G sorted duplicate-free runs (keys shared across runs, empty runs)
+    -> sorted unique keys and the rank of every row, against numpy."""
+    from paper_2109_09812_b200.dist import CudaBackend
+    rng = np.random.default_rng(G * 100 + D)
+    pool = rng.integers(0, 1 << 32, size=(max(4, n // 2), D), dtype=np.uint64).astype(np.uint32)
+    pool[: len(pool) // 3, 0] = pool[0, 0]                  # long shared prefixes on word 0
+    runs = []
+    for g in range(G):
+        m = 0 if (g == 1 and G > 2) else int(rng.integers(1, max(2, 2 * n // G)))
+        pick = np.unique(rng.integers(0, len(pool), size=m))
+        run = pool[pick]
+        order = np.lexsort(run.T[::-1])
+        run = run[order]
+        keep = np.ones(len(run), bool)
+        keep[1:] = np.any(run[1:] != run[:-1], axis=1)
+        runs.append(run[keep])
+    keys = np.concatenate(runs) if runs else np.empty((0, D), np.uint32)
+    counts = [len(r) for r in runs]
+    uniq, inv = np.unique(keys, axis=0, return_inverse=True)      # numpy sorts rows lexicographically
+    be = CudaBackend(torch.device("cuda", 0))
+    mine, rank_of = be.merge_unique(torch.from_numpy(keys.view(np.int32)).cuda(), counts)
+    assert np.array_equal(mine.cpu().numpy().view(np.uint32), uniq)
+    assert np.array_equal(rank_of.view(-1).cpu().numpy().view(np.uint32), inv.reshape(-1).astype(np.uint32))
