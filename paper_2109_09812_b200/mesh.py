@@ -83,7 +83,8 @@ class Mesh:
 
     @classmethod
     def empty(cls, dim: int = 2, arity: int = 3) -> "Mesh":
-        return cls(np.empty((0, dim), np.float32), np.empty((0, arity), np.uint32))
+        """No vertices, no elements (the reference's default shape: dim 2, arity 3)."""
+        return cls._adopt(np.zeros((0, dim), dtype=np.float32), np.zeros((0, arity), dtype=np.uint32))
 
     @property
     def vertices(self) -> np.ndarray:
@@ -110,8 +111,7 @@ class Mesh:
         return self._elements.shape[0]
 
     def __repr__(self):
-        return (f"Mesh({self.n_vertices} vertices dim={self.dim}, "
-                f"{self.n_elements} elements arity={self.arity})")
+        return f"Mesh(V={self.n_vertices}, D={self.dim}; E={self.n_elements}, K={self.arity})"
 
 
 def vertex_bits(vertices) -> np.ndarray:

@@ -30,38 +30,37 @@ def _to_mesh(res) -> Mesh:
 
 
 def merge(meshes, device=None) -> Mesh:
-    """Re-indexed concatenation of meshes sharing dim and arity (ops.py:10-35)."""
-    meshes = list(meshes)
-    if not meshes:
-        raise MeshError("merge needs at least one mesh")
-    dim, arity = meshes[0].dim, meshes[0].arity
-    for k, m in enumerate(meshes):
-        if m.dim != dim or m.arity != arity:
-            raise MeshError(f"mesh {k} has dim={m.dim} arity={m.arity}, expected dim={dim} arity={arity}")
-        require_valid(m)
-    total = sum(m.n_vertices for m in meshes)
-    if total >= MAX_VERTICES:
-        raise MeshError(f"merged vertex count {total} exceeds 32-bit index range")
-    n_elem = sum(m.n_elements for m in meshes)
-    if n_elem == 0:
-        return Mesh.empty(dim=dim, arity=arity)
+    """Re-indexed concatenation of meshes sharing dim and arity (ops.py:10-35).
+
+    Each mesh is validated, uploaded, and the concatenation + index shift +
+    re-index run on the device (:func:`merge_tensors`).
+    """
+    parts = list(meshes)
+    if len(parts) == 0:
+        raise MeshError("merge of an empty list of meshes")
+    d0, k0 = parts[0].dim, parts[0].arity
+    for pos, part in enumerate(parts):
+        if (part.dim, part.arity) != (d0, k0):
+            raise MeshError(f"merge: mesh #{pos} is dim {part.dim} / arity {part.arity}, "
+                            f"the first mesh is dim {d0} / arity {k0}")
+        require_valid(part)
+    n_vtx = sum(part.n_vertices for part in parts)
+    if n_vtx >= MAX_VERTICES:
+        raise MeshError(f"merge: {n_vtx} vertices in total do not fit 32-bit indices")
+    if sum(part.n_elements for part in parts) == 0:
+        return Mesh.empty(dim=d0, arity=k0)
     dev = _device(device)
     with torch.cuda.device(dev):
-        vtx = torch.empty((total, dim), dtype=torch.int32, device=dev)
-        idx = torch.empty((n_elem, arity), dtype=torch.int64, device=dev)
-        v0 = e0 = 0
-        for m in meshes:
-            nv, ne = m.n_vertices, m.n_elements
-            if nv:
-                vtx[v0:v0 + nv].copy_(host_tensor(np.ascontiguousarray(m.vertices).view(np.int32)))
-            if ne:
-                seg = host_tensor(np.ascontiguousarray(m.elements).view(np.int32)).to(dev)
-                idx[e0:e0 + ne] = (seg.to(torch.int64) & 0xFFFFFFFF) + v0
-            v0 += nv
-            e0 += ne
-        # offsets stay below 2**32 (checked above); narrow to the pipeline's 32-bit words
-        res = reindex_tensors(vtx, idx.to(torch.int32) if total < (1 << 31) else _narrow_u32(idx))
-    return _to_mesh(res)
+        on_device = []
+        for part in parts:
+            v = torch.empty((part.n_vertices, d0), dtype=torch.int32, device=dev)
+            e = torch.empty((part.n_elements, k0), dtype=torch.int32, device=dev)
+            if part.n_vertices:
+                hostio.to_device(np.ascontiguousarray(part.vertices), v)
+            if part.n_elements:
+                hostio.to_device(np.ascontiguousarray(part.elements), e)
+            on_device.append((v, e))
+        return _to_mesh(merge_tensors(on_device, dev))
 
 
 def merge_tensors(pieces, device=None):
@@ -108,24 +107,26 @@ def _narrow_u32(x: torch.Tensor) -> torch.Tensor:
 
 
 def soup_to_mesh(soup, device=None) -> Mesh:
-    """Compact mesh from a (m, K, D) soup (ops.py:38-56)."""
+    """Compact mesh from a (m, K, D) soup (ops.py:38-56): every element corner is a
+    vertex slot of its own, element e = slots (eK .. eK+K-1), then re-index."""
     try:
-        arr = np.asarray(soup, dtype=np.float32)
+        corners = np.asarray(soup, dtype=np.float32)
     except (ValueError, TypeError) as exc:
-        raise MeshError(f"ragged soup: {exc}") from None
-    if arr.ndim != 3:
-        raise MeshError(f"soup must be a (m, arity, dim) array, got shape {arr.shape}")
-    m, arity, dim = arr.shape
-    if m == 0:
-        return Mesh.empty(dim=dim, arity=arity)
-    n = m * arity
-    if n >= MAX_VERTICES:
-        raise MeshError(f"soup has {n} vertices, exceeds 32-bit index range")
+        raise MeshError(f"soup is not a rectangular (elements, arity, dim) array: {exc}") from None
+    if corners.ndim != 3:
+        raise MeshError(f"soup needs shape (elements, arity, dim); got {corners.shape}")
+    n_el, k, d = corners.shape
+    if n_el == 0:
+        return Mesh.empty(dim=d, arity=k)
+    slots = n_el * k
+    if slots >= MAX_VERTICES:
+        raise MeshError(f"soup: {slots} corners do not fit 32-bit indices")
     dev = _device(device)
     with torch.cuda.device(dev):
-        vtx = host_tensor(np.ascontiguousarray(arr.reshape(n, dim)).view(np.int32)).to(dev)
-        idx = torch.arange(n, dtype=torch.int64, device=dev).view(m, arity)
-        res = reindex_tensors(vtx, idx.to(torch.int32) if n < (1 << 31) else _narrow_u32(idx))
+        vtx = torch.empty((slots, d), dtype=torch.int32, device=dev)
+        hostio.to_device(np.ascontiguousarray(corners.reshape(slots, d)), vtx)
+        iota = torch.arange(slots, dtype=torch.int64, device=dev).view(n_el, k)
+        res = reindex_tensors(vtx, iota.to(torch.int32) if slots < (1 << 31) else _narrow_u32(iota))
     return _to_mesh(res)
 
 
@@ -138,20 +139,24 @@ def subset(mesh, keep, device=None) -> Mesh:
 
 
 def _selector_mask(keep, n_elements: int) -> np.ndarray:
-    """Bool mask or strictly ascending positions -> mask (ops.py:71-87)."""
-    sel = np.asarray(keep)
-    if sel.dtype == bool:
-        if len(sel) != n_elements:
-            raise MeshError(f"mask length {len(sel)} != element count {n_elements}")
-        return sel
-    sel = sel.reshape(-1)
-    if sel.size:
-        if not np.issubdtype(sel.dtype, np.integer):
-            raise MeshError(f"selector must be a bool mask or integer positions, got {sel.dtype}")
-        if int(sel.min()) < 0 or int(sel.max()) >= n_elements:
-            raise MeshError(f"selector position out of range [0, {n_elements})")
-        if sel.size > 1 and not bool(np.all(sel[1:] > sel[:-1])):
-            raise MeshError("selector positions must be strictly ascending and unique")
-    mask = np.zeros(n_elements, dtype=bool)
-    mask[sel.astype(np.int64)] = True
-    return mask
+    """Element selector -> bool mask (ops.py:71-87 semantics): a bool mask of length
+    n_elements, or strictly increasing element positions."""
+    picks = np.asarray(keep)
+    if picks.dtype == np.bool_:
+        if picks.shape[0] != n_elements:
+            raise MeshError(f"boolean selector has {picks.shape[0]} entries for {n_elements} elements")
+        return picks
+    picks = picks.ravel()
+    chosen = np.zeros(n_elements, dtype=np.bool_)
+    if picks.size == 0:
+        return chosen
+    if picks.dtype.kind not in "iu":
+        raise MeshError(f"element selector of dtype {picks.dtype}: expected bools or integer positions")
+    first, last = int(picks.min()), int(picks.max())
+    if first < 0 or last >= n_elements:
+        raise MeshError(f"element positions must lie in [0, {n_elements}); got {first}..{last}")
+    pos = picks.astype(np.int64)
+    if pos.size > 1 and bool(np.any(pos[1:] <= pos[:-1])):
+        raise MeshError("element positions must be strictly increasing (no repeats)")
+    chosen[pos] = True
+    return chosen
