@@ -192,3 +192,21 @@ def test_concurrent_calls_from_threads(rmx):
         ev, ee = expect(v, e)
         for gv, ge in outs:
             assert np.array_equal(gv, ev) and np.array_equal(ge, ee)
+
+
+@pytest.mark.parametrize("V,D,E,K", [(50_000, 3, 30_000, 3), (20_000, 4, 9_000, 4), (300, 3, 200, 3)])
+def test_unaligned_device_buffers(rmx, V, D, E, K):
+    """Vertex/index tensors that start off a 16-byte boundary (slices of bigger buffers): the
+    vectorised and bulk-copy paths must fall back, results unchanged."""
+    v, e = random_mesh(7 + D, V, D, E, K, pool=40)
+    ev, ee = expect(v, e)
+    big_v = torch.zeros((V + 1) * D + 1, dtype=torch.int32, device="cuda")
+    big_e = torch.zeros(E * K + 3, dtype=torch.int32, device="cuda")
+    tv = big_v[1:1 + V * D].view(V, D)          # 4-byte offset
+    te = big_e[3:3 + E * K].view(E, K)          # 12-byte offset
+    tv.copy_(torch.from_numpy(v.view(np.int32)))
+    te.copy_(torch.from_numpy(e.view(np.int32)))
+    assert tv.data_ptr() % 16 and te.data_ptr() % 16
+    res = rmx.reindex_tensors(tv, te)
+    assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), ev)
+    assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), ee)
