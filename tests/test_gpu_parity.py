@@ -304,3 +304,16 @@ def test_small_path_limits_vs_oracle(rmx, V, D, E, K, mesh_path):
     assert np.array_equal(out.elements, ref["elements"])
     for f in FIELDS:
         assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
+
+
+@pytest.mark.parametrize("D,pool", [(9, None), (16, None), (32, None), (12, 3), (32, 2), (6, 5)])
+def test_wide_dims_vs_oracle(rmx, D, pool, mesh_path):
+    """D up to RMX_MAX_DIM = 32 words per vertex: the generic-width AoS rows (random bits) and the
+    generic packed path (few varying bits), both mesh paths where they apply, scratch included."""
+    words, idx = random_bits_mesh(D * 7 + (pool or 0), 20_000, D, 9_000, 3, pool)
+    ref = O.reindex(words, idx)
+    out, sc = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
