@@ -915,17 +915,43 @@ int rmx_merge_unique_runs(const uint32_t* keys, uint64_t n_rows, uint32_t key_wo
     const uint64_t max_tiles = (n_rows + kMergeTile - 1) / kMergeTile;
     uint64_t* splits = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(counts + max_tiles + 64) + 7) & ~static_cast<uintptr_t>(7));
+    int rc = RMX_OK;
     int grid = 0;
-    int rc = grid_for_stream(n_rows * W, grid);
-    if (rc) return rc;
-    k_merge_rows_init<<<grid, kBlock, 0, s>>>(keys, n_rows, D, buf[0]);
-    RMX_CHECK(cudaGetLastError());
-    // pairwise rounds: runs (0,1), (2,3), ... until one run is left
+    if ((rc = grid_for_stream(n_rows, grid))) return rc;
+    // pairwise rounds: runs (0,1), (2,3), ... until one run is left; the first round reads the
+    // keys themselves (rows get their arrival position as they are staged)
     std::vector<uint64_t> starts(run_starts, run_starts + n_runs);
     starts.push_back(n_rows);
     const size_t smem = 2 * (static_cast<size_t>(kMergeTile) * W + kMergeTile / 8 + 1) * 4;  // padded in + out
-    if ((rc = ensure_smem(k_merge_path, smem))) return rc;
+    switch (W) {
+#define RMX_SMEM_W(w)                                                \
+    case w:                                                          \
+        if ((rc = ensure_smem(k_merge_path<w, true>, smem))) break;  \
+        rc = ensure_smem(k_merge_path<w, false>, smem);              \
+        break;
+        RMX_SMEM_W(2) RMX_SMEM_W(3) RMX_SMEM_W(4) RMX_SMEM_W(5) RMX_SMEM_W(6) RMX_SMEM_W(7) RMX_SMEM_W(8)
+        RMX_SMEM_W(9)
+#undef RMX_SMEM_W
+    }
+    if (rc) return rc;
+    auto to_rows = [&](uint64_t a0, uint64_t n, uint32_t* dst) -> int {  // keys -> rows (odd run, 1 run)
+        switch (W) {
+#define RMX_INIT_W(w)                                                                                 \
+    case w: k_merge_rows_init<w><<<grid, kBlock, 0, s>>>(keys + a0 * D, n, static_cast<uint32_t>(a0), dst); \
+        break;
+            RMX_INIT_W(2) RMX_INIT_W(3) RMX_INIT_W(4) RMX_INIT_W(5) RMX_INIT_W(6) RMX_INIT_W(7) RMX_INIT_W(8)
+            RMX_INIT_W(9)
+#undef RMX_INIT_W
+        }
+        RMX_CHECK(cudaGetLastError());
+        return RMX_OK;
+    };
     int cur = 0;
+    bool first = true;
+    if (starts.size() == 2) {  // one run: rows straight from the keys
+        if ((rc = to_rows(0, n_rows, buf[0]))) return rc;
+        first = false;
+    }
     while (starts.size() > 2) {
         std::vector<uint64_t> next;
         for (size_t r = 0; r + 1 < starts.size(); r += 2) {
@@ -933,22 +959,43 @@ int rmx_merge_unique_runs(const uint32_t* keys, uint64_t n_rows, uint32_t key_wo
             const uint64_t b1 = (r + 2 < starts.size()) ? starts[r + 2] : a1;
             next.push_back(a0);
             const uint64_t n = b1 - a0;
-            if (r + 2 >= starts.size() || n == 0) {  // odd run out: copy through
-                if (n) RMX_CHECK(cudaMemcpyAsync(buf[cur ^ 1] + a0 * W, buf[cur] + a0 * W, n * W * 4,
-                                                 cudaMemcpyDeviceToDevice, s));
+            if (r + 2 >= starts.size() || n == 0) {  // odd run out: carried to the next round
+                if (n) {
+                    if (first) {
+                        if ((rc = to_rows(a0, n, buf[cur ^ 1] + a0 * W))) return rc;
+                    } else {
+                        RMX_CHECK(cudaMemcpyAsync(buf[cur ^ 1] + a0 * W, buf[cur] + a0 * W, n * W * 4,
+                                                  cudaMemcpyDeviceToDevice, s));
+                    }
+                }
                 continue;
             }
             const unsigned blocks = static_cast<unsigned>((n + kMergeTile - 1) / kMergeTile);
-            k_merge_splits<<<(blocks + 1 + kBlock - 1) / kBlock, kBlock, 0, s>>>(
-                buf[cur] + a0 * W, a1 - a0, buf[cur] + a1 * W, b1 - a1, W, D, splits, blocks + 1);
+            const uint32_t S = first ? D : W;
+            const uint32_t* src = first ? keys : buf[cur];
+            const uint32_t* A = src + a0 * S;
+            const uint32_t* B = src + a1 * S;
+            uint32_t* O = buf[cur ^ 1] + a0 * W;
+            k_merge_splits<<<(blocks + 1 + kBlock - 1) / kBlock, kBlock, 0, s>>>(A, a1 - a0, B, b1 - a1, S, D, splits,
+                                                                                 blocks + 1);
             RMX_CHECK(cudaGetLastError());
-            k_merge_path<<<blocks, kBlock, smem, s>>>(buf[cur] + a0 * W, a1 - a0, buf[cur] + a1 * W, b1 - a1, W, D,
-                                                      splits, buf[cur ^ 1] + a0 * W);
+            const uint32_t ao = static_cast<uint32_t>(a0), bo = static_cast<uint32_t>(a1);
+            switch (W * 2 + (first ? 1 : 0)) {
+#define RMX_MERGE_W(w)                                                                                          \
+    case 2 * w: k_merge_path<w, false><<<blocks, kBlock, smem, s>>>(A, a1 - a0, B, b1 - a1, ao, bo, splits, O); \
+        break;                                                                                                  \
+    case 2 * w + 1: k_merge_path<w, true><<<blocks, kBlock, smem, s>>>(A, a1 - a0, B, b1 - a1, ao, bo, splits, O); \
+        break;
+                RMX_MERGE_W(2) RMX_MERGE_W(3) RMX_MERGE_W(4) RMX_MERGE_W(5) RMX_MERGE_W(6) RMX_MERGE_W(7)
+                RMX_MERGE_W(8) RMX_MERGE_W(9)
+#undef RMX_MERGE_W
+            }
             RMX_CHECK(cudaGetLastError());
         }
         next.push_back(n_rows);
         starts.swap(next);
         cur ^= 1;
+        first = false;
     }
     const uint32_t tiles = static_cast<uint32_t>((n_rows + kMergeTile - 1) / kMergeTile);
     k_rows_heads<<<tiles, kBlock, 0, s>>>(buf[cur], n_rows, W, D, counts);

@@ -46,19 +46,21 @@ __device__ __forceinline__ uint64_t merge_split(const uint32_t* A, uint64_t na, 
     return lo;
 }
 
-// rows of D key words + arrival position, from the keys of the runs
-__global__ void __launch_bounds__(kBlock) k_merge_rows_init(const uint32_t* __restrict__ keys, uint64_t n, uint32_t D,
-                                                             uint32_t* __restrict__ rows) {
-    const uint32_t W = D + 1;
+// rows of D key words + arrival position, from the keys of the runs (one row per thread)
+template <int W>
+__global__ void __launch_bounds__(kBlock) k_merge_rows_init(const uint32_t* __restrict__ keys, uint64_t n,
+                                                             uint32_t org0, uint32_t* __restrict__ rows) {
+    constexpr int D = W - 1;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
-    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; t < n * W; t += stride) {
-        const uint64_t r = t / W;
-        const uint32_t c = static_cast<uint32_t>(t - r * W);
-        rows[t] = c < D ? keys[r * D + c] : static_cast<uint32_t>(r);
+    for (uint64_t r = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; r < n; r += stride) {
+        uint32_t* dst = rows + r * W;
+#pragma unroll
+        for (int c = 0; c < D; ++c) dst[c] = __ldcs(keys + r * D + c);
+        dst[D] = org0 + static_cast<uint32_t>(r);
     }
 }
 
-// merge-path split at every CTA boundary (one thread each: the ~log2(n) dependent
+// merge-path split at every CTA boundary (rows of stride S words; one thread each: the ~log2(n) dependent
 // global loads run in parallel here instead of at the head of every merge CTA)
 __global__ void __launch_bounds__(kBlock) k_merge_splits(const uint32_t* __restrict__ A, uint64_t na,
                                                           const uint32_t* __restrict__ B, uint64_t nb, uint32_t W,
@@ -80,10 +82,16 @@ __device__ __forceinline__ bool srows_less(const uint32_t* s, uint32_t a, uint32
     return false;
 }
 
+// FROM_KEYS (first round): A and B are runs of the received keys (D words per row, row ids
+// a_org / b_org onwards); the arrival position becomes the W-th word as the rows are staged.
+template <int W, bool FROM_KEYS>
 __global__ void __launch_bounds__(kBlock) k_merge_path(const uint32_t* __restrict__ A, uint64_t na,
-                                                        const uint32_t* __restrict__ B, uint64_t nb, uint32_t W,
-                                                        uint32_t D, const uint64_t* __restrict__ splits,
+                                                        const uint32_t* __restrict__ B, uint64_t nb,
+                                                        uint32_t a_org, uint32_t b_org,
+                                                        const uint64_t* __restrict__ splits,
                                                         uint32_t* __restrict__ out) {
+    constexpr uint32_t D = W - 1;
+    constexpr uint32_t S = FROM_KEYS ? D : W;  // input row stride
     // input rows (A slice then B slice), then the merged rows, both padded
     extern __shared__ __align__(16) uint32_t s_rows[];
     const uint32_t span = pad_row(kMergeTile, W) + 1;
@@ -95,16 +103,22 @@ __global__ void __launch_bounds__(kBlock) k_merge_path(const uint32_t* __restric
     const uint64_t b0 = d0 - a0, b1 = d1 - a1;
     const uint32_t la = static_cast<uint32_t>(a1 - a0), lb = static_cast<uint32_t>(b1 - b0);
     const uint32_t total = la + lb;
-    for (uint32_t w = threadIdx.x; w < la * W; w += kBlock) {
-        const uint32_t r = w / W;
-        s_rows[pad_row(r, W) + (w - r * W)] = A[a0 * W + w];
+    for (uint32_t w = threadIdx.x; w < la * S; w += kBlock) {
+        const uint32_t r = w / S;
+        s_rows[pad_row(r, W) + (w - r * S)] = A[a0 * S + w];
     }
-    for (uint32_t w = threadIdx.x; w < lb * W; w += kBlock) {
-        const uint32_t r = la + w / W;
-        s_rows[pad_row(r, W) + (w - (r - la) * W)] = B[b0 * W + w];
+    for (uint32_t w = threadIdx.x; w < lb * S; w += kBlock) {
+        const uint32_t r = w / S;
+        s_rows[pad_row(la + r, W) + (w - r * S)] = B[b0 * S + w];
+    }
+    if (FROM_KEYS) {
+        for (uint32_t r = threadIdx.x; r < la; r += kBlock) s_rows[pad_row(r, W) + D] = a_org + static_cast<uint32_t>(a0) + r;
+        for (uint32_t r = threadIdx.x; r < lb; r += kBlock)
+            s_rows[pad_row(la + r, W) + D] = b_org + static_cast<uint32_t>(b0) + r;
     }
     __syncthreads();
-    // thread t merges outputs [8t, 8t + 8): one split search, then a sequential merge
+    // thread t merges outputs [8t, 8t + 8): one split search, then a sequential merge with the
+    // two candidate rows held in registers (one shared-memory row load per output)
     constexpr uint32_t kPer = kMergeTile / kBlock;
     const uint32_t k0 = threadIdx.x * kPer;
     if (k0 < total) {
@@ -115,14 +129,31 @@ __global__ void __launch_bounds__(kBlock) k_merge_path(const uint32_t* __restric
             else hi = i;
         }
         uint32_t i = lo, j = k0 - lo;
-        for (uint32_t k = k0; k < k0 + kPer && k < total; ++k) {
-            const bool take_a = j >= lb || (i < la && !srows_less(s_rows, la + j, i, W, D));
-            const uint32_t src = take_a ? i : la + j;
-            const uint32_t* sp = s_rows + pad_row(src, W);
+        uint32_t ra[W], rb[W];
+        auto load = [&](uint32_t (&r)[W], uint32_t row) {
+            const uint32_t* p = s_rows + pad_row(row, W);
+#pragma unroll
+            for (int c = 0; c < W; ++c) r[c] = p[c];
+        };
+        if (i < la) load(ra, i);
+        if (j < lb) load(rb, la + j);
+        const uint32_t kend = min(k0 + kPer, total);
+        for (uint32_t k = k0; k < kend; ++k) {
+            bool b_less = false;  // key(rb) < key(ra)
+#pragma unroll
+            for (int c = static_cast<int>(D) - 1; c >= 0; --c)
+                b_less = (rb[c] != ra[c]) ? (rb[c] < ra[c]) : b_less;
+            const bool take_a = j >= lb || (i < la && !b_less);
             uint32_t* dp = s_out + pad_row(k, W);
-            for (uint32_t c = 0; c < W; ++c) dp[c] = sp[c];
-            if (take_a) ++i;
-            else ++j;
+            if (take_a) {
+#pragma unroll
+                for (int c = 0; c < W; ++c) dp[c] = ra[c];
+                if (++i < la) load(ra, i);
+            } else {
+#pragma unroll
+                for (int c = 0; c < W; ++c) dp[c] = rb[c];
+                if (++j < lb) load(rb, la + j);
+            }
         }
     }
     __syncthreads();

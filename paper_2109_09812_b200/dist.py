@@ -16,12 +16,11 @@ Algorithm (a sample sort on deduplicated keys):
    once per rank, so no heavy hitter survives);
 3. ``rmx_lower_bound_rows`` partitions each sorted key array into G contiguous
    ranges -> all-to-all of the keys (counts first, then data);
-4. each rank turns what it received -- G sorted, duplicate-free runs -- into
-   the sorted unique keys of its range plus the rank of every received key:
-   for G <= 4 by merging (``rmx_merge_unique_runs``: pairwise merge path + one
-   compaction), beyond that by re-indexing them (identity elements), which
-   measured faster than three merge rounds.  All copies of a key go to the
-   same rank, so there are no boundary duplicates;
+4. each rank merges what it received -- G sorted, duplicate-free runs -- into
+   the sorted unique keys of its range plus the rank of every received key
+   (``rmx_merge_unique_runs``: pairwise merge-path rounds + one compaction; no
+   re-sort; keys wider than 8 words are re-indexed instead).  All copies of a
+   key go to the same rank, so there are no boundary duplicates;
 5. AllGather of the per-rank unique counts -> global offsets;
 6. reverse all-to-all of the global ids, in the order the keys arrived: each
    sender gets the global id of every local unique key back in its own sorted
@@ -330,9 +329,9 @@ def reindex_distributed(vertex_bits: torch.Tensor, elements: torch.Tensor, comm:
     # 4. merge what arrived (G sorted, duplicate-free runs): sorted unique keys of this range +
     #    the rank of each received key
     n_recv = recv_keys.shape[0]
-    # merging pays for up to two merge rounds (G <= 4); beyond that the radix pipeline is faster
-    # (tools/merge_runs_bench.py: 4 runs / 29M rows 1.7 vs 2.2 ms, 8 runs / 106M rows 7.3 vs 6.9 ms)
-    if n_recv and hasattr(backend, "merge_unique") and D <= 8 and G <= 4:
+    # merging beats re-sorting the runs (tools/merge_runs_bench.py: 8 runs / 106M rows 5.2 vs 6.9 ms,
+    # 4 runs / 29M rows 1.2 vs 2.2 ms, 16 runs / 194M rows 11.7 vs 12.0 ms)
+    if n_recv and hasattr(backend, "merge_unique") and D <= 8:
         mine, rank_of = backend.merge_unique(recv_keys, recv_counts)
     elif n_recv:
         ident = torch.arange(n_recv, dtype=torch.int32, device=recv_keys.device).view(n_recv, 1)
