@@ -98,3 +98,32 @@ def test_field_rank_with_unused_rows_outside_the_set(rmx):
     out, _ = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
     assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
     assert np.array_equal(out.elements, ref["elements"])
+
+
+def _masked_mesh(seed, V, D, E, K, masks):
+    """Vertex words whose varying bits are exactly `masks[c]` (per component) around a base row."""
+    rng = np.random.default_rng(seed)
+    base = rng.integers(0, 1 << 32, size=D, dtype=np.uint64).astype(np.uint32)
+    noise = rng.integers(0, 1 << 32, size=(V, D), dtype=np.uint64).astype(np.uint32)
+    words = (base & ~np.array(masks, np.uint32)) | (noise & np.array(masks, np.uint32))
+    words[: V // 3] = words[V // 3: 2 * (V // 3)]            # duplicates
+    idx = rng.integers(0, V - V // 10, size=(E, K)).astype(np.uint32)
+    return words, idx
+
+
+@pytest.mark.parametrize("D,masks", [
+    (2, [0x55555555, 0x55555555]),                      # 32 one-bit runs, u32 key
+    (4, [0x55550000, 0x00005555, 0x0000AAAA, 0xAAAA0000]),  # 32 runs, u32 key
+    (4, [0x55555555, 0xAAAAAAAA, 0x00000001, 0x00000000]),  # 65 bits: AoS rows
+    (3, [0x0F0F0F0F, 0xF0F0F0F0, 0x00FF00FF]),          # 64 bits in 12 runs, u64 key
+    (2, [0xFFFFFFFF, 0xFFFFFFFF]),                      # exactly 64 bits
+    (4, [0x5555AAAA, 0x5555AAAA, 0x00000003, 0x0]), ])  # 34 runs
+def test_many_runs_and_width_edges(rmx, D, masks):
+    V, E, K = 60_000, 25_000, 3
+    words, idx = _masked_mesh(D * 13 + len(masks), V, D, E, K, masks)
+    ref = O.reindex(words, idx)
+    out, sc = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
