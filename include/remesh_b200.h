@@ -184,6 +184,16 @@ int rmx_gen_lattice_soup_range(int kind, uint32_t nx, uint32_t ny, uint32_t nz, 
                                uint32_t* out_idx, void* stream);
 
 /*
+ * subset (reference pkg/src/remeshx/ops.py:59-68) on the device: the elements
+ * e with keep[e] != 0 (u8 per element, device), in order, into out_idx
+ * (capacity n_elements x arity); their number to *d_kept (device).
+ */
+size_t rmx_select_workspace_bytes(uint64_t n_elements);
+int rmx_select_elements(const uint32_t* idx, uint64_t n_elements, uint32_t arity, const uint8_t* keep,
+                        uint32_t* out_idx, uint64_t* d_kept, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/*
  * merge (reference pkg/src/remeshx/ops.py:29-34) on the device: out[i] =
  * idx[i] + offset (mod 2^32), the index array of one piece shifted by the
  * vertex count of the pieces before it in the concatenation.

@@ -30,7 +30,7 @@ EXPORTS = (
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
     "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy", "rmx_offset_indices",
     "rmx_welded_tile_sizes", "rmx_gen_welded_tile", "rmx_scatter_rows", "rmx_merge_workspace_bytes",
-    "rmx_merge_unique_runs",
+    "rmx_merge_unique_runs", "rmx_select_workspace_bytes", "rmx_select_elements",
 )
 
 
@@ -82,6 +82,8 @@ _SIGNATURES = {
     "rmx_gen_welded_tile": (_int, [_u32, _u32, _u64, _int, _vp, _vp, _vp]),
     "rmx_scatter_rows": (_int, [_vp, _u64, _u32, _vp, _u32, _vp, _vp, _vp]),
     "rmx_merge_workspace_bytes": (_sz, [_u64, _u32]),
+    "rmx_select_workspace_bytes": (_sz, [_u64]),
+    "rmx_select_elements": (_int, [_vp, _u64, _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rmx_merge_unique_runs": (_int, [_vp, _u64, _u32, ctypes.POINTER(_u64), _u32, _vp, _vp, _vp, _vp, _sz, _vp]),
 }
 

@@ -861,6 +861,31 @@ int rmx_gather_u32(const uint32_t* table, uint64_t n_table, const uint32_t* idx,
     return RMX_OK;
 }
 
+size_t rmx_select_workspace_bytes(uint64_t n_elements) {
+    return static_cast<size_t>((n_elements + kKeepTile - 1) / kKeepTile) * 4 + 256;
+}
+
+int rmx_select_elements(const uint32_t* idx, uint64_t n_elements, uint32_t arity, const uint8_t* keep,
+                        uint32_t* out_idx, uint64_t* d_kept, void* workspace, size_t workspace_bytes, void* stream) {
+    g_err[0] = '\0';
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!d_kept || arity < 1) return RMX_EINVAL;
+    RMX_CHECK(cudaMemsetAsync(d_kept, 0, sizeof(uint64_t), s));
+    if (n_elements == 0) return RMX_OK;
+    if (!idx || !keep || !out_idx) return RMX_EINVAL;
+    if (n_elements >= (1ull << 32)) return RMX_ERANGE;
+    if (!workspace || workspace_bytes < rmx_select_workspace_bytes(n_elements)) return RMX_ENOSPC;
+    uint32_t* counts = static_cast<uint32_t*>(workspace);
+    const uint32_t tiles = static_cast<uint32_t>((n_elements + kKeepTile - 1) / kKeepTile);
+    k_keep_count<<<tiles, kBlock, 0, s>>>(keep, n_elements, counts);
+    RMX_CHECK(cudaGetLastError());
+    k_rows_scan<<<1, 1024, 0, s>>>(counts, tiles, reinterpret_cast<unsigned long long*>(d_kept));
+    RMX_CHECK(cudaGetLastError());
+    k_keep_compact<<<tiles, kBlock, 0, s>>>(idx, n_elements, arity, keep, counts, out_idx);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int rmx_offset_indices(const uint32_t* idx, uint64_t n, uint32_t offset, uint32_t* out, void* stream) {
     g_err[0] = '\0';
     if (n == 0) return RMX_OK;

@@ -88,4 +88,54 @@ __global__ void __launch_bounds__(kBlock) k_scatter_rows(const uint32_t* __restr
     }
 }
 
+// subset (reference ops.py:59-68) on the device: the selected elements
+// (keep[e] != 0) in order.  Reduce-then-scan over tiles of 2048 elements:
+// k_keep_count counts per tile, k_rows_scan (rmx_merge.cuh) scans the counts,
+// k_keep_compact writes each kept element to its rank.
+constexpr uint32_t kKeepTile = 2048;
+
+__global__ void __launch_bounds__(kBlock) k_keep_count(const uint8_t* __restrict__ keep, uint64_t n,
+                                                       uint32_t* __restrict__ counts) {
+    __shared__ uint32_t s_red[kWarps];
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kKeepTile;
+    uint32_t c = 0;
+    for (uint64_t e = t0 + threadIdx.x; e < min(n, t0 + kKeepTile); e += kBlock) c += keep[e] ? 1u : 0u;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31u) == 0u) s_red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kWarps; ++w) t += s_red[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_keep_compact(const uint32_t* __restrict__ idx, uint64_t n, uint32_t K,
+                                                         const uint8_t* __restrict__ keep,
+                                                         const uint32_t* __restrict__ prefix,
+                                                         uint32_t* __restrict__ out) {
+    __shared__ uint32_t s_warp[kWarps];
+    const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kKeepTile;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t running = prefix[blockIdx.x];
+    for (uint64_t e0 = t0; e0 < min(n, t0 + kKeepTile); e0 += kBlock) {
+        const uint64_t e = e0 + threadIdx.x;
+        const bool k = e < n && keep[e];
+        const uint32_t bal = __ballot_sync(kFull, k);
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, all = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            before += (static_cast<uint32_t>(w) < warp) ? s_warp[w] : 0u;
+            all += s_warp[w];
+        }
+        __syncthreads();
+        if (k) {
+            const uint64_t dst = running + before + __popc(bal & lanemask_lt());
+            for (uint32_t s = 0; s < K; ++s) out[dst * K + s] = idx[e * K + s];
+        }
+        running += all;
+    }
+}
+
 }  // namespace rmx

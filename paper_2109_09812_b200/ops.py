@@ -138,6 +138,39 @@ def subset(mesh, keep, device=None) -> Mesh:
     return reindex(sub, device)[0]
 
 
+def subset_tensors(vertex_bits: torch.Tensor, elements: torch.Tensor, keep: torch.Tensor):
+    """Device-resident subset (ops.py:59-68): ``keep`` is a device bool mask over the elements
+    or strictly increasing element positions; the selected elements are compacted on the device
+    (``rmx_select_elements``) and re-indexed.  Returns a DeviceResult."""
+    from . import _native
+    E, K = elements.shape
+    dev = elements.device
+    with torch.cuda.device(dev):
+        if keep.dtype == torch.bool:
+            if keep.shape != (E,):
+                raise MeshError(f"boolean selector has {tuple(keep.shape)} entries for {E} elements")
+            mask = keep.to(torch.uint8)
+        else:
+            pos = keep.reshape(-1).to(device=dev, dtype=torch.int64)
+            if pos.numel():
+                if bool((pos < 0).any()) or bool((pos >= E).any()):
+                    raise MeshError(f"element positions must lie in [0, {E})")
+                if pos.numel() > 1 and bool((pos[1:] <= pos[:-1]).any()):
+                    raise MeshError("element positions must be strictly increasing (no repeats)")
+            mask = torch.zeros(E, dtype=torch.uint8, device=dev)
+            mask[pos] = 1
+        lib = _native.lib()
+        out = torch.empty_like(elements)
+        kept = torch.zeros(1, dtype=torch.int64, device=dev)
+        ws = torch.empty(max(1, int(lib.rmx_select_workspace_bytes(E))), dtype=torch.uint8, device=dev)
+        _native.check(lib.rmx_select_elements(elements.contiguous().data_ptr() if E else None, E, K,
+                                              mask.data_ptr() if E else None, out.data_ptr() if E else None,
+                                              kept.data_ptr(), ws.data_ptr(), ws.numel(),
+                                              torch.cuda.current_stream(dev).cuda_stream))
+        n_kept = int(kept.item())
+        return reindex_tensors(vertex_bits, out[:n_kept])
+
+
 def _selector_mask(keep, n_elements: int) -> np.ndarray:
     """Element selector -> bool mask (ops.py:71-87 semantics): a bool mask of length
     n_elements, or strictly increasing element positions."""

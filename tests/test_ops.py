@@ -144,3 +144,41 @@ def test_merge_tensors_errors(cuda_ok):
     b = (torch.zeros((3, 3), dtype=torch.int32, device="cuda"), torch.zeros((1, 3), dtype=torch.int32, device="cuda"))
     with pytest.raises(rmx.MeshError):
         rmx.merge_tensors([a, b])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,case", _cases("subset"), ids=[c[0] for c in _cases("subset")])
+def test_subset_tensors_matches_reference(cuda_ok, name, case):
+    """The device-resident subset (compaction kernel + re-index) against the reference subset."""
+    import torch
+
+    import paper_2109_09812_b200 as rmx
+    v = torch.from_numpy(case["in_vtx"].view(np.int32).copy()).cuda()
+    e = torch.from_numpy(case["in_idx"].view(np.int32).copy()).cuda()
+    keep = torch.from_numpy(case["keep"]).cuda()
+    for sel in (keep, torch.zeros(e.shape[0], dtype=torch.bool, device="cuda").index_fill_(0, keep, True)):
+        res = rmx.subset_tensors(v, e, sel)
+        assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), case["out_vtx"])
+        assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), case["out_idx"])
+
+
+@pytest.mark.gpu
+def test_subset_tensors_large_and_errors(cuda_ok):
+    import torch
+
+    import paper_2109_09812_b200 as rmx
+    from oracle import remesh_oracle as O
+    rng = np.random.default_rng(3)
+    V, E, K = 100_000, 150_000, 3
+    words = (rng.integers(0, 50, size=(V, 3)).astype(np.uint32) * np.uint32(0x01000193))
+    idx = rng.integers(0, V, size=(E, K)).astype(np.uint32)
+    mask = rng.random(E) < 0.3
+    ref = O.reindex(words, idx[mask])
+    res = rmx.subset_tensors(torch.from_numpy(words.view(np.int32)).cuda(), torch.from_numpy(idx.view(np.int32)).cuda(),
+                             torch.from_numpy(mask).cuda())
+    assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), ref["elements"])
+    with pytest.raises(rmx.MeshError):
+        rmx.subset_tensors(torch.zeros((3, 2), dtype=torch.int32, device="cuda"),
+                           torch.zeros((4, 3), dtype=torch.int32, device="cuda"),
+                           torch.tensor([2, 1], device="cuda"))
