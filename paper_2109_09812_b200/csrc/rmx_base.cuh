@@ -49,6 +49,25 @@ constexpr int kFieldWords = kFieldValues / 32;
 constexpr int kMaxRankDim = 4;
 __host__ __device__ inline size_t pk_base(int P) { return 4 + 3 * static_cast<size_t>(P); }
 __host__ __device__ inline size_t pk_rank_base(int P) { return pk_base(P) + 8 + 4 * kMaxRuns; }
-__host__ __device__ inline size_t plan_words(int P) { return pk_rank_base(P) + RMX_MAX_DIM; }
+
+// Value ranks (D <= kMaxRankDim, packed mode): the bits of one component in
+// the packed key (its runs and ranked field: contiguous, kMinValueBits ..
+// kMaxValueBits wide) are a value cv of that component.  Structured
+// coordinates -- lattices, grids, quantised meshes -- take few distinct cv per
+// axis although their bits vary widely (C2: 5001 values in 16 bits).  When
+// the key gets narrower (fewer 8-bit passes, or u32 instead of u64 keys) cv is
+// replaced by its rank among the values that occur: monotone and injective on
+// them, so key order and equality are unchanged.  The value sets come from
+// k_valueset (a strided sample first, to skip the full pass when even the
+// sample needs the full width), the tables from k_value_plan.
+//   [0] state: 0 off, 1 full value-set pass wanted, 2 keys carry value ranks
+//   [1] candidate components (bit c)
+//   [4 + 4c ..] component c: old low bit, old width, new low bit, new width | ranked << 31
+constexpr int kMinValueBits = 4;
+constexpr int kMaxValueBits = 16;
+constexpr int kValueWords = (1 << kMaxValueBits) / 32;
+constexpr uint32_t kValueSetBytes = 192 * 1024;  // k_valueset byte maps: sum of 2^w over the candidates
+__host__ __device__ inline size_t pk_value_base(int P) { return pk_rank_base(P) + RMX_MAX_DIM; }
+__host__ __device__ inline size_t plan_words(int P) { return pk_value_base(P) + 4 + 4 * kMaxRankDim; }
 
 }  // namespace rmx

@@ -70,14 +70,14 @@ int rank_force() {
     return v;
 }
 
-// packed-key path tiles (RMX_PK_IPT = 8 | 12 | 16 selects the sort tile, tuning)
+// packed-key sort tiles: RMX_PK_CFG (below) selects rows per thread, tuning only
 constexpr int kPkUniqIpt = 12;
 constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
 int pk_sort_ipt() {
     static int v = [] {
         const char* e = std::getenv("RMX_PK_CFG");
-        const int x = e ? std::atoi(e) : 12;
-        return (x == 8 || x == 12 || x == 16) ? x : 12;
+        const int x = e ? std::atoi(e) : 24;
+        return (x == 12 || x == 16 || x == 20 || x == 24 || x == 28) ? x : 24;
     }();
     return v;
 }
@@ -95,6 +95,7 @@ struct Layout {
     size_t pk_counts, pk_totals;  // packed passes: [256][ntiles_pk] tile counts / column scans, [256] totals
     size_t pk_digits;             // packed passes: [V] digit byte of the current pass per row
     size_t ukeys;                 // packed key of every unique row (K3' -> unpack)
+    size_t rank16, vinv, vsets;   // value ranks (D <= kMaxRankDim): rank tables, inverse tables, value sets
     size_t total;
 };
 
@@ -125,7 +126,11 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.pk_totals = take(256 * 4);
     L.pk_digits = take(static_cast<size_t>(V) + 16);
     L.ukeys = take(static_cast<size_t>(V) * 8);
+    const size_t vr_dim = L.D <= kMaxRankDim ? static_cast<size_t>(L.D) : 0;
+    L.rank16 = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
+    L.vinv = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
     L.ctl_begin = off;
+    L.vsets = take(vr_dim * kValueWords * 4);
     L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
@@ -277,6 +282,37 @@ int launch_pack(const PackArgs& a, cudaStream_t s) {
     return RMX_OK;
 }
 
+// RMX_VALUE_RANK=0 turns value ranks off (read per call: tests switch it at run time)
+bool value_rank_enabled() {
+    const char* e = std::getenv("RMX_VALUE_RANK");
+    return !(e && e[0] == '0');
+}
+
+template <int D_CT>
+int launch_valueset(const ValueSetArgs& a, uint64_t items, cudaStream_t s) {
+    int sms = 0;
+    int rc = device_sms(sms);
+    if (rc) return rc;
+    const size_t smem = kValueSetBytes + 16;  // + a spare byte for the components that are not candidates
+    if ((rc = ensure_smem(k_valueset<D_CT>, smem))) return rc;
+    const uint64_t want = (items + kVsThreads - 1) / kVsThreads;
+    const int grid = static_cast<int>(want < static_cast<uint64_t>(sms) ? (want ? want : 1) : sms);
+    k_valueset<D_CT><<<grid, kVsThreads, smem, s>>>(a);
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+int dispatch_valueset(const ValueSetArgs& a, int dim, cudaStream_t s) {
+    const uint64_t items = a.shift ? (static_cast<uint64_t>(a.n) >> a.shift) + 256 : a.n;
+    switch (dim) {
+        case 1: return launch_valueset<1>(a, items, s);
+        case 2: return launch_valueset<2>(a, items, s);
+        case 3: return launch_valueset<3>(a, items, s);
+        case 4: return launch_valueset<4>(a, items, s);
+        default: return RMX_OK;
+    }
+}
+
 int dispatch_pack(const PackArgs& a, cudaStream_t s) {
     switch (a.dim) {
         case 1: return launch_pack<1>(a, s);
@@ -302,12 +338,13 @@ int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     return RMX_OK;
 }
 
-// RMX_PK_CFG = "<rows per thread>x<CTAs per SM>" (tuning aid; default 12x3)
+// RMX_PK_CFG = "<rows per thread>x<CTAs per SM>" (tuning aid; default 24x2: 6144-row tiles,
+// two CTAs per SM -- measured against 8..32 rows x 1..4 CTAs on C2 / C3 / C5s)
 int pk_minb() {
     static int v = [] {
         const char* e = std::getenv("RMX_PK_CFG");
         const char* x = e ? std::strchr(e, 'x') : nullptr;
-        return x ? std::atoi(x + 1) : 3;
+        return x ? std::atoi(x + 1) : 2;
     }();
     return v;
 }
@@ -322,11 +359,11 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     RMX_CHECK(cudaGetLastError());
     const int cfg = pk_sort_ipt() * 10 + pk_minb();
     switch (cfg) {
-        case 84: return launch_downsweep<8, 4>(a, s);
-        case 124: return launch_downsweep<12, 4>(a, s);
+        case 123: return launch_downsweep<12, 3>(a, s);
         case 162: return launch_downsweep<16, 2>(a, s);
-        case 163: return launch_downsweep<16, 3>(a, s);
-        default: return launch_downsweep<12, 3>(a, s);
+        case 202: return launch_downsweep<20, 2>(a, s);
+        case 282: return launch_downsweep<28, 2>(a, s);
+        default: return launch_downsweep<24, 2>(a, s);
     }
 }
 
@@ -592,9 +629,25 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     // ---- packed-key path (kernels exit at once in AoS mode)
     if ((rc = cond_begin(gc, kSlotPkA))) return rc;
+    uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
+    uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
+    if (L.D <= kMaxRankDim && value_rank_enabled()) {  // value ranks: sample, decide, full set, tables
+        uint32_t* vsets = reinterpret_cast<uint32_t*>(base + L.vsets);
+        const uint32_t shift = V >= (1ull << 22) ? 6u : 0u;
+        ValueSetArgs va{vtx, flags, idx, plan, fields, vsets, d_status, static_cast<uint32_t>(V), shift, vec};
+        if (shift && (rc = dispatch_valueset(va, L.D, s))) return rc;
+        ValuePlanArgs pa{plan, vsets, rank16, vinv, d_status, L.D, 0};
+        k_value_plan<<<1, 1024, 0, s>>>(pa);
+        RMX_CHECK(cudaGetLastError());
+        va.shift = 0u;
+        if ((rc = dispatch_valueset(va, L.D, s))) return rc;
+        pa.final_pass = 1;
+        k_value_plan<<<1, 1024, 0, s>>>(pa);
+        RMX_CHECK(cudaGetLastError());
+    }
     {
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), fields,
-                   d_status, static_cast<uint32_t>(V), L.D, vec};
+                   rank16, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
     if ((rc = cond_end(gc))) return rc;
@@ -637,8 +690,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
                        sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
         if ((rc = launch_unique_pk(a, s))) return rc;
-        UnpackPkArgs u{plan, vtx, idx, vary, fields, ukeys, out_vtx, reinterpret_cast<unsigned long long*>(d_count),
-                       d_status, L.D, aligned16(out_vtx) ? 1 : 0};
+        UnpackPkArgs u{plan, vtx, idx, vary, fields, ukeys, vinv, out_vtx,
+                       reinterpret_cast<unsigned long long*>(d_count), d_status, L.D, aligned16(out_vtx) ? 1 : 0};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
     if ((rc = cond_end(gc))) return rc;

@@ -252,48 +252,360 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
     }
 }
 
-// Cleaned row (D_CT words) -> packed key with the plan's runs (run r takes
-// len bits of component comp from bit src and puts them at bit dst).  The first
-// kRegRuns runs live in registers (typical meshes need one per component).
+// Cleaned row (D_CT <= kMaxRankDim words) -> packed key, one component at a
+// time: component c occupies key bits [lo_c, lo_c + w_c) (rmx_base.cuh), its
+// value cv_c is its first run (src0, mask0 -> bit 0 of cv; in registers), any
+// further runs of c (rare: a shared-memory loop) and its ranked field (looked
+// up in the shared field table, placed at frel).  All in 32-bit arithmetic.
 template <int D_CT>
 struct RowPacker {
-    static constexpr int kRegRuns = 4;
-    static constexpr int kRanked = D_CT <= kMaxRankDim ? D_CT : 0;
-    uint32_t rc[kRegRuns], rs[kRegRuns], rm[kRegRuns], rd[kRegRuns];
-    uint32_t fd[kRanked > 0 ? kRanked : 1];  // destination bit of a ranked field, 64 = none
+    static_assert(D_CT >= 1 && D_CT <= kMaxRankDim, "per-component packing covers D <= kMaxRankDim");
+    uint32_t src0[D_CT], msk0[D_CT], frel[D_CT], fmsk[D_CT], lo[D_CT], xr[D_CT];  // xr: extra runs [xr & 0xFFFF, xr >> 16)
     const uint32_t* s_runs;
-    const uint16_t* s_rank;                  // [D_CT][kFieldValues]
-    uint32_t nruns;
+    const uint16_t* s_rank;  // [D_CT][kFieldValues]
 
-    __device__ __forceinline__ RowPacker(const uint32_t* runs, uint32_t n, const uint32_t* rk, const uint16_t* ranks)
-        : s_runs(runs), s_rank(ranks), nruns(n) {
+    __device__ __forceinline__ RowPacker(const uint32_t* plan, const uint32_t* runs, uint32_t nruns, const uint16_t* ranks)
+        : s_runs(runs), s_rank(ranks) {
+        const uint32_t* rk = plan + pk_rank_base(4 * D_CT);
+        const uint32_t* vb = plan + pk_value_base(4 * D_CT);
 #pragma unroll
-        for (int r = 0; r < kRegRuns; ++r) {
-            const bool on = static_cast<uint32_t>(r) < n;
-            rc[r] = on ? runs[4 * r] : 0u;
-            rs[r] = on ? runs[4 * r + 1] : 0u;
-            rm[r] = on ? low_mask(runs[4 * r + 2]) : 0u;
-            rd[r] = on ? runs[4 * r + 3] : 0u;
+        for (int c = 0; c < D_CT; ++c) {
+            const uint32_t l = vb[4 + 4 * c];
+            lo[c] = min(l, 63u);
+            src0[c] = 0u;
+            msk0[c] = 0u;
+            uint32_t b = nruns, e = 0;
+            for (uint32_t r = 0; r < nruns; ++r) {
+                if (runs[4 * r] != static_cast<uint32_t>(c)) continue;
+                if (b == nruns) {  // the component's first run sits at its low bit
+                    b = r;
+                    src0[c] = runs[4 * r + 1];
+                    msk0[c] = low_mask(runs[4 * r + 2]);
+                }
+                e = r + 1;
+            }
+            xr[c] = b < e ? ((b + 1) | (e << 16)) : 0u;
+            const bool ranked = rk[c] >> 31;
+            frel[c] = ranked ? (rk[c] & 0xFFFFu) - l : 0u;
+            fmsk[c] = ranked ? 0xFFFFFFFFu : 0u;  // branch-free: the table entry is masked off
         }
-#pragma unroll
-        for (int c = 0; c < kRanked; ++c) fd[c] = (rk[c] >> 31) ? (rk[c] & 0xFFFFu) : 64u;
+    }
+
+    // no value bits at all (k_valueset: components that are not candidates)
+    __device__ __forceinline__ void clear(int c) {
+        msk0[c] = 0u;
+        fmsk[c] = 0u;
+        xr[c] = 0u;
+    }
+
+    __device__ __forceinline__ uint32_t value(int c, uint32_t w) const {
+        uint32_t v = (w >> src0[c]) & msk0[c];
+        for (uint32_t q = xr[c] & 0xFFFFu; q < (xr[c] >> 16); ++q) {
+            const uint32_t* ru = s_runs + 4 * q;
+            v |= ((w >> ru[1]) & low_mask(ru[2])) << (ru[3] - lo[c]);
+        }
+        return v | ((static_cast<uint32_t>(s_rank[c * kFieldValues + (w >> kFieldLo)]) << frel[c]) & fmsk[c]);
     }
 
     __device__ __forceinline__ uint64_t operator()(const uint32_t (&k)[D_CT]) const {
         uint64_t key = 0;
 #pragma unroll
-        for (int r = 0; r < kRegRuns; ++r)
-            key |= static_cast<uint64_t>((pick<D_CT>(k, rc[r]) >> rs[r]) & rm[r]) << rd[r];
-        for (uint32_t r = kRegRuns; r < nruns; ++r) {
-            const uint32_t* ru = s_runs + 4 * r;
-            key |= static_cast<uint64_t>((pick<D_CT>(k, ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
-        }
-#pragma unroll
-        for (int c = 0; c < kRanked; ++c)
-            if (fd[c] < 64u) key |= static_cast<uint64_t>(s_rank[c * kFieldValues + (k[c] >> kFieldLo)]) << fd[c];
+        for (int c = 0; c < D_CT; ++c) key |= static_cast<uint64_t>(value(c, k[c])) << lo[c];
         return key;
     }
 };
+
+// ---------------------------------------------------------------------------
+// Value ranks (rmx_base.cuh): the layout of each component in the packed key
+// before and after, the transform k_pack applies and k_unpack_pk inverts.
+template <int D_CT>
+struct ValueMap {
+    static constexpr int kN = (D_CT > 0 && D_CT <= kMaxRankDim) ? D_CT : 1;
+    uint32_t lo[kN], w[kN], nlo[kN], nw[kN];
+    uint32_t ranked;  // bit c: component c carries its value rank
+    bool on;
+
+    __device__ __forceinline__ void load(const uint32_t* plan) {
+        on = false;
+        ranked = 0u;
+        if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) {
+            const uint32_t* vb = plan + pk_value_base(4 * D_CT);
+            on = vb[0] == 2u;
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) {
+                const uint32_t* e = vb + 4 + 4 * c;
+                w[c] = e[1];
+                nw[c] = e[3] & 0xFFFFu;
+                lo[c] = min(e[0], 63u);  // a zero-width component may sit at bit 64
+                nlo[c] = min(e[2], 63u);
+                ranked |= (e[3] >> 31) << c;
+            }
+        }
+    }
+    // key with value ranks from the component values (rank16: [c][2^kMaxValueBits] rank of every occurring value)
+    template <int DP>
+    __device__ __forceinline__ uint64_t ranked_key(const RowPacker<DP>& pack, const uint32_t (&k)[DP],
+                                                   const uint16_t* __restrict__ rank16) const {
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < DP; ++c) {
+            uint32_t v = pack.value(c, k[c]);
+            if ((ranked >> c) & 1u) v = __ldg(rank16 + (static_cast<size_t>(c) << kMaxValueBits) + v);
+            out |= static_cast<uint64_t>(v) << nlo[c];
+        }
+        return out;
+    }
+    // inverse (inv: [c][2^kMaxValueBits] value of every rank)
+    __device__ __forceinline__ uint64_t from_rank(uint64_t key, const uint16_t* __restrict__ inv) const {
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < kN; ++c) {
+            uint32_t v = static_cast<uint32_t>(key >> nlo[c]) & low_mask(nw[c]);
+            if ((ranked >> c) & 1u) v = __ldg(inv + (static_cast<size_t>(c) << kMaxValueBits) + v);
+            out |= static_cast<uint64_t>(v) << lo[c];
+        }
+        return out;
+    }
+};
+
+// Shared-memory run list + field-rank table for RowPacker (k_pack, k_valueset).
+template <int D_CT>
+__device__ __forceinline__ void load_packer(const uint32_t* plan, const uint32_t* fields, uint32_t* s_runs,
+                                            uint16_t* s_rank) {
+    const int D = D_CT > 0 ? D_CT : 1;
+    const uint32_t* pk = plan + pk_base(4 * D);
+    for (uint32_t i = threadIdx.x; i < 4 * pk[4]; i += blockDim.x) s_runs[i] = pk[8 + i];
+    if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(fields, plan + pk_rank_base(4 * D_CT), D_CT, s_rank, nullptr);
+}
+
+// Occurring packed values of every candidate component over the used rows
+// (shift > 0: rows k << shift only -- the sample that decides whether the full
+// pass can pay).  One 1024-thread CTA per SM keeps a byte per possible value
+// (2^w bytes per component, <= kValueSetBytes in all: plan_body drops the
+// widest candidates beyond that) and sets it with plain stores: lanes that hit
+// the same value merge instead of serialising as shared atomics on one bitmap
+// word would (structured coordinates crowd a few words).  At the end the bytes
+// are folded into bit words and OR-ed into vsets.
+struct ValueSetArgs {
+    const uint32_t* vtx;
+    const uint8_t* flags;
+    const uint32_t* idx;  // idx[0]: the replacement row
+    const uint32_t* plan;
+    const uint32_t* fields;
+    uint32_t* vsets;  // [D][kValueWords]
+    const uint32_t* status;
+    uint32_t n;
+    uint32_t shift;
+    int vec;
+};
+
+constexpr int kVsThreads = 1024;
+
+template <int D_CT>
+__global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
+    static_assert(D_CT >= 1 && D_CT <= kMaxRankDim, "value ranks cover D <= kMaxRankDim");
+    extern __shared__ __align__(16) uint8_t s_map[];  // [sum of 2^w over candidates]
+    const uint32_t* pk = a.plan + pk_base(4 * D_CT);
+    const uint32_t* vb = a.plan + pk_value_base(4 * D_CT);
+    __shared__ uint32_t s_runs[4 * kMaxRuns];
+    __shared__ uint16_t s_rank[D_CT * kFieldValues];
+    if (*a.status || pk[0] == 0u || (a.shift == 0u && vb[0] != 1u)) return;  // uniform
+    const uint32_t cand = vb[1];
+    if (!cand) return;
+    load_packer<D_CT>(a.plan, a.fields, s_runs, s_rank);
+    ValueMap<D_CT> vm;
+    vm.load(a.plan);
+    uint32_t off[D_CT];
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int c = 0; c < D_CT; ++c) {
+        off[c] = bytes;
+        if ((cand >> c) & 1u) bytes += 1u << vm.w[c];
+    }
+    for (uint32_t i = threadIdx.x; i < bytes / 16u + 1u; i += kVsThreads) reinterpret_cast<uint4*>(s_map)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    RowPacker<D_CT> pack(a.plan, s_runs, pk[4], s_rank);
+#pragma unroll
+    for (int c = 0; c < D_CT; ++c)
+        if (!((cand >> c) & 1u)) {  // value 0 into a spare byte past the maps: no branch per row
+            pack.clear(c);
+            off[c] = bytes;
+        }
+    // unused rows stand for the replacement row (used, so its values are in the sets anyway)
+    uint32_t ref[D_CT];
+#pragma unroll
+    for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(a.vtx + static_cast<size_t>(a.idx[0]) * D_CT + c);
+    auto note = [&](const uint32_t (&k)[D_CT], bool used) {
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) s_map[off[c] + pack.value(c, used ? k[c] : ref[c])] = 1u;
+    };
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kVsThreads;
+    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kVsThreads + threadIdx.x;
+    if (a.shift) {
+        // sample: the first kSampleRun rows of every (kSampleRun << shift) -- contiguous reads
+        constexpr uint32_t kSampleRun = 256;
+        const uint64_t ns = ((static_cast<uint64_t>(a.n) >> a.shift) + kSampleRun) & ~static_cast<uint64_t>(kSampleRun - 1);
+        for (uint64_t s = start; s < ns; s += stride) {
+            const uint64_t i = ((s / kSampleRun) * kSampleRun << a.shift) + (s % kSampleRun);
+            if (i < a.n) {
+                uint32_t k[D_CT];
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
+                note(k, a.flags[i] != 0);
+            }
+        }
+    } else {
+        uint64_t done = 0;
+        if constexpr (D_CT == 3) {
+            if (a.vec) {  // two groups of 4 rows in flight per thread
+                const uint64_t ng = a.n >> 2;
+                const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
+                const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
+                auto group = [&](const uint4& x, const uint4& y, const uint4& z, uint32_t f) {
+                    const uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) note(k[j], ((f >> (8 * j)) & 255u) != 0u);
+                };
+                uint64_t g = start;
+                for (; g + stride < ng; g += 2 * stride) {
+                    const uint64_t h = g + stride;
+                    const uint4 x0 = __ldcs(v4 + 3 * g), y0 = __ldcs(v4 + 3 * g + 1), z0 = __ldcs(v4 + 3 * g + 2);
+                    const uint4 x1 = __ldcs(v4 + 3 * h), y1 = __ldcs(v4 + 3 * h + 1), z1 = __ldcs(v4 + 3 * h + 2);
+                    const uint32_t f0 = __ldcs(f4 + g), f1 = __ldcs(f4 + h);
+                    group(x0, y0, z0, f0);
+                    group(x1, y1, z1, f1);
+                }
+                if (g < ng) group(__ldcs(v4 + 3 * g), __ldcs(v4 + 3 * g + 1), __ldcs(v4 + 3 * g + 2), __ldcs(f4 + g));
+                done = ng << 2;
+            }
+        }
+        for (uint64_t i = done + start; i < a.n; i += stride) {
+            uint32_t k[D_CT];
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
+            note(k, a.flags[i] != 0);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < D_CT; ++c) {
+        if (!((cand >> c) & 1u)) continue;
+        const uint32_t words = vm.w[c] > 5u ? (1u << (vm.w[c] - 5u)) : 1u;
+        const uint32_t nbytes = 1u << vm.w[c];
+        for (uint32_t j = threadIdx.x; j < words; j += kVsThreads) {
+            uint32_t x = 0u;
+            for (uint32_t q = 0; q < 8u && 4u * (8u * j + q) < nbytes; ++q) {
+                const uint32_t b4 = reinterpret_cast<const uint32_t*>(s_map + off[c])[8u * j + q];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x |= ((b4 >> (8 * e)) & 1u) << (4u * q + e);
+            }
+            if (x) atomicOr(a.vsets + c * kValueWords + j, x);
+        }
+    }
+}
+
+// One CTA of 1024 threads.  final == 0 (after the sample): keep the candidates
+// whose sampled value count already needs fewer bits, and ask for the full
+// pass when that alone would shorten the key (state 1).  final == 1 (after the
+// full pass): exact counts; if the key gets shorter, build the rank tables,
+// lay the components out again and update the plan (key words, bits, passes,
+// final buffer) -- state 2.  Otherwise state 0 and the keys stay as they are.
+struct ValuePlanArgs {
+    uint32_t* plan;
+    const uint32_t* vsets;
+    uint16_t* rank16;  // [D][2^kMaxValueBits] rank of every occurring value
+    uint16_t* vinv;    // [D][2^kMaxValueBits] value of every rank
+    const uint32_t* status;
+    int dim;
+    int final_pass;
+};
+
+__device__ __forceinline__ uint32_t bits_for(uint32_t count) { return count <= 1u ? 0u : 32u - __clz(count - 1u); }
+
+__global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
+    __shared__ uint32_t s_warp[32];
+    const int D = a.dim;
+    if (*a.status || D > kMaxRankDim) return;
+    uint32_t* plan = a.plan;
+    uint32_t* pk = plan + pk_base(4 * D);
+    uint32_t* vb = plan + pk_value_base(4 * D);
+    if (pk[0] == 0u) return;
+    const uint32_t state = vb[0];
+    const uint32_t cand = vb[1];
+    if (a.final_pass ? state != 1u : cand == 0u) return;  // uniform
+    const uint32_t old_bits = pk[2], old_npass = pk[3], old_kw = pk[1];
+    uint32_t w[kMaxRankDim], cnt[kMaxRankDim];
+    for (int c = 0; c < D; ++c) w[c] = vb[4 + 4 * c + 1];
+    __syncthreads();  // every thread has read the plan before thread 0 rewrites it
+    const uint32_t t = threadIdx.x;
+    for (int c = 0; c < D; ++c) {
+        cnt[c] = 0u;
+        if (!((cand >> c) & 1u)) continue;
+        const uint32_t* set = a.vsets + c * kValueWords;
+        uint32_t tot;
+        (void)block_exclusive_scan<32>(__popc(set[2 * t]) + __popc(set[2 * t + 1]), s_warp, tot);
+        __syncthreads();
+        cnt[c] = tot;
+    }
+    uint32_t ranked = 0, nbits = 0;
+    for (int c = 0; c < D; ++c) {
+        const bool r = ((cand >> c) & 1u) && bits_for(cnt[c]) < w[c];
+        if (r) ranked |= 1u << c;
+        nbits += r ? bits_for(cnt[c]) : w[c];
+    }
+    const uint32_t npass = (nbits + 7u) / 8u;
+    const bool gain = npass < old_npass || (old_kw == 2u && nbits <= 32u);
+    (void)old_bits;
+    if (!a.final_pass) {
+        if (t == 0) {
+            vb[0] = gain ? 1u : 0u;
+            vb[1] = gain ? ranked : 0u;
+        }
+        return;
+    }
+    if (!gain) {
+        if (t == 0) vb[0] = 0u;
+        return;
+    }
+    for (int c = 0; c < D; ++c) {
+        if (!((ranked >> c) & 1u)) continue;
+        const uint32_t* set = a.vsets + c * kValueWords;
+        const uint32_t s0 = set[2 * t], s1 = set[2 * t + 1];
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan<32>(__popc(s0) + __popc(s1), s_warp, tot);
+        __syncthreads();
+        uint16_t* inv = a.vinv + (static_cast<size_t>(c) << kMaxValueBits);
+        uint16_t* rnk = a.rank16 + (static_cast<size_t>(c) << kMaxValueBits);
+        uint32_t r = ex;
+        for (uint32_t h = 0; h < 2u; ++h) {
+            uint32_t m = h ? s1 : s0;
+            while (m) {
+                const uint32_t v = ((2u * t + h) << 5) + __ffs(m) - 1u;
+                inv[r] = static_cast<uint16_t>(v);
+                rnk[v] = static_cast<uint16_t>(r);
+                ++r;
+                m &= m - 1u;
+            }
+        }
+    }
+    if (t == 0) {
+        uint32_t run = 0;
+        for (int c = D - 1; c >= 0; --c) {
+            const bool r = (ranked >> c) & 1u;
+            const uint32_t width = r ? bits_for(cnt[c]) : w[c];
+            vb[4 + 4 * c + 2] = run;
+            vb[4 + 4 * c + 3] = width | (r ? (1u << 31) : 0u);
+            run += width;
+        }
+        pk[1] = run > 32u ? 2u : 1u;
+        pk[2] = run;
+        pk[3] = npass;
+        plan[0] = npass & 1u;
+        plan[1] = npass;
+        vb[1] = ranked;
+        vb[0] = 2u;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // K1b': packed keys + origins, histogram of packed digit 0.
@@ -306,6 +618,7 @@ struct PackArgs {
     size_t vals_off;  // words
     uint8_t* digits;  // [n] packed digit 0 per row (read by the first upsweep)
     const uint32_t* fields;  // [D][kFieldWords] occurring sign+exponent fields (K1a)
+    const uint16_t* rank16;  // value-rank tables (k_value_plan)
     const uint32_t* status;
     uint32_t n;
     int dim;
@@ -349,7 +662,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
         uint32_t ref[D_CT];
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(repl + c);
-        const RowPacker<D_CT> pack(s_runs, nruns, rk, s_rank);
+        const RowPacker<D_CT> pack0(a.plan, s_runs, nruns, s_rank);
+        ValueMap<D_CT> vm;
+        vm.load(a.plan);
+        auto pack = [&](const uint32_t (&k)[D_CT]) { return vm.on ? vm.ranked_key(pack0, k, a.rank16) : pack0(k); };
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
             if (a.vec) {
@@ -902,6 +1218,7 @@ struct UnpackPkArgs {
     const uint32_t* vary;
     const uint32_t* fields;
     const void* ukeys;
+    const uint16_t* vinv;   // value-rank inverse tables (k_value_plan)
     uint32_t* out_vtx;
     const unsigned long long* count;
     const uint32_t* status;
@@ -946,6 +1263,12 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
     const bool wide = pk[1] == 2u;
     const uint64_t* k64 = static_cast<const uint64_t*>(a.ukeys);
     const uint32_t* k32 = static_cast<const uint32_t*>(a.ukeys);
+    ValueMap<D_CT> vm;
+    vm.load(a.plan);
+    auto load_key = [&](uint64_t i) {
+        const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+        return vm.on ? vm.from_rank(key, a.vinv) : key;
+    };
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t t0 = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     uint64_t done = 0;
@@ -956,8 +1279,7 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
             for (uint64_t g = t0; g < ng; g += stride) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const uint64_t i = 4 * g + r;
-                    const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+                    const uint64_t key = load_key(4 * g + r);
                     unpack_row<D_CT>(key, w + r * D_CT, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
                 }
                 uint4* dst = reinterpret_cast<uint4*>(a.out_vtx + 4 * g * D_CT);
@@ -969,7 +1291,7 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
         }
     }
     for (uint64_t i = done + t0; i < U; i += stride) {
-        const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+        const uint64_t key = load_key(i);
         unpack_row<D_CT>(key, a.out_vtx + i * D, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
     }
 }

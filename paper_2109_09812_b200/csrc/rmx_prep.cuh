@@ -230,9 +230,13 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
     const int P = 4 * D;
     uint32_t* pk = plan + pk_base(P);
     uint32_t* rk = plan + pk_rank_base(P);
-    uint32_t bits = 0, runs = 0;
+    uint32_t* vb = plan + pk_value_base(P);
+    vb[0] = 0u;
+    vb[1] = 0u;
+    uint32_t bits = 0, runs = 0, cand = 0;
     bool fits = true;
     for (int c = D - 1; c >= 0 && fits; --c) {
+        const uint32_t c_lo = bits;
         uint32_t m = vary[c];
         // field rank (see rmx_base.cuh) when it needs fewer bits than the varying field bits
         uint32_t rank_bits = 0;
@@ -268,8 +272,32 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
                 bits += rank_bits;
             }
         }
+        if (fits && D <= kMaxRankDim) {  // component c occupies key bits [c_lo, bits)
+            const uint32_t w = bits - c_lo;
+            uint32_t* e = vb + 4 + 4 * c;
+            e[0] = c_lo;
+            e[1] = w;
+            e[2] = c_lo;
+            e[3] = w;
+            if (w >= static_cast<uint32_t>(kMinValueBits) && w <= static_cast<uint32_t>(kMaxValueBits)) cand |= 1u << c;
+        }
     }
     if (fits) {
+        for (;;) {  // the value-set byte maps must fit one CTA: drop the widest candidates
+            uint32_t need = 0, widest = 0, wmax = 0;
+            for (int c = 0; c < D && c < kMaxRankDim; ++c) {
+                if (!((cand >> c) & 1u)) continue;
+                const uint32_t w = vb[4 + 4 * c + 1];
+                need += 1u << w;
+                if (w > wmax) {
+                    wmax = w;
+                    widest = static_cast<uint32_t>(c);
+                }
+            }
+            if (need <= kValueSetBytes) break;
+            cand &= ~(1u << widest);
+        }
+        vb[1] = cand;
         const uint32_t npass = (bits + 7u) / 8u;
         pk[0] = 1u;
         pk[1] = bits > 32u ? 2u : 1u;

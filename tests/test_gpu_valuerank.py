@@ -1,0 +1,170 @@
+"""GPU: packed keys with value ranks (rmx_base.cuh) against the oracle.
+
+Each component takes its values from a small set of words whose varying
+bits span 4..17 bits, so a component's packed value cv can be replaced by
+its rank among the occurring values.  Results must be bit-exact against the
+oracle (incl. scratch) with value ranks on and off (RMX_VALUE_RANK=0), and
+rmx_plan_info must report the key width a Python model of the plan predicts.
+Meshes of >= 2^22 rows take the sampled decision first (the first 256 rows of
+every 16384); one of them is built so that the sample promises a gain the
+full set does not deliver -- the plan must fall back to the plain packed key.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import FIELDS
+from oracle import remesh_oracle as O
+from test_gpu_fieldrank import plan_info
+
+pytestmark = pytest.mark.gpu
+
+BASE = np.uint32(0x3F800000)  # 1.0f: sign and exponent field constant, no field rank
+
+
+@pytest.fixture(scope="module")
+def rmx(cuda_ok):
+    import paper_2109_09812_b200 as p
+    return p
+
+
+@pytest.fixture
+def value_rank_off():
+    old = os.environ.get("RMX_VALUE_RANK")
+    os.environ["RMX_VALUE_RANK"] = "0"
+    yield
+    if old is None:
+        del os.environ["RMX_VALUE_RANK"]
+    else:
+        os.environ["RMX_VALUE_RANK"] = old
+
+
+def value_set(rng, m, b):
+    """m distinct values in [0, 2^b) including 0 and 2^b - 1 (so all b bits vary)."""
+    if m <= 2:
+        return np.array([0, (1 << b) - 1][:m], np.uint32)
+    mid = rng.choice(np.arange(1, (1 << b) - 1, dtype=np.uint32), size=m - 2, replace=False)
+    return np.concatenate([[0, (1 << b) - 1], mid]).astype(np.uint32)
+
+
+def set_mesh(seed, V, E, K, comps):
+    """comps: per component (m distinct values, b varying bits, mantissa shift)."""
+    rng = np.random.default_rng(seed)
+    D = len(comps)
+    words = np.empty((V, D), np.uint32)
+    for c, (m, b, sh) in enumerate(comps):
+        vals = value_set(rng, m, b)
+        words[:, c] = BASE | (vals[rng.integers(0, len(vals), size=V)] << np.uint32(sh))
+    idx = rng.integers(0, V, size=(E, K)).astype(np.uint32)
+    idx[0, 0] = 0
+    return words, idx
+
+
+def bits_for(n):
+    return 0 if n <= 1 else int(n - 1).bit_length()
+
+
+def model_bits(words, idx):
+    """(plain packed bits, bits with value ranks) of the plan for `set_mesh` data (< 2^22 rows)."""
+    used = np.zeros(words.shape[0], bool)
+    used[idx.reshape(-1)] = True
+    u = words[used]
+    ref = words[idx[0, 0]]
+    w = [bin(int(np.bitwise_or.reduce(u[:, c] ^ ref[c]))).count("1") for c in range(words.shape[1])]
+    m = [len(np.unique(u[:, c])) for c in range(words.shape[1])]
+    bits = sum(w)
+    npass, kw = (bits + 7) // 8, 2 if bits > 32 else 1
+    if words.shape[1] > 4:
+        return bits, bits
+    cand = [4 <= wc <= 16 for wc in w]
+    while sum(1 << wc for cd, wc in zip(cand, w) if cd) > 192 * 1024:   # byte maps of one CTA
+        widest = max((wc, -c) for c, (cd, wc) in enumerate(zip(cand, w)) if cd)
+        cand[-widest[1]] = False
+
+    def gain(nb):
+        return (nb + 7) // 8 < npass or (kw == 2 and nb <= 32)
+
+    if not any(cand) or not gain(sum(0 if cd else wc for cd, wc in zip(cand, w))):
+        return bits, bits
+    ranked = [cd and bits_for(mc) < wc for cd, wc, mc in zip(cand, w, m)]
+    nb = sum(bits_for(mc) if r else wc for r, wc, mc in zip(ranked, w, m))
+    return bits, (nb if gain(nb) else bits)
+
+
+def check(rmx, words, idx):
+    ref = O.reindex(words, idx)
+    out, sc = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
+    for f in FIELDS:
+        assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
+
+
+CASES = [
+    # seed, V, E, K, [(m, b, shift) per component]
+    (1, 200_000, 90_000, 3, [(5001, 16, 7), (5001, 16, 7), (64, 8, 15)]),   # C2-like: 40 -> 32 bits
+    (2, 150_000, 60_000, 4, [(151, 12, 11), (151, 12, 11), (149, 12, 3), (97, 10, 0)]),  # C3-like
+    (3, 120_000, 50_000, 3, [(3, 16, 0), (2, 16, 7), (17, 16, 4)]),         # few values, wide spans
+    (4, 100_000, 40_000, 2, [(300, 17, 6), (300, 14, 0)]),                  # 17 bits: not a candidate
+    (5, 100_000, 40_000, 1, [(9, 4, 19)]),                                  # 4 bits, too few to gain
+    (6, 100_000, 40_000, 1, [(1000, 16, 0)]),                               # 16 -> 10 bits, 2 -> 2 passes
+    (7, 100_000, 40_000, 4, [(16, 16, 0), (16, 16, 0), (16, 16, 0), (16, 16, 0)]),  # 64 -> 28 bits (3 maps fit)
+    (8, 100_000, 40_000, 2, [(40_000, 16, 7), (2, 5, 0)]),                  # dense: ranks save nothing
+    (9, 30_000, 10_000, 6, [(7, 9, 0), (7, 9, 0), (7, 9, 0), (7, 9, 0), (7, 9, 0)]),  # D = 5: no value ranks
+]
+
+
+@pytest.mark.parametrize("seed,V,E,K,comps", CASES, ids=[f"case{c[0]}" for c in CASES])
+def test_value_rank_parity_and_width(rmx, seed, V, E, K, comps):
+    words, idx = set_mesh(seed, V, E, K, comps)
+    check(rmx, words, idx)
+    plain, ranked = model_bits(words, idx)
+    packed, kw, bits, passes = plan_info(rmx, words, idx)
+    assert packed == 1
+    assert bits == ranked, (bits, ranked, plain)
+    assert kw == (2 if bits > 32 else 1)
+    assert passes == (bits + 7) // 8
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 7])
+def test_value_rank_off_matches(rmx, value_rank_off, seed):
+    case = next(c for c in CASES if c[0] == seed)
+    words, idx = set_mesh(*case)
+    check(rmx, words, idx)
+    plain, _ = model_bits(words, idx)
+    assert plan_info(rmx, words, idx)[2] == plain
+
+
+def test_value_rank_with_unused_rows_outside_the_set(rmx):
+    """Unused rows hold values no used row has: they take the replacement row before ranking."""
+    words, idx = set_mesh(21, 80_000, 30_000, 3, [(300, 16, 7), (300, 16, 7), (5, 8, 0)])
+    used = np.zeros(words.shape[0], bool)
+    used[idx.reshape(-1)] = True
+    words[~used, 0] = BASE | np.uint32(0x7FFF80)
+    words[~used, 2] = np.uint32(0xC2000000)
+    check(rmx, words, idx)
+
+
+def test_sampled_decision_large(rmx):
+    """>= 2^22 rows: the strided sample decides, the full set confirms (C2-like sets)."""
+    V = (1 << 22) + 4099
+    words, idx = set_mesh(31, V, V // 3, 3, [(3001, 16, 7), (3001, 16, 7), (64, 8, 15)])
+    check(rmx, words, idx)
+    assert plan_info(rmx, words, idx)[2] == 12 + 12 + 6
+
+
+def test_sampled_decision_misled(rmx):
+    """The sample (the first 256 rows of every 16384) sees 16 values per axis, the other rows
+    ~all 2^16: the full pass must find no gain and keep the plain packed key."""
+    V = 1 << 22
+    rng = np.random.default_rng(41)
+    words = np.empty((V, 2), np.uint32)
+    in_sample = (np.arange(V) % 16384) < 256
+    for c in range(2):
+        words[:, c] = BASE | (rng.integers(0, 1 << 16, size=V).astype(np.uint32) << np.uint32(7))
+        small = rng.integers(0, 16, size=int(in_sample.sum())).astype(np.uint32) << np.uint32(7 + 12)
+        words[in_sample, c] = BASE | small
+    idx = np.arange(V, dtype=np.uint32).reshape(-1, 4)
+    check(rmx, words, idx)
+    assert plan_info(rmx, words, idx)[2] == 32
