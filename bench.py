@@ -173,11 +173,16 @@ def run_reference(args):
     emit(line)
 
 
-def executed_model(V, I, U, D, KW, npass):
+def mask_list(m):
+    return "[" + ",".join(str(c) for c in range(32) if (m >> c) & 1) + "]"
+
+
+def executed_model(V, I, U, D, KW, npass, value_ranks=False):
     """Algorithmic HBM bytes of one packed-path step (the kernels that ran)."""
     passes = sum(8 * KW + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass))
     return int((4 * I + 2 * V)                       # mark: indices in, flags cleared + set
                + (4 * D + 1) * V                     # vary: rows + flags
+               + ((4 * D + 1) * V * 65 // 64 if value_ranks else 0)  # value sets: 1/64 sample + full pass
                + (4 * D + 1) * V + (4 * KW + 1) * V  # pack: rows + flags in, keys + digit 0 out
                + passes * V                          # LSD passes
                + 4 * KW * V                          # head count
@@ -232,6 +237,9 @@ def run_b200(args):
     pinfo = (ctypes.c_uint32 * 4)()
     _native.check(lib.rmx_plan_info(ws.data_ptr(), V, D, stream.cuda_stream, pinfo))
     packed, key_words, vbits, executed = (int(x) for x in pinfo)
+    kinfo = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_plan_key_info(ws.data_ptr(), V, D, stream.cuda_stream, kinfo))
+    field_mask, value_mask, bits_before_vr = int(kinfo[0]), int(kinfo[1]), int(kinfo[2])
 
     # per-stage CUDA events for every timed step (recorded on the launching stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
@@ -279,7 +287,8 @@ def run_b200(args):
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     nominal = (32 * D * D + 44 * D + 15) * V + 16 * E * K + 4 * D * expect_u
-    executed_bytes = executed_model(V, E * K, expect_u, D, key_words, executed) if packed else None
+    executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0)
+                      if packed else None)
     value = V * world / (ms * 1e-3)
 
     # end-to-end through the public host API (pinned host buffers, copies inside the timed region)
@@ -357,7 +366,9 @@ def run_b200(args):
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
                                     else "one onesweep LSD pass: k_sort_pass"),
-                         "key": (f"packed {vbits} varying bits in {key_words} x u32" if packed
+                         "key": (f"packed {vbits} key bits in {key_words} x u32 (field ranks on components "
+                                 f"{mask_list(field_mask)}, value ranks on {mask_list(value_mask)}: "
+                                 f"{bits_before_vr} bits before value ranks)" if packed
                                  else f"{D} x u32 words"),
                          "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
                          "executed_passes": executed, "nominal_passes": 4 * D},
@@ -366,6 +377,7 @@ def run_b200(args):
                 "achieved_gbs": executed_bytes / (ms * 1e-3) / 1e9 if executed_bytes else None,
                 "frac": executed_bytes / (ms * 1e-3) / 1e9 / hbm if executed_bytes else None,
                 "note": "algorithmic bytes of the kernels that ran (DESIGN.md (d)): mark 4I+2V, vary (4D+1)V, "
+                        "value sets (4D+1)V x 65/64 when value ranks ran, "
                         "pack (4D+1)V+(4KW+1)V, per pass <= (8KW+10)V, head count 4KW V, unique (4KW+12)V+4KW U, "
                         "unpack (4KW+4D)U, map fill 12V, remap 12I",
                 "survey_nominal_bytes": nominal,

@@ -140,9 +140,13 @@ int rmx_kernel_launches(uint32_t dim);
  * 8-bit digit is constant over all keys are skipped; when at most 64 key bits
  * vary, the varying bits are packed into one u32/u64 key (order-preserving).
  * rmx_last_executed_passes returns the executed sort passes;
- * rmx_plan_info fills info[4] = {packed, key words, varying bits, passes}. */
+ * rmx_plan_info fills info[4] = {packed, key words, varying bits, passes};
+ * rmx_plan_key_info fills info[4] = {field-ranked components (bit mask),
+ * value-ranked components (bit mask), key bits before value ranks, key bits}
+ * (zeros unless packed). */
 int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream);
 int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
+int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
 /* Tuning diagnostic: look-back statistics {windows, spins, look-backs, 0} of
  * the AoS sort passes when built with -DRMX_PHASES (otherwise zeros; returns 0). */

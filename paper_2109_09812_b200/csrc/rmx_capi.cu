@@ -826,10 +826,12 @@ void rmx_graph_destroy(rmx_graph* graph) {
 }
 
 int rmx_kernel_launches(uint32_t dim) {
-    // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes, pack,
+    // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes,
+    // [dim <= kMaxRankDim: value-set sample (meshes of >= 2^22 rows), value plan, value set, value plan], pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
-    return 6 + static_cast<int>(4 * dim) + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
+    const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 4 : 0;
+    return 6 + static_cast<int>(4 * dim) + value_ranks + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
 }
 
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
@@ -870,6 +872,33 @@ int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
     info[1] = h[2] ? h[3] : 0u;  // key words
     info[2] = h[2] ? h[4] : 0u;  // varying bits
     info[3] = h[1];  // executed sort passes
+    return RMX_OK;
+}
+
+int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t pk[8] = {0}, rk[RMX_MAX_DIM] = {0}, vb[4 + 4 * kMaxRankDim] = {0};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char* plan = static_cast<const char*>(workspace) + L.plan;
+    RMX_CHECK(cudaMemcpyAsync(pk, plan + pk_base(L.P) * 4, sizeof(pk), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(rk, plan + pk_rank_base(L.P) * 4, sizeof(rk), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(vb, plan + pk_value_base(L.P) * 4, sizeof(vb), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    for (int k = 0; k < 4; ++k) info[k] = 0u;
+    if (!pk[0]) return RMX_OK;
+    uint32_t fmask = 0, plain = pk[2];
+    for (int c = 0; c < L.D && c < 32; ++c)
+        if (rk[c] >> 31) fmask |= 1u << c;
+    const bool vr = L.D <= kMaxRankDim && vb[0] == 2u;
+    if (vr) {
+        plain = 0;
+        for (int c = 0; c < L.D; ++c) plain += vb[4 + 4 * c + 1];
+    }
+    info[0] = fmask;                // components whose sign+exponent field is ranked
+    info[1] = vr ? vb[1] : 0u;      // components replaced by their value rank
+    info[2] = plain;                // key bits before value ranks
+    info[3] = pk[2];                // key bits
     return RMX_OK;
 }
 

@@ -306,6 +306,10 @@ __device__ __forceinline__ uint32_t lookback_digit(const uint64_t* desc, uint32_
     }
 }
 
+// L2 prefetch of the line holding p (streaming loops: the loads of a later
+// iteration start while this one computes, without holding registers)
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);

@@ -469,6 +469,12 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
                 uint64_t g = start;
                 for (; g + stride < ng; g += 2 * stride) {
                     const uint64_t h = g + stride;
+                    if (h + 2 * stride < ng) {  // the next iteration's rows and flags
+                        prefetch_l2(v4 + 3 * (g + 2 * stride));
+                        prefetch_l2(v4 + 3 * (h + 2 * stride));
+                        prefetch_l2(f4 + g + 2 * stride);
+                        prefetch_l2(f4 + h + 2 * stride);
+                    }
                     const uint4 x0 = __ldcs(v4 + 3 * g), y0 = __ldcs(v4 + 3 * g + 1), z0 = __ldcs(v4 + 3 * g + 2);
                     const uint4 x1 = __ldcs(v4 + 3 * h), y1 = __ldcs(v4 + 3 * h + 1), z1 = __ldcs(v4 + 3 * h + 2);
                     const uint32_t f0 = __ldcs(f4 + g), f1 = __ldcs(f4 + h);
@@ -673,6 +679,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
                 const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
                 const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
                 for (uint64_t g = start; g < ng; g += stride) {
+                    if (g + 2 * stride < ng) {  // two iterations ahead
+                        prefetch_l2(v4 + 3 * (g + 2 * stride));
+                        prefetch_l2(f4 + g + 2 * stride);
+                    }
                     const uint4 x = __ldcs(v4 + 3 * g), y = __ldcs(v4 + 3 * g + 1), z = __ldcs(v4 + 3 * g + 2);
                     const uint32_t f = __ldcs(f4 + g);
                     uint32_t k[4][3] = {{x.x, x.y, x.z}, {x.w, y.x, y.y}, {y.z, y.w, z.x}, {z.y, z.z, z.w}};
