@@ -152,6 +152,12 @@ def cpu_port_rate(cfg: str, steps: int, warmup: int):
     sample = (f"first {CPU_SAMPLE_ELEMS:,} elements of the {cfg} soup ({len(v):,} vertex slots); "
               f"median of {len(times)} after {warmup} warm-up; numpy port of remeshx.reindex "
               f"(np.lexsort is single-threaded, the chunked steps use the reference pool)")
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:  # noqa: BLE001
+        phys = None
+    sample += f"; host: {os.cpu_count()} logical / {phys} physical cores"
     return len(v) / med, oracle.host_threads(), sample, med
 
 
@@ -287,6 +293,7 @@ def run_b200(args):
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     nominal = (32 * D * D + 44 * D + 15) * V + 16 * E * K + 4 * D * expect_u
+    compulsory = 4 * D * V + 8 * E * K + 4 * D * expect_u
     executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0)
                       if packed else None)
     value = V * world / (ms * 1e-3)
@@ -381,6 +388,10 @@ def run_b200(args):
                         "pack (4D+1)V+(4KW+1)V, per pass <= (8KW+10)V, head count 4KW V, unique (4KW+12)V+4KW U, "
                         "unpack (4KW+4D)U, map fill 12V, remap 12I",
                 "survey_nominal_bytes": nominal,
+                "compulsory_bytes": compulsory,
+                "compulsory_frac": compulsory / (ms * 1e-3) / 1e9 / hbm,
+                "compulsory_note": "SURVEY 8(d) compulsory I/O 4DV + 4I + 4DU + 4I (read vertices and indices, "
+                                   "write unique rows and indices once)",
                 "survey_note": "SURVEY 8(d) nominal model (32D^2+44D+15)V+16I+4DU counts 4D byte passes of 16 B "
                                "rows; the packed path executes fewer, narrower passes"},
             "stage_ms": stage_ms,

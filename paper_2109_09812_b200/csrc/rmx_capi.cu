@@ -71,7 +71,10 @@ int rank_force() {
 }
 
 // packed-key sort tiles: RMX_PK_CFG (below) selects rows per thread, tuning only
-constexpr int kPkUniqIpt = 12;
+#ifndef RMX_UNIQ_IPT
+#define RMX_UNIQ_IPT 12
+#endif
+constexpr int kPkUniqIpt = RMX_UNIQ_IPT;
 constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
 int pk_sort_ipt() {
     static int v = [] {

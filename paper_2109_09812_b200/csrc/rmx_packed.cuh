@@ -1210,7 +1210,10 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
 }
 
 template <int IPT>
-__global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
+#ifndef RMX_UNIQ_MINB
+#define RMX_UNIQ_MINB 3
+#endif
+__global__ void __launch_bounds__(kBlock, RMX_UNIQ_MINB) k_unique_pk(UniquePkArgs a) {
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
