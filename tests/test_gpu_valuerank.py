@@ -9,7 +9,6 @@ Meshes of >= 2^22 rows take the sampled decision first (the first 256 rows of
 every 16384); one of them is built so that the sample promises a gain the
 full set does not deliver -- the plan must fall back to the plain packed key.
 """
-import os
 
 import numpy as np
 import pytest
@@ -29,15 +28,15 @@ def rmx(cuda_ok):
     return p
 
 
+@pytest.fixture(autouse=True)
+def value_rank_default(monkeypatch):
+    """Width assertions need the default (value ranks on), whatever the suite runs under."""
+    monkeypatch.delenv("RMX_VALUE_RANK", raising=False)
+
+
 @pytest.fixture
-def value_rank_off():
-    old = os.environ.get("RMX_VALUE_RANK")
-    os.environ["RMX_VALUE_RANK"] = "0"
-    yield
-    if old is None:
-        del os.environ["RMX_VALUE_RANK"]
-    else:
-        os.environ["RMX_VALUE_RANK"] = old
+def value_rank_off(monkeypatch):
+    monkeypatch.setenv("RMX_VALUE_RANK", "0")
 
 
 def value_set(rng, m, b):
@@ -110,7 +109,7 @@ CASES = [
     (5, 100_000, 40_000, 1, [(9, 4, 19)]),                                  # 4 bits, too few to gain
     (6, 100_000, 40_000, 1, [(1000, 16, 0)]),                               # 16 -> 10 bits, 2 -> 2 passes
     (7, 100_000, 40_000, 4, [(16, 16, 0), (16, 16, 0), (16, 16, 0), (16, 16, 0)]),  # 64 -> 28 bits (3 maps fit)
-    (8, 100_000, 40_000, 2, [(40_000, 16, 7), (2, 5, 0)]),                  # dense: ranks save nothing
+    (8, 100_000, 40_000, 2, [(40_000, 16, 7), (2, 5, 0)]),                  # ~30K used values: 21 -> 16 bits
     (9, 30_000, 10_000, 6, [(7, 9, 0), (7, 9, 0), (7, 9, 0), (7, 9, 0), (7, 9, 0)]),  # D = 5: no value ranks
 ]
 
