@@ -34,7 +34,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
 
 // Per-W tile sizes (rows per tile = 256 x IPT), chosen by measurement on B200.
 template <int W>
-struct SortIpt { static constexpr int v = W == 2 ? 16 : (W == 3 ? 16 : (W == 4 ? 12 : (W == 5 ? 10 : 2))); };
+struct SortIpt { static constexpr int v = W == 2 ? 16 : (W == 3 ? 16 : (W == 4 ? 20 : (W == 5 ? 16 : 2))); };
 template <int W>
 struct UniqIpt { static constexpr int v = W == 2 ? 16 : (W == 3 ? 12 : (W == 4 ? 8 : (W == 5 ? 8 : 2))); };
 
