@@ -219,6 +219,38 @@ int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
 
 int grid_for_stream(uint64_t items, int& grid);
 
+// ---- launches ------------------------------------------------------------------
+// run_pipeline launches its kernels with programmatic stream serialization
+// (each kernel starts with pdl_enter(), rmx_common.cuh): the next kernel's
+// launch and CTA ramp-up overlap the previous kernel's tail.  Off while a
+// graph is captured and with RMX_PDL=0.
+thread_local bool t_pdl = false;
+
+bool pdl_enabled() {
+    const char* e = std::getenv("RMX_PDL");  // read per call: tests switch it at run time
+    return !(e && e[0] == '0');
+}
+
+struct PdlScope {
+    explicit PdlScope(bool on) { t_pdl = on; }
+    ~PdlScope() { t_pdl = false; }
+};
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = t_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // ---- kernel dispatch by compile-time width --------------------------------
 template <int D_CT>
 int launch_build(const BuildArgs& a, cudaStream_t s) {
@@ -226,7 +258,7 @@ int launch_build(const BuildArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(k_build_rows<D_CT>, smem, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
     if (rc) return rc;
-    k_build_rows<D_CT><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(launch(k_build_rows<D_CT>, grid, kBlock, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -238,7 +270,7 @@ int launch_pass(const SortArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(kern, smem, a.ntiles, grid);
     if (rc) return rc;
-    kern<<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(launch(kern, grid, kBlock, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -250,7 +282,7 @@ int launch_unique(const UniqueArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(kern, smem, a.ntiles, grid);
     if (rc) return rc;
-    kern<<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(launch(kern, grid, kBlock, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -260,7 +292,7 @@ int launch_vary(const VaryArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(k_vary<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
     if (rc) return rc;
-    k_vary<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(launch(k_vary<D_CT>, grid, kBlock, 0, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -280,7 +312,7 @@ int launch_pack(const PackArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(k_pack<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
     if (rc) return rc;
-    k_pack<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(launch(k_pack<D_CT>, grid, kBlock, 0, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -300,7 +332,7 @@ int launch_valueset(const ValueSetArgs& a, uint64_t items, cudaStream_t s) {
     if ((rc = ensure_smem(k_valueset<D_CT>, smem))) return rc;
     const uint64_t want = (items + kVsThreads - 1) / kVsThreads;
     const int grid = static_cast<int>(want < static_cast<uint64_t>(sms) ? (want ? want : 1) : sms);
-    k_valueset<D_CT><<<grid, kVsThreads, smem, s>>>(a);
+    RMX_CHECK(launch(k_valueset<D_CT>, grid, kVsThreads, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -336,7 +368,7 @@ int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     // passes past kCommonPasses run only for > 40-bit keys: 4 tiles per CTA there, so that when
     // they do not run (the common case) the exiting grid is a quarter the size
     const uint32_t tpc = a.pass >= kCommonPasses ? 4u : 1u;
-    k_pk_downsweep<IPT, MINB><<<(a.ntiles + tpc - 1) / tpc, kBlock, smem, s>>>(a, tpc);
+    RMX_CHECK(launch(k_pk_downsweep<IPT, MINB>, (a.ntiles + tpc - 1) / tpc, kBlock, smem, s, a, tpc));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -356,9 +388,9 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = grid_for_stream(static_cast<uint64_t>((a.ntiles + kUpGroup - 1) / kUpGroup) * kBlock, grid);
     if (rc) return rc;
-    k_pk_upsweep<<<grid, kBlock, 0, s>>>(a, static_cast<uint32_t>(pk_sort_tile()));
+    RMX_CHECK(launch(k_pk_upsweep, grid, kBlock, 0, s, a, static_cast<uint32_t>(pk_sort_tile())));
     RMX_CHECK(cudaGetLastError());
-    k_pk_colscan<<<256, 1024, 0, s>>>(a);
+    RMX_CHECK(launch(k_pk_colscan, 256, 1024, 0, s, a));
     RMX_CHECK(cudaGetLastError());
     const int cfg = pk_sort_ipt() * 10 + pk_minb();
     switch (cfg) {
@@ -375,7 +407,7 @@ int launch_unique_pk(const UniquePkArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = persistent_grid(k_unique_pk<kPkUniqIpt>, smem, a.ntiles, grid);
     if (rc) return rc;
-    k_unique_pk<kPkUniqIpt><<<grid, kBlock, smem, s>>>(a);
+    RMX_CHECK(launch(k_unique_pk<kPkUniqIpt>, grid, kBlock, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -385,7 +417,7 @@ int launch_unpack_pk_d(const UnpackPkArgs& a, uint64_t max_rows, cudaStream_t s)
     int grid = 0;
     int rc = grid_for_stream(max_rows, grid);
     if (rc) return rc;
-    k_unpack_pk<D_CT><<<grid, kBlock, 0, s>>>(a);
+    RMX_CHECK(launch(k_unpack_pk<D_CT>, grid, kBlock, 0, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -542,6 +574,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         std::snprintf(g_err, sizeof(g_err), "null buffer");
         return RMX_EINVAL;
     }
+    const PdlScope pdl(gc == nullptr && pdl_enabled());
     const Layout L = make_layout(V, D);
     if (!ws || ws_bytes < L.total) {
         std::snprintf(g_err, sizeof(g_err), "workspace %zu bytes < required %zu", ws_bytes, L.total);
@@ -582,12 +615,12 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         int grid = 0;
         rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
         if (rc) return rc;
-        k_mark<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(launch(k_mark, grid, kBlock, 0, s, a));
         RMX_CHECK(cudaGetLastError());
         if (V) {
             rc = grid_for_stream((V + 31) / 32, grid);
             if (rc) return rc;
-            k_expand_marks<<<grid, kBlock, 0, s>>>(bits, V, flags);
+            RMX_CHECK(launch(k_expand_marks, grid, kBlock, 0, s, bits, V, flags));
             RMX_CHECK(cudaGetLastError());
         }
     }
@@ -602,7 +635,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    k_plan<<<1, 32, 0, s>>>(vary, fields, plan, L.D, d_status, gc ? gc->gh : GraphHandles{});
+    RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, gc ? gc->gh : GraphHandles{}));
     RMX_CHECK(cudaGetLastError());
     if ((rc = rec.mark())) return rc;
     // ---- AoS path (kernels exit at once in packed mode)
@@ -617,7 +650,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         int grid = 0;
         rc = grid_for_stream(V, grid);
         if (rc) return rc;
-        k_first_hist<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(launch(k_first_hist, grid, kBlock, 0, s, a));
         RMX_CHECK(cudaGetLastError());
     }
     if ((rc = cond_end(gc))) return rc;
@@ -640,12 +673,12 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         ValueSetArgs va{vtx, flags, idx, plan, fields, vsets, d_status, static_cast<uint32_t>(V), shift, vec};
         if (shift && (rc = dispatch_valueset(va, L.D, s))) return rc;
         ValuePlanArgs pa{plan, vsets, rank16, vinv, d_status, L.D, 0};
-        k_value_plan<<<1, 1024, 0, s>>>(pa);
+        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
         RMX_CHECK(cudaGetLastError());
         va.shift = 0u;
         if ((rc = dispatch_valueset(va, L.D, s))) return rc;
         pa.final_pass = 1;
-        k_value_plan<<<1, 1024, 0, s>>>(pa);
+        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
         RMX_CHECK(cudaGetLastError());
     }
     {
@@ -683,10 +716,10 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                         static_cast<uint32_t>(kPkUniqTile), L.D};
         int grid = 0;
         if ((rc = grid_for_stream(static_cast<uint64_t>(L.ntiles3_pk) * kBlock, grid))) return rc;
-        k_head_count_pk<<<grid, kBlock, 0, s>>>(h);
+        RMX_CHECK(launch(k_head_count_pk, grid, kBlock, 0, s, h));
         RMX_CHECK(cudaGetLastError());
-        k_tile_scan<<<1, 1024, 0, s>>>(counts, L.ntiles3_pk, plan, L.D, reinterpret_cast<unsigned long long*>(d_count),
-                                       d_status);
+        RMX_CHECK(launch(k_tile_scan, 1, 1024, 0, s, counts, L.ntiles3_pk, plan, L.D, reinterpret_cast<unsigned long long*>(d_count),
+                                       d_status));
         RMX_CHECK(cudaGetLastError());
         void* ukeys = base + L.ukeys;
         UniquePkArgs a{rows0, rows1, L.vals_off, plan, counts, fill, d_status, ukeys,
@@ -701,9 +734,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = rec.mark())) return rc;
     {
         const uint64_t threads = (V + 1) / 2;
-        k_map_fill<<<static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s>>>(plan, rows0, rows1, map,
+        RMX_CHECK(launch(k_map_fill, static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s, plan, rows0, rows1, map,
                                                                                           static_cast<uint32_t>(V),
-                                                                                          d_status);
+                                                                                          d_status));
         RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
@@ -713,7 +746,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         int grid = 0;
         rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
         if (rc) return rc;
-        k_remap<<<grid, kBlock, 0, s>>>(a);
+        RMX_CHECK(launch(k_remap, grid, kBlock, 0, s, a));
         RMX_CHECK(cudaGetLastError());
     }
     return rec.mark();

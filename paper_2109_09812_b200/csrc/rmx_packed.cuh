@@ -163,6 +163,7 @@ struct FieldSet {
 
 template <int D_CT>
 __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;  // uniform
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* repl = a.vtx + static_cast<size_t>(a.idx[0]) * D;
@@ -403,6 +404,7 @@ constexpr int kVsThreads = 1024;
 
 template <int D_CT>
 __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     static_assert(D_CT >= 1 && D_CT <= kMaxRankDim, "value ranks cover D <= kMaxRankDim");
     extern __shared__ __align__(16) uint8_t s_map[];  // [sum of 2^w over candidates]
     const uint32_t* pk = a.plan + pk_base(4 * D_CT);
@@ -529,6 +531,7 @@ struct ValuePlanArgs {
 __device__ __forceinline__ uint32_t bits_for(uint32_t count) { return count <= 1u ? 0u : 32u - __clz(count - 1u); }
 
 __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     __shared__ uint32_t s_warp[32];
     const int D = a.dim;
     if (*a.status || D > kMaxRankDim) return;
@@ -633,6 +636,7 @@ struct PackArgs {
 
 template <int D_CT>
 __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
@@ -778,6 +782,7 @@ __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
 // key: k_pack and every downsweep also emit the next pass's digit per row),
 // 16 digits per 16-byte load, kUpGroup tiles per CTA iteration.
 __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !pk_pass_active(a)) return;
     __shared__ uint32_t s_h[kUpGroup * 256];
     const uint32_t ngroups = (a.ntiles + kUpGroup - 1u) / kUpGroup;
@@ -818,6 +823,7 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t ti
 // (one coalesced 16-byte access), a block scan joins the threads, a running
 // carry joins the chunks.
 __global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !pk_pass_active(a)) return;
     __shared__ uint32_t s_warp[32];
     uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.cstride;
@@ -979,6 +985,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
 // that a pass which does not run costs a small grid) consecutive tiles.
 template <int IPT, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a, uint32_t tiles_per_cta) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !pk_pass_active(a)) return;
     extern __shared__ __align__(128) uint32_t smem[];
     const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
@@ -1035,6 +1042,7 @@ __device__ __forceinline__ void head_count_body(const HeadCountArgs& a) {
 }
 
 __global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
@@ -1046,6 +1054,7 @@ __global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
 // the total is the output vertex count.
 __global__ void __launch_bounds__(1024) k_tile_scan(uint32_t* counts, uint32_t ntiles, const uint32_t* plan, int dim,
                                                     unsigned long long* total_out, const uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || plan[pk_base(4 * dim)] == 0u) return;
     __shared__ uint32_t s_warp[32];
     const uint32_t per = (ntiles + 1023u) / 1024u;
@@ -1214,6 +1223,7 @@ template <int IPT>
 #define RMX_UNIQ_MINB 3
 #endif
 __global__ void __launch_bounds__(kBlock, RMX_UNIQ_MINB) k_unique_pk(UniquePkArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
@@ -1241,6 +1251,7 @@ struct UnpackPkArgs {
 
 template <int D_CT>
 __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);

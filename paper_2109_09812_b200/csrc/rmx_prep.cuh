@@ -27,6 +27,7 @@ struct MarkArgs {
 };
 
 __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31u;
@@ -82,6 +83,7 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
 // flags |= bit set (one word of 32 vertices per thread; words with no bit
 // set -- all of them when no warp took the scattered path -- cost one load).
 __global__ void __launch_bounds__(kBlock) k_expand_marks(const uint32_t* bits, uint64_t n_vtx, uint8_t* flags) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t nw = (n_vtx + 31) >> 5;
     for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; w < nw; w += stride) {
@@ -125,6 +127,7 @@ __device__ __forceinline__ void rl_push(uint32_t& st, uint32_t d, uint32_t* bins
 
 template <int D_CT>
 __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const int D = D_CT > 0 ? D_CT : a.dim;
     const int W = D + 1;
     __shared__ uint32_t s_hist[4 * 256];
@@ -339,6 +342,7 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
 
 __global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status,
                        GraphHandles gh) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || threadIdx.x != 0) return;  // graph: every conditional keeps its default 0
     plan_body(vary, fields, plan, D);
     if (gh.n) {
@@ -368,6 +372,7 @@ struct HistArgs {
 };
 
 __global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || a.plan[3] == 0u || a.plan[pk_base(4 * a.dim)] != 0u) return;
     __shared__ uint32_t s_h[256];
     s_h[threadIdx.x] = 0u;

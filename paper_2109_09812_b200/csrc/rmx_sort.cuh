@@ -52,6 +52,7 @@ struct SortMinBlocks { static constexpr int v = (W_CT == 4 || W_CT == 5) ? 2 : 3
 
 template <int W_CT, int IPT>
 __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(SortArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     using T = SortTraits<W_CT, IPT>;
     constexpr int TILE = T::kTile;
     const int W = W_CT > 0 ? W_CT : a.dim + 1;

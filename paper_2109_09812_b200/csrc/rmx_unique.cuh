@@ -45,6 +45,7 @@ struct UniqueTraits {
 
 template <int W_CT, int IPT>
 __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     using T = UniqueTraits<W_CT, IPT>;
     constexpr int TILE = T::kTile;
     const int D = W_CT > 0 ? W_CT - 1 : a.dim;
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
 __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const uint32_t* rows0,
                                                       const uint32_t* rows1, uint32_t* map, uint32_t n,
                                                       const uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status) return;
     const uint4* pairs = reinterpret_cast<const uint4*>(plan[0] ? rows0 : rows1);
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
@@ -239,6 +241,7 @@ struct RemapArgs {
 };
 
 __global__ void __launch_bounds__(kBlock) k_remap(RemapArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
