@@ -25,6 +25,7 @@ library.  There is no CPU fallback: a missing library raises.
 from __future__ import annotations
 
 import ctypes
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -301,6 +302,8 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
     E, K = elements.shape
     if E == 0:
         return Mesh.empty(dim=D, arity=K), ReindexScratch(vertices, elements, 0, dev)
+    if vertices.nbytes + elements.nbytes <= SMALL_CALL_BYTES:
+        return _reindex_small(vertices, elements, dev)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev)
         vtx_d = torch.empty((V, D), dtype=torch.int32, device=dev)
@@ -317,6 +320,67 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
             raise InvalidMeshError(validate(_Arrays(vertices, elements)))
         host_v = hostio.to_host(out_v[:count]).view(np.float32)
         host_e = hostio.to_host(out_e).view(np.uint32)
+    return Mesh._adopt(host_v, host_e), ReindexScratch(vertices, elements, count, dev)
+
+
+# Meshes up to this many input bytes take one staged round trip: one pinned
+# buffer up, one launch, one pinned buffer down, one synchronisation.
+SMALL_CALL_BYTES = 4 << 20
+
+
+class _SmallBuffers(threading.local):
+    """Per-thread, per-device device + pinned host buffers of the small-call path (grown on demand)."""
+
+    def __init__(self):
+        self.by_dev = {}
+
+    def get(self, dev: torch.device, nbytes: int):
+        cur = self.by_dev.get(dev)
+        if cur is None or cur[0].numel() < nbytes:
+            cap = max(nbytes, 1 << 20)
+            cur = (torch.empty(cap, dtype=torch.uint8, device=dev),
+                   torch.empty(cap, dtype=torch.uint8, pin_memory=True))
+            self.by_dev[dev] = cur
+        return cur
+
+
+_small = _SmallBuffers()
+
+
+def _reindex_small(vertices: np.ndarray, elements: np.ndarray, dev: torch.device):
+    """reindex() for small meshes: [vertices | elements] up in one copy, [info | out vertices |
+    out elements] down in one copy, one stream synchronisation."""
+    V, D = vertices.shape
+    E, K = elements.shape
+    nv, ne = vertices.nbytes, elements.nbytes
+
+    def al(x):
+        return (x + 255) & ~255
+
+    o_idx = al(nv)
+    o_info = al(o_idx + ne)
+    o_ov = o_info + 16
+    o_oe = al(o_ov + nv)
+    o_ws = al(o_oe + ne)
+    wsb = workspace_bytes(V, D, E, K)
+    with torch.cuda.device(dev):
+        dbuf, hbuf = _small.get(dev, o_ws + wsb)
+        h = hbuf.numpy()
+        h[:nv] = vertices.reshape(-1).view(np.uint8)
+        h[o_idx:o_idx + ne] = elements.reshape(-1).view(np.uint8)
+        stream = torch.cuda.current_stream(dev)
+        dbuf[:o_idx + ne].copy_(hbuf[:o_idx + ne], non_blocking=True)
+        base = dbuf.data_ptr()
+        lib = _native.lib()
+        _raise_for(lib.rmx_reindex(base, V, D, base + o_idx, E, K, base + o_ov, base + o_oe, base + o_info,
+                                   base + o_info + 8, base + o_ws, wsb, None, stream.cuda_stream))
+        hbuf[o_info:o_oe + ne].copy_(dbuf[o_info:o_oe + ne], non_blocking=True)
+        stream.synchronize()
+        count, status = (int(x) for x in h[o_info:o_info + 16].view(np.int64))
+        if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+            raise InvalidMeshError(validate(_Arrays(vertices, elements)))
+        host_v = h[o_ov:o_ov + count * D * 4].view(np.float32).reshape(count, D).copy()
+        host_e = h[o_oe:o_oe + ne].view(np.uint32).reshape(E, K).copy()
     return Mesh._adopt(host_v, host_e), ReindexScratch(vertices, elements, count, dev)
 
 

@@ -210,3 +210,53 @@ def test_unaligned_device_buffers(rmx, V, D, E, K):
     res = rmx.reindex_tensors(tv, te)
     assert np.array_equal(res.vertices.cpu().numpy().view(np.uint32), ev)
     assert np.array_equal(res.elements.cpu().numpy().view(np.uint32), ee)
+
+
+@pytest.mark.parametrize("V,D,E,K", [(320, 3, 128, 3), (20_000, 3, 9_000, 4), (60_000, 5, 30_000, 3),
+                                     (100_000, 2, 60_000, 3)])
+def test_small_call_path_matches_staged_path(rmx, monkeypatch, V, D, E, K):
+    """reindex() stages meshes <= SMALL_CALL_BYTES through one pinned round trip; with the limit at
+    0 the same meshes take the general path (separate copies, pageable staging).  Both match the
+    oracle incl. the lazy scratch, and errors are the same."""
+    from paper_2109_09812_b200 import pipeline
+    v, e = random_mesh(7 + V, V, D, E, K, pool=40)
+    ev, ee = expect(v, e)
+    ref = O.reindex(v.view(np.float32), e)
+    for limit in (pipeline.SMALL_CALL_BYTES, 0):
+        monkeypatch.setattr(pipeline, "SMALL_CALL_BYTES", limit)
+        out, sc = rmx.reindex(rmx.Mesh(v.view(np.float32), e))
+        assert np.array_equal(out.vertices.view(np.uint32), ev)
+        assert np.array_equal(out.elements, ee)
+        assert sc.new_count == len(ev)
+        assert np.array_equal(np.asarray(sc.org_id), ref["org_id"])
+        bad = e.copy()
+        bad[E // 2, 0] = V + 3
+        with pytest.raises(rmx.InvalidMeshError) as ei:
+            rmx.reindex(rmx.Mesh(v.view(np.float32), bad))
+        assert [(i.element, i.slot, i.index) for i in ei.value.issues] == [(E // 2, 0, V + 3)]
+
+
+def test_small_call_path_threads(rmx):
+    """Per-thread staging buffers: concurrent small reindex() calls do not interfere."""
+    import threading
+    jobs = [random_mesh(300 + t, [300, 4000, 9000, 30_000][t % 4], 1 + t % 4, 500 + 100 * t, 3, pool=30)
+            for t in range(8)]
+    want = [expect(v, e) for v, e in jobs]
+    errors = []
+
+    def run(k):
+        try:
+            v, e = jobs[k]
+            for _ in range(10):
+                out, _ = rmx.reindex(rmx.Mesh(v.view(np.float32), e))
+                assert np.array_equal(out.vertices.view(np.uint32), want[k][0])
+                assert np.array_equal(out.elements, want[k][1])
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(len(jobs))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors[0]
