@@ -487,6 +487,11 @@ struct Recorder {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// the AoS rows path can only be chosen when more than 64 key bits may vary
+bool aos_possible(int D) { return 32 * D > 64; }
+// packed passes that can run: ceil(32 D / 8) digits, at most kMaxPackedPasses
+int packed_passes_max(int D) { return 4 * D < kMaxPackedPasses ? 4 * D : kMaxPackedPasses; }
+
 // small meshes take the one-CTA path (RMX_SMALL=0 forces the large-mesh pipeline, for tests)
 bool small_path(uint64_t V, uint32_t D, uint64_t I) {
     if (V < 1 || V > kSmallV || D > kSmallD || V * D > kSmallWords || I > kSmallI) return false;
@@ -638,14 +643,18 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, gc ? gc->gh : GraphHandles{}));
     RMX_CHECK(cudaGetLastError());
     if ((rc = rec.mark())) return rc;
-    // ---- AoS path (kernels exit at once in packed mode)
+    // ---- AoS path (kernels exit at once in packed mode).  With D <= 2 at most 64 bits vary, which
+    // the packed key always holds (plan_body: every run is >= 1 bit, so <= 64 runs), and direct
+    // launches skip the AoS kernels (their stage events are still recorded); a captured graph keeps
+    // every section so that each conditional handle has its node.
+    const bool aos = aos_possible(L.D) || gc != nullptr;
     if ((rc = cond_begin(gc, kSlotAosA))) return rc;
-    {
+    if (aos) {
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    {
+    if (aos) {
         HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D};
         int grid = 0;
         rc = grid_for_stream(V, grid);
@@ -657,9 +666,11 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
         if ((rc = cond_begin(gc, kSlotAosPass + p))) return rc;
-        SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D, p,
-                   rank_force()};
-        if ((rc = dispatch_pass(a, s))) return rc;
+        if (aos) {
+            SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
+                       p, rank_force()};
+            if ((rc = dispatch_pass(a, s))) return rc;
+        }
         if ((rc = cond_end(gc))) return rc;
         if ((rc = rec.mark())) return rc;
     }
@@ -689,6 +700,10 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
+        if (!gc && p >= packed_passes_max(L.D)) {  // a packed key of D = 1 words has at most 4 digits
+            if ((rc = rec.mark())) return rc;
+            continue;
+        }
         if ((rc = cond_begin(gc, slot_pk_pass(L.P, p)))) return rc;
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), reinterpret_cast<uint8_t*>(base + L.pk_digits),
@@ -700,7 +715,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // ---- K3 unique + bucketed pairs (one of the two runs), K3b map fill
     uint32_t* fill = reinterpret_cast<uint32_t*>(base + L.fill);
     if ((rc = cond_begin(gc, kSlotAosB))) return rc;
-    {
+    if (aos) {
         UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, fill, d_status,
                      out_vtx, reinterpret_cast<unsigned long long*>(d_count),
                      sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
@@ -867,7 +882,9 @@ int rmx_kernel_launches(uint32_t dim) {
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
     const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 4 : 0;
-    return 6 + static_cast<int>(4 * dim) + value_ranks + 1 + 3 * kMaxPackedPasses + 1 + 4 + 2;
+    const int D = static_cast<int>(dim);
+    const int aos = aos_possible(D) ? 2 + 4 * D + 1 : 0;  // build_rows, first_hist, passes, unique
+    return 4 + aos + value_ranks + 1 + 3 * packed_passes_max(D) + 4 + 2;
 }
 
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
