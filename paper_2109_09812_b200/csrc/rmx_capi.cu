@@ -99,6 +99,8 @@ struct Layout {
     size_t pk_digits;             // packed passes: [V] digit byte of the current pass per row
     size_t ukeys;                 // packed key of every unique row (K3' -> unpack)
     size_t rank16, vinv, vsets;   // value ranks (D <= kMaxRankDim): rank tables, inverse tables, value sets
+    size_t gplan, svary, sfields; // the plan guessed from a sample of the rows, and its inputs
+    size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
     size_t total;
 };
 
@@ -132,8 +134,12 @@ Layout make_layout(uint64_t V, uint32_t D) {
     const size_t vr_dim = L.D <= kMaxRankDim ? static_cast<size_t>(L.D) : 0;
     L.rank16 = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
     L.vinv = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
+    L.gplan = take(plan_words(L.P) * 4);
     L.ctl_begin = off;
     L.vsets = take(vr_dim * kValueWords * 4);
+    L.svary = take(vr_dim * 4);
+    L.vstate = take(16);
+    L.sfields = take(vr_dim * kFieldWords * 4);
     L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
@@ -635,8 +641,36 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     // K1a varying bits of the cleaned vertex set, then the plan (packed or AoS)
     const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
-    {
-        VaryArgs a{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec};
+    const bool value_ranks = L.D <= kMaxRankDim && value_rank_enabled();
+    uint32_t* gplan = reinterpret_cast<uint32_t*>(base + L.gplan);
+    uint32_t* svary = reinterpret_cast<uint32_t*>(base + L.svary);
+    uint32_t* sfields = reinterpret_cast<uint32_t*>(base + L.sfields);
+    uint32_t* vsets = reinterpret_cast<uint32_t*>(base + L.vsets);
+    if (value_ranks) {
+        // value ranks: K1a over a sample -> guessed plan -> the sample's value sets -> worth it?
+        // -> one full pass: exact K1a outputs + (if worth it) every used row's values
+        // (the full pass checks the rows against the sample instead of recomputing K1a when it
+        // collects values; k_vary then copies the sample's outputs, or computes them when the
+        // pass found a row outside the sample or did not run)
+        const uint32_t shift = V >= (1ull << 22) ? 6u : 0u;
+        uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
+        VaryArgs sa{vtx, flags, idx, svary, sfields, d_status, static_cast<uint32_t>(V), L.D, vec, shift,
+                    nullptr, nullptr, nullptr};
+        if ((rc = dispatch_vary(sa, s))) return rc;
+        RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, GraphHandles{}));
+        ValueSetArgs va{vtx, flags, idx, gplan, sfields, vsets, svary, vstate, d_status, static_cast<uint32_t>(V),
+                        shift, vec};
+        if (shift && (rc = dispatch_valueset(va, L.D, s))) return rc;
+        ValuePlanArgs pd{gplan, vsets, nullptr, nullptr, d_status, L.D, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
+        va.shift = 0u;
+        if ((rc = dispatch_valueset(va, L.D, s))) return rc;
+        VaryArgs fa{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
+                    vstate, svary, sfields};
+        if ((rc = dispatch_vary(fa, s))) return rc;
+    } else {
+        VaryArgs a{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
+                   nullptr, nullptr, nullptr};
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
@@ -678,17 +712,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = cond_begin(gc, kSlotPkA))) return rc;
     uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
     uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
-    if (L.D <= kMaxRankDim && value_rank_enabled()) {  // value ranks: sample, decide, full set, tables
-        uint32_t* vsets = reinterpret_cast<uint32_t*>(base + L.vsets);
-        const uint32_t shift = V >= (1ull << 22) ? 6u : 0u;
-        ValueSetArgs va{vtx, flags, idx, plan, fields, vsets, d_status, static_cast<uint32_t>(V), shift, vec};
-        if (shift && (rc = dispatch_valueset(va, L.D, s))) return rc;
-        ValuePlanArgs pa{plan, vsets, rank16, vinv, d_status, L.D, 0};
-        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
-        RMX_CHECK(cudaGetLastError());
-        va.shift = 0u;
-        if ((rc = dispatch_valueset(va, L.D, s))) return rc;
-        pa.final_pass = 1;
+    if (value_ranks) {  // rank tables and the new key layout (exact plan, value sets of the full pass)
+        ValuePlanArgs pa{plan, vsets, rank16, vinv, d_status, L.D, 1, gplan, svary, sfields, vary, fields};
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
         RMX_CHECK(cudaGetLastError());
     }
@@ -878,10 +903,11 @@ void rmx_graph_destroy(rmx_graph* graph) {
 
 int rmx_kernel_launches(uint32_t dim) {
     // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes,
-    // [dim <= kMaxRankDim: value-set sample (meshes of >= 2^22 rows), value plan, value set, value plan], pack,
+    // [dim <= kMaxRankDim: K1a over a sample, guessed plan, value-set sample (meshes of >= 2^22 rows),
+    //  value plan, value sets + K1a check in one pass, K1a copy / fallback, value plan], pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
-    const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 4 : 0;
+    const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 6 : 0;
     const int D = static_cast<int>(dim);
     const int aos = aos_possible(D) ? 2 + 4 * D + 1 : 0;  // build_rows, first_hist, passes, unique
     return 4 + aos + value_ranks + 1 + 3 * packed_passes_max(D) + 4 + 2;

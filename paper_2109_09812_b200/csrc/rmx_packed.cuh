@@ -123,7 +123,26 @@ struct VaryArgs {
     uint32_t n;
     int dim;
     int vec;  // vtx and flags 16-byte aligned
+    uint32_t shift;  // > 0: only the sample rows (sample_row), for the guessed plan of the value sets
+    // after the value-set pass (k_valueset): vstate bit 0 = it checked the rows against the
+    // sample's varying bits and field sets, bit 1 = some row fell outside them.  Checked and
+    // clean: the sample's outputs are exact and are copied; otherwise the full K1a runs.
+    const uint32_t* vstate;
+    const uint32_t* sample_vary;
+    const uint32_t* sample_fields;
 };
+
+constexpr uint32_t kVstateChecked = 1u, kVstateMiss = 2u;
+
+// The sample that guesses the value-rank layout: the first kSampleRun rows of
+// every kSampleRun << shift (contiguous reads).
+constexpr uint32_t kSampleRun = 256;
+__host__ __device__ inline uint64_t sample_count(uint64_t n, uint32_t shift) {
+    return ((n >> shift) + kSampleRun) & ~static_cast<uint64_t>(kSampleRun - 1);
+}
+__host__ __device__ inline uint64_t sample_row(uint64_t s, uint32_t shift) {
+    return ((s / kSampleRun) * kSampleRun << shift) + (s % kSampleRun);
+}
 
 // Occurring sign+exponent fields of one component: a per-thread window of 32
 // exponents (one register per sign) centred on a sample word -- the thread's
@@ -166,6 +185,18 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;  // uniform
     const int D = D_CT > 0 ? D_CT : a.dim;
+    if (a.vstate) {
+        const uint32_t st = *a.vstate;
+        if (st == kVstateChecked) {  // checked and clean: the sample's outputs are exact
+            if (blockIdx.x == 0) {
+                if (threadIdx.x < static_cast<unsigned>(D)) a.vary[threadIdx.x] = a.sample_vary[threadIdx.x];
+                if (D <= kMaxRankDim)
+                    for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(D) * kFieldWords; i += kBlock)
+                        a.fields[i] = a.sample_fields[i];
+            }
+            return;
+        }
+    }
     const uint32_t* repl = a.vtx + static_cast<size_t>(a.idx[0]) * D;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
@@ -192,8 +223,24 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
             }
         };
         uint64_t done = 0;
+        if (a.shift) {  // sample rows only
+            const uint64_t ns = sample_count(a.n, a.shift);
+            for (uint64_t q = start; q < ns; q += stride) {
+                const uint64_t i = sample_row(q, a.shift);
+                if (i < a.n && a.flags[i]) {
+                    uint32_t k[D_CT];
+#pragma unroll
+                    for (int c = 0; c < D_CT; ++c) {
+                        k[c] = __ldg(a.vtx + i * D_CT + c);
+                        vor[c] |= k[c] ^ ref[c];
+                    }
+                    note(k);
+                }
+            }
+            done = a.n;
+        }
         if constexpr (D_CT == 3) {
-            if (a.vec) {
+            if (a.vec && !a.shift) {
                 const uint64_t ng = a.n >> 2;
                 const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
                 const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
@@ -379,24 +426,32 @@ __device__ __forceinline__ void load_packer(const uint32_t* plan, const uint32_t
     if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(fields, plan + pk_rank_base(4 * D_CT), D_CT, s_rank, nullptr);
 }
 
-// Occurring packed values of every candidate component over the used rows
-// (shift > 0: rows k << shift only -- the sample that decides whether the full
-// pass can pay).  One 1024-thread CTA per SM keeps a byte per possible value
-// (2^w bytes per component, <= kValueSetBytes in all: plan_body drops the
-// widest candidates beyond that) and sets it with plain stores: lanes that hit
-// the same value merge instead of serialising as shared atomics on one bitmap
-// word would (structured coordinates crowd a few words).  At the end the bytes
-// are folded into bit words and OR-ed into vsets.
+// Occurring packed values of every candidate component over the used rows.
+// The packing (the plan argument) is the one guessed from a sample of the rows
+// (k_vary over the sample + k_plan): the sample pass (shift > 0) collects the
+// sample's values to decide whether value ranks can pay, and the full pass --
+// which also computes the exact varying bits and field sets of K1a, so that the
+// vertices are read once for both -- collects every used row's values when
+// they can.  k_value_plan then keeps a component only if its exact varying bits
+// and field set equal the sample's (same packing, so the same values).
+// One 1024-thread CTA per SM keeps a byte per possible value (2^w bytes per
+// component, <= kValueSetBytes in all: plan_body drops the widest candidates
+// beyond that) and sets it with plain stores: lanes that hit the same value
+// merge instead of serialising as shared atomics on one bitmap word would
+// (structured coordinates crowd a few words).  At the end the bytes are folded
+// into bit words and OR-ed into vsets.
 struct ValueSetArgs {
     const uint32_t* vtx;
     const uint8_t* flags;
-    const uint32_t* idx;  // idx[0]: the replacement row
-    const uint32_t* plan;
-    const uint32_t* fields;
-    uint32_t* vsets;  // [D][kValueWords]
+    const uint32_t* idx;     // idx[0]: the replacement row
+    const uint32_t* plan;    // the guessed plan (its packing defines the values)
+    const uint32_t* fields;  // the field sets it was made from
+    uint32_t* vsets;         // [D][kValueWords]
+    const uint32_t* guess_vary;  // the sample's varying bits (the full pass checks the rows against them)
+    uint32_t* vstate;        // full pass: kVstateChecked | kVstateMiss (for k_vary)
     const uint32_t* status;
     uint32_t n;
-    uint32_t shift;
+    uint32_t shift;          // > 0: the sample rows only (sample_row)
     int vec;
 };
 
@@ -411,9 +466,13 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     const uint32_t* vb = a.plan + pk_value_base(4 * D_CT);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
     __shared__ uint16_t s_rank[D_CT * kFieldValues];
-    if (*a.status || pk[0] == 0u || (a.shift == 0u && vb[0] != 1u)) return;  // uniform
+    if (*a.status) return;  // uniform
+    const bool sets = pk[0] != 0u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
+    if (!sets) return;  // (the full pass: k_vary computes K1a's outputs instead)
+    // the full pass also checks every used row against the sample's varying bits and field sets
+    const bool check = a.vstate != nullptr && a.shift == 0u;
+    __shared__ uint32_t s_fset[D_CT * kFieldWords];  // the sample's field sets (check)
     const uint32_t cand = vb[1];
-    if (!cand) return;
     load_packer<D_CT>(a.plan, a.fields, s_runs, s_rank);
     ValueMap<D_CT> vm;
     vm.load(a.plan);
@@ -424,9 +483,14 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
         off[c] = bytes;
         if ((cand >> c) & 1u) bytes += 1u << vm.w[c];
     }
-    for (uint32_t i = threadIdx.x; i < bytes / 16u + 1u; i += kVsThreads) reinterpret_cast<uint4*>(s_map)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < bytes / 16u + 1u; i += kVsThreads)
+        reinterpret_cast<uint4*>(s_map)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = threadIdx.x; i < D_CT * kFieldWords; i += kVsThreads) s_fset[i] = check ? a.fields[i] : 0u;
     __syncthreads();
     RowPacker<D_CT> pack(a.plan, s_runs, pk[4], s_rank);
+    uint32_t gvary[D_CT], miss = 0u;
+#pragma unroll
+    for (int c = 0; c < D_CT; ++c) gvary[c] = check ? a.guess_vary[c] : 0u;
 #pragma unroll
     for (int c = 0; c < D_CT; ++c)
         if (!((cand >> c) & 1u)) {  // value 0 into a spare byte past the maps: no branch per row
@@ -434,21 +498,26 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
             off[c] = bytes;
         }
     // unused rows stand for the replacement row (used, so its values are in the sets anyway)
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kVsThreads;
+    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kVsThreads + threadIdx.x;
     uint32_t ref[D_CT];
 #pragma unroll
     for (int c = 0; c < D_CT; ++c) ref[c] = __ldg(a.vtx + static_cast<size_t>(a.idx[0]) * D_CT + c);
     auto note = [&](const uint32_t (&k)[D_CT], bool used) {
+        if (check && used) {
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) {
+                const uint32_t f = k[c] >> kFieldLo;
+                miss |= ((k[c] ^ ref[c]) & ~gvary[c]) | (~(s_fset[c * kFieldWords + (f >> 5)] >> (f & 31u)) & 1u);
+            }
+        }
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) s_map[off[c] + pack.value(c, used ? k[c] : ref[c])] = 1u;
     };
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kVsThreads;
-    const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kVsThreads + threadIdx.x;
     if (a.shift) {
-        // sample: the first kSampleRun rows of every (kSampleRun << shift) -- contiguous reads
-        constexpr uint32_t kSampleRun = 256;
-        const uint64_t ns = ((static_cast<uint64_t>(a.n) >> a.shift) + kSampleRun) & ~static_cast<uint64_t>(kSampleRun - 1);
-        for (uint64_t s = start; s < ns; s += stride) {
-            const uint64_t i = ((s / kSampleRun) * kSampleRun << a.shift) + (s % kSampleRun);
+        const uint64_t ns = sample_count(a.n, a.shift);
+        for (uint64_t q = start; q < ns; q += stride) {
+            const uint64_t i = sample_row(q, a.shift);
             if (i < a.n) {
                 uint32_t k[D_CT];
 #pragma unroll
@@ -459,7 +528,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     } else {
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
-            if (a.vec) {  // two groups of 4 rows in flight per thread
+            if (a.vec) {  // 4 rows = 3 x 16 B of vertex words + one flag word per thread iteration
                 const uint64_t ng = a.n >> 2;
                 const uint4* v4 = reinterpret_cast<const uint4*>(a.vtx);
                 const uint32_t* f4 = reinterpret_cast<const uint32_t*>(a.flags);
@@ -469,21 +538,13 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
                     for (int j = 0; j < 4; ++j) note(k[j], ((f >> (8 * j)) & 255u) != 0u);
                 };
                 uint64_t g = start;
-                for (; g + stride < ng; g += 2 * stride) {
-                    const uint64_t h = g + stride;
-                    if (h + 2 * stride < ng) {  // the next iteration's rows and flags
+                for (; g < ng; g += stride) {
+                    if (g + 2 * stride < ng) {  // two iterations ahead
                         prefetch_l2(v4 + 3 * (g + 2 * stride));
-                        prefetch_l2(v4 + 3 * (h + 2 * stride));
                         prefetch_l2(f4 + g + 2 * stride);
-                        prefetch_l2(f4 + h + 2 * stride);
                     }
-                    const uint4 x0 = __ldcs(v4 + 3 * g), y0 = __ldcs(v4 + 3 * g + 1), z0 = __ldcs(v4 + 3 * g + 2);
-                    const uint4 x1 = __ldcs(v4 + 3 * h), y1 = __ldcs(v4 + 3 * h + 1), z1 = __ldcs(v4 + 3 * h + 2);
-                    const uint32_t f0 = __ldcs(f4 + g), f1 = __ldcs(f4 + h);
-                    group(x0, y0, z0, f0);
-                    group(x1, y1, z1, f1);
+                    group(__ldcs(v4 + 3 * g), __ldcs(v4 + 3 * g + 1), __ldcs(v4 + 3 * g + 2), __ldcs(f4 + g));
                 }
-                if (g < ng) group(__ldcs(v4 + 3 * g), __ldcs(v4 + 3 * g + 1), __ldcs(v4 + 3 * g + 2), __ldcs(f4 + g));
                 done = ng << 2;
             }
         }
@@ -493,6 +554,10 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
             for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
             note(k, a.flags[i] != 0);
         }
+    }
+    if (check) {
+        const uint32_t m = __reduce_or_sync(kFull, miss);
+        if ((threadIdx.x & 31u) == 0u) atomicOr(a.vstate, kVstateChecked | (m ? kVstateMiss : 0u));
     }
     __syncthreads();
 #pragma unroll
@@ -512,20 +577,28 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     }
 }
 
-// One CTA of 1024 threads.  final == 0 (after the sample): keep the candidates
-// whose sampled value count already needs fewer bits, and ask for the full
-// pass when that alone would shorten the key (state 1).  final == 1 (after the
-// full pass): exact counts; if the key gets shorter, build the rank tables,
-// lay the components out again and update the plan (key words, bits, passes,
-// final buffer) -- state 2.  Otherwise state 0 and the keys stay as they are.
+// One CTA of 1024 threads.  final == 0 (on the guessed plan, after the sample
+// pass): keep the candidates whose sampled value count already needs fewer
+// bits, and ask for value sets in the full pass when that alone would shorten
+// the key (guessed plan state 1).  final == 1 (on the exact plan, after the full
+// pass): keep the candidates packed exactly as guessed, count their values; if
+// the key gets shorter, build the rank tables, lay the components out again and
+// update the plan (key words, bits, passes, final buffer) -- state 2.
+// Otherwise the keys stay as they are.
 struct ValuePlanArgs {
-    uint32_t* plan;
+    uint32_t* plan;          // decide: the guessed plan; final: the exact plan
     const uint32_t* vsets;
-    uint16_t* rank16;  // [D][2^kMaxValueBits] rank of every occurring value
-    uint16_t* vinv;    // [D][2^kMaxValueBits] value of every rank
+    uint16_t* rank16;        // [D][2^kMaxValueBits] rank of every occurring value
+    uint16_t* vinv;          // [D][2^kMaxValueBits] value of every rank
     const uint32_t* status;
     int dim;
     int final_pass;
+    // final: the guess and what it was made from, against the exact K1a outputs
+    const uint32_t* gplan;
+    const uint32_t* svary;
+    const uint32_t* sfields;
+    const uint32_t* vary;
+    const uint32_t* fields;
 };
 
 __device__ __forceinline__ uint32_t bits_for(uint32_t count) { return count <= 1u ? 0u : 32u - __clz(count - 1u); }
@@ -539,9 +612,19 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
     uint32_t* pk = plan + pk_base(4 * D);
     uint32_t* vb = plan + pk_value_base(4 * D);
     if (pk[0] == 0u) return;
-    const uint32_t state = vb[0];
-    const uint32_t cand = vb[1];
-    if (a.final_pass ? state != 1u : cand == 0u) return;  // uniform
+    uint32_t cand = vb[1];
+    if (a.final_pass) {
+        // the value sets hold the guessed packing's values: keep the components packed the same way
+        const uint32_t* gvb = a.gplan + pk_value_base(4 * D);
+        if (a.gplan[pk_base(4 * D)] == 0u || gvb[0] != 1u) return;  // uniform
+        cand &= gvb[1];
+        for (int c = 0; c < D; ++c) {
+            bool same = a.vary[c] == a.svary[c];
+            for (int w = 0; w < kFieldWords; ++w) same = same && a.fields[c * kFieldWords + w] == a.sfields[c * kFieldWords + w];
+            if (!same) cand &= ~(1u << c);
+        }
+    }
+    if (cand == 0u) return;  // uniform
     const uint32_t old_bits = pk[2], old_npass = pk[3], old_kw = pk[1];
     uint32_t w[kMaxRankDim], cnt[kMaxRankDim];
     for (int c = 0; c < D; ++c) w[c] = vb[4 + 4 * c + 1];

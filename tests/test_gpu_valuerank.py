@@ -167,3 +167,37 @@ def test_sampled_decision_misled(rmx):
     idx = np.arange(V, dtype=np.uint32).reshape(-1, 4)
     check(rmx, words, idx)
     assert plan_info(rmx, words, idx)[2] == 32
+
+
+def _sample_mask(V):
+    return (np.arange(V) % 16384) < 256   # the rows the guess is made from (V >= 2^22)
+
+
+@pytest.mark.parametrize("what", ["bits", "fields", "both"])
+def test_guess_from_the_sample_is_wrong(rmx, what):
+    """Rows outside the sampled blocks carry varying bits / sign+exponent fields the sample never
+    saw: the value-set pass flags the miss, K1a is recomputed, the components whose packing changed
+    lose their value ranks -- and the result stays exact."""
+    V = 1 << 22
+    rng = np.random.default_rng(71)
+    words = np.empty((V, 3), np.uint32)
+    for c in range(3):
+        words[:, c] = BASE | (rng.integers(0, 300, size=V).astype(np.uint32) << np.uint32(11))
+    out = ~_sample_mask(V)
+    pick = np.flatnonzero(out)[rng.integers(0, int(out.sum()), size=50)]
+    if what in ("bits", "both"):
+        words[pick[:25], 0] |= np.uint32(1 << 2)                 # a mantissa bit the sample lacks
+    if what in ("fields", "both"):
+        words[pick[25:], 1] = np.uint32(0x40A00000)              # 5.0f: a binade the sample lacks
+    idx = np.arange(V, dtype=np.uint32).reshape(-1, 4)
+    check(rmx, words, idx)
+    packed, kw, bits, passes = plan_info(rmx, words, idx)
+    assert packed == 1 and passes == (bits + 7) // 8
+
+
+def test_guess_from_the_sample_is_right(rmx):
+    """The common case: the sample sees every value's bits, the full pass only checks."""
+    V = (1 << 22) + 77
+    words, idx = set_mesh(72, V, V // 4, 4, [(700, 14, 9), (700, 14, 9), (9, 6, 0)])
+    check(rmx, words, idx)
+    assert plan_info(rmx, words, idx)[2] == 10 + 10 + 4
