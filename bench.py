@@ -187,8 +187,10 @@ def executed_model(V, I, U, D, KW, npass, value_ranks=False):
     """Algorithmic HBM bytes of one packed-path step (the kernels that ran)."""
     passes = sum(8 * KW + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass))
     return int((4 * I + 2 * V)                       # mark: indices in, flags cleared + set
-               + (4 * D + 1) * V                     # vary: rows + flags
-               + ((4 * D + 1) * V * 65 // 64 if value_ranks else 0)  # value sets: 1/64 sample + full pass
+               # K1a: rows + flags -- with value ranks over a 1/64 sample only, the full value-set pass
+               # (sample + full) checks the rows against it instead
+               + ((4 * D + 1) * V // 64 if value_ranks else (4 * D + 1) * V)
+               + ((4 * D + 1) * V * 65 // 64 if value_ranks else 0)
                + (4 * D + 1) * V + (4 * KW + 1) * V  # pack: rows + flags in, keys + digit 0 out
                + passes * V                          # LSD passes
                + 4 * KW * V                          # head count
@@ -393,8 +395,8 @@ def run_b200(args):
                 "executed_bytes": executed_bytes,
                 "achieved_gbs": executed_bytes / (ms * 1e-3) / 1e9 if executed_bytes else None,
                 "frac": executed_bytes / (ms * 1e-3) / 1e9 / hbm if executed_bytes else None,
-                "note": "algorithmic bytes of the kernels that ran (DESIGN.md (d)): mark 4I+2V, vary (4D+1)V, "
-                        "value sets (4D+1)V x 65/64 when value ranks ran, "
+                "note": "algorithmic bytes of the kernels that ran (DESIGN.md (d)): mark 4I+2V, vary (4D+1)V "
+                        "(with value ranks: a 1/64 sample, and value sets (4D+1)V x 65/64), "
                         "pack (4D+1)V+(4KW+1)V, per pass <= (8KW+10)V, head count 4KW V, unique (4KW+12)V+4KW U, "
                         "unpack (4KW+4D)U, map fill 12V, remap 12I",
                 "survey_nominal_bytes": nominal,
