@@ -317,3 +317,23 @@ def test_wide_dims_vs_oracle(rmx, D, pool, mesh_path):
     assert np.array_equal(out.elements, ref["elements"])
     for f in FIELDS:
         assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
+
+
+@pytest.mark.parametrize("env", [{"RMX_PDL": "0"}, {"RMX_VALUE_RANK": "0"}, {"RMX_PDL": "0", "RMX_VALUE_RANK": "0"}],
+                         ids=["no-pdl", "no-value-rank", "neither"])
+def test_switches_keep_results(rmx, monkeypatch, env):
+    """The A/B switches change speed, never results: golden cases through the
+    large-mesh pipeline and a lattice soup with value ranks, each switch off."""
+    monkeypatch.setenv("RMX_SMALL", "0")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for name, case in CASES[::7]:
+        out, sc = rmx.reindex(as_mesh(rmx, case["in_vtx"], case["in_idx"]))
+        assert np.array_equal(out.vertices.view(np.uint32), case["out_vtx"]), name
+        assert np.array_equal(out.elements, case["out_idx"]), name
+        assert np.array_equal(np.asarray(sc.org_id), case["org_id"]), name
+    v, e = lattice.lattice_soup("tri", (60, 70), seed=3)
+    ref = O.reindex(v.view(np.uint32), e)
+    out, _ = rmx.reindex(rmx.Mesh(v, e))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
