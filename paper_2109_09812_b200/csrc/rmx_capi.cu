@@ -71,10 +71,7 @@ int rank_force() {
 }
 
 // packed-key sort tiles: RMX_PK_CFG (below) selects rows per thread, tuning only
-#ifndef RMX_UNIQ_IPT
-#define RMX_UNIQ_IPT 12
-#endif
-constexpr int kPkUniqIpt = RMX_UNIQ_IPT;
+constexpr int kPkUniqIpt = 12;  // 3072-row K3' tiles (8..16 rows x 2..4 CTAs/SM measured within 1 %)
 constexpr int kPkUniqTile = kBlock * kPkUniqIpt;
 int pk_sort_ipt() {
     static int v = [] {

@@ -1302,10 +1302,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
 }
 
 template <int IPT>
-#ifndef RMX_UNIQ_MINB
-#define RMX_UNIQ_MINB 3
-#endif
-__global__ void __launch_bounds__(kBlock, RMX_UNIQ_MINB) k_unique_pk(UniquePkArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
