@@ -1140,17 +1140,7 @@ __global__ void __launch_bounds__(1024) k_tile_scan(uint32_t* counts, uint32_t n
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || plan[pk_base(4 * dim)] == 0u) return;
     __shared__ uint32_t s_warp[32];
-    const uint32_t per = (ntiles + 1023u) / 1024u;
-    const uint32_t lo = min(ntiles, threadIdx.x * per), hi = min(ntiles, lo + per);
-    uint32_t sum = 0;
-    for (uint32_t i = lo; i < hi; ++i) sum += counts[i];
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<32>(sum, s_warp, tot);
-    for (uint32_t i = lo; i < hi; ++i) {
-        const uint32_t c = counts[i];
-        counts[i] = run;
-        run += c;
-    }
+    const uint32_t tot = block_scan_counts(counts, ntiles, s_warp);
     if (threadIdx.x == 0) *total_out = tot;
 }
 
