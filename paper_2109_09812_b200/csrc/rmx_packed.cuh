@@ -363,6 +363,58 @@ struct RowPacker {
     }
 };
 
+// Inverse of RowPacker: component value cv -> the component's word (the
+// replacement row's bits outside the varying mask, the first run and any
+// further runs deposited back, the ranked field looked up in the inverse field
+// table).
+template <int D_CT>
+struct RowUnpacker {
+    static_assert(D_CT >= 1 && D_CT <= kMaxRankDim, "per-component unpacking covers D <= kMaxRankDim");
+    uint32_t src0[D_CT], msk0[D_CT], frel[D_CT], fmask[D_CT], lo[D_CT], xr[D_CT], cst[D_CT];
+    bool ranked[D_CT];
+    const uint32_t* s_runs;
+    const uint16_t* s_value;  // [D_CT][kFieldValues] field of every field rank
+
+    __device__ __forceinline__ RowUnpacker(const uint32_t* plan, const uint32_t* runs, uint32_t nruns,
+                                           const uint16_t* values, const uint32_t* s_const)
+        : s_runs(runs), s_value(values) {
+        const uint32_t* rk = plan + pk_rank_base(4 * D_CT);
+        const uint32_t* vb = plan + pk_value_base(4 * D_CT);
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) {
+            const uint32_t l = vb[4 + 4 * c];
+            lo[c] = min(l, 63u);
+            src0[c] = 0u;
+            msk0[c] = 0u;
+            uint32_t b = nruns, e = 0;
+            for (uint32_t r = 0; r < nruns; ++r) {
+                if (runs[4 * r] != static_cast<uint32_t>(c)) continue;
+                if (b == nruns) {
+                    b = r;
+                    src0[c] = runs[4 * r + 1];
+                    msk0[c] = low_mask(runs[4 * r + 2]);
+                }
+                e = r + 1;
+            }
+            xr[c] = b < e ? ((b + 1) | (e << 16)) : 0u;
+            ranked[c] = rk[c] >> 31;
+            frel[c] = ranked[c] ? (rk[c] & 0xFFFFu) - l : 0u;
+            fmask[c] = ranked[c] ? low_mask((rk[c] >> 16) & 0xFFu) : 0u;
+            cst[c] = s_const[c];
+        }
+    }
+
+    __device__ __forceinline__ uint32_t word(int c, uint32_t v) const {
+        uint32_t w = cst[c] | ((v & msk0[c]) << src0[c]);
+        for (uint32_t q = xr[c] & 0xFFFFu; q < (xr[c] >> 16); ++q) {
+            const uint32_t* ru = s_runs + 4 * q;
+            w |= ((v >> (ru[3] - lo[c])) & low_mask(ru[2])) << ru[1];
+        }
+        if (ranked[c]) w |= static_cast<uint32_t>(s_value[c * kFieldValues + ((v >> frel[c]) & fmask[c])]) << kFieldLo;
+        return w;
+    }
+};
+
 // ---------------------------------------------------------------------------
 // Value ranks (rmx_base.cuh): the layout of each component in the packed key
 // before and after, the transform k_pack applies and k_unpack_pk inverts.
@@ -1368,14 +1420,27 @@ __global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
     uint64_t done = 0;
     if constexpr (D_CT == 3 || D_CT == 4) {
         if (a.vec) {  // 4 rows per thread, written as D_CT 16-byte stores
+            const RowUnpacker<D_CT> up(a.plan, s_runs, nruns, s_value, s_const);
+            // key (value ranks inverted per component) -> component value -> word
+            auto unpack4 = [&](uint64_t i, uint32_t* w) {
+                const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) {
+                    uint32_t v;
+                    if (vm.on) {
+                        v = static_cast<uint32_t>(key >> vm.nlo[c]) & low_mask(vm.nw[c]);
+                        if ((vm.ranked >> c) & 1u) v = __ldg(a.vinv + (static_cast<size_t>(c) << kMaxValueBits) + v);
+                    } else {
+                        v = static_cast<uint32_t>(key >> up.lo[c]) & low_mask(vm.w[c]);
+                    }
+                    w[c] = up.word(c, v);
+                }
+            };
             uint32_t w[4 * D_CT];
             const uint64_t ng = U >> 2;
             for (uint64_t g = t0; g < ng; g += stride) {
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint64_t key = load_key(4 * g + r);
-                    unpack_row<D_CT>(key, w + r * D_CT, D, s_const, s_runs, nruns, s_rbeg, s_rend, s_rk, s_value);
-                }
+                for (int r = 0; r < 4; ++r) unpack4(4 * g + r, w + r * D_CT);
                 uint4* dst = reinterpret_cast<uint4*>(a.out_vtx + 4 * g * D_CT);
 #pragma unroll
                 for (int q = 0; q < D_CT; ++q)
