@@ -147,6 +147,10 @@ int rmx_kernel_launches(uint32_t dim);
 int rmx_last_executed_passes(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream);
 int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
+/* Diagnostic of the value-rank guess (D <= 4): info[4] = {key bits of the plan guessed from the
+ * sample, value sets judged worth collecting (0/1), candidate components, full-pass check state
+ * (bit 0 checked, bit 1 a row fell outside the sample)}. */
+int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
 /* Tuning diagnostic: look-back statistics {windows, spins, look-backs, 0} of
  * the AoS sort passes when built with -DRMX_PHASES (otherwise zeros; returns 0). */

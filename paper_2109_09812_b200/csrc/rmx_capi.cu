@@ -97,6 +97,7 @@ struct Layout {
     size_t ukeys;                 // packed key of every unique row (K3' -> unpack)
     size_t rank16, vinv, vsets;   // value ranks (D <= kMaxRankDim): rank tables, inverse tables, value sets
     size_t gplan, svary, sfields; // the plan guessed from a sample of the rows, and its inputs
+    size_t vsets_b;               // value sets of the odd sample blocks (saturation estimate)
     size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
     size_t total;
 };
@@ -134,6 +135,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.gplan = take(plan_words(L.P) * 4);
     L.ctl_begin = off;
     L.vsets = take(vr_dim * kValueWords * 4);
+    L.vsets_b = take(vr_dim * kValueWords * 4);
     L.svary = take(vr_dim * 4);
     L.vstate = take(16);
     L.sfields = take(vr_dim * kFieldWords * 4);
@@ -655,13 +657,25 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                     nullptr, nullptr, nullptr};
         if ((rc = dispatch_vary(sa, s))) return rc;
         RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, GraphHandles{}));
+        uint32_t* vsets_b = reinterpret_cast<uint32_t*>(base + L.vsets_b);
         ValueSetArgs va{vtx, flags, idx, gplan, sfields, vsets, svary, vstate, d_status, static_cast<uint32_t>(V),
-                        shift, vec};
-        if (shift && (rc = dispatch_valueset(va, L.D, s))) return rc;
-        ValuePlanArgs pd{gplan, vsets, nullptr, nullptr, d_status, L.D, 0, nullptr, nullptr, nullptr, nullptr, nullptr};
+                        shift, vec, 0, gplan, 0};
+        if (shift) {  // the sample's value sets, even blocks into vsets and odd blocks into vsets_b
+            if ((rc = dispatch_valueset(va, L.D, s))) return rc;
+            ValueSetArgs vb_args = va;
+            vb_args.vsets = vsets_b;
+            vb_args.parity = 1;
+            if ((rc = dispatch_valueset(vb_args, L.D, s))) return rc;
+        }
+        ValuePlanArgs pd{gplan, vsets, shift ? vsets_b : nullptr, nullptr, nullptr, d_status, L.D, 0, nullptr,
+                         nullptr, nullptr, nullptr, nullptr, nullptr};
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
         va.shift = 0u;
         if ((rc = dispatch_valueset(va, L.D, s))) return rc;
+        // decide again on the full pass's value sets (tight lower bounds even where a row fell
+        // outside the sample): the second chance below runs only if value ranks can still pay
+        pd.vsets_b = nullptr;
+        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
         VaryArgs fa{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
                     vstate, svary, sfields};
         if ((rc = dispatch_vary(fa, s))) return rc;
@@ -710,7 +724,15 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
     uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
     if (value_ranks) {  // rank tables and the new key layout (exact plan, value sets of the full pass)
-        ValuePlanArgs pa{plan, vsets, rank16, vinv, d_status, L.D, 1, gplan, svary, sfields, vary, fields};
+        uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
+        // second chance when a row fell outside the sample: value sets again with the exact packing
+        RMX_CHECK(launch(k_vsets_reset, 1, kBlock, 0, s, vsets, static_cast<uint32_t>(L.D * kValueWords), vstate,
+                         d_status));
+        ValueSetArgs ra{vtx, flags, idx, plan, fields, vsets, nullptr, vstate, d_status, static_cast<uint32_t>(V),
+                        0u, vec, 1, gplan, 0};
+        if ((rc = dispatch_valueset(ra, L.D, s))) return rc;
+        ValuePlanArgs pa{plan, vsets, nullptr, rank16, vinv, d_status, L.D, 1, vstate, gplan, svary, sfields, vary,
+                         fields};
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
         RMX_CHECK(cudaGetLastError());
     }
@@ -906,11 +928,12 @@ void rmx_graph_destroy(rmx_graph* graph) {
 
 int rmx_kernel_launches(uint32_t dim) {
     // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes,
-    // [dim <= kMaxRankDim: K1a over a sample, guessed plan, value-set sample (meshes of >= 2^22 rows),
-    //  value plan, value sets + K1a check in one pass, K1a copy / fallback, value plan], pack,
+    // [dim <= kMaxRankDim: K1a over a sample, guessed plan, value-set sample x 2 (meshes of >= 2^22 rows),
+    //  value plan, value sets + K1a check in one pass, value plan, K1a copy / fallback, second-chance reset +
+    //  value sets (exit unless a row fell outside the sample), value plan], pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
-    const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 6 : 0;
+    const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 10 : 0;
     const int D = static_cast<int>(dim);
     const int aos = aos_possible(D) ? 2 + 4 * D + 1 : 0;  // build_rows, first_hist, passes, unique
     return 4 + aos + value_ranks + 1 + 3 * packed_passes_max(D) + 4 + 2;
@@ -981,6 +1004,25 @@ int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* 
     info[1] = vr ? vb[1] : 0u;      // components replaced by their value rank
     info[2] = plain;                // key bits before value ranks
     info[3] = pk[2];                // key bits
+    return RMX_OK;
+}
+
+int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    for (int k = 0; k < 4; ++k) info[k] = 0u;
+    if (L.D > kMaxRankDim) return RMX_OK;
+    uint32_t pk[8] = {0}, vb[2] = {0}, st = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char* base = static_cast<const char*>(workspace);
+    RMX_CHECK(cudaMemcpyAsync(pk, base + L.gplan + pk_base(L.P) * 4, sizeof(pk), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(vb, base + L.gplan + pk_value_base(L.P) * 4, sizeof(vb), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(&st, base + L.vstate, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    info[0] = pk[0] ? pk[2] : 0u;  // key bits of the plan guessed from the sample
+    info[1] = vb[0];               // 1: value sets judged worth collecting
+    info[2] = vb[1];               // candidate components
+    info[3] = st;                  // kVstateChecked | kVstateMiss of the full pass
     return RMX_OK;
 }
 

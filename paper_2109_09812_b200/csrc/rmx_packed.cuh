@@ -134,14 +134,19 @@ struct VaryArgs {
 
 constexpr uint32_t kVstateChecked = 1u, kVstateMiss = 2u;
 
-// The sample that guesses the value-rank layout: the first kSampleRun rows of
-// every kSampleRun << shift (contiguous reads).
+// The sample that guesses the value-rank layout: one run of kSampleRun rows in
+// every kSampleRun << shift (contiguous reads), at a hashed offset inside its
+// period -- a fixed offset aliases with periodic data (a grid stored row by
+// row showed the same few columns in every run).
 constexpr uint32_t kSampleRun = 256;
 __host__ __device__ inline uint64_t sample_count(uint64_t n, uint32_t shift) {
     return ((n >> shift) + kSampleRun) & ~static_cast<uint64_t>(kSampleRun - 1);
 }
 __host__ __device__ inline uint64_t sample_row(uint64_t s, uint32_t shift) {
-    return ((s / kSampleRun) * kSampleRun << shift) + (s % kSampleRun);
+    const uint64_t b = s / kSampleRun;
+    const uint64_t period = static_cast<uint64_t>(kSampleRun) << shift;
+    const uint64_t jitter = shift ? (static_cast<uint32_t>(b * 0x9E3779B1ull) >> 8) % (period - kSampleRun + 1) : 0u;
+    return b * period + jitter + (s % kSampleRun);
 }
 
 // Occurring sign+exponent fields of one component: a per-thread window of 32
@@ -223,18 +228,28 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
             }
         };
         uint64_t done = 0;
-        if (a.shift) {  // sample rows only
+        if (a.shift) {  // sample rows only, 4 in flight per thread
             const uint64_t ns = sample_count(a.n, a.shift);
-            for (uint64_t q = start; q < ns; q += stride) {
-                const uint64_t i = sample_row(q, a.shift);
-                if (i < a.n && a.flags[i]) {
-                    uint32_t k[D_CT];
+            constexpr int kB = 4;
+            for (uint64_t q0 = start; q0 < ns; q0 += kB * stride) {
+                uint32_t k[kB][D_CT];
+                bool used[kB];
 #pragma unroll
-                    for (int c = 0; c < D_CT; ++c) {
-                        k[c] = __ldg(a.vtx + i * D_CT + c);
-                        vor[c] |= k[c] ^ ref[c];
+                for (int j = 0; j < kB; ++j) {
+                    const uint64_t q = q0 + j * stride;
+                    const uint64_t i = sample_row(q, a.shift);
+                    const bool ok = q < ns && i < a.n;
+                    used[j] = ok && a.flags[i] != 0;
+#pragma unroll
+                    for (int c = 0; c < D_CT; ++c) k[j][c] = ok ? __ldg(a.vtx + i * D_CT + c) : ref[c];
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    if (used[j]) {
+#pragma unroll
+                        for (int c = 0; c < D_CT; ++c) vor[c] |= k[j][c] ^ ref[c];
+                        note(k[j]);
                     }
-                    note(k);
                 }
             }
             done = a.n;
@@ -505,6 +520,11 @@ struct ValueSetArgs {
     uint32_t n;
     uint32_t shift;          // > 0: the sample rows only (sample_row)
     int vec;
+    // second chance (redo != 0): after a miss, collect again with the exact plan (plan = the exact
+    // plan, fields = the exact field sets), if the guessed plan (gplan) had found value ranks worth it
+    int redo;
+    const uint32_t* gplan;
+    int parity;              // sample pass: even or odd sample blocks (two sets for the saturation test)
 };
 
 constexpr int kVsThreads = 1024;
@@ -519,10 +539,17 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     __shared__ uint32_t s_runs[4 * kMaxRuns];
     __shared__ uint16_t s_rank[D_CT * kFieldValues];
     if (*a.status) return;  // uniform
-    const bool sets = pk[0] != 0u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
+    bool sets;
+    if (a.redo) {
+        const uint32_t* gvb = a.gplan + pk_value_base(4 * D_CT);
+        sets = (*a.vstate & kVstateMiss) && a.gplan[pk_base(4 * D_CT)] != 0u && gvb[0] == 1u && pk[0] != 0u &&
+               vb[1] != 0u;
+    } else {
+        sets = pk[0] != 0u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
+    }
     if (!sets) return;  // (the full pass: k_vary computes K1a's outputs instead)
     // the full pass also checks every used row against the sample's varying bits and field sets
-    const bool check = a.vstate != nullptr && a.shift == 0u;
+    const bool check = !a.redo && a.vstate != nullptr && a.shift == 0u;
     __shared__ uint32_t s_fset[D_CT * kFieldWords];  // the sample's field sets (check)
     const uint32_t cand = vb[1];
     load_packer<D_CT>(a.plan, a.fields, s_runs, s_rank);
@@ -566,16 +593,26 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
 #pragma unroll
         for (int c = 0; c < D_CT; ++c) s_map[off[c] + pack.value(c, used ? k[c] : ref[c])] = 1u;
     };
-    if (a.shift) {
-        const uint64_t ns = sample_count(a.n, a.shift);
-        for (uint64_t q = start; q < ns; q += stride) {
-            const uint64_t i = sample_row(q, a.shift);
-            if (i < a.n) {
-                uint32_t k[D_CT];
+    if (a.shift) {  // the even (parity 0) or odd (parity 1) sample blocks, 4 rows in flight per thread
+        const uint64_t ns = sample_count(a.n, a.shift) / 2 + kSampleRun;
+        constexpr int kB = 4;
+        for (uint64_t q0 = start; q0 < ns; q0 += kB * stride) {
+            uint32_t k[kB][D_CT];
+            bool ok[kB], used[kB];
 #pragma unroll
-                for (int c = 0; c < D_CT; ++c) k[c] = __ldg(a.vtx + i * D_CT + c);
-                note(k, a.flags[i] != 0);
+            for (int j = 0; j < kB; ++j) {
+                const uint64_t q = q0 + j * stride;
+                const uint64_t qq =
+                    (2 * (q / kSampleRun) + static_cast<uint64_t>(a.parity)) * kSampleRun + q % kSampleRun;
+                const uint64_t i = sample_row(qq, a.shift);
+                ok[j] = q < ns && i < a.n;
+                used[j] = ok[j] && a.flags[i] != 0;
+#pragma unroll
+                for (int c = 0; c < D_CT; ++c) k[j][c] = ok[j] ? __ldg(a.vtx + i * D_CT + c) : ref[c];
             }
+#pragma unroll
+            for (int j = 0; j < kB; ++j)
+                if (ok[j]) note(k[j], used[j]);
         }
     } else {
         uint64_t done = 0;
@@ -629,6 +666,14 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     }
 }
 
+// Before the second chance: the value sets hold the guessed packing's values -- start over.
+__global__ void __launch_bounds__(kBlock) k_vsets_reset(uint32_t* vsets, uint32_t words, const uint32_t* vstate,
+                                                         const uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*status || !(*vstate & kVstateMiss)) return;
+    for (uint32_t i = threadIdx.x; i < words; i += kBlock) vsets[i] = 0u;
+}
+
 // One CTA of 1024 threads.  final == 0 (on the guessed plan, after the sample
 // pass): keep the candidates whose sampled value count already needs fewer
 // bits, and ask for value sets in the full pass when that alone would shorten
@@ -640,12 +685,14 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
 struct ValuePlanArgs {
     uint32_t* plan;          // decide: the guessed plan; final: the exact plan
     const uint32_t* vsets;
+    const uint32_t* vsets_b; // decide after the sample: the odd sample blocks' sets (vsets: the even ones)
     uint16_t* rank16;        // [D][2^kMaxValueBits] rank of every occurring value
     uint16_t* vinv;          // [D][2^kMaxValueBits] value of every rank
     const uint32_t* status;
     int dim;
     int final_pass;
     // final: the guess and what it was made from, against the exact K1a outputs
+    const uint32_t* vstate;
     const uint32_t* gplan;
     const uint32_t* svary;
     const uint32_t* sfields;
@@ -667,10 +714,12 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
     uint32_t cand = vb[1];
     if (a.final_pass) {
         // the value sets hold the guessed packing's values: keep the components packed the same way
+        // (after a miss the second chance collected them with the exact packing: all valid)
         const uint32_t* gvb = a.gplan + pk_value_base(4 * D);
         if (a.gplan[pk_base(4 * D)] == 0u || gvb[0] != 1u) return;  // uniform
-        cand &= gvb[1];
-        for (int c = 0; c < D; ++c) {
+        const bool redone = (*a.vstate & kVstateMiss) != 0u;
+        if (!redone) cand &= gvb[1];
+        for (int c = 0; c < D && !redone; ++c) {
             bool same = a.vary[c] == a.svary[c];
             for (int w = 0; w < kFieldWords; ++w) same = same && a.fields[c * kFieldWords + w] == a.sfields[c * kFieldWords + w];
             if (!same) cand &= ~(1u << c);
@@ -690,6 +739,21 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
         (void)block_exclusive_scan<32>(__popc(set[2 * t]) + __popc(set[2 * t + 1]), s_warp, tot);
         __syncthreads();
         cnt[c] = tot;
+        if (a.vsets_b) {
+            // two halves of the sample, A (vsets) and B (vsets_b): the number of values that occur is
+            // estimated as |A| |B| / |A and B| (capture-recapture) -- a set the sample saturates
+            // (lattice axes: both halves see every value) stays small, while ordered data whose
+            // halves see different values (grids stored row by row) is not mistaken for one
+            const uint32_t* sb = a.vsets_b + c * kValueWords;
+            uint32_t nb, ni;
+            (void)block_exclusive_scan<32>(__popc(sb[2 * t]) + __popc(sb[2 * t + 1]), s_warp, nb);
+            __syncthreads();
+            (void)block_exclusive_scan<32>(__popc(sb[2 * t] & set[2 * t]) + __popc(sb[2 * t + 1] & set[2 * t + 1]),
+                                           s_warp, ni);
+            __syncthreads();
+            const uint64_t est = ni ? static_cast<uint64_t>(tot) * nb / ni : (1ull << 32);
+            cnt[c] = static_cast<uint32_t>(min(est, static_cast<uint64_t>(0xFFFFFFFFu)));
+        }
     }
     uint32_t ranked = 0, nbits = 0;
     for (int c = 0; c < D; ++c) {
