@@ -328,6 +328,14 @@ bool value_rank_enabled() {
     return !(e && e[0] == '0');
 }
 
+// Value ranks cost the sample kernels and one read of the vertices; a saved 8-bit pass pays for
+// that from ~2^25 rows on (C1, 3.15M rows: 0.37 ms with, 0.36 without; grid_quads(1024), 5.2M
+// rows ranked to 3 passes: 0.44 vs 0.36 ms).  RMX_VALUE_RANK_MIN overrides the row count (tests).
+uint64_t value_rank_min_rows() {
+    const char* e = std::getenv("RMX_VALUE_RANK_MIN");
+    return e ? std::strtoull(e, nullptr, 10) : (1ull << 25);
+}
+
 template <int D_CT>
 int launch_valueset(const ValueSetArgs& a, uint64_t items, cudaStream_t s) {
     int sms = 0;
@@ -640,7 +648,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     // K1a varying bits of the cleaned vertex set, then the plan (packed or AoS)
     const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
-    const bool value_ranks = L.D <= kMaxRankDim && value_rank_enabled();
+    const bool value_ranks = L.D <= kMaxRankDim && value_rank_enabled() && V >= value_rank_min_rows();
     uint32_t* gplan = reinterpret_cast<uint32_t*>(base + L.gplan);
     uint32_t* svary = reinterpret_cast<uint32_t*>(base + L.svary);
     uint32_t* sfields = reinterpret_cast<uint32_t*>(base + L.sfields);
@@ -928,7 +936,8 @@ void rmx_graph_destroy(rmx_graph* graph) {
 
 int rmx_kernel_launches(uint32_t dim) {
     // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes,
-    // [dim <= kMaxRankDim: K1a over a sample, guessed plan, value-set sample x 2 (meshes of >= 2^22 rows),
+    // [dim <= kMaxRankDim, meshes of >= 2^25 rows (value_rank_min_rows): K1a over a sample, guessed plan,
+    //  value-set sample x 2,
     //  value plan, value sets + K1a check in one pass, value plan, K1a copy / fallback, second-chance reset +
     //  value sets (exit unless a row fell outside the sample), value plan], pack,
     // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),

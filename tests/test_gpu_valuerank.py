@@ -30,8 +30,10 @@ def rmx(cuda_ok):
 
 @pytest.fixture(autouse=True)
 def value_rank_default(monkeypatch):
-    """Width assertions need the default (value ranks on), whatever the suite runs under."""
+    """Width assertions need value ranks on, whatever the suite runs under, and on the small
+    meshes of these tests (by default only meshes of >= 2^25 rows use them)."""
     monkeypatch.delenv("RMX_VALUE_RANK", raising=False)
+    monkeypatch.setenv("RMX_VALUE_RANK_MIN", "0")
 
 
 @pytest.fixture
@@ -201,3 +203,14 @@ def test_guess_from_the_sample_is_right(rmx):
     words, idx = set_mesh(72, V, V // 4, 4, [(700, 14, 9), (700, 14, 9), (9, 6, 0)])
     check(rmx, words, idx)
     assert plan_info(rmx, words, idx)[2] == 10 + 10 + 4
+
+
+def test_small_meshes_skip_value_ranks(rmx, monkeypatch):
+    """Below RMX_VALUE_RANK_MIN rows (default 2^25) the sample kernels and the value-set pass would
+    cost more than a saved pass: the plain packed key is used."""
+    monkeypatch.delenv("RMX_VALUE_RANK_MIN")
+    case = next(c for c in CASES if c[0] == 1)
+    words, idx = set_mesh(*case)
+    check(rmx, words, idx)
+    plain, _ = model_bits(words, idx)
+    assert plan_info(rmx, words, idx)[2] == plain
