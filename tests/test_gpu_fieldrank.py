@@ -42,7 +42,8 @@ def raw_varying_bits(words, idx):
     return int(sum(bin(int(v)).count("1") for v in x))
 
 
-def plan_info(rmx, words, idx):
+def plan_info(rmx, words, idx, guess=None):
+    """rmx_plan_info of a fresh call; with ``guess`` (a list) also rmx_plan_guess_info into it."""
     from paper_2109_09812_b200 import _native, pipeline
     V, D = words.shape
     E, K = idx.shape
@@ -56,6 +57,10 @@ def plan_info(rmx, words, idx):
     pipeline.launch(vt, V, D, it, E, K, ov, oe, info, ws, None, s)
     pinfo = (ctypes.c_uint32 * 4)()
     _native.check(_native.lib().rmx_plan_info(ws.data_ptr(), V, D, s.cuda_stream, pinfo))
+    if guess is not None:
+        g = (ctypes.c_uint32 * 4)()
+        _native.check(_native.lib().rmx_plan_guess_info(ws.data_ptr(), V, D, s.cuda_stream, g))
+        guess[:] = [int(x) for x in g]
     return [int(x) for x in pinfo]
 
 

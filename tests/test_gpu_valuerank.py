@@ -171,20 +171,29 @@ def test_sampled_decision_misled(rmx):
     assert plan_info(rmx, words, idx)[2] == 32
 
 
-def _sample_mask(V):
-    return (np.arange(V) % 16384) < 256   # the rows the guess is made from (V >= 2^22)
+def _sample_mask(V, shift=6, run=256):
+    """The rows the guess is made from (mirror of rmx_packed.cuh:sample_row, meshes >= 2^22 rows)."""
+    period = run << shift
+    mask = np.zeros(V, bool)
+    for b in range((V >> shift) // run + 1):
+        jitter = (((b * 0x9E3779B1) & 0xFFFFFFFF) >> 8) % (period - run + 1)
+        lo = b * period + jitter
+        mask[lo:min(lo + run, V)] = True
+    return mask
 
 
 @pytest.mark.parametrize("what", ["bits", "fields", "both"])
-def test_guess_from_the_sample_is_wrong(rmx, what):
-    """Rows outside the sampled blocks carry varying bits / sign+exponent fields the sample never
-    saw: the value-set pass flags the miss, K1a is recomputed, the components whose packing changed
-    lose their value ranks -- and the result stays exact."""
+def test_guess_from_the_sample_is_wrong(rmx, monkeypatch, what):
+    """Rows outside the sampled runs carry varying bits / sign+exponent fields the sample never
+    saw: the value-set pass flags the miss, K1a is recomputed, the decision is taken again and the
+    second chance collects the values with the exact packing -- the components whose packing grew
+    past 16 bits lose their ranks, the others keep them, and the result stays exact."""
     V = 1 << 22
     rng = np.random.default_rng(71)
     words = np.empty((V, 3), np.uint32)
     for c in range(3):
-        words[:, c] = BASE | (rng.integers(0, 300, size=V).astype(np.uint32) << np.uint32(11))
+        vals = value_set(rng, 300, 16)
+        words[:, c] = BASE | (vals[rng.integers(0, 300, size=V)] << np.uint32(7))
     out = ~_sample_mask(V)
     pick = np.flatnonzero(out)[rng.integers(0, int(out.sum()), size=50)]
     if what in ("bits", "both"):
@@ -193,8 +202,13 @@ def test_guess_from_the_sample_is_wrong(rmx, what):
         words[pick[25:], 1] = np.uint32(0x40A00000)              # 5.0f: a binade the sample lacks
     idx = np.arange(V, dtype=np.uint32).reshape(-1, 4)
     check(rmx, words, idx)
-    packed, kw, bits, passes = plan_info(rmx, words, idx)
+    guess = []
+    packed, kw, bits, passes = plan_info(rmx, words, idx, guess)
     assert packed == 1 and passes == (bits + 7) // 8
+    assert guess[3] == 3      # the full pass checked the rows and found some outside the sample
+    assert guess[1] == 1      # ... and value ranks still paid
+    monkeypatch.setenv("RMX_VALUE_RANK", "0")
+    assert bits < plan_info(rmx, words, idx)[2]
 
 
 def test_guess_from_the_sample_is_right(rmx):
@@ -202,7 +216,9 @@ def test_guess_from_the_sample_is_right(rmx):
     V = (1 << 22) + 77
     words, idx = set_mesh(72, V, V // 4, 4, [(700, 14, 9), (700, 14, 9), (9, 6, 0)])
     check(rmx, words, idx)
-    assert plan_info(rmx, words, idx)[2] == 10 + 10 + 4
+    guess = []
+    assert plan_info(rmx, words, idx, guess)[2] == 10 + 10 + 4
+    assert guess[1] == 1 and guess[3] == 1  # worth collecting; checked, no row outside the sample
 
 
 def test_small_meshes_skip_value_ranks(rmx, monkeypatch):
