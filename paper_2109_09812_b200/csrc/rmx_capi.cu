@@ -735,7 +735,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
         // second chance when a row fell outside the sample: value sets again with the exact packing
         RMX_CHECK(launch(k_vsets_reset, 1, kBlock, 0, s, vsets, static_cast<uint32_t>(L.D * kValueWords), vstate,
-                         d_status));
+                         static_cast<const uint32_t*>(gplan), static_cast<const uint32_t*>(vary),
+                         static_cast<const uint32_t*>(svary), static_cast<const uint32_t*>(fields),
+                         static_cast<const uint32_t*>(sfields), L.D, static_cast<const uint32_t*>(d_status)));
         ValueSetArgs ra{vtx, flags, idx, plan, fields, vsets, nullptr, vstate, d_status, static_cast<uint32_t>(V),
                         0u, vec, 1, gplan, 0};
         if ((rc = dispatch_valueset(ra, L.D, s))) return rc;

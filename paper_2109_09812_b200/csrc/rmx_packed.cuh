@@ -132,7 +132,7 @@ struct VaryArgs {
     const uint32_t* sample_fields;
 };
 
-constexpr uint32_t kVstateChecked = 1u, kVstateMiss = 2u;
+constexpr uint32_t kVstateChecked = 1u, kVstateMiss = 2u, kVstateRedo = 4u;
 
 // The sample that guesses the value-rank layout: one run of kSampleRun rows in
 // every kSampleRun << shift (contiguous reads), at a hashed offset inside its
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     bool sets;
     if (a.redo) {
         const uint32_t* gvb = a.gplan + pk_value_base(4 * D_CT);
-        sets = (*a.vstate & kVstateMiss) && a.gplan[pk_base(4 * D_CT)] != 0u && gvb[0] == 1u && pk[0] != 0u &&
+        sets = (*a.vstate & kVstateRedo) && a.gplan[pk_base(4 * D_CT)] != 0u && gvb[0] == 1u && pk[0] != 0u &&
                vb[1] != 0u;
     } else {
         sets = pk[0] != 0u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
@@ -666,11 +666,31 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     }
 }
 
-// Before the second chance: the value sets hold the guessed packing's values -- start over.
-__global__ void __launch_bounds__(kBlock) k_vsets_reset(uint32_t* vsets, uint32_t words, const uint32_t* vstate,
-                                                         const uint32_t* status) {
+// After a miss and the exact K1a: a second chance is needed only if a candidate component's
+// packing changed (exact varying bits or field set differ from the sample's) -- misses in other
+// components leave the candidates' value sets valid.  If so: kVstateRedo and start the sets over.
+__global__ void __launch_bounds__(kBlock) k_vsets_reset(uint32_t* vsets, uint32_t words, uint32_t* vstate,
+                                                         const uint32_t* gplan, const uint32_t* vary,
+                                                         const uint32_t* svary, const uint32_t* fields,
+                                                         const uint32_t* sfields, int D, const uint32_t* status) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    __shared__ uint32_t s_redo;
     if (*status || !(*vstate & kVstateMiss)) return;
+    if (threadIdx.x == 0) {
+        const uint32_t* gvb = gplan + pk_value_base(4 * D);
+        bool redo = false;
+        if (gplan[pk_base(4 * D)] != 0u && gvb[0] == 1u)
+            for (int c = 0; c < D; ++c) {
+                if (!((gvb[1] >> c) & 1u)) continue;
+                bool same = vary[c] == svary[c];
+                for (int w = 0; w < kFieldWords; ++w) same = same && fields[c * kFieldWords + w] == sfields[c * kFieldWords + w];
+                redo = redo || !same;
+            }
+        s_redo = redo ? 1u : 0u;
+        if (redo) *vstate |= kVstateRedo;
+    }
+    __syncthreads();
+    if (!s_redo) return;
     for (uint32_t i = threadIdx.x; i < words; i += kBlock) vsets[i] = 0u;
 }
 
@@ -717,7 +737,7 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
         // (after a miss the second chance collected them with the exact packing: all valid)
         const uint32_t* gvb = a.gplan + pk_value_base(4 * D);
         if (a.gplan[pk_base(4 * D)] == 0u || gvb[0] != 1u) return;  // uniform
-        const bool redone = (*a.vstate & kVstateMiss) != 0u;
+        const bool redone = (*a.vstate & kVstateRedo) != 0u;
         if (!redone) cand &= gvb[1];
         for (int c = 0; c < D && !redone; ++c) {
             bool same = a.vary[c] == a.svary[c];
