@@ -230,3 +230,19 @@ def test_small_meshes_skip_value_ranks(rmx, monkeypatch):
     check(rmx, words, idx)
     plain, _ = model_bits(words, idx)
     assert plan_info(rmx, words, idx)[2] == plain
+
+
+def test_sample_sees_no_used_row(rmx):
+    """Every sampled row is unused: the guess is built from nothing (all components constant), the
+    full pass finds every used row outside it, K1a is recomputed -- the result stays exact."""
+    V = 1 << 22
+    rng = np.random.default_rng(91)
+    words = np.empty((V, 3), np.uint32)
+    for c in range(3):
+        vals = value_set(rng, 200, 16)
+        words[:, c] = BASE | (vals[rng.integers(0, 200, size=V)] << np.uint32(7))
+    outside = np.flatnonzero(~_sample_mask(V))
+    idx = outside[rng.integers(0, len(outside), size=(V // 8, 3))].astype(np.uint32)
+    check(rmx, words, idx)
+    packed, kw, bits, passes = plan_info(rmx, words, idx)
+    assert packed == 1 and passes == (bits + 7) // 8
