@@ -13,7 +13,8 @@
  * except the host-side `rmx_scratch` struct itself are DEVICE pointers; every
  * call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy default)
  * and never allocates: the caller owns every buffer, including the
- * workspace sized by rmx_workspace_bytes().
+ * workspace sized by rmx_workspace_bytes() (256-byte aligned, as
+ * cudaMalloc and torch allocations are; RMX_EINVAL otherwise).
  *
  * Vertex data is handled exclusively as uint32 words (the reference's
  * `vertex_bits`, mesh.py:91-94): ordering is raw unsigned bit order,

@@ -592,6 +592,10 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         std::snprintf(g_err, sizeof(g_err), "null buffer");
         return RMX_EINVAL;
     }
+    if (reinterpret_cast<uintptr_t>(ws) % kAlign) {  // bulk copies and 16-byte loads of workspace arrays
+        std::snprintf(g_err, sizeof(g_err), "workspace must be %zu-byte aligned", kAlign);
+        return RMX_EINVAL;
+    }
     const PdlScope pdl(gc == nullptr && pdl_enabled());
     const Layout L = make_layout(V, D);
     if (!ws || ws_bytes < L.total) {

@@ -337,3 +337,29 @@ def test_switches_keep_results(rmx, monkeypatch, env):
     out, _ = rmx.reindex(rmx.Mesh(v, e))
     assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
     assert np.array_equal(out.elements, ref["elements"])
+
+
+def test_misaligned_workspace_is_einval(rmx):
+    """The workspace is carved into 256-byte aligned arrays that bulk copies and 16-byte loads
+    read: a misaligned workspace pointer is rejected before any launch."""
+    import torch
+    from paper_2109_09812_b200 import _native
+    V, D, E, K = 4096, 3, 1024, 3
+    g = torch.Generator().manual_seed(3)
+    vtx = torch.randint(0, 1 << 20, (V, D), generator=g, dtype=torch.int32).cuda()
+    idx = torch.randint(0, V, (E, K), generator=g, dtype=torch.int32).cuda()
+    out_v = torch.empty((V, D), dtype=torch.int32, device="cuda")
+    out_e = torch.empty((E, K), dtype=torch.int32, device="cuda")
+    info = torch.zeros(2, dtype=torch.int64, device="cuda")
+    lib = _native.lib()
+    wsb = lib.rmx_workspace_bytes(V, D, E, K)
+    ws = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
+    args = [vtx.data_ptr(), V, D, idx.data_ptr(), E, K, out_v.data_ptr(), out_e.data_ptr(),
+            info.data_ptr(), info.data_ptr() + 8]
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = lib.rmx_reindex(*args, ws.data_ptr() + 16, wsb, None, stream)
+    assert rc == _native.RMX_EINVAL and b"aligned" in lib.rmx_strerror(rc)
+    assert lib.rmx_reindex(*args, ws.data_ptr(), wsb, None, stream) == _native.RMX_OK
+    torch.cuda.synchronize()
+    count, status = (int(x) for x in info.cpu())
+    assert status == 0 and 0 < count <= V
