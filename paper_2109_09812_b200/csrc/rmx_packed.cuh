@@ -1456,7 +1456,7 @@ struct UnpackPkArgs {
 };
 
 template <int D_CT>
-__global__ void __launch_bounds__(kBlock) k_unpack_pk(UnpackPkArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) k_unpack_pk(UnpackPkArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const int D = D_CT > 0 ? D_CT : a.dim;
