@@ -1244,8 +1244,20 @@ __device__ __forceinline__ void head_count_body(const HeadCountArgs& a) {
         const uint64_t base = static_cast<uint64_t>(t) * a.tile;
         const uint64_t end = min(base + a.tile, static_cast<uint64_t>(a.n));
         uint32_t cnt = 0;
+        uint64_t from = base;
+        if constexpr (KW == 1) {  // 4 keys per 16-byte load (tiles start at multiples of 4 rows)
+            const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+            const uint64_t end4 = end & ~static_cast<uint64_t>(3);
+#pragma unroll 2
+            for (uint64_t g = base + 4u * threadIdx.x; g < end4; g += 4u * kBlock) {
+                const uint4 w = __ldg(k4 + (g >> 2));
+                cnt += (g == 0 || w.x != __ldg(keys + g - 1)) ? 1u : 0u;
+                cnt += (w.y != w.x ? 1u : 0u) + (w.z != w.y ? 1u : 0u) + (w.w != w.z ? 1u : 0u);
+            }
+            from = max(end4, base);
+        }
 #pragma unroll 4
-        for (uint64_t g = base + threadIdx.x; g < end; g += kBlock)
+        for (uint64_t g = from + threadIdx.x; g < end; g += kBlock)
             cnt += (g == 0 || __ldg(keys + g) != __ldg(keys + g - 1)) ? 1u : 0u;
         cnt = warp_sum(cnt);
         if ((threadIdx.x & 31u) == 0u) s_red[threadIdx.x >> 5] = cnt;
