@@ -41,22 +41,48 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-CONFIGS = {  # name -> (kind, kind id, cells, dim, arity)
-    "C1": ("tri", 0, (625, 800, 0), 3, 3),
-    "C2": ("tri", 0, (5000, 5000, 0), 3, 3),
-    "C3": ("tet", 1, (150, 150, 148), 4, 4),
+CONFIGS = {  # name -> (kind, kind id, cells, dim, arity, scrambled coordinates)
+    "C1": ("tri", 0, (625, 800, 0), 3, 3, False),
+    "C2": ("tri", 0, (5000, 5000, 0), 3, 3, False),
+    "C2s": ("tri", 0, (5000, 5000, 0), 3, 3, True),
+    "C3": ("tet", 1, (150, 150, 148), 4, 4, False),
 }
 CONFIG_TEXT = {
     "C1": "1M-triangle float3 soup (3.15M verts, 5% unused)",
     "C2": "50M-triangle float3 soup on 1xB200 (157.5M verts, 5% unused)",
+    "C2s": "C2 with real-valued coordinates: the low 11 mantissa bits of every word scrambled "
+           "(oracle/lattice.py:scramble_words; 157.5M verts, > 64 varying key bits)",
     "C3": "20M-tet mesh, float3 position + float scalar payload (83.9M verts, D=4)",
 }
 METRIC = "input vertices re-indexed/sec (device-timed)"
-CPU_SAMPLE_ELEMS = 1_000_000       # C2 prefix sample for the CPU port: 3.15M vertex slots
+CPU_SAMPLE_ELEMS = 1_000_000       # C2 prefix sample for the GPU arm's cpu_baseline: 3.15M vertex slots
+L2_NOTE = "inputs >= 1.6 GB > 126 MB L2, no flush needed"
+
+
+def workload_config(cfg: str, world: int = 1) -> dict:
+    """The `config` of both arms' JSON lines (identical for the same workload)."""
+    from oracle import lattice
+    kind, _, cells, D, K, _ = CONFIGS[cfg]
+    sz = lattice.soup_sizes(kind, cells[:2] if kind == "tri" else cells)
+    return {"workload": f"{cfg}: {CONFIG_TEXT[cfg]}", "n_vertices": sz["n_vertices"], "n_elements": sz["n_elem"],
+            "arity": K, "dim": D, "unique": sz["n_points"],
+            "parallelism": "single" if world == 1 else f"replicas x{world}", "l2": L2_NOTE}
+
+
+def host_workload(cfg: str, n_elem_take=None):
+    """(vertices float32 (V, D), elements uint32 (E, K)) of a config, generated on the host."""
+    from oracle import lattice
+    kind, _, cells, _, _, scrambled = CONFIGS[cfg]
+    v, e = lattice.lattice_soup(kind, cells[:2] if kind == "tri" else cells, seed=0, n_elem_take=n_elem_take)
+    if scrambled:
+        v = lattice.scramble_words(v).view(np.float32)
+    return v, e
 
 
 def peaks():
@@ -134,13 +160,19 @@ def dist_env():
     return rank, world, local
 
 
+def host_cores_note():
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:  # noqa: BLE001
+        phys = None
+    return f"host: {os.cpu_count()} logical / {phys} physical cores"
+
+
 def cpu_port_rate(cfg: str, steps: int, warmup: int):
-    """Time the oracle port of the reference on a bounded prefix sample (host cores)."""
-    import numpy as np  # noqa: F401
-    from oracle import lattice, remesh_oracle as oracle
-    kind, _, cells, _, _ = CONFIGS[cfg]
-    cells = cells[:2] if kind == "tri" else cells
-    v, e = lattice.lattice_soup(kind, cells, seed=0, n_elem_take=CPU_SAMPLE_ELEMS)
+    """The GPU arm's cpu_baseline: the oracle port of the reference on a bounded prefix sample."""
+    from oracle import remesh_oracle as oracle
+    v, e = host_workload(cfg, CPU_SAMPLE_ELEMS)
     for _ in range(max(0, warmup)):
         oracle.reindex(v, e)
     times = []
@@ -151,29 +183,45 @@ def cpu_port_rate(cfg: str, steps: int, warmup: int):
     med = statistics.median(times)
     sample = (f"first {CPU_SAMPLE_ELEMS:,} elements of the {cfg} soup ({len(v):,} vertex slots); "
               f"median of {len(times)} after {warmup} warm-up; numpy port of remeshx.reindex "
-              f"(np.lexsort is single-threaded, the chunked steps use the reference pool)")
-    try:
-        import psutil
-        phys = psutil.cpu_count(logical=False)
-    except Exception:  # noqa: BLE001
-        phys = None
-    sample += f"; host: {os.cpu_count()} logical / {phys} physical cores"
+              f"(np.lexsort is single-threaded, the chunked steps use the reference pool); {host_cores_note()}")
     return len(v) / med, oracle.host_threads(), sample, med
 
 
 def run_reference(args):
+    """The reference arm: the reference algorithm (the numpy port of remeshx.reindex,
+    oracle/remesh_oracle.py -- same numpy kernels, checked against remeshx on the golden cases
+    and within 4 % of its time on C1) on the host cores, on the FULL workload of the GPU arm's
+    config.  BASELINE.md section 3 protocol for C2/C3: R = 1 timed run (one run is 1.5-3 min);
+    the warm-up runs the same code on a 1M-element prefix of the soup, untimed."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 5))
-    warm = min(args.warmup, 1)
-    rate, cores, sample, med = cpu_port_rate(args.config, steps, warm)
+    from oracle import remesh_oracle as oracle
+    t_gen = time.perf_counter()
+    v, e = host_workload(args.config)
+    t_gen = time.perf_counter() - t_gen
+    wv, we = host_workload(args.config, CPU_SAMPLE_ELEMS)
+    oracle.reindex(wv, we)
+    del wv, we
+    t = time.perf_counter()
+    res = oracle.reindex(v, e)
+    dt = time.perf_counter() - t
+    cfg = workload_config(args.config, world)
+    assert res["new_count"] == cfg["unique"], (res["new_count"], cfg["unique"])
+    rate = len(v) / dt
+    sample = (f"the full {args.config} workload ({len(v):,} vertex slots, {len(e):,} elements), 1 timed run "
+              f"(BASELINE.md section 3: R=1 for C2/C3) after 1 untimed warm-up on its first "
+              f"{CPU_SAMPLE_ELEMS:,} elements; numpy port of remeshx.reindex (np.lexsort is single-threaded, the "
+              f"chunked steps use the reference pool of {oracle.host_threads()} threads); {host_cores_note()}; "
+              f"input generated on the host in {t_gen:.0f} s (untimed)")
     line = {
-        "metric": METRIC, "value": rate, "unit": "verts/s", "n_gpus": world, "steps": steps, "warmup": warm,
-        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.config}: {CONFIG_TEXT[args.config]}", "sample": sample},
-        "cpu_baseline": {"value": rate, "unit": "verts/s", "cores": cores, "kind": "port", "sample": sample},
+        "metric": METRIC, "value": rate, "unit": "verts/s", "n_gpus": world, "steps": 1, "warmup": 0,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic", "impl": "reference", "config": cfg,
+        "requested": {"steps": args.steps, "warmup": args.warmup,
+                      "note": "one full-size CPU run takes minutes: R=1 as BASELINE.md section 3 specifies"},
+        "cpu_baseline": {"value": rate, "unit": "verts/s", "cores": oracle.host_threads(), "kind": "port",
+                         "sample": sample},
         "e2e": {"value": rate, "unit": "verts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -200,32 +248,38 @@ def executed_model(V, I, U, D, KW, npass, value_ranks=False):
                + 12 * I)                             # remap: indices + map in, indices out
 
 
-def run_b200(args):
-    import numpy as np
+def device_workload(cfg: str, dev, stream, rank: int = 0):
+    """(vtx int32 (V, D), idx int32 (E, K), expected unique count) generated on the device."""
     import torch
 
-    from paper_2109_09812_b200 import _native, build, pipeline
-
-    rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if not os.path.exists(_native.LIB_PATH):
-        build.build()
+    from paper_2109_09812_b200 import _native, gen
     lib = _native.lib()
-
-    kind, kid, cells, D, K = CONFIGS[args.config]
+    kind, kid, cells, D, K, scrambled = CONFIGS[cfg]
     E64, V64 = ctypes.c_uint64(), ctypes.c_uint64()
     lib.rmx_lattice_sizes(kid, cells[0], cells[1], cells[2], 1 << 63, ctypes.byref(E64), ctypes.byref(V64))
     E, V = E64.value, V64.value
-    stream = torch.cuda.Stream(dev)
     vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
     idx = torch.empty((E, K), dtype=torch.int32, device=dev)
     with torch.cuda.stream(stream):
         _native.check(lib.rmx_gen_lattice_soup(kid, cells[0], cells[1], cells[2], rank, 1 << 63, vtx.data_ptr(),
                                                idx.data_ptr(), stream.cuda_stream))
+        if scrambled:
+            vtx = gen.scramble_tensor(vtx)
+    stream.synchronize()
+    expect_u = (cells[0] + 1) * (cells[1] + 1) * ((cells[2] + 1) if kind == "tet" else 1)
+    return vtx, idx, expect_u
+
+
+def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, world: int = 1, clocks=None):
+    """Device time of `steps` back-to-back rmx_reindex calls on a config (inputs in HBM), the per-stage
+    times of a second region with stage events, and the dominant kernel's roofline."""
+    import torch
+
+    from paper_2109_09812_b200 import _native, pipeline
+    lib = _native.lib()
+    kind, _, cells, D, K, _ = CONFIGS[cfg]
+    vtx, idx, expect_u = device_workload(cfg, dev, stream, rank)
+    V, E = vtx.shape[0], idx.shape[0]
     out_v = torch.empty((V, D), dtype=torch.int32, device=dev)
     out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
     info = torch.zeros(2, dtype=torch.int64, device=dev)
@@ -236,12 +290,11 @@ def run_b200(args):
     def step(events=None):
         pipeline.launch(vtx, V, D, idx, E, K, out_v, out_e, info, ws, None, stream, events)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, warmup)):
         step()
     stream.synchronize()
     count, status = (int(x) for x in info.cpu())
-    expect_u = (cells[0] + 1) * (cells[1] + 1) * ((cells[2] + 1) if kind == "tet" else 1)
-    assert status == 0 and count == expect_u, (count, status, expect_u)
+    assert status == 0 and count == expect_u, (cfg, count, status, expect_u)
     pinfo = (ctypes.c_uint32 * 4)()
     _native.check(lib.rmx_plan_info(ws.data_ptr(), V, D, stream.cuda_stream, pinfo))
     packed, key_words, vbits, executed = (int(x) for x in pinfo)
@@ -250,7 +303,7 @@ def run_b200(args):
     field_mask, value_mask, bits_before_vr = int(kinfo[0]), int(kinfo[1]), int(kinfo[2])
 
     # per-stage CUDA events for every timed step (recorded on the launching stream)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
     with torch.cuda.stream(stream):
         for row in ev:
             for e_ in row:
@@ -258,6 +311,7 @@ def run_b200(args):
     stream.synchronize()
     handles = [[e_.cuda_event for e_ in row] for row in ev]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.rmx_kernel_launches_total()
 
     # timed region 1 (the headline): K plain steps.  Timed region 2: K steps with a CUDA event
     # between every stage, for the per-stage / per-pass times -- an event between two kernels
@@ -265,30 +319,26 @@ def run_b200(args):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with (clocks or _NullCtx()):
         t0.record(stream)
-        for k in range(args.steps):
+        for _ in range(steps):
             step()
         t1.record(stream)
         stream.synchronize()
-        torch.cuda.synchronize(dev)
-        ms = t0.elapsed_time(t1) / args.steps
-        t0.record(stream)
-        for k in range(args.steps):
-            step(handles[k])
-        t1.record(stream)
-        stream.synchronize()
     torch.cuda.synchronize(dev)
-    ms_staged = t0.elapsed_time(t1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = t0.elapsed_time(t1) / steps
+    launches = (lib.rmx_kernel_launches_total() - launches0) / steps
+    t0.record(stream)
+    for k in range(steps):
+        step(handles[k])
+    t1.record(stream)
+    stream.synchronize()
+    ms_staged = t0.elapsed_time(t1) / steps
     stage_ms = {}
     for k in range(1, n_ev):
-        vals = [ev[s][k - 1].elapsed_time(ev[s][k]) for s in range(args.steps)]
+        vals = [ev[s][k - 1].elapsed_time(ev[s][k]) for s in range(steps)]
         stage_ms[names[k]] = sum(vals) / len(vals)
-    # dominant kernel: one executed onesweep pass (packed-key or AoS rows)
+    # dominant kernel: one executed LSD pass (packed-key or AoS rows)
     pass_names = [n for n in names if n.startswith("pk_pass_" if packed else "sort_pass_")]
     active = sorted((stage_ms[n] for n in pass_names), reverse=True)[:executed]
     pass_ms = sum(active) / max(1, len(active))
@@ -304,16 +354,102 @@ def run_b200(args):
         pass_bytes = 2 * row_bytes * V
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
-    nominal = (32 * D * D + 44 * D + 15) * V + 16 * E * K + 4 * D * expect_u
-    compulsory = 4 * D * V + 8 * E * K + 4 * D * expect_u
     executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0)
                       if packed else None)
-    value = V * world / (ms * 1e-3)
+    res = {
+        "V": V, "E": E, "D": D, "K": K, "U": expect_u, "ms": ms, "ms_staged": ms_staged, "stage_ms": stage_ms,
+        "launches_per_step": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None,
+                     "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
+                                else "one onesweep LSD pass: k_sort_pass"),
+                     "key": (f"packed {vbits} key bits in {key_words} x u32 (field ranks on components "
+                             f"{mask_list(field_mask)}, value ranks on {mask_list(value_mask)}: "
+                             f"{bits_before_vr} bits before value ranks)" if packed
+                             else f"{D} x u32 words"),
+                     "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
+                     "executed_passes": executed, "nominal_passes": 4 * D},
+        "executed_bytes": executed_bytes,
+        "tensors": (vtx, idx),
+    }
+    del out_v, out_e, ws
+    return res
 
-    # end-to-end through the public host API (pinned host buffers, copies inside the timed region)
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def e2e_dropin(vtx, idx, steps: int):
+    """End to end through the reference-facing operator: paper_2109_09812_b200.reindex(Mesh) with
+    numpy (pageable) arrays in and out, every host<->device copy inside the timed region."""
+    import torch
+
+    import paper_2109_09812_b200 as rmx
+    mesh = rmx.Mesh(vtx.cpu().numpy().view(np.float32), idx.cpu().numpy().view(np.uint32))
+    torch.cuda.empty_cache()
+    out, _ = rmx.reindex(mesh)          # warm-up (allocations, staging buffers)
+    count = out.n_vertices
+    del out
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        out, _ = rmx.reindex(mesh)
+        times.append(time.perf_counter() - t)
+        assert out.n_vertices == count
+        del out
+    el = statistics.median(times)
+    V, D = mesh.vertices.shape
+    E, K = mesh.elements.shape
+    h2d = (V * D + E * K) * 4
+    d2h = 16 + (count * D + E * K) * 4
+    return el, h2d, d2h, times
+
+
+def run_b200(args):
+    import torch
+
+    from paper_2109_09812_b200 import _native, build, pipeline
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not os.path.exists(_native.LIB_PATH):
+        build.build()
+    lib = _native.lib()
+    stream = torch.cuda.Stream(dev)
+    clk = ClockSampler(local)
+    main = time_device(args.config, args.steps, args.warmup, dev, stream, rank, world, clocks=clk)
+    V, E, D, K, expect_u = main["V"], main["E"], main["D"], main["K"], main["U"]
+    ms = main["ms"]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    hbm, _ = peaks()
+    nominal = (32 * D * D + 44 * D + 15) * V + 16 * E * K + 4 * D * expect_u
+    compulsory = 4 * D * V + 8 * E * K + 4 * D * expect_u
+    executed_bytes = main["executed_bytes"]
+    value = V * world / (ms * 1e-3)
+    vtx, idx = main.pop("tensors")
+
+    # end to end (host buffers, copies inside the timed region): the drop-in operator
+    # reindex(Mesh) is the headline; the pipelined ReindexStream is reported beside it
     e2e = None
     if not args.no_e2e:
-        del out_v, out_e, ws
+        el, h2d, d2h, dropin_times = e2e_dropin(vtx, idx, max(3, min(args.steps, 5)))
+        e2e = {"value": V * world / el, "unit": "verts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": el * 1e3, "steps": len(dropin_times), "api": "paper_2109_09812_b200.reindex(Mesh)",
+               "note": "the reference-facing operator (pipeline.py:133): numpy float32/uint32 arrays in, a new "
+                       "Mesh of numpy arrays out; median of the timed calls after one warm-up call",
+               "times_ms": [t * 1e3 for t in dropin_times]}
         torch.cuda.empty_cache()
         host_v = torch.empty((V, D), dtype=torch.int32, pin_memory=True)
         host_e = torch.empty((E, K), dtype=torch.int32, pin_memory=True)
@@ -321,7 +457,7 @@ def run_b200(args):
         host_e.copy_(idx)
         del vtx, idx
         torch.cuda.empty_cache()
-        # single-call latency: copies in, pipeline, copies out, nothing overlapped
+        # single-call latency from pinned buffers: copies in, pipeline, copies out, nothing overlapped
         rx = pipeline.Reindexer(V, D, E, K, dev)
         for _ in range(2):
             rx.run(host_v, host_e)
@@ -348,14 +484,31 @@ def run_b200(args):
             tt = torch.tensor([el], device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             el = float(tt.item())
-        h2d, d2h = rs.bytes_per_mesh(V, E, rs.last_counts[-1])
-        e2e = {"value": V * world / el, "unit": "verts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": el * 1e3, "steps": e2e_steps, "api": "paper_2109_09812_b200.ReindexStream.run",
-               "note": "one mesh per step, host pinned -> host pinned; H2D of the next mesh and D2H of the "
-                       "previous one overlap this mesh's kernels (fill and drain inside the timed region)",
-               "single_call_ms": latency * 1e3, "single_call_api": "paper_2109_09812_b200.Reindexer.run"}
-        del rs
+        sh2d, sd2h = rs.bytes_per_mesh(V, E, rs.last_counts[-1])
+        e2e["stream"] = {"value": V * world / el, "unit": "verts/s", "h2d_bytes_per_step": sh2d,
+                         "d2h_bytes_per_step": sd2h, "ms_per_step": el * 1e3, "steps": e2e_steps,
+                         "api": "paper_2109_09812_b200.ReindexStream.run",
+                         "note": "one mesh per step, pinned host -> pinned host; H2D of the next mesh and D2H of "
+                                 "the previous one overlap this mesh's kernels (fill and drain inside the timed "
+                                 "region)",
+                         "single_call_ms": latency * 1e3, "single_call_api": "paper_2109_09812_b200.Reindexer.run"}
+        del rs, host_v, host_e
         torch.cuda.empty_cache()
+    else:
+        del vtx, idx
+        torch.cuda.empty_cache()
+
+    # the other single-GPU workloads, device-timed the same way (default run only)
+    extra = {}
+    if not args.no_extra and args.config == "C2":
+        for cfg in ("C2s", "C3"):
+            r = time_device(cfg, max(3, min(args.steps, 5)), 3, dev, stream, rank, world)
+            r.pop("tensors")
+            extra[cfg] = {"workload": CONFIG_TEXT[cfg], "value": r["V"] / (r["ms"] * 1e-3), "unit": "verts/s",
+                          "ms_per_step": r["ms"], "n_vertices": r["V"], "unique": r["U"],
+                          "roofline": r["roofline"], "stage_ms": {k: v for k, v in r["stage_ms"].items() if v > 0.02},
+                          "launches_per_step": r["launches_per_step"]}
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -363,34 +516,22 @@ def run_b200(args):
         cpu = {"value": rate, "unit": "verts/s", "cores": cores, "kind": "port", "sample": sample}
 
     if rank == 0:
-        traffic = None
+        roof = main["roofline"]
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             try:
                 with open(tp) as f:
                     tj = json.load(f)
-                traffic = tj.get(args.config, {}).get("pass_dram_bytes_per_launch")
+                roof["traffic"] = tj.get(args.config, {}).get("pass_dram_bytes_per_launch")
             except Exception:
-                traffic = None
+                pass
         line = {
             "metric": METRIC, "value": value, "unit": "verts/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {CONFIG_TEXT[args.config]}", "n_vertices": V,
-                       "n_elements": E, "arity": K, "dim": D, "unique": expect_u,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "inputs 2.5 GB > 126 MB L2, no flush needed"},
+            "config": workload_config(args.config, world),
             "e2e": e2e,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
-                                    else "one onesweep LSD pass: k_sort_pass"),
-                         "key": (f"packed {vbits} key bits in {key_words} x u32 (field ranks on components "
-                                 f"{mask_list(field_mask)}, value ranks on {mask_list(value_mask)}: "
-                                 f"{bits_before_vr} bits before value ranks)" if packed
-                                 else f"{D} x u32 words"),
-                         "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
-                         "executed_passes": executed, "nominal_passes": 4 * D},
+            "roofline": roof,
             "pipeline_roofline": {
                 "executed_bytes": executed_bytes,
                 "achieved_gbs": executed_bytes / (ms * 1e-3) / 1e9 if executed_bytes else None,
@@ -406,14 +547,15 @@ def run_b200(args):
                                    "write unique rows and indices once)",
                 "survey_note": "SURVEY 8(d) nominal model (32D^2+44D+15)V+16I+4DU counts 4D byte passes of 16 B "
                                "rows; the packed path executes fewer, narrower passes"},
-            "stage_ms": stage_ms,
-            "staged_ms_per_step": ms_staged,
+            "stage_ms": main["stage_ms"],
+            "staged_ms_per_step": main["ms_staged"],
             "stage_note": "stage_ms and the roofline's launch_ms come from a second timed region of the same K "
                           "steps with a CUDA event between stages (events end the programmatic-dependent-launch "
                           "overlap at those boundaries: staged_ms_per_step)",
+            "workloads": extra or None,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": lib.rmx_kernel_launches(D) * args.steps,
+            "gpu_launches": int(round(main["launches_per_step"] * args.steps)),
         }
         emit(line)
     if world > 1:
@@ -604,6 +746,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C2s / C3 device-timed workloads")
     ap.add_argument("--dist", action="store_true", help="use the multi-GPU path even at N=1 (testing)")
     args = ap.parse_args()
     if args.impl == "reference":

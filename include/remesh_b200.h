@@ -136,6 +136,10 @@ const char* rmx_stage_name(uint32_t dim, int k);
  * constant digits) are still launched and return at once. */
 int rmx_kernel_launches(uint32_t dim);
 
+/* Kernels the re-indexing pipeline has launched in this process so far (all
+ * calls, all threads): the difference around a region counts its launches. */
+unsigned long long rmx_kernel_launches_total(void);
+
 /* Sort plan of the last call that used `workspace` (host-side diagnostic; it
  * reads the device plan, so it synchronises `stream`).  Digit passes whose
  * 8-bit digit is constant over all keys are skipped; when at most 64 key bits

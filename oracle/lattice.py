@@ -226,6 +226,23 @@ def lattice_expected(kind: str, cells, seed: int = 0, n_elem_take: int | None = 
 
 
 # ---------------------------------------------------------------------------
+# C2s: the C2 soup with real-valued coordinates.  Every float word w keeps its
+# sign, exponent and high mantissa bits and gets its low ``bits`` mantissa bits
+# XOR-ed with a hash of the whole word:
+#     w' = w ^ ((w * 2654435761 mod 2^32) >> (32 - bits))
+# Equal words stay equal (duplicates still weld) but >= 23 bits vary per
+# component, like scanned geometry: the key no longer packs into 64 bits.
+SCRAMBLE_BITS = 11
+
+
+def scramble_words(words: np.ndarray, bits: int = SCRAMBLE_BITS) -> np.ndarray:
+    """The C2s transform on uint32 words (any shape); returns a new uint32 array."""
+    w = np.asarray(words).view(np.uint32).astype(np.uint64)
+    h = ((w * np.uint64(2654435761)) & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - bits)
+    return (w ^ h).astype(np.uint32)
+
+
+# ---------------------------------------------------------------------------
 # C4: welded (indexed) tiles for merge (BASELINE configs[3], SURVEY 8(d)):
 # tile k = the triangulated n x n quad grid whose lattice rows start at
 # ``row0`` (C4: n = 5000, row0 = 4500 k -> 500 shared rows between

@@ -15,12 +15,14 @@ import importlib
 _BINDINGS = ("remeshx", "remeshx.pipeline", "remeshx.ops", "remeshx.bench", "remeshx.testing", "remeshx.cli")
 
 
-def make_reindex(remeshx):
+def make_reindex(remeshx, on_call=None):
     """A ``remeshx.reindex``-compatible function backed by the CUDA library."""
     from . import mesh as _mesh
     from .pipeline import reindex as _b200_reindex
 
     def reindex(mesh):
+        if on_call is not None:
+            on_call()
         try:
             out, sc = _b200_reindex(mesh)
         except _mesh.InvalidMeshError as err:
@@ -35,10 +37,11 @@ def make_reindex(remeshx):
     return reindex
 
 
-def install_into_remeshx() -> list[str]:
-    """Rebind every ``reindex`` name in the imported remeshx modules; returns the patched modules."""
+def install_into_remeshx(on_call=None) -> list[str]:
+    """Rebind every ``reindex`` name in the imported remeshx modules; returns the patched modules.
+    ``on_call`` (optional) is called once per reindex call (instrumentation)."""
     remeshx = importlib.import_module("remeshx")
-    fn = make_reindex(remeshx)
+    fn = make_reindex(remeshx, on_call)
     patched = []
     for name in _BINDINGS:
         try:

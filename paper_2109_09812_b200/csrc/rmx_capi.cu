@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -241,8 +242,12 @@ struct PdlScope {
     ~PdlScope() { t_pdl = false; }
 };
 
+// kernels launched by this process through the pipeline (rmx_kernel_launches_total)
+std::atomic<unsigned long long> g_launches{0};
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -607,6 +612,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = ensure_smem(k_small, smem))) return rc;
         SmallArgs a{vtx, static_cast<uint32_t>(V), D, idx, I, out_vtx, out_idx,
                     reinterpret_cast<unsigned long long*>(d_count), d_status, sc ? *sc : rmx_scratch{}};
+        g_launches.fetch_add(1, std::memory_order_relaxed);
         k_small<<<1, kSmallThreads, smem, s>>>(a);
         RMX_CHECK(cudaGetLastError());
         while (rec.k < rec.n) {  // stage events of a profiled call: all at the end
@@ -954,6 +960,8 @@ int rmx_kernel_launches(uint32_t dim) {
     return 4 + aos + value_ranks + 1 + 3 * packed_passes_max(D) + 4 + 2;
 }
 
+unsigned long long rmx_kernel_launches_total(void) { return g_launches.load(std::memory_order_relaxed); }
+
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
@@ -1137,7 +1145,9 @@ int rmx_scatter_rows(const uint32_t* src, uint64_t n, uint32_t words, const uint
 size_t rmx_merge_workspace_bytes(uint64_t n_rows, uint32_t key_words) {
     const uint64_t W = static_cast<uint64_t>(key_words) + 1;
     const uint64_t tiles = (n_rows + kMergeTile - 1) / kMergeTile;
-    return static_cast<size_t>(2 * n_rows * W * 4 + 256 + tiles * 4 + 256 + (tiles + 1) * 8 + 256);
+    // two row buffers (+64 words of slack each), tile counts (+64), up to 8 bytes of alignment
+    // padding before the splits, the splits: the same layout rmx_merge_unique_runs carves
+    return static_cast<size_t>(2 * (n_rows * W + 64) * 4 + (tiles + 64) * 4 + 8 + (tiles + 1) * 8 + 256);
 }
 
 int rmx_merge_unique_runs(const uint32_t* keys, uint64_t n_rows, uint32_t key_words, const uint64_t* run_starts,

@@ -10,6 +10,15 @@ namespace rmx {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
+// The one dynamic shared-memory declaration of the library: every kernel takes
+// its dynamic shared memory from here (declarations with different alignments
+// of the same extern array in one translation unit are ill-formed).
+extern __shared__ __align__(128) unsigned char rmx_dyn_smem[];
+template <typename T>
+__device__ __forceinline__ T* dyn_smem() {
+    return reinterpret_cast<T*>(rmx_dyn_smem);
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kBlock) k_merge_path(const uint32_t* __restric
     constexpr uint32_t D = W - 1;
     constexpr uint32_t S = FROM_KEYS ? D : W;  // input row stride
     // input rows (A slice then B slice), then the merged rows, both padded
-    extern __shared__ __align__(16) uint32_t s_rows[];
+    uint32_t* s_rows = dyn_smem<uint32_t>();
     const uint32_t span = pad_row(kMergeTile, W) + 1;
     uint32_t* s_out = s_rows + span;
     const uint64_t n = na + nb;

@@ -533,7 +533,7 @@ template <int D_CT>
 __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     static_assert(D_CT >= 1 && D_CT <= kMaxRankDim, "value ranks cover D <= kMaxRankDim");
-    extern __shared__ __align__(16) uint8_t s_map[];  // [sum of 2^w over candidates]
+    uint8_t* s_map = dyn_smem<uint8_t>();  // [sum of 2^w over candidates]
     const uint32_t* pk = a.plan + pk_base(4 * D_CT);
     const uint32_t* vb = a.plan + pk_value_base(4 * D_CT);
     __shared__ uint32_t s_runs[4 * kMaxRuns];
@@ -555,12 +555,20 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
     load_packer<D_CT>(a.plan, a.fields, s_runs, s_rank);
     ValueMap<D_CT> vm;
     vm.load(a.plan);
-    uint32_t off[D_CT];
+    uint32_t off[D_CT], vmask[D_CT];
     uint32_t bytes = 0;
 #pragma unroll
     for (int c = 0; c < D_CT; ++c) {
         off[c] = bytes;
-        if ((cand >> c) & 1u) bytes += 1u << vm.w[c];
+        vmask[c] = 0u;
+        if ((cand >> c) & 1u) {
+            bytes += 1u << vm.w[c];
+            // a row outside the sample can pack to a wider value (a field above every sampled
+            // field ranks to the field count, which needs one more bit when that count is a power
+            // of two): such a row sets kVstateMiss and its sets are rebuilt, but its store must
+            // stay inside this component's map
+            vmask[c] = low_mask(vm.w[c]);
+        }
     }
     for (uint32_t i = threadIdx.x; i < bytes / 16u + 1u; i += kVsThreads)
         reinterpret_cast<uint4*>(s_map)[i] = make_uint4(0, 0, 0, 0);
@@ -591,7 +599,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
             }
         }
 #pragma unroll
-        for (int c = 0; c < D_CT; ++c) s_map[off[c] + pack.value(c, used ? k[c] : ref[c])] = 1u;
+        for (int c = 0; c < D_CT; ++c) s_map[off[c] + (pack.value(c, used ? k[c] : ref[c]) & vmask[c])] = 1u;
     };
     if (a.shift) {  // the even (parity 0) or odd (parity 1) sample blocks, 4 rows in flight per thread
         const uint64_t ns = sample_count(a.n, a.shift) / 2 + kSampleRun;
@@ -1206,7 +1214,7 @@ template <int IPT, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a, uint32_t tiles_per_cta) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !pk_pass_active(a)) return;
-    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* smem = dyn_smem<uint32_t>();
     const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
     for (uint32_t j = 0; j < tiles_per_cta; ++j) {
         const uint32_t tile = blockIdx.x * tiles_per_cta + j;
@@ -1445,7 +1453,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
     if (pk[0] == 0u) return;
-    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* smem = dyn_smem<uint32_t>();
     if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
     else unique_pk_body<1, IPT>(a, smem);
 }

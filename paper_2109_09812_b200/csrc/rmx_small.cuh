@@ -52,7 +52,7 @@ __device__ __forceinline__ bool small_less(const uint32_t* keys, uint32_t D, uin
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_small(SmallArgs a) {
-    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* smem = dyn_smem<uint32_t>();
     const uint32_t V = a.V, D = a.D;
     uint32_t* s_key = smem;                                       // [V * D]
     uint16_t* s_ord = reinterpret_cast<uint16_t*>(s_key + V * D); // [kSmallV] sorted position -> row

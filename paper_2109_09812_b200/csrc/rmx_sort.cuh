@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
     const int nshift = 8 * (nxt & 3);
     uint32_t* ctr = a.counters + a.pass;
 
-    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* smem = dyn_smem<uint32_t>();
     const size_t tw = static_cast<size_t>(TILE) * W;
     uint32_t* s_rows = smem;                          // [TILE * W]
     uint32_t* s_whist = smem + tw;                    // [warp][256] digit counters

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
     uint2* __restrict__ pairs = reinterpret_cast<uint2*>(a.plan[0] ? const_cast<uint32_t*>(a.rows0)
                                                                     : const_cast<uint32_t*>(a.rows1));
 
-    extern __shared__ __align__(128) uint32_t smem[];
+    uint32_t* smem = dyn_smem<uint32_t>();
     const size_t tw = static_cast<size_t>(TILE) * W;
     uint32_t* s_rows = smem;
     uint2* s_pairs = reinterpret_cast<uint2*>(smem + tw);     // tile pairs, bucket order

@@ -33,8 +33,17 @@ class _Stager:
         self.pool = ThreadPoolExecutor(self.threads, thread_name_prefix="rmx-stage")
         self.bufs = [torch.empty(chunk, dtype=torch.uint8, pin_memory=True) for _ in range(depth)]
         self.views = [b.numpy() for b in self.bufs]
-        self.events = [torch.cuda.Event() for _ in range(depth)]
+        self._events = {}  # device index -> one event per buffer (an event binds to its first device)
         self.lock = threading.Lock()
+
+    def events(self, stream: torch.cuda.Stream) -> list:
+        dev = stream.device.index
+        ev = self._events.get(dev)
+        if ev is None:
+            with torch.cuda.device(stream.device):
+                ev = [torch.cuda.Event() for _ in range(self.depth)]
+            self._events[dev] = ev
+        return ev
 
     def _pcopy(self, dst: np.ndarray, src: np.ndarray) -> None:
         """dst[:] = src with the worker threads (1-D uint8 views of equal length)."""
@@ -53,15 +62,16 @@ class _Stager:
         d = dst.view(-1).view(torch.uint8)
         n = s.shape[0]
         with self.lock, torch.cuda.stream(stream):
+            events = self.events(stream)
             used = [False] * self.depth
             for k, off in enumerate(range(0, n, self.chunk)):
                 i = k % self.depth
                 m = min(self.chunk, n - off)
                 if used[i]:
-                    self.events[i].synchronize()  # the copy engine is done with this buffer
+                    events[i].synchronize()  # the copy engine is done with this buffer
                 self._pcopy(self.views[i][:m], s[off:off + m])
                 d[off:off + m].copy_(self.bufs[i][:m], non_blocking=True)
-                self.events[i].record(stream)
+                events[i].record(stream)
                 used[i] = True
             stream.synchronize()  # the caller may free or reuse `src` right away
 
@@ -70,21 +80,22 @@ class _Stager:
         d = dst.reshape(-1).view(np.uint8)
         n = d.shape[0]
         with self.lock, torch.cuda.stream(stream):
+            events = self.events(stream)
             pending = []  # (buffer, offset, length) whose copy-in is in flight
             for k, off in enumerate(range(0, n, self.chunk)):
                 i = k % self.depth
                 m = min(self.chunk, n - off)
                 if len(pending) == self.depth:  # this buffer is next to drain: drain it first
-                    self._drain(pending.pop(0), d)
+                    self._drain(pending.pop(0), d, events)
                 self.bufs[i][:m].copy_(s[off:off + m], non_blocking=True)
-                self.events[i].record(stream)
+                events[i].record(stream)
                 pending.append((i, off, m))
             for item in pending:
-                self._drain(item, d)
+                self._drain(item, d, events)
 
-    def _drain(self, item, d: np.ndarray) -> None:
+    def _drain(self, item, d: np.ndarray, events: list) -> None:
         i, off, m = item
-        self.events[i].synchronize()
+        events[i].synchronize()
         self._pcopy(d[off:off + m], self.views[i][:m])
 
 

@@ -149,7 +149,7 @@ def subset_tensors(vertex_bits: torch.Tensor, elements: torch.Tensor, keep: torc
         if keep.dtype == torch.bool:
             if keep.shape != (E,):
                 raise MeshError(f"boolean selector has {tuple(keep.shape)} entries for {E} elements")
-            mask = keep.to(torch.uint8)
+            mask = keep.to(device=dev, dtype=torch.uint8)
         else:
             pos = keep.reshape(-1).to(device=dev, dtype=torch.int64)
             if pos.numel():
@@ -160,10 +160,11 @@ def subset_tensors(vertex_bits: torch.Tensor, elements: torch.Tensor, keep: torc
             mask = torch.zeros(E, dtype=torch.uint8, device=dev)
             mask[pos] = 1
         lib = _native.lib()
-        out = torch.empty_like(elements)
+        elements = elements.contiguous()
+        out = torch.empty((E, K), dtype=elements.dtype, device=dev)
         kept = torch.zeros(1, dtype=torch.int64, device=dev)
         ws = torch.empty(max(1, int(lib.rmx_select_workspace_bytes(E))), dtype=torch.uint8, device=dev)
-        _native.check(lib.rmx_select_elements(elements.contiguous().data_ptr() if E else None, E, K,
+        _native.check(lib.rmx_select_elements(elements.data_ptr() if E else None, E, K,
                                               mask.data_ptr() if E else None, out.data_ptr() if E else None,
                                               kept.data_ptr(), ws.data_ptr(), ws.numel(),
                                               torch.cuda.current_stream(dev).cuda_stream))

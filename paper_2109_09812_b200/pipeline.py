@@ -315,12 +315,38 @@ def reindex(mesh, device=None) -> tuple[Mesh, ReindexScratch]:
         info = torch.zeros(2, dtype=torch.int64, device=dev)
         ws = torch.empty(workspace_bytes(V, D, E, K), dtype=torch.uint8, device=dev)
         launch(vtx_d, V, D, idx_d, E, K, out_v, out_e, info, ws, None, stream)
-        count, status = (int(x) for x in info.cpu())
-        if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
-            raise InvalidMeshError(validate(_Arrays(vertices, elements)))
-        host_v = hostio.to_host(out_v[:count]).view(np.float32)
-        host_e = hostio.to_host(out_e).view(np.uint32)
+        del vtx_d, idx_d, ws
+        if _pinned_results():
+            # results land in pinned blocks of torch's caching host allocator (reused once the
+            # caller drops an earlier result): one DMA per array, no staging copy, no page faults
+            # in fresh numpy pages; the element copy starts before the count is known
+            host_info = torch.empty(2, dtype=torch.int64, pin_memory=True)
+            host_e_t = torch.empty((E, K), dtype=torch.int32, pin_memory=True)
+            host_info.copy_(info, non_blocking=True)
+            host_e_t.copy_(out_e, non_blocking=True)
+            stream.synchronize()
+            count, status = (int(x) for x in host_info)
+            if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+                raise InvalidMeshError(validate(_Arrays(vertices, elements)))
+            host_v_t = torch.empty((count, D), dtype=torch.int32, pin_memory=True)
+            if count:
+                host_v_t.copy_(out_v[:count], non_blocking=True)
+                stream.synchronize()
+            host_v = host_v_t.numpy().view(np.float32)
+            host_e = host_e_t.numpy().view(np.uint32)
+        else:
+            count, status = (int(x) for x in info.cpu())
+            if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+                raise InvalidMeshError(validate(_Arrays(vertices, elements)))
+            host_v = hostio.to_host(out_v[:count]).view(np.float32)
+            host_e = hostio.to_host(out_e).view(np.uint32)
     return Mesh._adopt(host_v, host_e), ReindexScratch(vertices, elements, count, dev)
+
+
+def _pinned_results() -> bool:
+    """RMX_PINNED_RESULTS=0: return results in ordinary pageable numpy arrays (staged copies)."""
+    import os
+    return os.environ.get("RMX_PINNED_RESULTS", "1") != "0"
 
 
 # Meshes up to this many input bytes take one staged round trip: one pinned

@@ -246,3 +246,30 @@ def test_sample_sees_no_used_row(rmx):
     check(rmx, words, idx)
     packed, kw, bits, passes = plan_info(rmx, words, idx)
     assert packed == 1 and passes == (bits + 7) // 8
+
+
+def test_outlier_field_in_the_last_full_width_candidate(rmx):
+    """ADVICE r1: three 16-bit candidates fill the value-set byte maps (3 x 2^16 = kValueSetBytes);
+    the last one's field is ranked among 4 sampled fields (2 bits).  Rows outside the sample carry a
+    field above every sampled one: under the guessed packing it ranks to 4 (3 bits), a value past
+    the component's map.  The value-set pass must keep the store inside the map (and flag the
+    miss); the result stays exact."""
+    V = 1 << 22
+    rng = np.random.default_rng(97)
+    fields = np.array([0x7F, 0x80, 0x81, 0x82], np.uint32)
+    words = np.empty((V, 3), np.uint32)
+    for c in range(3):
+        combos = np.stack([fields[rng.integers(0, 4, 300)],
+                           rng.integers(0, 1 << 14, 300).astype(np.uint32)], 1)
+        combos[:2] = [[0x7F, 0], [0x82, (1 << 14) - 1]]       # every field and mantissa bit varies
+        pick = combos[rng.integers(0, 300, size=V)]
+        words[:, c] = (pick[:, 0] << np.uint32(23)) | (pick[:, 1] << np.uint32(9))
+    out = np.flatnonzero(~_sample_mask(V))
+    far = out[rng.integers(0, len(out), size=50)]
+    words[far, 2] = (np.uint32(0x83) << np.uint32(23)) | (rng.integers(0, 1 << 14, 50).astype(np.uint32) << 9)
+    idx = np.arange(V, dtype=np.uint32).reshape(-1, 4)
+    check(rmx, words, idx)
+    guess = []
+    packed, kw, bits, passes = plan_info(rmx, words, idx, guess)
+    assert packed == 1 and passes == (bits + 7) // 8
+    assert guess[3] & 3 == 3  # checked, and rows outside the sample were found
