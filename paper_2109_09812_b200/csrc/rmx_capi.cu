@@ -82,7 +82,28 @@ int pk_sort_ipt() {
     }();
     return v;
 }
-int pk_sort_tile() { return kBlock * pk_sort_ipt(); }
+// RMX_DS=2 selects the slot-exchange downsweep (k_pk_downsweep2, rmx_packed.cuh) instead of the
+// staged one: measured on C2 within -2..+10 % of the staged kernel per pass (DESIGN.md (d)), kept
+// as the alternative.  RMX_DS2 = "<rows per thread>x<threads>x<CTAs per SM>" (default 16x256x3).
+// Both read per call (tests switch them); the workspace is sized for the smaller tile of the two.
+struct Ds2Cfg {
+    int ipt, nt, minb;
+};
+Ds2Cfg ds2_cfg() {
+    Ds2Cfg c{16, 256, 3};
+    const char* e = std::getenv("RMX_DS2");
+    if (e) {
+        int a = 0, b = 0, m = 0;
+        if (std::sscanf(e, "%dx%dx%d", &a, &b, &m) == 3) c = Ds2Cfg{a, b, m};
+    }
+    return c;
+}
+bool ds2_enabled() {
+    const char* e = std::getenv("RMX_DS");
+    return e && e[0] == '2';
+}
+int pk_sort_tile() { return ds2_enabled() ? ds2_cfg().ipt * ds2_cfg().nt : kBlock * pk_sort_ipt(); }
+constexpr int kMinPkSortTile = 256 * 12;  // the smallest packed sort tile of any configuration
 
 struct Layout {
     int D, W, P;
@@ -126,9 +147,10 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.map = take(static_cast<size_t>(V) * 4);
     L.plan = take(plan_words(L.P) * 4);
     L.pk_cstride = (L.ntiles_pk + kUpGroup - 1) / kUpGroup * kUpGroup;
-    L.pk_counts = take(static_cast<size_t>(L.pk_cstride) * 256 * 4);
+    const size_t max_tiles_pk = (V + kMinPkSortTile - 1) / kMinPkSortTile + kUpGroup;  // any tile choice
+    L.pk_counts = take(max_tiles_pk * 256 * 4);
     L.pk_totals = take(256 * 4);
-    L.pk_digits = take(static_cast<size_t>(V) + 16);
+    L.pk_digits = take(2 * (align_up(static_cast<size_t>(V) + 16)));  // two arrays: this pass's, the next's
     L.ukeys = take(static_cast<size_t>(V) * 8);
     const size_t vr_dim = L.D <= kMaxRankDim ? static_cast<size_t>(L.D) : 0;
     L.rank16 = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
@@ -149,7 +171,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     while (bits < 40 && (1ull << bits) < V) ++bits;
     L.bucket_shift = bits > 8 ? bits - 8 : 0;
     L.counters = take(static_cast<size_t>(L.P + 2 + kMaxPackedPasses + 1) * 4);
-    L.desc = take(static_cast<size_t>(L.ntiles > L.ntiles_pk ? L.ntiles : L.ntiles_pk) * 256 * 8);
+    L.desc = take(static_cast<size_t>(L.ntiles > max_tiles_pk ? L.ntiles : max_tiles_pk) * 256 * 8);
     L.desc3 = take(static_cast<size_t>(L.ntiles3) * 8);
     L.tile_counts = take(static_cast<size_t>(L.ntiles3_pk) * 4);
     L.ctl_end = off;
@@ -402,6 +424,16 @@ int pk_minb() {
     return v;
 }
 
+template <int IPT, int NT, int MINB>
+int launch_downsweep2(const SortPkArgs& a, cudaStream_t s) {
+    constexpr size_t smem = SortPk2Traits<2, IPT, NT>::smem_bytes();  // sized for u64 keys
+    int rc = ensure_smem(k_pk_downsweep2<IPT, NT, MINB>, smem);
+    if (rc) return rc;
+    RMX_CHECK(launch(k_pk_downsweep2<IPT, NT, MINB>, a.ntiles, NT, smem, s, a));
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
 int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = grid_for_stream(static_cast<uint64_t>((a.ntiles + kUpGroup - 1) / kUpGroup) * kBlock, grid);
@@ -410,6 +442,17 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     RMX_CHECK(cudaGetLastError());
     RMX_CHECK(launch(k_pk_colscan, 256, 1024, 0, s, a));
     RMX_CHECK(cudaGetLastError());
+    if (ds2_enabled()) {
+        const Ds2Cfg c = ds2_cfg();
+        switch (c.ipt * 10000 + c.nt * 10 + c.minb) {
+            case 240000 + 2562: return launch_downsweep2<24, 256, 2>(a, s);
+            case 160000 + 2563: return launch_downsweep2<16, 256, 3>(a, s);
+            case 120000 + 2564: return launch_downsweep2<12, 256, 4>(a, s);
+            case 80000 + 5123: return launch_downsweep2<8, 512, 3>(a, s);
+            case 160000 + 5122: return launch_downsweep2<16, 512, 2>(a, s);
+            default: return launch_downsweep2<12, 512, 2>(a, s);
+        }
+    }
     const int cfg = pk_sort_ipt() * 10 + pk_minb();
     switch (cfg) {
         case 123: return launch_downsweep<12, 3>(a, s);
@@ -769,9 +812,11 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
             continue;
         }
         if ((rc = cond_begin(gc, slot_pk_pass(L.P, p)))) return rc;
+        uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
+        const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
-                     reinterpret_cast<uint32_t*>(base + L.pk_totals), reinterpret_cast<uint8_t*>(base + L.pk_digits),
-                     d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride, L.D, p, rank_force()};
+                     reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,
+                     dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride, L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = cond_end(gc))) return rc;
         if ((rc = rec.mark())) return rc;

@@ -985,7 +985,9 @@ struct SortPkArgs {
     const uint32_t* plan;
     uint32_t* counts;      // [256][ntiles] per-tile digit counts -> exclusive column scans
     uint32_t* totals;      // [256] digit totals of this pass
-    uint8_t* digits;       // [n] this pass's digit per row (written by k_pack / the previous downsweep)
+    const uint8_t* digits; // [n] this pass's digit per row (written by k_pack / the previous downsweep)
+    uint8_t* digits_out;   // [n] the next pass's digit per row, at the row's output position (the other
+                           // of two arrays: a downsweep reads this pass's digits while it writes)
     const uint32_t* status;
     uint32_t n;
     uint32_t ntiles;
@@ -1202,7 +1204,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
             if (q < tile_n) {
                 out_k[dst[u]] = k[u];
                 out_v[dst[u]] = v[u];
-                if (emit_next) a.digits[dst[u]] = static_cast<uint8_t>(k[u] >> (shift + 8));
+                if (emit_next) a.digits_out[dst[u]] = static_cast<uint8_t>(k[u] >> (shift + 8));
             }
         }
     }
@@ -1222,6 +1224,254 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a, uin
         if (j) __syncthreads();  // the next tile's bulk copy overwrites the staging buffers
         if (wide) sort_pk_body<2, IPT>(a, smem, tile, j);
         else sort_pk_body<1, IPT>(a, smem, tile, j);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2' downsweep, slot-exchange version (k_pk_downsweep2, the default).  The
+// tile is staged by TMA bulk copies (u32 keys travel as interleaved (key,
+// origin) pairs between passes, so one 8-byte row per bulk byte range; the
+// first pass stages k_pack's keys, origins = row numbers; the last pass writes
+// keys and origins as separate arrays for K3'; u64 keys keep separate arrays).
+// Rows are ranked warp-striped (round r of warp w = row w*32*IPT + 32r + lane)
+// with the rank mode fixed at compile time, then each thread moves its rows
+// from their staged position to their tile slot IN PLACE (all rows read into
+// registers, a barrier, all rows stored at their slots) and the tile leaves in
+// slot order: per row one linear and one scattered 8-byte shared access, where
+// the staged version read keys and origins by a slot->row index (three
+// scattered accesses).  NT threads: 512-thread CTAs put 32 warps on an SM for
+// the latency-bound ranking chains at the 64 registers two such CTAs allow.
+template <int KW, int IPT, int NT>
+struct SortPk2Traits {
+    static constexpr int kTile = NT * IPT;
+    static constexpr int kNW = NT / 32;
+    // staged / exchanged rows (u32 key + origin pairs; u64 keys + origins), per-warp digit
+    // counters, digit destinations, scan scratch, barrier
+    static __host__ __device__ constexpr size_t smem_bytes() {
+        return static_cast<size_t>(kTile) * (KW == 1 ? 8 : 12) + (kNW * 256 + 256 + kNW + 8) * 4 + 16;
+    }
+};
+
+enum : int { kPkInKeys = 0, kPkInPairs = 1, kPkInSoa = 2 };  // pass input: k_pack keys | pairs | arrays
+enum : int { kPkOutPairs = 0, kPkOutSoa = 1 };                // pass output: pairs | arrays
+
+// warp_rank with the multi-split strategy fixed at compile time (no register
+// pressure from the strategies not taken)
+template <int IPT, bool PARTIAL, int MODE>
+__device__ __forceinline__ void warp_rank_ct(uint32_t (&pk)[IPT], uint32_t* wh) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t d = pk[r];
+        uint32_t peers;
+        if constexpr (MODE == kRankMatch) {
+            peers = __match_any_sync(kFull, d);
+        } else {
+            peers = kFull;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) bit_plane_and(peers, d, 1u << b);
+            if (PARTIAL) peers &= __ballot_sync(kFull, d < 256u);
+        }
+        const bool valid = !PARTIAL || d < 256u;
+        const uint32_t ds = hsw(d & 255u);
+        const uint32_t before = valid ? wh[ds] : 0u;
+        __syncwarp();
+        if (valid && (peers & lt) == 0u) wh[ds] = before + __popc(peers);
+        __syncwarp();
+        pk[r] = (ds << 16) | (before + __popc(peers & lt));
+    }
+}
+
+template <int KW, int IPT, int NT, int IN, int OUT, int MODE>
+__device__ __forceinline__ void sort_pk2_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile) {
+    using Key = typename PkKey<KW>::T;
+    using Tr = SortPk2Traits<KW, IPT, NT>;
+    constexpr int TILE = Tr::kTile, NW = Tr::kNW;
+    const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
+    uint32_t* ib = src ? a.buf1 : a.buf0;
+    uint32_t* ob = src ? a.buf0 : a.buf1;
+    const int shift = 8 * a.pass;
+    const bool emit_next = static_cast<uint32_t>(a.pass) + 1u < a.plan[pk_base(4 * a.dim) + 3];
+
+    // KW == 1: s_p[TILE] pairs (or s_k32[TILE] keys when staging k_pack's keys)
+    // KW == 2: s_k[TILE] keys, s_v[TILE] origins
+    uint2* s_p = reinterpret_cast<uint2*>(smem);
+    uint32_t* s_k32 = smem;
+    Key* s_k = reinterpret_cast<Key*>(smem);
+    uint32_t* s_v = smem + static_cast<size_t>(TILE) * 2;
+    uint32_t* s_wc = smem + static_cast<size_t>(TILE) * (KW == 1 ? 2 : 3);
+    uint32_t* s_gdst = s_wc + NW * 256;
+    uint32_t* s_warp = s_gdst + 256;
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_warp + NW + 6);  // 8-byte aligned (TILE even)
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t base = tile * static_cast<uint32_t>(TILE);
+    const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
+    const bool full = tile_n == static_cast<uint32_t>(TILE);
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+        if constexpr (KW == 1 && IN == kPkInPairs)
+            stage_tile(s_p, reinterpret_cast<const uint2*>(ib) + base, tile_n * 8u, s_bar);
+        else if constexpr (IN == kPkInKeys)
+            stage_tile(s_k, reinterpret_cast<const Key*>(ib) + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_bar);
+        else
+            stage_tile2(s_k, reinterpret_cast<const Key*>(ib) + base, tile_n * static_cast<uint32_t>(sizeof(Key)),
+                        s_v, ib + a.vals_off + base, tile_n * 4u, s_bar);
+    }
+    // this pass's digit of every row from the digit array (1 byte per row, written by k_pack / the
+    // previous pass at the row's position): coalesced loads in flight during the bulk copy, and no
+    // shared-memory read of the staged keys for ranking
+    uint32_t dg[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        dg[r] = (full || p < tile_n) ? static_cast<uint32_t>(__ldcs(a.digits + base + p)) : 0u;
+    }
+    // global row of this tile's digit-d run = (rows with smaller digits) + (digit-d rows of earlier tiles)
+    const uint32_t tot_d = tid < 256u ? a.totals[tid] : 0u;
+    uint32_t dummy;
+    const uint32_t excl_d = block_exclusive_scan<NW>(tot_d, s_warp, dummy);
+    const uint32_t run_base = tid < 256u ? excl_d + a.counts[static_cast<size_t>(tid) * a.cstride + tile] : 0u;
+    for (uint32_t i = tid; i < NW * 256u; i += NT) s_wc[i] = 0u;
+    __syncthreads();
+    mbar_wait(s_bar, 0u);
+
+    auto key_at = [&](uint32_t p) -> Key {
+        if constexpr (KW == 1 && IN == kPkInPairs) return s_p[p].x;
+        else if constexpr (KW == 1) return s_k32[p];
+        else return s_k[p];
+    };
+    uint32_t pk[IPT];
+    if (full) {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) pk[r] = dg[r];
+        warp_rank_ct<IPT, false, MODE>(pk, s_wc + warp * 256);
+    } else {
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            pk[r] = p < tile_n ? dg[r] : 256u;
+        }
+        warp_rank_ct<IPT, true, MODE>(pk, s_wc + warp * 256);
+    }
+    __syncthreads();
+    if (tid < 256u) {  // per digit: slot of every warp's first row, global destination of the tile's run
+        const uint32_t d = tid;
+        uint32_t wc[NW];
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            wc[w] = s_wc[w * 256 + hsw(d)];
+            cnt += wc[w];
+        }
+        uint32_t x = cnt;  // exclusive prefix over the digits: warp scan + the 8 warp totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+        }
+        if (lane == 31u) s_warp[warp] = x;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        uint32_t before = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) before += (static_cast<uint32_t>(w) < warp) ? s_warp[w] : 0u;
+        const uint32_t start = before + x - cnt;
+        uint32_t run = start;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            s_wc[w * 256 + hsw(d)] = run;
+            run += wc[w];
+        }
+        s_gdst[d] = run_base - start;  // mod 2^32; + tile slot gives the global row
+    }
+    __syncthreads();
+    // every row from its staged position to its tile slot, in place: all reads, a barrier, all writes
+    Key rk[IPT];
+    uint32_t rv[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        if (full || p < tile_n) {
+            pk[r] = s_wc[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu);
+            if constexpr (KW == 1 && IN == kPkInPairs) {
+                const uint2 x = s_p[p];
+                rk[r] = x.x;
+                rv[r] = x.y;
+            } else {
+                rk[r] = key_at(p);
+                if constexpr (IN == kPkInKeys) rv[r] = base + p;
+                else rv[r] = s_v[p];
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+        const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+        if (full || p < tile_n) {
+            if constexpr (KW == 1) {
+                s_p[pk[r]] = make_uint2(static_cast<uint32_t>(rk[r]), rv[r]);
+            } else {
+                s_k[pk[r]] = rk[r];
+                s_v[pk[r]] = rv[r];
+            }
+        }
+    }
+    __syncthreads();
+    // slot order out: consecutive slots of one digit are consecutive global rows
+#pragma unroll 4
+    for (uint32_t q = tid; q < tile_n; q += NT) {
+        Key key;
+        uint32_t val;
+        if constexpr (KW == 1) {
+            const uint2 x = s_p[q];
+            key = x.x;
+            val = x.y;
+        } else {
+            key = s_k[q];
+            val = s_v[q];
+        }
+        const uint32_t dst = s_gdst[static_cast<uint32_t>(key >> shift) & 255u] + q;
+        if constexpr (KW == 1 && OUT == kPkOutPairs) {
+            reinterpret_cast<uint2*>(ob)[dst] = make_uint2(static_cast<uint32_t>(key), val);
+        } else {
+            reinterpret_cast<Key*>(ob)[dst] = key;
+            ob[a.vals_off + dst] = val;
+        }
+        if (emit_next) a.digits_out[dst] = static_cast<uint8_t>(key >> (shift + 8));
+    }
+}
+
+template <int KW, int IPT, int NT, int IN, int OUT>
+__device__ __forceinline__ void sort_pk2_mode(const SortPkArgs& a, uint32_t* smem, uint32_t tile) {
+    // match when at most 16 digit bins are populated over the whole pass (cheap for low-entropy
+    // digits), ballots otherwise -- uniform per pass (the digit totals are global)
+    const uint32_t h = threadIdx.x < 256u ? a.totals[threadIdx.x] : 0u;
+    const int mode = choose_rank(h, a.rank_force == kRankAtomic ? kRankBallot : a.rank_force);
+    if (mode == kRankMatch) sort_pk2_body<KW, IPT, NT, IN, OUT, kRankMatch>(a, smem, tile);
+    else sort_pk2_body<KW, IPT, NT, IN, OUT, kRankBallot>(a, smem, tile);
+}
+
+template <int IPT, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_pk_downsweep2(SortPkArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*a.status || !pk_pass_active(a)) return;
+    const uint32_t tile = blockIdx.x;
+    if (tile >= a.ntiles) return;
+    uint32_t* smem = dyn_smem<uint32_t>();
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    const bool first = a.pass == 0, last = static_cast<uint32_t>(a.pass) + 1u == pk[3];
+    if (pk[1] == 2u) {  // u64 keys: separate key / origin arrays throughout
+        if (first) sort_pk2_mode<2, IPT, NT, kPkInKeys, kPkOutSoa>(a, smem, tile);
+        else sort_pk2_mode<2, IPT, NT, kPkInSoa, kPkOutSoa>(a, smem, tile);
+    } else if (first) {
+        if (last) sort_pk2_mode<1, IPT, NT, kPkInKeys, kPkOutSoa>(a, smem, tile);
+        else sort_pk2_mode<1, IPT, NT, kPkInKeys, kPkOutPairs>(a, smem, tile);
+    } else {
+        if (last) sort_pk2_mode<1, IPT, NT, kPkInPairs, kPkOutSoa>(a, smem, tile);
+        else sort_pk2_mode<1, IPT, NT, kPkInPairs, kPkOutPairs>(a, smem, tile);
     }
 }
 

@@ -319,8 +319,10 @@ def test_wide_dims_vs_oracle(rmx, D, pool, mesh_path):
         assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
 
 
-@pytest.mark.parametrize("env", [{"RMX_PDL": "0"}, {"RMX_VALUE_RANK": "0"}, {"RMX_PDL": "0", "RMX_VALUE_RANK": "0"}],
-                         ids=["no-pdl", "no-value-rank", "neither"])
+@pytest.mark.parametrize("env", [{"RMX_PDL": "0"}, {"RMX_VALUE_RANK": "0"}, {"RMX_PDL": "0", "RMX_VALUE_RANK": "0"},
+                                 {"RMX_DS": "2"}, {"RMX_DS": "2", "RMX_DS2": "24x256x2"},
+                                 {"RMX_DS": "2", "RMX_DS2": "12x256x4"}],
+                         ids=["no-pdl", "no-value-rank", "neither", "ds2", "ds2-24x256", "ds2-12x256"])
 def test_switches_keep_results(rmx, monkeypatch, env):
     """The A/B switches change speed, never results: golden cases through the
     large-mesh pipeline and a lattice soup with value ranks, each switch off."""
@@ -334,9 +336,19 @@ def test_switches_keep_results(rmx, monkeypatch, env):
         assert np.array_equal(np.asarray(sc.org_id), case["org_id"]), name
     v, e = lattice.lattice_soup("tri", (60, 70), seed=3)
     ref = O.reindex(v.view(np.uint32), e)
-    out, _ = rmx.reindex(rmx.Mesh(v, e))
+    out, sc = rmx.reindex(rmx.Mesh(v, e))
     assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
     assert np.array_equal(out.elements, ref["elements"])
+    assert np.array_equal(np.asarray(sc.org_id), ref["org_id"])
+    # u64 packed keys (> 32 varying bits, several partial tiles) through the same passes
+    rng = np.random.default_rng(5)
+    words = (rng.integers(0, 1 << 12, size=(50_000, 4)).astype(np.uint32) << np.uint32(9)) | np.uint32(0x3F800000)
+    idx = rng.integers(0, 50_000, size=(30_000, 3)).astype(np.uint32)
+    ref = O.reindex(words, idx)
+    out, sc = rmx.reindex(rmx.Mesh(words.view(np.float32), idx))
+    assert np.array_equal(out.vertices.view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(out.elements, ref["elements"])
+    assert np.array_equal(np.asarray(sc.org_id), ref["org_id"])
 
 
 def test_misaligned_workspace_is_einval(rmx):
