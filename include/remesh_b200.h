@@ -157,6 +157,12 @@ int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* 
  * (bit 0 checked, bit 1 a row fell outside the sample)}. */
 int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
+/* Hash mode of the last call that used `workspace` (keys wider than 64 bits, no
+ * scratch requested; synchronises `stream`): info[4] = {ran in hash mode,
+ * candidate rows (distinct keys per dedup tile), executed AoS passes over the
+ * candidates, rows per dedup tile}. */
+int rmx_hash_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
+
 /* Tuning diagnostic: look-back statistics {windows, spins, look-backs, 0} of
  * the AoS sort passes when built with -DRMX_PHASES (otherwise zeros; returns 0). */
 int rmx_debug_phase_cycles(unsigned long long* out, int n, int reset);

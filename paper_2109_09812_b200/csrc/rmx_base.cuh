@@ -25,7 +25,8 @@ constexpr int kWarps = kBlock / 32;
 // the (cleaned) vertex set, the varying bits are gathered into one u32/u64
 // key -- an order-preserving compaction, since the dropped bits are equal in
 // every row -- and the sort runs over (packed key, origin) pairs instead:
-//   [0] mode (1 = packed)        [1] key words KW (1 | 2)   [2] varying bits B
+//   [0] mode (0 = AoS rows, 1 = packed, 2 = hash: rmx_hash.cuh)
+//                                [1] key words KW (1 | 2)   [2] varying bits B
 //   [3] packed passes ceil(B/8)  [4] number of runs         [5..7] reserved
 //   [8 + 4r ..] run r: component, source bit, length, destination bit
 //   [8 + 4 kMaxRuns + c] field rank of component c: 0 = none, else
@@ -67,6 +68,13 @@ constexpr int kMinValueBits = 4;
 constexpr int kMaxValueBits = 16;
 constexpr int kValueWords = (1 << kMaxValueBits) / 32;
 constexpr uint32_t kValueSetBytes = 192 * 1024;  // k_valueset byte maps: sum of 2^w over the candidates
+// Hash mode (plan packed-section word 0 == 2, rmx_hash.cuh): keys wider than 64 bits are
+// deduplicated by a 32-bit hash first and only the distinct rows are sorted exactly.
+constexpr int kHashPasses = 2;       // hashed passes: the top 16 bits of the key hash
+constexpr int kHashTileRows = 8;     // rows per thread in the hash tile kernels
+constexpr int kHashTile = kBlock * kHashTileRows;
+constexpr int kHashMaxDim = 8;       // wider rows take the AoS path
+
 __host__ __device__ inline size_t pk_value_base(int P) { return pk_rank_base(P) + RMX_MAX_DIM; }
 __host__ __device__ inline size_t plan_words(int P) { return pk_value_base(P) + 4 + 4 * kMaxRankDim; }
 

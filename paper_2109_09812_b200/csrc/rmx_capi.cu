@@ -109,7 +109,7 @@ struct Layout {
     int D, W, P;
     uint32_t ntiles, ntiles3;
     size_t flags, rows0, rows1, map, plan;
-    size_t ctl_begin, markbits, hist, vary, fields, fill, counters, desc, desc3, ctl_end;
+    size_t ctl_begin, markbits, hist, vary, fields, fill, fill2, counters, desc, desc3, ctl_end;
     int bucket_shift;
     uint32_t ntiles_pk, ntiles3_pk, pk_cstride;
     size_t vals_off;  // words: origins of the packed-key path inside a row buffer
@@ -121,6 +121,10 @@ struct Layout {
     size_t gplan, svary, sfields; // the plan guessed from a sample of the rows, and its inputs
     size_t vsets_b;               // value sets of the odd sample blocks (saturation estimate)
     size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
+    size_t rank_of;               // hash mode: new index of every candidate row
+    size_t n_cand;                // hash mode: number of candidate rows
+    size_t hhist, hcounters;      // hash mode: histograms and tile counters of the hashed passes
+    uint32_t ntiles_hash;
     size_t total;
 };
 
@@ -151,7 +155,10 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.pk_counts = take(max_tiles_pk * 256 * 4);
     L.pk_totals = take(256 * 4);
     L.pk_digits = take(2 * (align_up(static_cast<size_t>(V) + 16)));  // two arrays: this pass's, the next's
-    L.ukeys = take(static_cast<size_t>(V) * 8);
+    L.ukeys = take(static_cast<size_t>(V) * 8);  // packed: unique keys; hash: (group, origin) per row
+    L.ntiles_hash = static_cast<uint32_t>((V + kHashTile - 1) / kHashTile);
+    const bool hash = L.D >= 3 && L.D <= kHashMaxDim;
+    L.rank_of = take(hash ? static_cast<size_t>(V) * 4 : 0);
     const size_t vr_dim = L.D <= kMaxRankDim ? static_cast<size_t>(L.D) : 0;
     L.rank16 = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
     L.vinv = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
@@ -161,12 +168,16 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.vsets_b = take(vr_dim * kValueWords * 4);
     L.svary = take(vr_dim * 4);
     L.vstate = take(16);
+    L.n_cand = take(16);
+    L.hhist = take(kHashPasses * 256 * 4);
+    L.hcounters = take(kHashPasses * 4 + 16);
     L.sfields = take(vr_dim * kFieldWords * 4);
     L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
     L.vary = take(static_cast<size_t>(L.D) * 4);
     L.fields = take(static_cast<size_t>(L.D) * kFieldWords * 4);
     L.fill = take(256 * 4);
+    L.fill2 = take(256 * 4);
     int bits = 0;
     while (bits < 40 && (1ull << bits) < V) ++bits;
     L.bucket_shift = bits > 8 ? bits - 8 : 0;
@@ -561,53 +572,81 @@ bool small_path(uint64_t V, uint32_t D, uint64_t I) {
 }
 
 // ---- graph launch path ------------------------------------------------------
-// run_pipeline emits its launches onto a capturing stream; each section that
-// may be a no-op for the data at hand (AoS vs packed, each sort pass) becomes
-// the body of an IF conditional node whose value k_plan sets on the device.
+// rmx_graph_create captures run_pipeline on a capturing stream (plain capture: every kernel
+// checks the device plan and exits when its section does not apply; the programmatic launch
+// dependencies become graph edges).
 constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
 
-struct GraphCtx {
-    cudaGraph_t g = nullptr;
-    cudaStream_t s = nullptr;
-    GraphHandles gh{};
-    cudaGraphNode_t cond = nullptr;
-};
+// hash mode (rmx_hash.cuh) for keys wider than 64 bits: D in [3, kHashMaxDim]; RMX_HASH=0 turns it
+// off (read per call: tests switch it at run time)
+bool hash_possible(int D) { return D >= 3 && D <= kHashMaxDim; }
+bool hash_enabled() {
+    const char* e = std::getenv("RMX_HASH");
+    return !(e && e[0] == '0');
+}
 
-// Close the current capture segment and open the body of IF(slot).
-int cond_begin(GraphCtx* gc, int slot) {
-    if (!gc) return RMX_OK;
-    cudaStreamCaptureStatus st;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t nd = 0;
-    RMX_CHECK(cudaStreamGetCaptureInfo(gc->s, &st, nullptr, nullptr, &deps, &nd));
-    cudaGraphNode_t dv[16];
-    if (nd > 16) return RMX_ECUDA;
-    for (size_t i = 0; i < nd; ++i) dv[i] = deps[i];
-    cudaGraph_t g = nullptr;
-    RMX_CHECK(cudaStreamEndCapture(gc->s, &g));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = gc->gh.h[slot];
-    cp.conditional.type = cudaGraphCondTypeIf;
-    cp.conditional.size = 1;
-    RMX_CHECK(cudaGraphAddNode(&gc->cond, gc->g, dv, nd, &cp));
-    RMX_CHECK(cudaStreamBeginCaptureToGraph(gc->s, cp.conditional.phGraph_out[0], nullptr, nullptr, 0, kCaptureMode));
+template <int D_CT>
+int launch_hash_build_d(const HashArgs& a, cudaStream_t s) {
+    int grid = 0;
+    int rc = persistent_grid(k_hash_build<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
+    if (rc) return rc;
+    RMX_CHECK(launch(k_hash_build<D_CT>, grid, kBlock, 0, s, a));
+    RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
 
-// Close the IF body and continue the main graph after the conditional node.
-int cond_end(GraphCtx* gc) {
-    if (!gc) return RMX_OK;
-    cudaGraph_t body = nullptr;
-    RMX_CHECK(cudaStreamEndCapture(gc->s, &body));
-    RMX_CHECK(cudaStreamBeginCaptureToGraph(gc->s, gc->g, &gc->cond, nullptr, 1, kCaptureMode));
+int dispatch_hash_build(const HashArgs& a, cudaStream_t s) {
+    switch (a.dim) {
+        case 3: return launch_hash_build_d<3>(a, s);
+        case 4: return launch_hash_build_d<4>(a, s);
+        default: return launch_hash_build_d<0>(a, s);
+    }
+}
+
+template <int W_CT, int IPT>
+int launch_hashed_pass(const SortArgs& a, cudaStream_t s) {
+    auto kern = k_sort_pass<W_CT, IPT, true>;
+    const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
+    int grid = 0;
+    int rc = persistent_grid(kern, smem, a.ntiles, grid);
+    if (rc) return rc;
+    RMX_CHECK(launch(kern, grid, kBlock, smem, s, a));
+    RMX_CHECK(cudaGetLastError());
     return RMX_OK;
+}
+
+template <int D_CT>
+int launch_hash_dedup_d(const HashArgs& a, cudaStream_t s) {
+    const size_t smem = hash_dedup_smem(a.dim);
+    int rc = ensure_smem(k_hash_dedup<D_CT>, smem);
+    if (rc) return rc;
+    RMX_CHECK(launch(k_hash_dedup<D_CT>, a.ntiles, kBlock, smem, s, a));
+    RMX_CHECK(cudaGetLastError());
+    return RMX_OK;
+}
+
+// the two hashed passes (rows0 -> rows1 -> rows0) and the per-tile dedup
+int launch_hash_groups(const HashArgs& ha, SortArgs sa, cudaStream_t s) {
+    int rc = RMX_OK;
+    for (int hp = 0; hp < kHashPasses && rc == RMX_OK; ++hp) {
+        sa.pass = hp;
+        switch (ha.dim) {
+            case 3: rc = launch_hashed_pass<4, SortIpt<4>::v>(sa, s); break;
+            case 4: rc = launch_hashed_pass<5, SortIpt<5>::v>(sa, s); break;
+            default: rc = launch_hashed_pass<0, SortIpt<0>::v>(sa, s); break;
+        }
+    }
+    if (rc) return rc;
+    switch (ha.dim) {
+        case 3: return launch_hash_dedup_d<3>(ha, s);
+        case 4: return launch_hash_dedup_d<4>(ha, s);
+        default: return launch_hash_dedup_d<0>(ha, s);
+    }
 }
 
 int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* idx, uint64_t E, uint32_t K,
                  uint32_t* out_vtx, uint32_t* out_idx, uint64_t* d_count, uint32_t* d_status, void* ws,
-                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events,
-                 GraphCtx* gc = nullptr) {
+                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events) {
     g_err[0] = '\0';
     if (D < 1 || K < 1) {
         std::snprintf(g_err, sizeof(g_err), "dim and arity must be >= 1 (got %u, %u)", D, K);
@@ -644,7 +683,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         std::snprintf(g_err, sizeof(g_err), "workspace must be %zu-byte aligned", kAlign);
         return RMX_EINVAL;
     }
-    const PdlScope pdl(gc == nullptr && pdl_enabled());
+    const PdlScope pdl(pdl_enabled());
     const Layout L = make_layout(V, D);
     if (!ws || ws_bytes < L.total) {
         std::snprintf(g_err, sizeof(g_err), "workspace %zu bytes < required %zu", ws_bytes, L.total);
@@ -699,7 +738,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (V == 0) {  // every index is out of range; status is set
         return RMX_OK;
     }
-    // K1a varying bits of the cleaned vertex set, then the plan (packed or AoS)
+    // K1a varying bits of the cleaned vertex set, then the plan (packed, hash or AoS)
     const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
     const bool value_ranks = L.D <= kMaxRankDim && value_rank_enabled() && V >= value_rank_min_rows();
     uint32_t* gplan = reinterpret_cast<uint32_t*>(base + L.gplan);
@@ -717,7 +756,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         VaryArgs sa{vtx, flags, idx, svary, sfields, d_status, static_cast<uint32_t>(V), L.D, vec, shift,
                     nullptr, nullptr, nullptr};
         if ((rc = dispatch_vary(sa, s))) return rc;
-        RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, GraphHandles{}));
+        RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, 0));
         uint32_t* vsets_b = reinterpret_cast<uint32_t*>(base + L.vsets_b);
         ValueSetArgs va{vtx, flags, idx, gplan, sfields, vsets, svary, vstate, d_status, static_cast<uint32_t>(V),
                         shift, vec, 0, gplan, 0};
@@ -746,42 +785,22 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, gc ? gc->gh : GraphHandles{}));
+    // hash mode (rmx_hash.cuh) replaces the whole-set AoS sort unless the caller wants the scratch
+    // arrays of the stable sort (org_id, perm: only the AoS path produces them) or RMX_HASH=0
+    const bool hash_ok = hash_possible(L.D) && sc == nullptr && hash_enabled();
+    RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0));
     RMX_CHECK(cudaGetLastError());
     if ((rc = rec.mark())) return rc;
-    // ---- AoS path (kernels exit at once in packed mode).  With D <= 2 at most 64 bits vary, which
-    // the packed key always holds (plan_body: every run is >= 1 bit, so <= 64 runs), and direct
-    // launches skip the AoS kernels (their stage events are still recorded); a captured graph keeps
-    // every section so that each conditional handle has its node.
-    const bool aos = aos_possible(L.D) || gc != nullptr;
-    if ((rc = cond_begin(gc, kSlotAosA))) return rc;
+    // ---- AoS rows of the whole vertex set (AoS mode only).  With D <= 2 at most 64 bits vary,
+    // which the packed key always holds (plan_body: every run is >= 1 bit, so <= 64 runs): no AoS
+    // kernels then (their stage events are still recorded).
+    const bool aos = aos_possible(L.D);
     if (aos) {
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    if (aos) {
-        HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D};
-        int grid = 0;
-        rc = grid_for_stream(V, grid);
-        if (rc) return rc;
-        RMX_CHECK(launch(k_first_hist, grid, kBlock, 0, s, a));
-        RMX_CHECK(cudaGetLastError());
-    }
-    if ((rc = cond_end(gc))) return rc;
-    if ((rc = rec.mark())) return rc;
-    for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
-        if ((rc = cond_begin(gc, kSlotAosPass + p))) return rc;
-        if (aos) {
-            SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
-                       p, rank_force()};
-            if ((rc = dispatch_pass(a, s))) return rc;
-        }
-        if ((rc = cond_end(gc))) return rc;
-        if ((rc = rec.mark())) return rc;
-    }
-    // ---- packed-key path (kernels exit at once in AoS mode)
-    if ((rc = cond_begin(gc, kSlotPkA))) return rc;
+    // ---- packed keys (packed mode) or hashes (hash mode)
     uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
     uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
     if (value_ranks) {  // rank tables and the new key layout (exact plan, value sets of the full pass)
@@ -799,41 +818,68 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
         RMX_CHECK(cudaGetLastError());
     }
+    uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
+    const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
     {
-        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, reinterpret_cast<uint8_t*>(base + L.pk_digits), fields,
-                   rank16, d_status, static_cast<uint32_t>(V), L.D, vec};
+        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
+                   L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
-    if ((rc = cond_end(gc))) return rc;
+    HashArgs ha{vtx, flags, idx, plan, rows0, rows1, reinterpret_cast<uint32_t*>(base + L.hhist),
+                reinterpret_cast<uint2*>(base + L.ukeys), reinterpret_cast<uint32_t*>(base + L.n_cand), hist,
+                reinterpret_cast<const uint32_t*>(base + L.rank_of), d_status, static_cast<uint32_t>(V),
+                L.ntiles_hash, L.D, vec};
+    if (hash_ok && (rc = dispatch_hash_build(ha, s))) return rc;
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
-        if (!gc && p >= packed_passes_max(L.D)) {  // a packed key of D = 1 words has at most 4 digits
+        if (p >= packed_passes_max(L.D)) {  // a packed key of D = 1 words has at most 4 digits
             if ((rc = rec.mark())) return rc;
             continue;
         }
-        if ((rc = cond_begin(gc, slot_pk_pass(L.P, p)))) return rc;
-        uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
-        const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,
-                     dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride, L.D, p, rank_force()};
+                     dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride,
+                     L.D, p, rank_force()};
         if ((rc = launch_sort_pk(a, s))) return rc;
-        if ((rc = cond_end(gc))) return rc;
         if ((rc = rec.mark())) return rc;
     }
-    // ---- K3 unique + bucketed pairs (one of the two runs), K3b map fill
+    // ---- hash mode: candidate groups of the hash-sorted rows, one AoS row per group
+    if (hash_ok) {
+        SortArgs hs{rows0, rows1, plan, reinterpret_cast<uint32_t*>(base + L.hhist), desc,
+                    reinterpret_cast<uint32_t*>(base + L.hcounters), d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
+                    0, rank_force(), nullptr};
+        if ((rc = launch_hash_groups(ha, hs, s))) return rc;
+    }
+    if ((rc = rec.mark())) return rc;
+    // ---- exact AoS sort: the whole vertex set (AoS mode) or the candidate rows (hash mode)
+    const uint32_t* n_cand = reinterpret_cast<const uint32_t*>(base + L.n_cand);
+    if (aos) {
+        HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, n_cand};
+        int grid = 0;
+        rc = grid_for_stream(V, grid);
+        if (rc) return rc;
+        RMX_CHECK(launch(k_first_hist, grid, kBlock, 0, s, a));
+        RMX_CHECK(cudaGetLastError());
+    }
+    if ((rc = rec.mark())) return rc;
+    for (int p = 0; p < L.P; ++p) {  // K2 onesweep passes, least significant digit first
+        if (aos) {
+            SortArgs a{rows0, rows1, plan, hist, desc, counters, d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
+                       p, rank_force(), n_cand};
+            if ((rc = dispatch_pass(a, s))) return rc;
+        }
+        if ((rc = rec.mark())) return rc;
+    }
+    // ---- K3 unique + bucketed pairs (AoS / hash, or packed), K3b map fill
     uint32_t* fill = reinterpret_cast<uint32_t*>(base + L.fill);
-    if ((rc = cond_begin(gc, kSlotAosB))) return rc;
     if (aos) {
         UniqueArgs a{rows0, rows1, plan, desc3, counters + L.P, fill, d_status,
                      out_vtx, reinterpret_cast<unsigned long long*>(d_count),
                      sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
-                     sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D, L.bucket_shift};
+                     sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3, L.D, L.bucket_shift, n_cand};
         if ((rc = dispatch_unique(a, s))) return rc;
     }
-    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
-    if ((rc = cond_begin(gc, kSlotPkB))) return rc;
     {
         uint32_t* counts = reinterpret_cast<uint32_t*>(base + L.tile_counts);
         HeadCountArgs h{rows0, rows1, plan, counts, d_status, static_cast<uint32_t>(V), L.ntiles3_pk,
@@ -854,14 +900,28 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        reinterpret_cast<unsigned long long*>(d_count), d_status, L.D, aligned16(out_vtx) ? 1 : 0};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
-    if ((rc = cond_end(gc))) return rc;
     if ((rc = rec.mark())) return rc;
     {
         const uint64_t threads = (V + 1) / 2;
-        RMX_CHECK(launch(k_map_fill, static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s, plan, rows0, rows1, map,
-                                                                                          static_cast<uint32_t>(V),
-                                                                                          d_status));
+        const unsigned grid = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
+        RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
+                         static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1), map,
+                         static_cast<uint32_t>(V), static_cast<const uint32_t*>(d_status), L.D, 0, n_cand));
         RMX_CHECK(cudaGetLastError());
+        if (hash_ok) {  // rank_of[group] from the candidates' pairs, then map[origin]
+            RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
+                             static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1),
+                             reinterpret_cast<uint32_t*>(base + L.rank_of), static_cast<uint32_t>(V),
+                             static_cast<const uint32_t*>(d_status), L.D, 2, n_cand));
+            RMX_CHECK(cudaGetLastError());
+            RMX_CHECK(launch(k_hash_pairs, L.ntiles_hash, kBlock, 0, s, ha,
+                             reinterpret_cast<uint32_t*>(base + L.fill2), L.bucket_shift));
+            RMX_CHECK(cudaGetLastError());
+            RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
+                             static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1), map,
+                             static_cast<uint32_t>(V), static_cast<const uint32_t*>(d_status), L.D, 3, n_cand));
+            RMX_CHECK(cudaGetLastError());
+        }
     }
     if ((rc = rec.mark())) return rc;
     // K4 remap
@@ -932,48 +992,30 @@ int rmx_graph_create(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim
         std::snprintf(g_err, sizeof(g_err), "dim %u outside [1, %d]", dim, RMX_MAX_DIM);
         return RMX_EINVAL;
     }
-    GraphCtx gc;
-    RMX_CHECK(cudaStreamCreateWithFlags(&gc.s, cudaStreamNonBlocking));
+    cudaStream_t cs = nullptr;
+    cudaGraph_t cg = nullptr;
+    RMX_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     int rc = RMX_OK;
-    if (cudaGraphCreate(&gc.g, 0) != cudaSuccess) rc = RMX_ECUDA;
-    const int P = 4 * static_cast<int>(dim);
-    // Default: no conditional nodes (every kernel skips itself when its section does not apply)
-    // and launches captured with programmatic dependencies, as the direct path runs them --
-    // measured faster than IF nodes around the sections (C1 0.36 vs 0.52 ms, grid_quads(64) 0.10
-    // vs 0.22 ms).  RMX_GRAPH_COND=1 keeps the device-set IF nodes (k_plan sets them); the one-CTA
-    // small-mesh path and the zero-element case have no sections either way.
-    const char* ce = std::getenv("RMX_GRAPH_COND");
-    const bool no_cond = !(ce && ce[0] == '1');
-    const bool plain = no_cond || n_elements == 0 || small_path(n_vertices, dim, n_elements * arity);
-    gc.gh.n = plain ? 0 : kSlotAosPass + P + kMaxPackedPasses;
-    for (int i = 0; i < gc.gh.n && rc == RMX_OK; ++i)
-        if (cudaGraphConditionalHandleCreate(&gc.gh.h[i], gc.g, 0, cudaGraphCondAssignDefault) != cudaSuccess)
-            rc = RMX_ECUDA;
     bool capturing = false;
-    if (rc == RMX_OK) {
-        if (cudaStreamBeginCaptureToGraph(gc.s, gc.g, nullptr, nullptr, 0, kCaptureMode) == cudaSuccess) {
-            capturing = true;
-            rc = run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
-                              d_status, workspace, workspace_bytes, scratch, gc.s, nullptr, 0, no_cond ? nullptr : &gc);
-        } else {
-            rc = RMX_ECUDA;
-        }
+    if (cudaStreamBeginCapture(cs, kCaptureMode) == cudaSuccess) {
+        capturing = true;
+        rc = run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
+                          d_status, workspace, workspace_bytes, scratch, cs, nullptr, 0);
+    } else {
+        rc = RMX_ECUDA;
     }
-    if (capturing) {
-        cudaGraph_t g = nullptr;
-        if (cudaStreamEndCapture(gc.s, &g) != cudaSuccess && rc == RMX_OK) rc = RMX_ECUDA;
-    }
+    if (capturing && cudaStreamEndCapture(cs, &cg) != cudaSuccess && rc == RMX_OK) rc = RMX_ECUDA;
     cudaGraphExec_t exec = nullptr;
     if (rc == RMX_OK) {
-        const cudaError_t e = cudaGraphInstantiate(&exec, gc.g, 0);
+        const cudaError_t e = cudaGraphInstantiate(&exec, cg, 0);
         if (e != cudaSuccess) {
             std::snprintf(g_err, sizeof(g_err), "graph instantiate: %s", cudaGetErrorString(e));
             rc = RMX_ECUDA;
         }
     }
     (void)cudaGetLastError();
-    if (gc.g) cudaGraphDestroy(gc.g);
-    cudaStreamDestroy(gc.s);
+    if (cg) cudaGraphDestroy(cg);
+    cudaStreamDestroy(cs);
     if (rc != RMX_OK) return rc;
     *out = new rmx_graph{exec};
     return RMX_OK;
@@ -992,41 +1034,44 @@ void rmx_graph_destroy(rmx_graph* graph) {
 }
 
 int rmx_kernel_launches(uint32_t dim) {
-    // mark + expand, vary, plan, build_rows, first_hist, 4*dim AoS passes,
+    // mark + expand, vary, plan, [D >= 3: build_rows], pack,
     // [dim <= kMaxRankDim, meshes of >= 2^25 rows (value_rank_min_rows): K1a over a sample, guessed plan,
-    //  value-set sample x 2,
-    //  value plan, value sets + K1a check in one pass, value plan, K1a copy / fallback, second-chance reset +
-    //  value sets (exit unless a row fell outside the sample), value plan], pack,
-    // kMaxPackedPasses x (upsweep, colscan, downsweep), unique (AoS),
+    //  value-set sample x 2, value plan, value sets + K1a check in one pass, value plan, second-chance
+    //  reset + value sets + value plan (exit unless a row fell outside the sample)],
+    // packed_passes_max x (upsweep, colscan, downsweep),
+    // [3 <= D <= kHashMaxDim, no scratch: hash build, 2 hashed passes, dedup, rank map fill, pairs, map fill],
+    // [D >= 3: first_hist, 4 D AoS passes, unique (AoS)],
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
     const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 10 : 0;
     const int D = static_cast<int>(dim);
-    const int aos = aos_possible(D) ? 2 + 4 * D + 1 : 0;  // build_rows, first_hist, passes, unique
-    return 4 + aos + value_ranks + 1 + 3 * packed_passes_max(D) + 4 + 2;
+    const int aos = aos_possible(D) ? 1 + 1 + 4 * D + 1 : 0;
+    const int hash = (hash_possible(D) && hash_enabled()) ? 7 : 0;
+    return 4 + value_ranks + 1 + 3 * packed_passes_max(D) + aos + hash + 4 + 2;
 }
 
 unsigned long long rmx_kernel_launches_total(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + 1 + kMaxPackedPasses + 4; }
+int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + kMaxPackedPasses + 2 + 4; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
     static thread_local char buf[32];
     const int P = static_cast<int>(4 * dim);
-    static const char* head[] = {"start", "mark", "vary", "plan", "build_rows", "first_hist"};
+    static const char* head[] = {"start", "mark", "vary", "plan", "build_rows", "pack"};
     if (k >= 0 && k < 6) return head[k];
     k -= 6;
-    if (k < P) {
-        std::snprintf(buf, sizeof(buf), "sort_pass_%d", k);
-        return buf;
-    }
-    k -= P;
-    if (k == 0) return "pack";
-    k -= 1;
     if (k < kMaxPackedPasses) {
         std::snprintf(buf, sizeof(buf), "pk_pass_%d", k);
         return buf;
     }
     k -= kMaxPackedPasses;
+    if (k == 0) return "hash_groups";
+    if (k == 1) return "first_hist";
+    k -= 2;
+    if (k < P) {
+        std::snprintf(buf, sizeof(buf), "sort_pass_%d", k);
+        return buf;
+    }
+    k -= P;
     static const char* tail[] = {"unique", "unique_pk", "map_fill", "remap"};
     if (k >= 0 && k < 4) return tail[k];
     return "";
@@ -1041,10 +1086,10 @@ int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
     RMX_CHECK(cudaMemcpyAsync(h, plan, 8, cudaMemcpyDeviceToHost, s));
     RMX_CHECK(cudaMemcpyAsync(h + 2, plan + pk_base(L.P) * 4, 16, cudaMemcpyDeviceToHost, s));
     RMX_CHECK(cudaStreamSynchronize(s));
-    info[0] = h[2];  // packed mode
+    info[0] = h[2];  // mode: 0 AoS rows, 1 packed keys, 2 hash (rmx_hash.cuh)
     info[1] = h[2] ? h[3] : 0u;  // key words
     info[2] = h[2] ? h[4] : 0u;  // varying bits
-    info[3] = h[1];  // executed sort passes
+    info[3] = h[2] == 1u ? h[5] : h[1];  // executed sort passes (hash mode: of the candidate rows)
     return RMX_OK;
 }
 
@@ -1091,6 +1136,24 @@ int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void
     info[1] = vb[0];               // 1: value sets judged worth collecting
     info[2] = vb[1];               // candidate components
     info[3] = st;                  // kVstateChecked | kVstateMiss of the full pass
+    return RMX_OK;
+}
+
+int rmx_hash_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t pk0 = 0, nc = 0, pl[2] = {0, 0};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char* base = static_cast<const char*>(workspace);
+    RMX_CHECK(cudaMemcpyAsync(&pk0, base + L.plan + pk_base(L.P) * 4, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(&nc, base + L.n_cand, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(pl, base + L.plan, 8, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    const bool hash = pk0 == 2u;
+    info[0] = hash ? 1u : 0u;                      // the call ran in hash mode
+    info[1] = hash ? nc : 0u;                      // candidate rows (distinct keys per dedup tile)
+    info[2] = hash ? pl[1] : 0u;                   // executed AoS passes over the candidates
+    info[3] = static_cast<uint32_t>(kHashTile);    // rows per dedup tile
     return RMX_OK;
 }
 

@@ -17,6 +17,8 @@
 //                       (pipeline.py:72-113, primitives.py:43-69)
 //   K3b  k_map_fill     map[org] = new_idx from the bucket-major pairs
 //   K4   k_remap        out_idx = map[idx] (remap_elements pipeline.py:116-130)
+//   hash k_hash_*       keys wider than 64 bits: dedup by hash, exact sort of the
+//                       distinct rows only (rmx_hash.cuh)
 //   small k_small       the whole pipeline in one CTA for small meshes (rmx_small.cuh)
 //   merge k_merge_path  sorted-run merge + unique of the multi-GPU exchange (rmx_merge.cuh)
 //   gen  k_gen_lattice  synthetic bench input (oracle/lattice.py recipe)
@@ -32,6 +34,7 @@
 #include "rmx_prep.cuh"
 #include "rmx_sort.cuh"
 #include "rmx_unique.cuh"
+#include "rmx_hash.cuh"
 #include "rmx_packed.cuh"
 #include "rmx_gen.cuh"
 #include "rmx_steps.cuh"

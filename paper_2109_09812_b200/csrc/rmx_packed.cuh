@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
         sets = (*a.vstate & kVstateRedo) && a.gplan[pk_base(4 * D_CT)] != 0u && gvb[0] == 1u && pk[0] != 0u &&
                vb[1] != 0u;
     } else {
-        sets = pk[0] != 0u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
+        sets = pk[0] == 1u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
     }
     if (!sets) return;  // (the full pass: k_vary computes K1a's outputs instead)
     // the full pass also checks every used row against the sample's varying bits and field sets
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
     uint32_t* plan = a.plan;
     uint32_t* pk = plan + pk_base(4 * D);
     uint32_t* vb = plan + pk_value_base(4 * D);
-    if (pk[0] == 0u) return;
+    if (pk[0] != 1u) return;
     uint32_t cand = vb[1];
     if (a.final_pass) {
         // the value sets hold the guessed packing's values: keep the components packed the same way
@@ -869,7 +869,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     __shared__ uint32_t s_runs[4 * kMaxRuns];
     constexpr int kLut = (D_CT > 0 && D_CT <= kMaxRankDim) ? D_CT * kFieldValues : 1;
     __shared__ uint16_t s_rank[kLut];
-    if (*a.status || pk[0] == 0u) return;  // uniform
+    if (*a.status || pk[0] != 1u) return;  // uniform (packed mode only)
     const uint32_t nruns = pk[4];
     const bool wide = pk[1] == 2u;
     const uint32_t* rk = a.plan + pk_rank_base(4 * D);
@@ -1534,7 +1534,7 @@ __global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    if (pk[0] == 0u) return;
+    if (pk[0] != 1u) return;  // packed mode only
     if (pk[1] == 2u) head_count_body<2>(a);
     else head_count_body<1>(a);
 }
@@ -1544,7 +1544,7 @@ __global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
 __global__ void __launch_bounds__(1024) k_tile_scan(uint32_t* counts, uint32_t ntiles, const uint32_t* plan, int dim,
                                                     unsigned long long* total_out, const uint32_t* status) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
-    if (*status || plan[pk_base(4 * dim)] == 0u) return;
+    if (*status || plan[pk_base(4 * dim)] != 1u) return;
     __shared__ uint32_t s_warp[32];
     const uint32_t tot = block_scan_counts(counts, ntiles, s_warp);
     if (threadIdx.x == 0) *total_out = tot;
@@ -1702,7 +1702,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    if (pk[0] == 0u) return;
+    if (pk[0] != 1u) return;  // packed mode only
     uint32_t* smem = dyn_smem<uint32_t>();
     if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
     else unique_pk_body<1, IPT>(a, smem);
@@ -1731,7 +1731,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_unpack_pk(UnpackPkArgs a) {
     if (*a.status) return;
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
-    if (pk[0] == 0u) return;
+    if (pk[0] != 1u) return;  // packed mode only
     __shared__ uint32_t s_runs[4 * kMaxRuns];
     __shared__ uint32_t s_const[RMX_MAX_DIM];  // replacement bits outside the varying mask
     __shared__ uint32_t s_rbeg[RMX_MAX_DIM];   // run range of each component

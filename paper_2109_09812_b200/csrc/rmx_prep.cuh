@@ -219,17 +219,10 @@ __global__ void __launch_bounds__(kBlock) k_build_rows(BuildArgs a) {
 //    key is compacted to a u32/u64 and sorted in ceil(B/8) passes; and
 //  * AoS mode -- a byte pass executes iff its digit is not constant over all
 //    keys; passes chain to the next executed one, buffers ping-pong.
-// Conditional-node handles of the graph launch path (rmx_graph_*): k_plan
-// switches on exactly the sections that do work; n = 0 for direct launches
-// (there every kernel checks the plan and exits at once instead).
-enum GraphSlot { kSlotAosA = 0, kSlotAosB = 1, kSlotPkA = 2, kSlotPkB = 3, kSlotAosPass = 4 };
-__host__ __device__ inline int slot_pk_pass(int P, int p) { return kSlotAosPass + P + p; }
-struct GraphHandles {
-    unsigned long long h[kSlotAosPass + 4 * RMX_MAX_DIM + kMaxPackedPasses];
-    int n;
-};
-
-__device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D) {
+// allow_hash: when the key does not pack into 64 bits, take hash mode (rmx_hash.cuh) instead of
+// sorting the whole vertex set as AoS rows; the AoS pass schedule is made either way (hash mode
+// sorts its candidate rows with it).
+__device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, bool allow_hash) {
     const int P = 4 * D;
     uint32_t* pk = plan + pk_base(P);
     uint32_t* rk = plan + pk_rank_base(P);
@@ -319,7 +312,8 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
         return;
     }
     pk[0] = 0u;
-    uint32_t cur = 0, executed = 0, first = static_cast<uint32_t>(P), prev = static_cast<uint32_t>(P);
+    // AoS mode builds the rows in buffer 0; hash mode sorts its candidate rows from buffer 1
+    uint32_t cur = allow_hash ? 1u : 0u, executed = 0, first = static_cast<uint32_t>(P), prev = static_cast<uint32_t>(P);
     for (int p = 0; p < P; ++p) {
         const int comp = D - 1 - (p >> 2);
         const bool ex = ((vary[comp] >> (8 * (p & 3))) & 255u) != 0u;
@@ -337,27 +331,21 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
     plan[0] = cur;
     plan[1] = executed;
     plan[2] = first;
-    plan[3] = (first < static_cast<uint32_t>(P) && first >= 4u) ? 1u : 0u;  // histogram not made by K1b
+    plan[3] = (first < static_cast<uint32_t>(P) && first >= 4u) ? 1u : 0u;  // histogram not made by K1b / k_hash_dedup
+    if (allow_hash) {  // rows grouped by hash, deduplicated per tile, the candidates sorted as AoS rows
+        pk[0] = 2u;
+        pk[1] = 0u;
+        pk[2] = 0u;
+        pk[3] = 0u;  // no packed passes
+        pk[4] = 0u;
+    }
 }
 
 __global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status,
-                       GraphHandles gh) {
+                       int allow_hash) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
-    if (*status || threadIdx.x != 0) return;  // graph: every conditional keeps its default 0
-    plan_body(vary, fields, plan, D);
-    if (gh.n) {
-        const int P = 4 * D;
-        const uint32_t* pk = plan + pk_base(P);
-        const bool packed = pk[0] != 0u;
-        cudaGraphSetConditional(gh.h[kSlotAosA], packed ? 0u : 1u);
-        cudaGraphSetConditional(gh.h[kSlotAosB], packed ? 0u : 1u);
-        cudaGraphSetConditional(gh.h[kSlotPkA], packed ? 1u : 0u);
-        cudaGraphSetConditional(gh.h[kSlotPkB], packed ? 1u : 0u);
-        for (int p = 0; p < P; ++p)
-            cudaGraphSetConditional(gh.h[kSlotAosPass + p], (!packed && plan[4 + p]) ? 1u : 0u);
-        for (int p = 0; p < kMaxPackedPasses; ++p)
-            cudaGraphSetConditional(gh.h[slot_pk_pass(P, p)], (packed && static_cast<uint32_t>(p) < pk[3]) ? 1u : 0u);
-    }
+    if (*status || threadIdx.x != 0) return;
+    plan_body(vary, fields, plan, D, allow_hash != 0);
 }
 
 // Histogram of the first executed pass when it lies outside component D-1
@@ -369,11 +357,14 @@ struct HistArgs {
     const uint32_t* status;
     uint32_t n;
     int dim;
+    const uint32_t* n_cand;  // hash mode: the rows are the n_cand candidate rows
 };
 
 __global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
-    if (*a.status || a.plan[3] == 0u || a.plan[pk_base(4 * a.dim)] != 0u) return;
+    const uint32_t mode = a.plan[pk_base(4 * a.dim)];
+    if (*a.status || a.plan[3] == 0u || mode == 1u) return;
+    const uint32_t n = mode == 2u ? *a.n_cand : a.n;
     __shared__ uint32_t s_h[256];
     s_h[threadIdx.x] = 0u;
     __syncthreads();
@@ -382,7 +373,7 @@ __global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
     const int shift = 8 * static_cast<int>(p & 3u);
     const int W = a.dim + 1;
     uint32_t rl = 0u;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < a.n;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * kBlock)
         rl_push(rl, (__ldcs(a.rows + i * W + comp) >> shift) & 255u, s_h);
     if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include "rmx_base.cuh"
+#include "rmx_hashfn.cuh"
 
 namespace rmx {
 
@@ -29,6 +30,7 @@ struct SortArgs {
     int dim;
     int pass;
     int rank_force;  // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
+    const uint32_t* n_cand;  // hash mode: the rows are the n_cand candidate rows
 };
 
 template <int W_CT, int IPT>
@@ -50,28 +52,41 @@ __device__ __forceinline__ uint32_t pick_word(const uint4& v, int comp) {
 template <int W_CT>
 struct SortMinBlocks { static constexpr int v = (W_CT == 4 || W_CT == 5) ? 2 : 3; };
 
-template <int W_CT, int IPT>
+// HASHED (hash mode, rmx_hash.cuh): the digit is byte 2 + pass of hash_key(row) -- two passes
+// group the whole vertex set by the top 16 bits of its key hash (a.hist / a.counters are then the
+// hashed passes' own arrays, a.pass is 0 or 1, rows0 -> rows1 -> rows0).
+template <int W_CT, int IPT, bool HASHED = false>
 __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(SortArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     using T = SortTraits<W_CT, IPT>;
     constexpr int TILE = T::kTile;
     const int W = W_CT > 0 ? W_CT : a.dim + 1;
+    const int D = W - 1;
     const int P = 4 * a.dim;
     if (*a.status) return;
     const uint32_t* plan = a.plan;
-    if (plan[4 + a.pass] == 0u) return;  // constant digit (or packed mode): nothing moves
-    const uint32_t src = plan[4 + P + a.pass];
+    const bool hash = plan[pk_base(P)] == 2u;
+    if (HASHED ? !hash : plan[4 + a.pass] == 0u) return;  // constant digit (or not this mode): nothing moves
+    // AoS mode sorts the whole vertex set, hash mode its n_cand candidate rows (HASHED: all rows)
+    const uint32_t n = (hash && !HASHED) ? *a.n_cand : a.n;
+    const uint32_t ntiles = (n + static_cast<uint32_t>(TILE) - 1u) / static_cast<uint32_t>(TILE);
+    const uint32_t src = HASHED ? static_cast<uint32_t>(a.pass & 1) : plan[4 + P + a.pass];
     const uint32_t* __restrict__ in = src ? a.rows1 : a.rows0;
     uint32_t* __restrict__ out = src ? a.rows0 : a.rows1;
     const int comp = a.dim - 1 - (a.pass >> 2);
-    const int shift = 8 * (a.pass & 3);
-    const uint32_t epoch = static_cast<uint32_t>(a.pass) + 1u;
-    const int nxt = static_cast<int>(plan[4 + 2 * P + a.pass]);
+    const int shift = HASHED ? 16 + 8 * a.pass : 8 * (a.pass & 3);
+    const uint32_t epoch = HASHED ? 200u + static_cast<uint32_t>(a.pass) : static_cast<uint32_t>(a.pass) + 1u;
+    const int nxt = HASHED ? P : static_cast<int>(plan[4 + 2 * P + a.pass]);
     // passes 0..3 are counted by K1b; later ones by the pass before them
     const bool count_next = nxt < P && nxt >= 4;
     const int ncomp = count_next ? a.dim - 1 - (nxt >> 2) : 0;
     const int nshift = 8 * (nxt & 3);
     uint32_t* ctr = a.counters + a.pass;
+    // the digit of a staged row
+    auto digit_of = [&](const uint32_t* row) -> uint32_t {
+        if constexpr (HASHED) return (hash_key<W_CT - 1>(row, D) >> shift) & 255u;
+        else return (row[comp] >> shift) & 255u;
+    };
 
     uint32_t* smem = dyn_smem<uint32_t>();
     const size_t tw = static_cast<size_t>(TILE) * W;
@@ -103,16 +118,16 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
         if (tid == 0) {
             const uint32_t t = atomicAdd(ctr, 1u);
             s_misc[0] = t;
-            if (t < a.ntiles) {
-                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
+            if (t < ntiles) {
+                const uint32_t tn = min(static_cast<uint32_t>(TILE), n - t * static_cast<uint32_t>(TILE));
                 stage_tile(s_rows, in + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
             }
         }
         for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
         __syncthreads();
         const uint32_t tile = s_misc[0];
-        if (tile >= a.ntiles) break;
-        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - tile * static_cast<uint32_t>(TILE));
+        if (tile >= ntiles) break;
+        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), n - tile * static_cast<uint32_t>(TILE));
         mbar_wait(s_bar, it & 1u);
 
         // ---- digits (+ next pass's histogram), stable warp ranks
@@ -123,15 +138,19 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
             uint32_t d = 256u;
             if (p < tile_n) {
                 uint32_t key, nkey = 0;
-                if constexpr (W_CT == 4) {
+                if constexpr (HASHED) {
+                    key = 0u;
+                    d = digit_of(s_rows + static_cast<size_t>(p) * W);
+                } else if constexpr (W_CT == 4) {
                     const uint4 v = reinterpret_cast<const uint4*>(s_rows)[p];
                     key = pick_word<4>(v, comp);
                     if (count_next) nkey = pick_word<4>(v, ncomp);
+                    d = (key >> shift) & 255u;
                 } else {
                     key = s_rows[static_cast<size_t>(p) * W + comp];
                     if (count_next) nkey = s_rows[static_cast<size_t>(p) * W + ncomp];
+                    d = (key >> shift) & 255u;
                 }
-                d = (key >> shift) & 255u;
                 if (count_next) atomicAdd(s_hnext + ((nkey >> nshift) & 255u), 1u);
             }
             pk[r] = d;
@@ -194,7 +213,14 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t q = q0 + u * kBlock;
-                    if (q < tile_n) dst[u] = s_gdst[(pick_word<4>(v[u], comp) >> shift) & 255u] + q;
+                    if (q < tile_n) {
+                        if constexpr (HASHED) {
+                            const uint32_t row[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                            dst[u] = s_gdst[digit_of(row)] + q;
+                        } else {
+                            dst[u] = s_gdst[(pick_word<4>(v[u], comp) >> shift) & 255u] + q;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -208,7 +234,7 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
                 const uint32_t slot = q / W;
                 const uint32_t c = q - slot * W;
                 const size_t p = s_src[slot];
-                const uint32_t dd = (s_rows[p * W + comp] >> shift) & 255u;
+                const uint32_t dd = digit_of(s_rows + p * W);
                 out[static_cast<size_t>(s_gdst[dd] + slot) * W + c] = s_rows[p * W + c];
             }
         }

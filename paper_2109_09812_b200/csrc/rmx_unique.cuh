@@ -32,6 +32,7 @@ struct UniqueArgs {
     uint32_t ntiles;
     int dim;
     int bucket_shift;   // bucket = org >> bucket_shift (<= 256 buckets)
+    const uint32_t* n_cand;  // hash mode: the rows are the n_cand candidate rows
 };
 
 template <int W_CT, int IPT>
@@ -50,7 +51,11 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
     constexpr int TILE = T::kTile;
     const int D = W_CT > 0 ? W_CT - 1 : a.dim;
     const int W = D + 1;
-    if (*a.status || a.plan[pk_base(4 * D)] != 0u) return;  // packed mode: k_unique_pk
+    const uint32_t mode = a.plan[pk_base(4 * D)];
+    if (*a.status || mode == 1u) return;  // packed mode: k_unique_pk
+    // AoS mode: the whole vertex set; hash mode: the n_cand candidate rows (their org is the group)
+    const uint32_t n = mode == 2u ? *a.n_cand : a.n;
+    const uint32_t ntiles = (n + static_cast<uint32_t>(TILE) - 1u) / static_cast<uint32_t>(TILE);
     const uint32_t* __restrict__ rows = a.plan[0] ? a.rows1 : a.rows0;
     uint2* __restrict__ pairs = reinterpret_cast<uint2*>(a.plan[0] ? const_cast<uint32_t*>(a.rows0)
                                                                     : const_cast<uint32_t*>(a.rows1));
@@ -78,17 +83,17 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
         if (tid == 0) {
             const uint32_t t = atomicAdd(a.counter, 1u);
             s_misc[0] = t;
-            if (t < a.ntiles) {
-                const uint32_t tn = min(static_cast<uint32_t>(TILE), a.n - t * static_cast<uint32_t>(TILE));
+            if (t < ntiles) {
+                const uint32_t tn = min(static_cast<uint32_t>(TILE), n - t * static_cast<uint32_t>(TILE));
                 stage_tile(s_rows, rows + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
             }
         }
         s_bcnt[tid] = 0u;
         __syncthreads();
         const uint32_t tile = s_misc[0];
-        if (tile >= a.ntiles) break;
+        if (tile >= ntiles) break;
         const uint32_t base = tile * static_cast<uint32_t>(TILE);
-        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
+        const uint32_t tile_n = min(static_cast<uint32_t>(TILE), n - base);
         if (tile > 0 && tid < static_cast<uint32_t>(D)) s_prev[tid] = rows[static_cast<size_t>(base - 1) * W + tid];
         __syncthreads();
         mbar_wait(s_bar, it & 1u);
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
         }
         __syncthreads();
         const uint32_t tprefix = s_misc[2];
-        if (tid == 0 && tile == a.ntiles - 1) *a.count = static_cast<unsigned long long>(tprefix) + ttotal;
+        if (tid == 0 && tile == ntiles - 1) *a.count = static_cast<unsigned long long>(tprefix) + ttotal;
 
         // ---- phase 2: new index per slot, bucketed pairs, unique rows out
         uint32_t running = tprefix + wexcl;
@@ -212,12 +217,19 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
 // K3b: map[org] = new_idx from the bucket-major pair array (streaming reads;
 // the stores of concurrently running CTAs fall in one or two buckets, i.e. an
 // L2-resident window of map, so partial sectors merge before write-back).
+// mode_want: 0 = the final map of the packed / AoS modes (exits in hash mode); 2 = hash mode's
+// rank_of[group] from the n_cand candidate pairs; 3 = hash mode's final map (k_hash_pairs' pairs,
+// in the buffer the candidate pairs were not in).
 __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const uint32_t* rows0,
                                                       const uint32_t* rows1, uint32_t* map, uint32_t n,
-                                                      const uint32_t* status) {
+                                                      const uint32_t* status, int dim, int mode_want,
+                                                      const uint32_t* n_cand) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status) return;
-    const uint4* pairs = reinterpret_cast<const uint4*>(plan[0] ? rows0 : rows1);
+    const bool hash = plan[pk_base(4 * dim)] == 2u;
+    if (hash != (mode_want >= 2)) return;
+    if (mode_want == 2) n = *n_cand;
+    const uint4* pairs = reinterpret_cast<const uint4*>((plan[0] != 0u) == (mode_want != 3) ? rows0 : rows1);
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
     if (2 * i + 1 < n) {
         const uint4 v = __ldcs(pairs + i);

@@ -56,3 +56,7 @@ def test_full_size_matches_reference_digests(cuda_ok, cfg):
         got[f] = sha(res.scratch[f])
     for k, v in got.items():
         assert v == ref[k], (cfg, k)
+    # without scratch the wide-key configs take hash mode (rmx_hash.cuh): the outputs must not change
+    plain = pipeline.reindex_tensors(vtx, idx)
+    assert plain.new_count == ref["new_count"]
+    assert sha(plain.vertices) == ref["out_vtx"] and sha(plain.elements) == ref["out_idx"]

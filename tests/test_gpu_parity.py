@@ -321,8 +321,8 @@ def test_wide_dims_vs_oracle(rmx, D, pool, mesh_path):
 
 @pytest.mark.parametrize("env", [{"RMX_PDL": "0"}, {"RMX_VALUE_RANK": "0"}, {"RMX_PDL": "0", "RMX_VALUE_RANK": "0"},
                                  {"RMX_DS": "2"}, {"RMX_DS": "2", "RMX_DS2": "24x256x2"},
-                                 {"RMX_DS": "2", "RMX_DS2": "12x256x4"}],
-                         ids=["no-pdl", "no-value-rank", "neither", "ds2", "ds2-24x256", "ds2-12x256"])
+                                 {"RMX_DS": "2", "RMX_DS2": "12x256x4"}, {"RMX_HASH": "0"}],
+                         ids=["no-pdl", "no-value-rank", "neither", "ds2", "ds2-24x256", "ds2-12x256", "no-hash"])
 def test_switches_keep_results(rmx, monkeypatch, env):
     """The A/B switches change speed, never results: golden cases through the
     large-mesh pipeline and a lattice soup with value ranks, each switch off."""

@@ -45,6 +45,12 @@ def main():
         vtx, idx = gen.lattice_soup_tensors("tri", (20000, 25000), seed=0, n_elem_take=E_all // 8)
         V, D = vtx.shape
         E = idx.shape[0]
+    elif a.config == "C2s":  # C2 with real-valued coordinates (oracle/lattice.py:scramble_words): hash mode
+        from paper_2109_09812_b200 import gen
+        vtx, idx = gen.lattice_soup_tensors("tri", (5000, 5000))
+        vtx = gen.scramble_tensor(vtx)
+        V, D = vtx.shape
+        E = idx.shape[0]
     else:
         kid, nx, ny, nz, D = CFG[a.config]
         E, V = ctypes.c_uint64(), ctypes.c_uint64()
@@ -73,6 +79,11 @@ def main():
         tot += ms
         print(f"{names[k]:>14s} {ms:8.3f} ms")
     print(f"{'total':>14s} {tot:8.3f} ms")
+    hi = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_hash_info(ws.data_ptr(), V, D, s.cuda_stream, hi))
+    if hi[0]:
+        print(f"hash mode: {hi[1]:,} candidate rows ({hi[1] / int(info[0]):.2f} per distinct key), "
+              f"{hi[2]} AoS passes over them, {hi[3]}-row dedup tiles")
     # whole-step time: direct launches vs the captured graph (conditional nodes)
     g = pipeline.PipelineGraph(vtx, V, D, idx, E, D, out_v, out_e, info, ws) if not a.no_compare else None
     for name, fn in [] if a.no_compare else (("direct", lambda: pipeline.launch(vtx, V, D, idx, E, D, out_v, out_e, info, ws, None, s)),
