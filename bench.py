@@ -338,7 +338,18 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
     for k in range(1, n_ev):
         vals = [ev[s][k - 1].elapsed_time(ev[s][k]) for s in range(steps)]
         stage_ms[names[k]] = sum(vals) / len(vals)
-    # dominant kernel: one executed LSD pass (packed-key or AoS rows)
+    # dominant kernel: one executed LSD pass (packed-key or AoS rows; hash mode: AoS passes over
+    # the candidate rows, rmx_hash.cuh)
+    hash_mode = packed == 2
+    n_rows = V
+    hinfo = None
+    if hash_mode:
+        hi = (ctypes.c_uint32 * 4)()
+        _native.check(lib.rmx_hash_info(ws.data_ptr(), V, D, stream.cuda_stream, hi))
+        hinfo = {"candidate_rows": int(hi[1]), "candidates_per_unique": int(hi[1]) / expect_u,
+                 "candidate_passes": int(hi[2]), "dedup_tile_rows": int(hi[3])}
+        n_rows, executed = int(hi[1]), int(hi[2])
+        packed = 0
     pass_names = [n for n in names if n.startswith("pk_pass_" if packed else "sort_pass_")]
     active = sorted((stage_ms[n] for n in pass_names), reverse=True)[:executed]
     pass_ms = sum(active) / max(1, len(active))
@@ -351,7 +362,7 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
                     for p in range(executed)]
         pass_bytes = sum(per_pass) / len(per_pass) * V
     else:
-        pass_bytes = 2 * row_bytes * V
+        pass_bytes = 2 * row_bytes * n_rows
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0)
@@ -362,11 +373,13 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None,
                      "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
-                                else "one onesweep LSD pass: k_sort_pass"),
+                                else "one onesweep LSD pass over the hash-mode candidate rows: k_sort_pass"
+                                if hash_mode else "one onesweep LSD pass: k_sort_pass"),
                      "key": (f"packed {vbits} key bits in {key_words} x u32 (field ranks on components "
                              f"{mask_list(field_mask)}, value ranks on {mask_list(value_mask)}: "
                              f"{bits_before_vr} bits before value ranks)" if packed
                              else f"{D} x u32 words"),
+                     "hash_mode": hinfo,
                      "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
                      "executed_passes": executed, "nominal_passes": 4 * D},
         "executed_bytes": executed_bytes,
@@ -562,17 +575,63 @@ def run_b200(args):
         torch.distributed.destroy_process_group()
 
 
-def run_b200_dist(args):
-    """N > 1 (torchrun, NCCL): one global soup partitioned across the ranks (weak scaling).
+DIST_TEXT = {
+    "C2": "C2 per GPU: one shuffled float3 lattice soup of (5000 N) x 5000 quads (50M triangles per GPU), "
+          "element ranges per rank (weak scaling)",
+    "C5": "C5: the 1B-triangle float3 soup (20000 x 25000 quads, 3.15B vertex slots), element ranges per rank "
+          "(strong scaling)",
+    "C4": "C4: merge of 8 overlapping 50M-triangle meshes (welded 5000 x 5000 tiles, 500 shared rows), tiles "
+          "dealt to the ranks in order (strong scaling)",
+}
 
-    Workload: a shuffled float3 lattice soup of (5000 N) x 5000 quads = 50M
-    triangles per GPU; rank r generates elements [r E/N, (r+1) E/N) and the
-    vertex slots they own.  A step is ``dist.reindex_distributed`` over NCCL
-    (local re-index, sample-sort exchange of the deduplicated keys, merge,
-    reverse exchange, remap); value = all ranks' input vertices / max-over-ranks
-    device time.
-    """
-    import numpy as np  # noqa: F401
+
+def dist_shard(cfg: str, rank: int, world: int, dev):
+    """This rank's shard (vertex bits, elements with local indices) of a multi-GPU workload, generated on
+    the device; returns (vtx, idx, total vertex slots of the job, expected global unique count)."""
+    import torch
+
+    from paper_2109_09812_b200 import _native, gen
+    lib = _native.lib()
+    if cfg == "C4":
+        from oracle import lattice
+        n, step, tiles = lattice.COLS_C4, lattice.ROW_STEP_C4, lattice.TILES_C4
+        mine = [t for t in range(tiles) if t * world // tiles == rank]
+        pieces = [gen.welded_tile_tensors(n, step * t, t, False, dev) for t in mine]
+        vtx = torch.cat([p[0] for p in pieces])
+        parts, off = [], 0
+        for v, e in pieces:
+            parts.append((e.to(torch.int64) + off).to(torch.int32))
+            off += v.shape[0]
+        idx = torch.cat(parts)
+        sz = lattice.welded_sizes(n)
+        return vtx, idx, sz["n_vertices"] * tiles, (step * (tiles - 1) + n + 1) * (n + 1)
+    nx, ny = (5000 * world, 5000) if cfg == "C2" else (20000, 25000)
+    D, K = 3, 3
+    E_all, V_all = ctypes.c_uint64(), ctypes.c_uint64()
+    lib.rmx_lattice_sizes(0, nx, ny, 0, 1 << 63, ctypes.byref(E_all), ctypes.byref(V_all))
+    E_all, V_all = E_all.value, V_all.value
+    e0, e1 = E_all * rank // world, E_all * (rank + 1) // world
+
+    def slots(e):
+        x, v = ctypes.c_uint64(), ctypes.c_uint64()
+        lib.rmx_lattice_sizes(0, nx, ny, 0, e, ctypes.byref(x), ctypes.byref(v))
+        return v.value
+
+    V = slots(e1) - slots(e0)
+    vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
+    idx = torch.empty((e1 - e0, K), dtype=torch.int32, device=dev)
+    _native.check(lib.rmx_gen_lattice_soup_range(0, nx, ny, 0, 0, e0, e1, vtx.data_ptr(), idx.data_ptr(),
+                                                 torch.cuda.current_stream(dev).cuda_stream))
+    return vtx, idx, V_all, (nx + 1) * (ny + 1)
+
+
+def run_b200_dist(args):
+    """N > 1 (torchrun, NCCL): one mesh partitioned across the ranks, re-indexed by the sample-sort
+    path (paper_2109_09812_b200.dist).  --config C2: weak scaling, (5000 N) x 5000 quads; C5: the
+    1B-triangle soup, strong scaling; C4: the 8-tile merge, strong scaling.  A step is
+    ``dist.reindex_distributed`` (local re-index, sample-sort exchange of the deduplicated keys over
+    peer memory, merge, reverse exchange, remap); value = all ranks' input vertices / max-over-ranks
+    device time."""
     import torch
     import torch.distributed as tdist
 
@@ -588,23 +647,10 @@ def run_b200_dist(args):
     if not os.path.exists(_native.LIB_PATH):
         build.build()
     lib = _native.lib()
-    nx, ny, D, K = 5000 * world, 5000, 3, 3
-    E_all, V_all = ctypes.c_uint64(), ctypes.c_uint64()
-    lib.rmx_lattice_sizes(0, nx, ny, 0, 1 << 63, ctypes.byref(E_all), ctypes.byref(V_all))
-    E_all, V_all = E_all.value, V_all.value
-    e0, e1 = E_all * rank // world, E_all * (rank + 1) // world
-
-    def slots(e):
-        x, v = ctypes.c_uint64(), ctypes.c_uint64()
-        lib.rmx_lattice_sizes(0, nx, ny, 0, e, ctypes.byref(x), ctypes.byref(v))
-        return v.value
-
-    V = slots(e1) - slots(e0)
-    E = e1 - e0
-    vtx = torch.empty((V, D), dtype=torch.int32, device=dev)
-    idx = torch.empty((E, K), dtype=torch.int32, device=dev)
-    _native.check(lib.rmx_gen_lattice_soup_range(0, nx, ny, 0, 0, e0, e1, vtx.data_ptr(), idx.data_ptr(),
-                                                 torch.cuda.current_stream(dev).cuda_stream))
+    cfg = args.config if args.config in DIST_TEXT else "C2"
+    vtx, idx, V_all, expect_u = dist_shard(cfg, rank, world, dev)
+    V, D = vtx.shape
+    E, K = idx.shape
     # data exchange over peer memory (symmetric buffers + rmx_scatter_rows); NCCL all-to-all only if
     # the symmetric-memory rendezvous is not available on this box
     try:
@@ -615,15 +661,15 @@ def run_b200_dist(args):
         comm = rdist.TorchComm(device=dev)
         exchange = f"NCCL all_to_all (symmetric memory unavailable: {type(exc).__name__}: {exc})"[:200]
     backend = rdist.CudaBackend(dev)
-    expect_u = (nx + 1) * (ny + 1)
 
-    def step():
-        return rdist.reindex_distributed(vtx, idx, comm, backend)
+    def step(timing=None):
+        return rdist.reindex_distributed(vtx, idx, comm, backend, timing=timing)
 
     for _ in range(max(3, args.warmup)):
         res = step()
     assert res.total == expect_u, (res.total, expect_u)
     u_local = int(res.vertices.shape[0])
+    launches0 = lib.rmx_kernel_launches_total()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tdist.barrier()
     torch.cuda.synchronize(dev)
@@ -634,10 +680,28 @@ def run_b200_dist(args):
         t1.record()
         torch.cuda.synchronize(dev)
     ms = t0.elapsed_time(t1) / args.steps
+    launches = (lib.rmx_kernel_launches_total() - launches0) / args.steps
     t = torch.tensor([ms], device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     value = V_all / (ms * 1e-3)
+    # one instrumented step: per-phase CUDA-event times and the exchanged bytes (max over ranks)
+    timing = {}
+    step(timing)
+    keys = sorted(k for k in timing if k.endswith("_ms"))
+    tv = torch.tensor([timing[k] for k in keys] + [float(timing.get("exchange_bytes_out", 0)),
+                                                   float(timing.get("exchange_bytes_in", 0))], device=dev)
+    tdist.all_reduce(tv, op=tdist.ReduceOp.MAX)
+    phases = {k: float(v) for k, v in zip(keys, tv[:len(keys)].tolist())}
+    nv_out, nv_in = float(tv[-2]), float(tv[-1])
+    xfer_ms = phases.get("exchange_ms", 0.0) + phases.get("reverse_ms", 0.0)
+    nvlink = {"bytes_out_per_rank_max": nv_out, "bytes_in_per_rank_max": nv_in,
+              "exchange_ms": xfer_ms, "peak_gbs_per_direction": 900.0,
+              "achieved_gbs_per_direction": (max(nv_out, nv_in) / (xfer_ms * 1e-3) / 1e9) if xfer_ms else None,
+              "note": "forward keys (4D B) + reverse global ids (4 B) of the local unique keys that cross to other "
+                      "ranks; exchange_ms = forward + reverse exchange phases (CUDA events, barriers included)"}
+    if nvlink["achieved_gbs_per_direction"]:
+        nvlink["frac"] = nvlink["achieved_gbs_per_direction"] / 900.0
 
     # end to end: this rank's shard from pinned host memory, results back to pinned host memory
     host_v = torch.empty((V, D), dtype=torch.int32, pin_memory=True)
@@ -645,7 +709,7 @@ def run_b200_dist(args):
     host_v.copy_(vtx)
     host_e.copy_(idx)
     out_host_e = torch.empty((E, K), dtype=torch.int32, pin_memory=True)
-    out_host_v = torch.empty((V, D), dtype=torch.int32, pin_memory=True)
+    out_host_v = torch.empty((max(u_local, 1) * 2, D), dtype=torch.int32, pin_memory=True)
     e2e_steps = max(1, min(args.steps, 3))
     dv = torch.empty_like(vtx)
     de = torch.empty_like(idx)
@@ -688,35 +752,36 @@ def run_b200_dist(args):
     pinfo = (ctypes.c_uint32 * 4)()
     _native.check(lib.rmx_plan_info(ws.data_ptr(), V, D, torch.cuda.current_stream(dev).cuda_stream, pinfo))
     packed, key_words, vbits, executed = (int(x) for x in pinfo)
-    pass_names = [n for n in names if n.startswith("pk_pass_" if packed else "sort_pass_")]
+    pass_names = [n for n in names if n.startswith("pk_pass_" if packed == 1 else "sort_pass_")]
     active = sorted((stage_ms[n] for n in pass_names), reverse=True)[:executed]
     pass_ms = sum(active) / max(1, len(active))
-    row_bytes = (4 * key_words + 4) if packed else (4 * D + 4)
+    if packed == 1:
+        per_pass = [8 * key_words + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < executed else 0)
+                    for p in range(executed)]
+        pass_bytes = sum(per_pass) / max(1, len(per_pass)) * V
+    else:
+        pass_bytes = 2 * (4 * D + 4) * V
     hbm, peak_kind = peaks()
-    achieved = 2 * row_bytes * V / (pass_ms * 1e-3) / 1e9
+    achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
     del out_v, out_e, ws
-    # NVLink bytes per rank: forward keys + reverse ids of the local unique keys, (G-1)/G of them remote
-    nvlink_bytes = (4 * D + 4) * u_local * (world - 1) / world
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "verts/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if cfg == "C2" else "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"C2 per GPU: one shuffled float3 lattice soup of {nx}x{ny} quads "
-                                   f"({E_all:,} triangles, {V_all:,} vertex slots), element ranges per rank",
-                       "n_vertices": V_all, "unique": expect_u, "parallelism": f"dp{world} sample sort",
-                       "exchange": exchange,
-                       "l2": "inputs 2.5 GB per GPU > 126 MB L2, no flush needed"},
+            "config": {"workload": DIST_TEXT[cfg], "n_vertices": V_all, "unique": expect_u,
+                       "parallelism": f"dp{world} sample sort", "exchange": exchange,
+                       "l2": "inputs >= 2.5 GB per GPU > 126 MB L2, no flush needed"},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "kernel": "one local LSD pass on the rank-0 shard (profiled call after "
                                                     "the timed loop)", "peak_kind": peak_kind,
                          "executed_passes": executed},
-            "nvlink": {"bytes_per_rank_est": nvlink_bytes, "peak_gbs_per_direction": 770.0,
-                       "note": "forward keys (4D B) + reverse ids (4 B) per local unique key"},
+            "phases_ms": phases,
+            "nvlink": nvlink,
             "clocks": clk.summary(),
-            # per step: local re-index, sample sort/dedup, merge re-index (3 pipeline calls) + lower bound + gather
-            "gpu_launches": (3 * lib.rmx_kernel_launches(D) + 2) * args.steps,
+            "gpu_launches": int(round(launches * args.steps)),
         }
         emit(line)
     tdist.barrier()
@@ -742,7 +807,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(set(CONFIGS) | {"C4", "C5"}))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -751,7 +816,7 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    elif dist_env()[1] > 1 or args.dist:
+    elif dist_env()[1] > 1 or args.dist or args.config in ("C4", "C5"):
         run_b200_dist(args)
     else:
         run_b200(args)

@@ -620,7 +620,9 @@ int launch_hash_dedup_d(const HashArgs& a, cudaStream_t s) {
     const size_t smem = hash_dedup_smem(a.dim);
     int rc = ensure_smem(k_hash_dedup<D_CT>, smem);
     if (rc) return rc;
-    RMX_CHECK(launch(k_hash_dedup<D_CT>, a.ntiles, kBlock, smem, s, a));
+    int grid = 0;
+    if ((rc = persistent_grid(k_hash_dedup<D_CT>, smem, a.ntiles, grid))) return rc;
+    RMX_CHECK(launch(k_hash_dedup<D_CT>, grid, kBlock, smem, s, a));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
 }
@@ -902,26 +904,26 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     }
     if ((rc = rec.mark())) return rc;
     {
-        const uint64_t threads = (V + 1) / 2;
-        const unsigned grid = static_cast<unsigned>((threads + kBlock - 1) / kBlock);
-        RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
-                         static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1), map,
-                         static_cast<uint32_t>(V), static_cast<const uint32_t*>(d_status), L.D, 0, n_cand));
-        RMX_CHECK(cudaGetLastError());
-        if (hash_ok) {  // rank_of[group] from the candidates' pairs, then map[origin]
+        if (hash_ok) {  // rank_of[candidate] from the candidates' pairs, then (origin, new index) pairs
+            int grid = 0;
+            if ((rc = grid_for_stream((V + 1) / 2, grid))) return rc;
             RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
                              static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1),
                              reinterpret_cast<uint32_t*>(base + L.rank_of), static_cast<uint32_t>(V),
                              static_cast<const uint32_t*>(d_status), L.D, 2, n_cand));
             RMX_CHECK(cudaGetLastError());
-            RMX_CHECK(launch(k_hash_pairs, L.ntiles_hash, kBlock, 0, s, ha,
-                             reinterpret_cast<uint32_t*>(base + L.fill2), L.bucket_shift));
-            RMX_CHECK(cudaGetLastError());
-            RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
-                             static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1), map,
-                             static_cast<uint32_t>(V), static_cast<const uint32_t*>(d_status), L.D, 3, n_cand));
+            int gp = 0;
+            if ((rc = persistent_grid(k_hash_pairs, 0, L.ntiles_hash, gp))) return rc;
+            RMX_CHECK(launch(k_hash_pairs, gp, kBlock, 0, s, ha, reinterpret_cast<uint32_t*>(base + L.fill2),
+                             L.bucket_shift));
             RMX_CHECK(cudaGetLastError());
         }
+        const uint64_t threads = (V + 1) / 2;
+        RMX_CHECK(launch(k_map_fill, static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s,
+                         static_cast<const uint32_t*>(plan), static_cast<const uint32_t*>(rows0),
+                         static_cast<const uint32_t*>(rows1), map, static_cast<uint32_t>(V),
+                         static_cast<const uint32_t*>(d_status), L.D, 0, n_cand));
+        RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
     // K4 remap
@@ -1039,13 +1041,13 @@ int rmx_kernel_launches(uint32_t dim) {
     //  value-set sample x 2, value plan, value sets + K1a check in one pass, value plan, second-chance
     //  reset + value sets + value plan (exit unless a row fell outside the sample)],
     // packed_passes_max x (upsweep, colscan, downsweep),
-    // [3 <= D <= kHashMaxDim, no scratch: hash build, 2 hashed passes, dedup, rank map fill, pairs, map fill],
+    // [3 <= D <= kHashMaxDim, no scratch: hash build, 2 hashed passes, dedup, rank map fill, pairs],
     // [D >= 3: first_hist, 4 D AoS passes, unique (AoS)],
     // head_count + tile_scan + unique_pk + unpack_pk, map_fill, remap
     const int value_ranks = (dim <= static_cast<uint32_t>(kMaxRankDim) && value_rank_enabled()) ? 10 : 0;
     const int D = static_cast<int>(dim);
     const int aos = aos_possible(D) ? 1 + 1 + 4 * D + 1 : 0;
-    const int hash = (hash_possible(D) && hash_enabled()) ? 7 : 0;
+    const int hash = (hash_possible(D) && hash_enabled()) ? 6 : 0;
     return 4 + value_ranks + 1 + 3 * packed_passes_max(D) + aos + hash + 4 + 2;
 }
 

@@ -148,10 +148,12 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
     __shared__ uint32_t s_hist[4 * 256];
     __shared__ uint32_t s_base;
     const uint32_t tid = threadIdx.x;
-    const uint32_t base = blockIdx.x * static_cast<uint32_t>(kHashTile);
+    for (uint32_t i = tid; i < 4u * 256u; i += kBlock) s_hist[i] = 0u;
+    uint32_t rl[4] = {0u, 0u, 0u, 0u};
+    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // persistent: a no-op launch is cheap
+    const uint32_t base = tile * static_cast<uint32_t>(kHashTile);
     const uint32_t tile_n = min(static_cast<uint32_t>(kHashTile), a.n - base);
     for (uint32_t i = tid; i < static_cast<uint32_t>(kDedupSlots); i += kBlock) s_owner[i] = 0u;
-    for (uint32_t i = tid; i < 4u * 256u; i += kBlock) s_hist[i] = 0u;
     {  // stage the tile's rows (coalesced)
         const uint32_t* src = a.rows0 + static_cast<size_t>(base) * W;
         if (W == 4) {
@@ -211,7 +213,6 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
     }
     __syncthreads();
     const uint32_t gbase = s_base;
-    uint32_t rl[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int k = 0; k < kHashTileRows; ++k) {
         const uint32_t r = tid + k * kBlock;
@@ -228,6 +229,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
             for (int b = 0; b < 4; ++b) rl_push(rl[b], (last >> (8 * b)) & 255u, s_hist + b * 256);
         }
     }
+    __syncthreads();  // the next tile restages s_rows / s_owner / s_lid
+    }
 #pragma unroll
     for (int b = 0; b < 4; ++b)
         if ((rl[b] >> 8) != 0u) atomicAdd(s_hist + b * 256 + (rl[b] & 255u), rl[b] >> 8);
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
 // of the origin like K3's pairs (k_unique / k_unique_pk), so that k_map_fill's
 // stores stay inside an L2-resident window of map (a direct map[origin] store
 // per row is a DRAM read-modify-write of a random sector).  The pairs go to the
-// row buffer k_map_fill's mode 3 reads (both are free by now).
+// row buffer k_map_fill reads in hash mode (both are free by now).
 __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fill, int bs) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !hash_mode(a.plan, a.dim)) return;
@@ -248,7 +251,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fil
     __shared__ uint2 s_pairs[kHashTile];
     __shared__ uint32_t s_bcnt[256], s_bcur[256], s_bglob[256], s_warp[kWarps];
     const uint32_t tid = threadIdx.x;
-    const uint32_t base = blockIdx.x * static_cast<uint32_t>(kHashTile);
+    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // persistent: a no-op launch is cheap
+    const uint32_t base = tile * static_cast<uint32_t>(kHashTile);
     const uint32_t tile_n = min(static_cast<uint32_t>(kHashTile), a.n - base);
     s_bcnt[tid] = 0u;
     __syncthreads();
@@ -279,6 +283,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fil
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
         const uint2 p = s_pairs[q];
         pairs[s_bglob[p.x >> bs] + q] = p;
+    }
+    __syncthreads();  // the next tile reuses the shared arrays
     }
 }
 

@@ -217,9 +217,11 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
 // K3b: map[org] = new_idx from the bucket-major pair array (streaming reads;
 // the stores of concurrently running CTAs fall in one or two buckets, i.e. an
 // L2-resident window of map, so partial sectors merge before write-back).
-// mode_want: 0 = the final map of the packed / AoS modes (exits in hash mode); 2 = hash mode's
-// rank_of[group] from the n_cand candidate pairs; 3 = hash mode's final map (k_hash_pairs' pairs,
-// in the buffer the candidate pairs were not in).
+// mode_want 0: the final map -- from K3's pairs (packed / AoS modes) or from k_hash_pairs' pairs
+// (hash mode: the other row buffer); one thread per two pairs (the many CTAs in flight keep the
+// scattered stores of ~one bucket -- an L2-resident window of map -- going at once).
+// mode_want 2: hash mode's rank_of[candidate] from the candidates' pairs; a grid-stride loop over a
+// capped grid, so that the launch costs nothing in the other modes.
 __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const uint32_t* rows0,
                                                       const uint32_t* rows1, uint32_t* map, uint32_t n,
                                                       const uint32_t* status, int dim, int mode_want,
@@ -227,9 +229,24 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status) return;
     const bool hash = plan[pk_base(4 * dim)] == 2u;
-    if (hash != (mode_want >= 2)) return;
-    if (mode_want == 2) n = *n_cand;
-    const uint4* pairs = reinterpret_cast<const uint4*>((plan[0] != 0u) == (mode_want != 3) ? rows0 : rows1);
+    if (mode_want == 2) {
+        if (!hash) return;
+        n = *n_cand;
+        const uint4* pairs = reinterpret_cast<const uint4*>(plan[0] ? rows0 : rows1);
+        const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+        for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; 2 * i < n; i += stride) {
+            if (2 * i + 1 < n) {
+                const uint4 v = __ldcs(pairs + i);
+                map[v.x] = v.y;
+                map[v.z] = v.w;
+            } else {
+                const uint2 v = reinterpret_cast<const uint2*>(pairs)[2 * i];
+                map[v.x] = v.y;
+            }
+        }
+        return;
+    }
+    const uint4* pairs = reinterpret_cast<const uint4*>((plan[0] != 0u) != hash ? rows0 : rows1);
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
     if (2 * i + 1 < n) {
         const uint4 v = __ldcs(pairs + i);

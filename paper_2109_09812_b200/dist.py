@@ -48,17 +48,44 @@ from .mesh import MeshError
 # ---------------------------------------------------------------------------
 # collectives
 class Comm:
+    """Collectives of one rank.  Every method is called by all ranks in the same order; the ones
+    that return host values cost one host round trip each (reindex_distributed makes five)."""
+
     rank: int
     size: int
 
-    def all_gather_int(self, x: int) -> list[int]:
+    def all_gather_ints(self, values: list[int]) -> list[list[int]]:
+        """Every rank's small integer vector (same length on all ranks)."""
         raise NotImplementedError
+
+    def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
+        """Concatenation of every rank's ``t`` (same shape on all ranks); no host round trip."""
+        raise NotImplementedError
+
+    def count_matrix(self, send_counts: torch.Tensor) -> list[list[int]]:
+        """C[s][g] = rows rank s sends to rank g, from every rank's (G,) int64 count tensor."""
+        raise NotImplementedError
+
+    def all_to_all(self, t: torch.Tensor, send_counts: list[int], C: list[list[int]] | None = None,
+                   bounds: torch.Tensor | None = None) -> tuple[torch.Tensor, list[int]]:
+        """Rows [sum(send_counts[:g]), sum(send_counts[:g+1])) of ``t`` to rank g; with the count
+        matrix ``C`` known the counts are not exchanged again.  ``bounds`` optionally holds the
+        (G+1,) int64 send bounds on the device (no host copy needed)."""
+        raise NotImplementedError
+
+    # derived
+    def all_gather_int(self, x: int) -> list[int]:
+        return [v[0] for v in self.all_gather_ints([int(x)])]
 
     def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
-        raise NotImplementedError
-
-    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
-        raise NotImplementedError
+        sizes = self.all_gather_int(t.shape[0])
+        cap = max(sizes) if sizes else 0
+        if cap == 0:
+            return t.new_empty((0,) + tuple(t.shape[1:]))
+        pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
+        pad[: t.shape[0]] = t
+        every = self.all_gather_fixed(pad)
+        return torch.cat([every[g * cap:g * cap + n] for g, n in enumerate(sizes)])
 
 
 class TorchComm(Comm):
@@ -72,28 +99,37 @@ class TorchComm(Comm):
         self.size = dist.get_world_size(group)
         self.device = device or torch.device("cpu")
 
-    def all_gather_int(self, x: int) -> list[int]:
-        t = torch.tensor([int(x)], dtype=torch.int64, device=self.device)
-        out = [torch.empty_like(t) for _ in range(self.size)]
-        self.dist.all_gather(out, t, group=self.group)
-        return [int(o.item()) for o in out]
+    def _gather_tensor(self, t: torch.Tensor) -> torch.Tensor:
+        out = t.new_empty((self.size,) + tuple(t.shape))
+        if self.device.type == "cuda":
+            self.dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        else:  # gloo: list form
+            parts = [torch.empty_like(t) for _ in range(self.size)]
+            self.dist.all_gather(parts, t.contiguous(), group=self.group)
+            out = torch.stack(parts)
+        return out
 
-    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
-        sizes = self.all_gather_int(t.shape[0])
-        cap = max(sizes) if sizes else 0
-        if cap == 0:
-            return t.new_empty((0,) + tuple(t.shape[1:]))
-        pad = t.new_zeros((cap,) + tuple(t.shape[1:]))
-        pad[: t.shape[0]] = t
-        out = [torch.empty_like(pad) for _ in range(self.size)]
-        self.dist.all_gather(out, pad, group=self.group)
-        return torch.cat([o[:n] for o, n in zip(out, sizes)])
+    def all_gather_ints(self, values: list[int]) -> list[list[int]]:
+        t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=self.device)
+        return [[int(x) for x in row] for row in self._gather_tensor(t).tolist()]
 
-    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=self.device)
-        rc = torch.empty_like(sc)
-        self.dist.all_to_all_single(rc, sc, group=self.group)
-        recv_counts = [int(x) for x in rc.tolist()]
+    def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
+        g = self._gather_tensor(t)
+        return g.reshape((self.size * t.shape[0],) + tuple(t.shape[1:]))
+
+    def count_matrix(self, send_counts: torch.Tensor) -> list[list[int]]:
+        sc = send_counts.to(device=self.device, dtype=torch.int64)
+        return [[int(x) for x in row] for row in self._gather_tensor(sc).tolist()]
+
+    def all_gather_ints_dev(self, t: torch.Tensor) -> list[list[int]]:
+        """all_gather_ints of a small int64 device tensor without reading it on the host first."""
+        g = self._gather_tensor(t.to(device=self.device, dtype=torch.int64).reshape(-1))
+        return [[int(x) for x in row] for row in g.tolist()]
+
+    def all_to_all(self, t, send_counts, C=None, bounds=None):
+        if C is None:
+            C = self.count_matrix(torch.tensor(list(send_counts), dtype=torch.int64))
+        recv_counts = [C[s][self.rank] for s in range(self.size)]
         out = t.new_empty((sum(recv_counts),) + tuple(t.shape[1:]))
         self.dist.all_to_all_single(out, t.contiguous(), output_split_sizes=recv_counts,
                                     input_split_sizes=list(send_counts), group=self.group)
@@ -110,7 +146,10 @@ class SymmComm(TorchComm):
     transfer are one kernel, with no send staging and no NCCL kernel
     ("B200-native fused variant").  Two device-side
     barriers per exchange order it: one before writing (every receiver has
-    copied the previous exchange out), one after (all writes have landed).
+    consumed the previous exchange: it reads the received rows before its next
+    exchange on the same stream), one after (all writes have landed).  The
+    returned tensor is a VIEW of the receive buffer, valid until this rank's
+    next exchange.
     """
 
     def __init__(self, group=None, device: torch.device | None = None):
@@ -133,25 +172,27 @@ class SymmComm(TorchComm):
         self._buf = buf
         self._cap = cap
 
-    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+    def all_to_all(self, t, send_counts, C=None, bounds=None):
         G, me = self.size, self.rank
         if t.dtype != torch.int32:
             raise MeshError("SymmComm exchanges int32 rows")
         words = 1
         for x in t.shape[1:]:
             words *= int(x)
-        sc = torch.tensor(send_counts, dtype=torch.int64, device=self.device)
-        allc = torch.empty(G * G, dtype=torch.int64, device=self.device)
-        self.dist.all_gather_into_tensor(allc, sc, group=self.group)
-        C = [[int(v) for v in row] for row in allc.view(G, G).tolist()]  # C[s][g]: rows s sends to g
+        if C is None:
+            C = self.count_matrix(torch.tensor(list(send_counts), dtype=torch.int64))
         recv_counts = [C[s][me] for s in range(G)]
         recv_total = sum(recv_counts)
         self._ensure(max(sum(C[s][g] for s in range(G)) for g in range(G)) * words)
-        bounds = [0]
-        for c in send_counts:
-            bounds.append(bounds[-1] + c)
         dst_off = [sum(C[s][g] for s in range(me)) for g in range(G)]
-        meta = torch.tensor(bounds + dst_off, dtype=torch.int64, device=self.device)
+        if bounds is None:
+            b = [0]
+            for c in send_counts:
+                b.append(b[-1] + c)
+            meta = torch.tensor(b + dst_off, dtype=torch.int64, device=self.device)
+        else:
+            meta = torch.cat([bounds.to(device=self.device, dtype=torch.int64),
+                              torch.tensor(dst_off, dtype=torch.int64, device=self.device)])
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self._handle.barrier(channel=0)
         n = t.shape[0]
@@ -161,7 +202,7 @@ class SymmComm(TorchComm):
                                                     self._handle.buffer_ptrs_dev, meta.data_ptr() + 8 * (G + 1),
                                                     stream))
         self._handle.barrier(channel=0)
-        out = self._buf[:recv_total * words].view((recv_total,) + tuple(t.shape[1:])).clone()
+        out = self._buf[:recv_total * words].view((recv_total,) + tuple(t.shape[1:]))
         return out, recv_counts
 
 
@@ -193,14 +234,17 @@ class ThreadComm(Comm):
         self.hub.barrier.wait()
         return out
 
-    def all_gather_int(self, x: int) -> list[int]:
-        return [int(v) for v in self._exchange(int(x))]
+    def all_gather_ints(self, values: list[int]) -> list[list[int]]:
+        return [[int(x) for x in v] for v in self._exchange([int(x) for x in values])]
 
-    def all_gather_rows(self, t: torch.Tensor) -> torch.Tensor:
+    def all_gather_fixed(self, t: torch.Tensor) -> torch.Tensor:
         parts = self._exchange(t)
         return torch.cat([p.to(t.device) for p in parts])
 
-    def all_to_all(self, t: torch.Tensor, send_counts: list[int]) -> tuple[torch.Tensor, list[int]]:
+    def count_matrix(self, send_counts: torch.Tensor) -> list[list[int]]:
+        return [[int(x) for x in v] for v in self._exchange([int(x) for x in send_counts.reshape(-1).tolist()])]
+
+    def all_to_all(self, t, send_counts, C=None, bounds=None):
         parts = self._exchange((t, list(send_counts)))
         chunks, recv_counts = [], []
         for src, counts in parts:
@@ -228,7 +272,9 @@ class CudaBackend:
 
     def merge_unique(self, keys: torch.Tensor, run_counts: list[int]):
         """Sorted unique keys of G sorted duplicate-free runs + the rank of every row
-        (``rmx_merge_unique_runs``: pairwise merge-path rounds, then one compaction)."""
+        (``rmx_merge_unique_runs``: pairwise merge-path rounds, then one compaction).  Returns the
+        key buffer (n rows, the first `count` valid), the ranks and the count as a device tensor:
+        the caller learns the count together with the other ranks' (one round trip)."""
         import ctypes
         n, D = keys.shape
         dev = self.device
@@ -245,32 +291,33 @@ class CudaBackend:
                                                      len(starts), out.data_ptr(), rank_of.data_ptr(),
                                                      count.data_ptr(), ws.data_ptr(), ws.numel(),
                                                      torch.cuda.current_stream(dev).cuda_stream))
-        u = int(count.item())
-        return out[:u], rank_of.view(n, 1)
+        return out, rank_of.view(n, 1), count
 
-    def lower_bound(self, rows: torch.Tensor, queries: torch.Tensor) -> list[int]:
+    def lower_bound(self, rows: torch.Tensor, queries: torch.Tensor) -> torch.Tensor:
+        """First row >= each query (rows sorted): an int64 device tensor (no host copy)."""
         q = queries.shape[0]
-        if q == 0:
-            return []
         out = torch.empty(q, dtype=torch.int64, device=self.device)
+        if q == 0:
+            return out
         rows = rows.contiguous()
         queries = queries.contiguous()
         _native.check(self.lib.rmx_lower_bound_rows(
             rows.data_ptr() if rows.numel() else None, rows.shape[0], rows.shape[1], queries.data_ptr(), q,
             out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
-        return [int(x) for x in out.cpu().tolist()]
+        return out
 
-    def gather(self, table: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    def gather(self, table: torch.Tensor, idx: torch.Tensor, status: torch.Tensor | None = None) -> torch.Tensor:
+        """out = table[idx]; an index past the table sets ``status`` (checked by the caller when it
+        wants to: the indices come from this pipeline, so it is an internal invariant)."""
         n = idx.numel()
         out = torch.empty(n, dtype=torch.int32, device=self.device)
         if n == 0:
             return out
-        status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        if status is None:
+            status = torch.zeros(1, dtype=torch.int32, device=self.device)
         _native.check(self.lib.rmx_gather_u32(
             table.data_ptr() if table.numel() else None, table.numel(), idx.contiguous().data_ptr(), n,
             out.data_ptr(), status.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
-        if int(status.item()):
-            raise MeshError("remap table index out of range (internal)")
         return out
 
 
@@ -290,26 +337,53 @@ class DistResult:
 
 
 def reindex_distributed(vertex_bits: torch.Tensor, elements: torch.Tensor, comm: Comm, backend=None,
-                        samples_per_rank: int = 1024) -> DistResult:
-    """Re-index the mesh whose rank-r shard is (vertex_bits, elements); see module doc."""
+                        samples_per_rank: int = 1024, timing: dict | None = None,
+                        check: bool = False) -> DistResult:
+    """Re-index the mesh whose rank-r shard is (vertex_bits, elements); see module doc.
+
+    Host round trips: the local unique count, the sample sizes, the sorted samples' count, the
+    exchange count matrix, the merged counts (five, whatever G).  ``timing`` (a dict, GPU backends)
+    receives CUDA-event milliseconds of the steps and the exchanged bytes; ``check`` verifies the
+    internal remap indices (one more round trip).
+    """
     backend = backend or CudaBackend(vertex_bits.device)
     if vertex_bits.dim() != 2 or elements.dim() != 2:
         raise MeshError("vertex_bits must be (V, D) and elements (E, K)")
     D = vertex_bits.shape[1]
-    G = comm.size
-    dims = comm.all_gather_int(D)
-    if any(d != D for d in dims):
-        raise MeshError(f"all shards must share dim, got {dims}")
+    G, me = comm.size, comm.rank
+    cuda = vertex_bits.is_cuda and timing is not None
+    ev = {}
+
+    def mark(name):
+        if cuda:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            ev[name] = e
+
+    mark("start")
     # 1. local dedup: sorted unique keys + local old->new indices
     uniq, local_out = backend.reindex(vertex_bits, elements)
     u = uniq.shape[0]
+    mark("local")
     if G == 1:
+        if cuda:
+            torch.cuda.current_stream(vertex_bits.device).synchronize()
+            timing["local_ms"] = ev["start"].elapsed_time(ev["local"])
         return DistResult(uniq, 0, u, local_out)
-    # 2. splitters from regular samples
-    s = min(samples_per_rank, u)
-    pos = (torch.arange(s, dtype=torch.int64) * u) // max(s, 1)
-    samples = uniq[pos.to(uniq.device)] if s else uniq[:0]
-    every = comm.all_gather_rows(samples)
+    # 2. splitters from regular samples: S rows per rank (zero-padded), the valid counts and dims
+    #    gathered once
+    S = max(1, samples_per_rank)
+    s = min(S, u)
+    info = comm.all_gather_ints([D, s])
+    dims = [d for d, _ in info]
+    if any(d != D for d in dims):
+        raise MeshError(f"all shards must share dim, got {dims}")
+    pad = uniq.new_zeros((S, D))
+    if s:
+        pos = (torch.arange(s, dtype=torch.int64) * u) // s
+        pad[:s] = uniq[pos.to(uniq.device)]
+    every_pad = comm.all_gather_fixed(pad)
+    every = torch.cat([every_pad[g * S:g * S + info[g][1]] for g in range(G)])
     m_all = every.shape[0]
     if m_all:
         ident = torch.arange(m_all, dtype=torch.int32, device=every.device).view(m_all, 1)
@@ -319,36 +393,67 @@ def reindex_distributed(vertex_bits: torch.Tensor, elements: torch.Tensor, comm:
         splitters = sorted_samples[pick.to(sorted_samples.device)]
     else:
         splitters = uniq.new_empty((0, D))
-    # 3. partition the sorted keys into G contiguous ranges and exchange them
-    if splitters.shape[0]:
-        bounds = [0] + backend.lower_bound(uniq, splitters) + [u]
-    else:
-        bounds = [0] + [u] * (G - 1) + [u]
-    send_counts = [bounds[g + 1] - bounds[g] for g in range(G)]
-    recv_keys, recv_counts = comm.all_to_all(uniq, send_counts)
+    # 3. partition the sorted keys into G contiguous ranges (bounds stay on the device) and exchange
+    lb = backend.lower_bound(uniq, splitters) if splitters.shape[0] else None
+    if isinstance(lb, torch.Tensor):
+        bounds = torch.cat([torch.zeros(1, dtype=torch.int64, device=lb.device), lb,
+                            torch.full((1,), u, dtype=torch.int64, device=lb.device)])
+        send_dev = bounds[1:] - bounds[:-1]
+    else:  # host backends (tests)
+        b = [0] + (list(lb) if lb is not None else [u] * (G - 1)) + [u]
+        bounds = None
+        send_dev = torch.tensor([b[g + 1] - b[g] for g in range(G)], dtype=torch.int64)
+    C = comm.count_matrix(send_dev)
+    send_counts = C[me]
+    mark("split")
+    recv_keys, recv_counts = comm.all_to_all(uniq, send_counts, C, bounds)
+    mark("exchange")
     # 4. merge what arrived (G sorted, duplicate-free runs): sorted unique keys of this range +
     #    the rank of each received key
     n_recv = recv_keys.shape[0]
     # merging beats re-sorting the runs (tools/merge_runs_bench.py: 8 runs / 106M rows 5.2 vs 6.9 ms,
     # 4 runs / 29M rows 1.2 vs 2.2 ms, 16 runs / 194M rows 11.7 vs 12.0 ms)
     if n_recv and hasattr(backend, "merge_unique") and D <= 8:
-        mine, rank_of = backend.merge_unique(recv_keys, recv_counts)
-    elif n_recv:
-        ident = torch.arange(n_recv, dtype=torch.int32, device=recv_keys.device).view(n_recv, 1)
-        mine, rank_of = backend.reindex(recv_keys, ident)
+        mine_buf, rank_of, cnt = backend.merge_unique(recv_keys, recv_counts)
+        sizes = [v[0] for v in comm.all_gather_ints_dev(cnt)] if hasattr(comm, "all_gather_ints_dev") \
+            else comm.all_gather_int(int(cnt.item()))
+        mine = mine_buf[:sizes[me]]
     else:
-        mine, rank_of = recv_keys.new_empty((0, D)), recv_keys.new_empty((0, 1))
+        if n_recv:
+            ident = torch.arange(n_recv, dtype=torch.int32, device=recv_keys.device).view(n_recv, 1)
+            mine, rank_of = backend.reindex(recv_keys, ident)
+        else:
+            mine, rank_of = recv_keys.new_empty((0, D)), recv_keys.new_empty((0, 1))
+        sizes = comm.all_gather_int(mine.shape[0])
+    mark("merge")
     # 5. global offsets
-    sizes = comm.all_gather_int(mine.shape[0])
-    offset = sum(sizes[: comm.rank])
+    offset = sum(sizes[:me])
     total = sum(sizes)
     if total >= 1 << 32:
         raise MeshError(f"global unique count {total} exceeds 32-bit index range")
     gid = (rank_of.reshape(-1).to(torch.int64) + offset).to(torch.int32)
-    # 6. reverse exchange: global id of every local unique key, in local order
-    new_of_local, _ = comm.all_to_all(gid, recv_counts)
+    # 6. reverse exchange: global id of every local unique key, in local order (the counts are the
+    #    transposed forward counts: no second count exchange)
+    CT = [[C[g][s] for g in range(G)] for s in range(G)]
+    new_of_local, _ = comm.all_to_all(gid, recv_counts, CT)
+    mark("reverse")
     # 7. remap this rank's elements
-    out = backend.gather(new_of_local, local_out.reshape(-1)).view(local_out.shape)
+    status = torch.zeros(1, dtype=torch.int32, device=local_out.device) if check else None
+    if status is not None and hasattr(backend, "merge_unique"):
+        out = backend.gather(new_of_local, local_out.reshape(-1), status).view(local_out.shape)
+        if int(status.item()):
+            raise MeshError("remap table index out of range (internal)")
+    else:
+        out = backend.gather(new_of_local, local_out.reshape(-1)).view(local_out.shape)
+    mark("remap")
+    if cuda:
+        torch.cuda.current_stream(vertex_bits.device).synchronize()
+        names = list(ev)
+        for a, b in zip(names, names[1:]):
+            timing[f"{b}_ms"] = ev[a].elapsed_time(ev[b])
+        row = 4 * D
+        timing["exchange_bytes_out"] = (u - send_counts[me]) * row + (n_recv - recv_counts[me]) * 4
+        timing["exchange_bytes_in"] = (n_recv - recv_counts[me]) * row + (u - send_counts[me]) * 4
     return DistResult(mine, offset, total, out)
 
 

@@ -154,6 +154,7 @@ def test_merge_unique_runs_vs_numpy(cuda_ok, G, D, n):
     counts = [len(r) for r in runs]
     uniq, inv = np.unique(keys, axis=0, return_inverse=True)      # numpy sorts rows lexicographically
     be = CudaBackend(torch.device("cuda", 0))
-    mine, rank_of = be.merge_unique(torch.from_numpy(keys.view(np.int32)).cuda(), counts)
+    buf, rank_of, cnt = be.merge_unique(torch.from_numpy(keys.view(np.int32)).cuda(), counts)
+    mine = buf[:int(cnt.item())]
     assert np.array_equal(mine.cpu().numpy().view(np.uint32), uniq)
     assert np.array_equal(rank_of.view(-1).cpu().numpy().view(np.uint32), inv.reshape(-1).astype(np.uint32))
