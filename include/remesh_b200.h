@@ -39,6 +39,7 @@ extern "C" {
 
 /* bits of the device status word written by the pipeline */
 #define RMX_STATUS_INDEX_OUT_OF_RANGE 1u   /* reference: InvalidMeshError, mesh.py:103-105 */
+#define RMX_STATUS_LEAN_UNSUPPORTED 2u     /* rmx_reindex_lean: more than 64 key bits vary */
 
 /* largest vertex dimension the CUDA path accepts (reference: unbounded) */
 #define RMX_MAX_DIM 32
@@ -125,6 +126,23 @@ int rmx_graph_create(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim
                      const rmx_scratch* scratch, rmx_graph** out);
 int rmx_graph_launch(rmx_graph* graph, void* stream);
 void rmx_graph_destroy(rmx_graph* graph);
+
+/* Memory-lean re-index (opt-in, no reference counterpart:
+ * it breaks the pure-function contract of pipeline.py:133-157 on purpose).
+ * The caller's vertex buffer is OVERWRITTEN -- after the keys are built it is
+ * the second sort buffer -- and the unique rows (U x dim words) are left in the
+ * final sort buffer: *d_where = 0 -> the workspace at offset
+ * rmx_lean_result_offset(), 1 -> the vertex buffer itself.  Keys must pack into
+ * 64 bits (lattice-like and quantised data); otherwise RMX_STATUS_LEAN_UNSUPPORTED
+ * is set in *d_status and nothing is produced.  dim >= 3, n_vertices even and
+ * above the one-CTA size, no scratch.  Workspace about 40 B per vertex (C5:
+ * 3.15B vertices re-indexed on one 180 GB GPU). */
+size_t rmx_lean_workspace_bytes(uint64_t n_vertices, uint32_t dim, uint64_t n_elements, uint32_t arity);
+size_t rmx_lean_result_offset(uint64_t n_vertices, uint32_t dim);
+int rmx_reindex_lean(uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,
+                     uint64_t n_elements, uint32_t arity, uint32_t* out_idx, uint64_t* d_new_count,
+                     uint32_t* d_status, uint32_t* d_where, void* workspace, size_t workspace_bytes,
+                     void* stream);
 
 /* Number of stage-boundary events rmx_reindex_profiled records for `dim`, and
  * the name of the kernel that runs between event k-1 and event k. */

@@ -11,13 +11,13 @@ from . import gen, rmxio
 from .ops import merge, merge_tensors, soup_to_mesh, subset, subset_tensors
 from .rmxio import FormatError, read_bin, write_bin
 from .pipeline import (DeviceResult, PipelineGraph, ReindexScratch, Reindexer, ReindexStream, reindex,
-                       reindex_tensors, workspace_bytes)
+                       reindex_tensors, reindex_tensors_lean, workspace_bytes)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "Mesh", "Issue", "MeshError", "InvalidMeshError", "ReindexScratch", "DeviceResult",
-    "Reindexer", "ReindexStream", "PipelineGraph", "reindex", "reindex_tensors", "workspace_bytes", "merge", "merge_tensors", "soup_to_mesh", "subset_tensors", "subset",
+    "Reindexer", "ReindexStream", "PipelineGraph", "reindex", "reindex_tensors", "reindex_tensors_lean", "workspace_bytes", "merge", "merge_tensors", "soup_to_mesh", "subset_tensors", "subset",
     "read_bin", "write_bin", "FormatError", "gen", "rmxio",
     "validate", "require_valid", "dereference", "soups_equal", "bitwise_equal", "vertex_bits",
 ]

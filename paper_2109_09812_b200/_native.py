@@ -20,11 +20,13 @@ LIB_PATH = os.environ.get("RMX_LIB") or os.path.join(_HERE, LIB_NAME)
 
 RMX_OK, RMX_EINVAL, RMX_ERANGE, RMX_ECUDA, RMX_ENOSPC = 0, 1, 2, 3, 4
 RMX_STATUS_INDEX_OUT_OF_RANGE = 1
+RMX_STATUS_LEAN_UNSUPPORTED = 2
 RMX_MAX_DIM = 32
 
 # every symbol include/remesh_b200.h declares
 EXPORTS = (
-    "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex",
+    "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex", "rmx_lean_workspace_bytes",
+    "rmx_lean_result_offset", "rmx_reindex_lean",
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches", "rmx_kernel_launches_total",
     "rmx_last_executed_passes", "rmx_plan_info", "rmx_plan_key_info", "rmx_plan_guess_info", "rmx_hash_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
@@ -56,6 +58,9 @@ _SIGNATURES = {
     "rmx_version": (ctypes.c_char_p, []),
     "rmx_strerror": (ctypes.c_char_p, [_int]),
     "rmx_workspace_bytes": (_sz, [_u64, _u32, _u64, _u32]),
+    "rmx_lean_workspace_bytes": (_sz, [_u64, _u32, _u64, _u32]),
+    "rmx_lean_result_offset": (_sz, [_u64, _u32]),
+    "rmx_reindex_lean": (_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "rmx_reindex": (_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _sz,
                            ctypes.POINTER(Scratch), _vp]),
     "rmx_reindex_profiled": (_int, [_vp, _u64, _u32, _vp, _u64, _u32, _vp, _vp, _vp, _vp, _vp, _sz,

@@ -125,11 +125,16 @@ struct Layout {
     size_t n_cand;                // hash mode: number of candidate rows
     size_t hhist, hcounters;      // hash mode: histograms and tile counters of the hashed passes
     uint32_t ntiles_hash;
+    size_t repl;                  // lean: replacement row words, then a zero word (the row's index)
+    bool lean;
     size_t total;
 };
 
-Layout make_layout(uint64_t V, uint32_t D) {
+// lean = true: the memory-lean layout of rmx_reindex_lean (packed keys only; the caller's vertex
+// buffer doubles as the second sort buffer): one 12-byte-per-row sort buffer, no AoS / hash arrays.
+Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     Layout L{};
+    L.lean = lean;
     L.D = static_cast<int>(D);
     L.W = L.D + 1;
     L.P = 4 * L.D;
@@ -144,10 +149,10 @@ Layout make_layout(uint64_t V, uint32_t D) {
         off = align_up(off + bytes);
         return at;
     };
-    const size_t row_bytes = static_cast<size_t>(V) * L.W * 4 + 256;  // slack: bulk copies round up to 16 B
+    const size_t row_bytes = static_cast<size_t>(V) * (lean ? 3 : L.W) * 4 + 256;  // slack: bulk copies round up
     L.flags = take(V);
     L.rows0 = take(row_bytes);
-    L.rows1 = take(row_bytes);
+    L.rows1 = take(lean ? 0 : row_bytes);
     L.map = take(static_cast<size_t>(V) * 4);
     L.plan = take(plan_words(L.P) * 4);
     L.pk_cstride = (L.ntiles_pk + kUpGroup - 1) / kUpGroup * kUpGroup;
@@ -157,7 +162,7 @@ Layout make_layout(uint64_t V, uint32_t D) {
     L.pk_digits = take(2 * (align_up(static_cast<size_t>(V) + 16)));  // two arrays: this pass's, the next's
     L.ukeys = take(static_cast<size_t>(V) * 8);  // packed: unique keys; hash: (group, origin) per row
     L.ntiles_hash = static_cast<uint32_t>((V + kHashTile - 1) / kHashTile);
-    const bool hash = L.D >= 3 && L.D <= kHashMaxDim;
+    const bool hash = !lean && L.D >= 3 && L.D <= kHashMaxDim;
     L.rank_of = take(hash ? static_cast<size_t>(V) * 4 : 0);
     const size_t vr_dim = L.D <= kMaxRankDim ? static_cast<size_t>(L.D) : 0;
     L.rank16 = take(vr_dim * (size_t{1} << kMaxValueBits) * 2);
@@ -182,8 +187,9 @@ Layout make_layout(uint64_t V, uint32_t D) {
     while (bits < 40 && (1ull << bits) < V) ++bits;
     L.bucket_shift = bits > 8 ? bits - 8 : 0;
     L.counters = take(static_cast<size_t>(L.P + 2 + kMaxPackedPasses + 1) * 4);
-    L.desc = take(static_cast<size_t>(L.ntiles > max_tiles_pk ? L.ntiles : max_tiles_pk) * 256 * 8);
-    L.desc3 = take(static_cast<size_t>(L.ntiles3) * 8);
+    L.desc = take(lean ? 256 : static_cast<size_t>(L.ntiles > max_tiles_pk ? L.ntiles : max_tiles_pk) * 256 * 8);
+    L.desc3 = take(lean ? 256 : static_cast<size_t>(L.ntiles3) * 8);
+    L.repl = take((RMX_MAX_DIM + 4) * 4);  // lean: the replacement row (the vertex buffer is overwritten)
     L.tile_counts = take(static_cast<size_t>(L.ntiles3_pk) * 4);
     L.ctl_end = off;
     L.total = off;
@@ -646,10 +652,20 @@ int launch_hash_groups(const HashArgs& ha, SortArgs sa, cudaStream_t s) {
     }
 }
 
+// lean (rmx_reindex_lean): `vtx` is overwritten (it becomes the second sort buffer after k_pack has
+// read it), out_vtx is ignored -- the unique rows land in the final sort buffer, *d_where = 0
+// (workspace rows0) or 1 (the vertex buffer) --, only packed keys are supported (a plan that is not
+// packed sets RMX_STATUS_LEAN_UNSUPPORTED and the remaining kernels exit).
 int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* idx, uint64_t E, uint32_t K,
                  uint32_t* out_vtx, uint32_t* out_idx, uint64_t* d_count, uint32_t* d_status, void* ws,
-                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events) {
+                 size_t ws_bytes, const rmx_scratch* sc, cudaStream_t s, void* const* events, int n_events,
+                 bool lean = false, uint32_t* d_where = nullptr) {
     g_err[0] = '\0';
+    if (lean && (D < 3 || (V & 1u) || sc || !d_where || V <= kSmallV)) {
+        std::snprintf(g_err, sizeof(g_err), "lean mode needs dim >= 3, an even vertex count > %u, no scratch",
+                      static_cast<unsigned>(kSmallV));
+        return RMX_EINVAL;
+    }
     if (D < 1 || K < 1) {
         std::snprintf(g_err, sizeof(g_err), "dim and arity must be >= 1 (got %u, %u)", D, K);
         return RMX_EINVAL;
@@ -677,7 +693,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if (sc && sc->is_used && V) RMX_CHECK(cudaMemsetAsync(sc->is_used, 0, V, s));
         return RMX_OK;
     }
-    if ((V && !vtx) || !idx || !out_idx || (V && !out_vtx)) {
+    if ((V && !vtx) || !idx || !out_idx || (V && !out_vtx && !lean)) {
         std::snprintf(g_err, sizeof(g_err), "null buffer");
         return RMX_EINVAL;
     }
@@ -686,7 +702,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         return RMX_EINVAL;
     }
     const PdlScope pdl(pdl_enabled());
-    const Layout L = make_layout(V, D);
+    const Layout L = make_layout(V, D, lean);
     if (!ws || ws_bytes < L.total) {
         std::snprintf(g_err, sizeof(g_err), "workspace %zu bytes < required %zu", ws_bytes, L.total);
         return RMX_ENOSPC;
@@ -707,7 +723,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     char* base = static_cast<char*>(ws);
     uint8_t* flags = (sc && sc->is_used) ? sc->is_used : reinterpret_cast<uint8_t*>(base + L.flags);
     uint32_t* rows0 = reinterpret_cast<uint32_t*>(base + L.rows0);
-    uint32_t* rows1 = reinterpret_cast<uint32_t*>(base + L.rows1);
+    // lean: the vertex buffer is the second sort buffer once k_pack has read it
+    uint32_t* rows1 = lean ? const_cast<uint32_t*>(vtx) : reinterpret_cast<uint32_t*>(base + L.rows1);
     uint32_t* map = reinterpret_cast<uint32_t*>(base + L.map);
     uint32_t* plan = reinterpret_cast<uint32_t*>(base + L.plan);
     uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist);
@@ -789,14 +806,20 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = rec.mark())) return rc;
     // hash mode (rmx_hash.cuh) replaces the whole-set AoS sort unless the caller wants the scratch
     // arrays of the stable sort (org_id, perm: only the AoS path produces them) or RMX_HASH=0
-    const bool hash_ok = hash_possible(L.D) && sc == nullptr && hash_enabled();
+    const bool hash_ok = !lean && hash_possible(L.D) && sc == nullptr && hash_enabled();
     RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0));
     RMX_CHECK(cudaGetLastError());
+    uint32_t* repl = reinterpret_cast<uint32_t*>(base + L.repl);
+    if (lean) {  // packed keys only; keep the replacement row (k_unpack_pk reads it after the vertices are gone)
+        RMX_CHECK(launch(k_lean_prepare, 1, 32, 0, s, static_cast<const uint32_t*>(plan), vtx, idx, repl, L.D,
+                         d_status));
+        RMX_CHECK(cudaGetLastError());
+    }
     if ((rc = rec.mark())) return rc;
     // ---- AoS rows of the whole vertex set (AoS mode only).  With D <= 2 at most 64 bits vary,
     // which the packed key always holds (plan_body: every run is >= 1 bit, so <= 64 runs): no AoS
     // kernels then (their stage events are still recorded).
-    const bool aos = aos_possible(L.D);
+    const bool aos = aos_possible(L.D) && !lean;
     if (aos) {
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
@@ -898,8 +921,11 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
                        sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
         if ((rc = launch_unique_pk(a, s))) return rc;
-        UnpackPkArgs u{plan, vtx, idx, vary, fields, ukeys, vinv, out_vtx,
-                       reinterpret_cast<unsigned long long*>(d_count), d_status, L.D, aligned16(out_vtx) ? 1 : 0};
+        // lean: the unique rows go to the final sort buffer (read completely by k_unique_pk by then)
+        UnpackPkArgs u{plan, lean ? repl : vtx, lean ? repl + RMX_MAX_DIM : idx, vary, fields, ukeys, vinv,
+                       out_vtx, reinterpret_cast<unsigned long long*>(d_count), d_status, L.D,
+                       (lean || aligned16(out_vtx)) ? 1 : 0, lean ? rows0 : nullptr, lean ? rows1 : nullptr,
+                       d_where};
         if ((rc = launch_unpack_pk(u, V, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
@@ -969,6 +995,27 @@ int rmx_reindex(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, con
     return run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, out_vtx_bits, out_idx, d_new_count,
                         d_status, workspace, workspace_bytes, scratch, static_cast<cudaStream_t>(stream), nullptr,
                         0);
+}
+
+size_t rmx_lean_workspace_bytes(uint64_t n_vertices, uint32_t dim, uint64_t n_elements, uint32_t arity) {
+    (void)n_elements;
+    (void)arity;
+    if (dim < 3 || dim > RMX_MAX_DIM) return 0;
+    return make_layout(n_vertices, dim, true).total;
+}
+
+size_t rmx_lean_result_offset(uint64_t n_vertices, uint32_t dim) {
+    if (dim < 3 || dim > RMX_MAX_DIM) return 0;
+    return make_layout(n_vertices, dim, true).rows0;
+}
+
+int rmx_reindex_lean(uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,
+                     uint64_t n_elements, uint32_t arity, uint32_t* out_idx, uint64_t* d_new_count,
+                     uint32_t* d_status, uint32_t* d_where, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+    return run_pipeline(vtx_bits, n_vertices, dim, idx, n_elements, arity, nullptr, out_idx, d_new_count, d_status,
+                        workspace, workspace_bytes, nullptr, static_cast<cudaStream_t>(stream), nullptr, 0, true,
+                        d_where);
 }
 
 int rmx_reindex_profiled(const uint32_t* vtx_bits, uint64_t n_vertices, uint32_t dim, const uint32_t* idx,

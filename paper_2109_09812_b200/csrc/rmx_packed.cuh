@@ -966,6 +966,22 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Memory-lean mode (rmx_reindex_lean): the plan must be packed (the vertex buffer becomes the
+// second sort buffer, 12 bytes per row: at most u64 keys + u32 origins), and the replacement row
+// is kept for k_unpack_pk; repl[RMX_MAX_DIM] = 0 stands for its index.
+__global__ void k_lean_prepare(const uint32_t* plan, const uint32_t* vtx, const uint32_t* idx, uint32_t* repl,
+                               int dim, uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*status) return;
+    const uint32_t r0 = idx[0];
+    for (int c = threadIdx.x; c < dim; c += blockDim.x) repl[c] = vtx[static_cast<size_t>(r0) * dim + c];
+    if (threadIdx.x == 0) {
+        repl[RMX_MAX_DIM] = 0u;
+        if (plan[pk_base(4 * dim)] != 1u) atomicOr(status, RMX_STATUS_LEAN_UNSUPPORTED);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K2': one LSD pass over (packed key, origin) pairs, as reduce-then-scan:
 //   k_pk_upsweep   per-tile digit counts, reading the keys only
 //                  (counts stored digit-major: counts[d][tile])
@@ -1723,6 +1739,11 @@ struct UnpackPkArgs {
     const uint32_t* status;
     int dim;
     int vec;  // out_vtx 16-byte aligned
+    // lean mode (rmx_reindex_lean): the output rows go to the final sort buffer (buf0 or buf1 by the
+    // plan's parity), and *where records which
+    uint32_t* lean_buf0;
+    uint32_t* lean_buf1;
+    uint32_t* where;
 };
 
 template <int D_CT>
@@ -1761,6 +1782,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_unpack_pk(UnpackPkArgs a) {
     __syncthreads();
     const uint64_t U = *a.count;
     const bool wide = pk[1] == 2u;
+    if (a.lean_buf0) {
+        const uint32_t fin = a.plan[0];
+        a.out_vtx = fin ? a.lean_buf1 : a.lean_buf0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *a.where = fin;
+    }
     const uint64_t* k64 = static_cast<const uint64_t*>(a.ukeys);
     const uint32_t* k32 = static_cast<const uint32_t*>(a.ukeys);
     ValueMap<D_CT> vm;

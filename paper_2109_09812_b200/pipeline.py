@@ -201,6 +201,57 @@ def reindex_tensors(vertex_bits: torch.Tensor, elements: torch.Tensor, *, scratc
     return DeviceResult(out_v, out_e, count, sc)
 
 
+def reindex_tensors_lean(vertex_bits: torch.Tensor, elements: torch.Tensor, *,
+                         stream: torch.cuda.Stream | None = None) -> DeviceResult:
+    """Memory-lean device re-index (opt-in, tensor API only).
+
+    ``vertex_bits`` is OVERWRITTEN: once the sort keys are built it serves as the
+    second sort buffer, so the workspace is ~40 B per vertex instead of ~52 and
+    no output-vertex buffer of V rows is needed (C5, 3.15B vertex slots, fits
+    one 180 GB B200).  The returned vertices are a view of the workspace or of
+    ``vertex_bits``.  Needs keys that pack into 64 bits (lattice-like or
+    quantised data: MeshError otherwise), dim >= 3, an even vertex count; small
+    meshes take :func:`reindex_tensors`.  Not a drop-in for the reference
+    (which never mutates its input, pipeline.py:133-157).
+    """
+    lib = _native.lib()
+    if vertex_bits.dim() != 2 or elements.dim() != 2 or vertex_bits.element_size() != 4 \
+            or elements.element_size() != 4:
+        raise MeshError("vertex_bits must be (V, D) and elements (E, K) of 32-bit words")
+    if not vertex_bits.is_contiguous():
+        raise MeshError("lean mode works in place: vertex_bits must be contiguous")
+    V, D = vertex_bits.shape
+    E, K = elements.shape
+    if E == 0 or D < 3 or V % 2 or V <= 8192:
+        return reindex_tensors(vertex_bits, elements, stream=stream)
+    if V >= 1 << 32:
+        raise MeshError(f"vertex count {V} exceeds 32-bit index range")
+    dev = vertex_bits.device
+    elements = elements.contiguous()
+    ws = torch.empty(int(lib.rmx_lean_workspace_bytes(V, D, E, K)), dtype=torch.uint8, device=dev)
+    out_e = torch.empty((E, K), dtype=torch.int32, device=dev)
+    info = torch.zeros(3, dtype=torch.int64, device=dev)  # count, status, where
+    s = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    base = info.data_ptr()
+    _raise_for(lib.rmx_reindex_lean(vertex_bits.data_ptr(), V, D, elements.data_ptr(), E, K, out_e.data_ptr(), base,
+                                    base + 8, base + 16, ws.data_ptr(), ws.numel(), s))
+    count, status, where = (int(x) for x in info.cpu())
+    if status & _native.RMX_STATUS_INDEX_OUT_OF_RANGE:
+        bad = torch.nonzero(elements.to(torch.int64) & 0xFFFFFFFF >= V).cpu().numpy()
+        host = elements.cpu().numpy().view(np.uint32)
+        from .mesh import Issue
+        raise InvalidMeshError([Issue(int(e), int(s_), int(host[e, s_])) for e, s_ in bad])
+    if status & _native.RMX_STATUS_LEAN_UNSUPPORTED:
+        raise MeshError("lean mode needs keys that pack into 64 bits; this vertex set varies in more "
+                        "(use reindex_tensors)")
+    if where == 0:
+        off = int(lib.rmx_lean_result_offset(V, D))
+        verts = ws[off:off + count * D * 4].view(torch.int32).view(count, D)
+    else:
+        verts = vertex_bits.view(-1)[:count * D].view(count, D)
+    return DeviceResult(verts, out_e, count, None)
+
+
 class ReindexScratch:
     """Intermediates of one run (reference ``ReindexScratch``, pipeline.py:24-38).
 
