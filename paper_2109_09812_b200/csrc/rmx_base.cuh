@@ -70,7 +70,9 @@ constexpr int kValueWords = (1 << kMaxValueBits) / 32;
 constexpr uint32_t kValueSetBytes = 192 * 1024;  // k_valueset byte maps: sum of 2^w over the candidates
 // Hash mode (plan packed-section word 0 == 2, rmx_hash.cuh): keys wider than 64 bits are
 // deduplicated by a 32-bit hash first and only the distinct rows are sorted exactly.
-constexpr int kHashPasses = 2;       // hashed passes: the top 16 bits of the key hash
+constexpr int kHashPasses = 3;       // hashed passes: the top 24 bits of the key hash (~9 rows per
+                                     // bucket in C2s, so a dedup tile splits few keys)
+constexpr int kHashShift0 = 8 * (4 - kHashPasses);  // the first hashed digit's bit offset
 constexpr int kHashTileRows = 8;     // rows per thread in the hash tile kernels
 constexpr int kHashTile = kBlock * kHashTileRows;
 constexpr int kHashMaxDim = 8;       // wider rows take the AoS path

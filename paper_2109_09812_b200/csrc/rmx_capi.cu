@@ -879,7 +879,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // ---- exact AoS sort: the whole vertex set (AoS mode) or the candidate rows (hash mode)
     const uint32_t* n_cand = reinterpret_cast<const uint32_t*>(base + L.n_cand);
     if (aos) {
-        HistArgs a{rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, n_cand};
+        HistArgs a{rows0, rows1, hist, plan, d_status, static_cast<uint32_t>(V), L.D, n_cand};
         int grid = 0;
         rc = grid_for_stream(V, grid);
         if (rc) return rc;

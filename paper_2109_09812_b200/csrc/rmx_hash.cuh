@@ -8,10 +8,11 @@
 // Hash mode instead
 //
 //   k_hash_build    cleaned AoS rows (key words, origin) and the histograms of
-//                   bytes 2 and 3 of h = hash_key(row) (rmx_hashfn.cuh)
-//   2 hashed passes k_sort_pass<..., HASHED>: the rows grouped by the top 16
-//                   bits of h -- equal keys land within a few thousand rows of
-//                   each other (C2s: ~2400 rows per 16-bit hash bucket)
+//                   the top kHashPasses bytes of h = hash_key(row) (rmx_hashfn.cuh)
+//   hashed passes   k_sort_pass<..., HASHED>: the rows grouped by the top 24
+//                   bits of h -- equal keys land next to each other, in buckets
+//                   of ~9 rows (C2s; 16 bits left ~2400-row buckets, which the
+//                   2048-row dedup tiles split: 1.8 candidates per key)
 //   k_hash_dedup    per tile of kHashTile rows, a shared-memory hash table of
 //                   the tile's distinct keys: one *candidate* row (key words,
 //                   group id) per distinct key of the tile, (group id, origin)
@@ -49,9 +50,9 @@ struct HashArgs {
     const uint8_t* flags;
     const uint32_t* idx;      // idx[0]: the replacement row (pipeline.py:148)
     const uint32_t* plan;
-    uint32_t* rows0;          // cleaned rows; after the hashed passes grouped by hash
-    uint32_t* rows1;          // candidate rows (the first buffer of the candidates' AoS sort)
-    uint32_t* hhist;          // [2][256] bytes 2 and 3 of the row hashes
+    uint32_t* rows0;          // cleaned rows (the hashed passes ping-pong rows0 / rows1); the grouped
+    uint32_t* rows1;          // rows end in buffer kHashPasses & 1, the candidate rows go to the other
+    uint32_t* hhist;          // [kHashPasses][256] the hashed digits' histograms
     uint2* grp_org;           // [n] (group id, origin) of every row, in hash-bucket order
     uint32_t* n_cand;         // number of candidate rows (tiles reserve ranges)
     uint32_t* hist;           // [4D][256]: passes 0..3 over the candidate rows
@@ -69,17 +70,17 @@ __global__ void __launch_bounds__(kBlock) k_hash_build(HashArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const int D = D_CT > 0 ? D_CT : a.dim;
     const int W = D + 1;
-    __shared__ uint32_t s_hist[2 * 256];
-    for (int i = threadIdx.x; i < 2 * 256; i += kBlock) s_hist[i] = 0u;
+    __shared__ uint32_t s_hist[kHashPasses * 256];
+    for (int i = threadIdx.x; i < kHashPasses * 256; i += kBlock) s_hist[i] = 0u;
     __syncthreads();
     if (*a.status || !hash_mode(a.plan, D)) return;  // uniform
     const uint32_t* repl = a.vtx + static_cast<size_t>(a.idx[0]) * D;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t start = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    uint32_t rl[2] = {0u, 0u};
+    uint32_t rl[kHashPasses] = {};
     auto note = [&](uint32_t h) {
-        rl_push(rl[0], (h >> 16) & 255u, s_hist);
-        rl_push(rl[1], h >> 24, s_hist + 256);
+#pragma unroll
+        for (int p = 0; p < kHashPasses; ++p) rl_push(rl[p], (h >> (kHashShift0 + 8 * p)) & 255u, s_hist + p * 256);
     };
     uint64_t done = 0;
     if constexpr (D_CT == 3) {
@@ -120,14 +121,16 @@ __global__ void __launch_bounds__(kBlock) k_hash_build(HashArgs a) {
         note(hash_key<D_CT>(k, D));
     }
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < kHashPasses; ++b)
         if ((rl[b] >> 8) != 0u) atomicAdd(s_hist + b * 256 + (rl[b] & 255u), rl[b] >> 8);
     __syncthreads();
-    for (int i = threadIdx.x; i < 2 * 256; i += kBlock)
+    for (int i = threadIdx.x; i < kHashPasses * 256; i += kBlock)
         if (s_hist[i]) atomicAdd(a.hhist + i, s_hist[i]);
 }
 
-constexpr int kDedupSlots = 2 * kHashTile;  // open-addressing table: load factor <= 1/2
+constexpr int kDedupSlotBits = 12;
+constexpr int kDedupSlots = 1 << kDedupSlotBits;  // open-addressing table: load factor <= 1/2
+static_assert(kDedupSlots == 2 * kHashTile, "dedup table sized for one tile at load factor 1/2");
 
 __host__ __device__ constexpr size_t hash_dedup_smem(int D) {
     return static_cast<size_t>(kHashTile) * (D + 1) * 4 + kDedupSlots * 4 + kHashTile * 4;
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
     const uint32_t tile_n = min(static_cast<uint32_t>(kHashTile), a.n - base);
     for (uint32_t i = tid; i < static_cast<uint32_t>(kDedupSlots); i += kBlock) s_owner[i] = 0u;
     {  // stage the tile's rows (coalesced)
-        const uint32_t* src = a.rows0 + static_cast<size_t>(base) * W;
+        const uint32_t* src = (kHashPasses & 1 ? a.rows1 : a.rows0) + static_cast<size_t>(base) * W;
         if (W == 4) {
             for (uint32_t i = tid; i < tile_n; i += kBlock)
                 reinterpret_cast<uint4*>(s_rows)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
         owner[k] = r;
         if (r >= tile_n) continue;
         const uint32_t* row = s_rows + static_cast<size_t>(r) * W;
-        uint32_t slot = hash_key<D_CT>(row, D) & (kDedupSlots - 1);
+        uint32_t slot = hash_slot(hash_key<D_CT>(row, D), kDedupSlotBits);
         for (;;) {
             uint32_t o = s_owner[slot];
             if (o == 0u) {
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
         const uint32_t gid = gbase + s_lid[owner[k]];
         __stcs(a.grp_org + base + r, make_uint2(gid, row[D]));
         if (owner[k] == r) {  // the candidate row of this key
-            uint32_t* dst = a.rows1 + static_cast<size_t>(gid) * W;
+            uint32_t* dst = (kHashPasses & 1 ? a.rows0 : a.rows1) + static_cast<size_t>(gid) * W;
             for (int c = 0; c < D; ++c) dst[c] = row[c];
             dst[D] = gid;
             const uint32_t last = row[D - 1];

@@ -312,8 +312,10 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
         return;
     }
     pk[0] = 0u;
-    // AoS mode builds the rows in buffer 0; hash mode sorts its candidate rows from buffer 1
-    uint32_t cur = allow_hash ? 1u : 0u, executed = 0, first = static_cast<uint32_t>(P), prev = static_cast<uint32_t>(P);
+    // AoS mode builds the rows in buffer 0; hash mode sorts its candidate rows from the buffer the
+    // grouped rows are not in
+    uint32_t cur = (allow_hash && !(kHashPasses & 1)) ? 1u : 0u, executed = 0, first = static_cast<uint32_t>(P),
+             prev = static_cast<uint32_t>(P);
     for (int p = 0; p < P; ++p) {
         const int comp = D - 1 - (p >> 2);
         const bool ex = ((vary[comp] >> (8 * (p & 3))) & 255u) != 0u;
@@ -351,7 +353,8 @@ __global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* p
 // Histogram of the first executed pass when it lies outside component D-1
 // (only then; exits immediately otherwise).
 struct HistArgs {
-    const uint32_t* rows;
+    const uint32_t* rows;    // buffer 0; the rows of the first executed pass are in rows_alt when its
+    const uint32_t* rows_alt;  // source parity says so (hash mode)
     uint32_t* hist;
     const uint32_t* plan;
     const uint32_t* status;
@@ -365,6 +368,8 @@ __global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
     const uint32_t mode = a.plan[pk_base(4 * a.dim)];
     if (*a.status || a.plan[3] == 0u || mode == 1u) return;
     const uint32_t n = mode == 2u ? *a.n_cand : a.n;
+    const int Pd = 4 * a.dim;
+    const uint32_t* rows = a.plan[4 + Pd + a.plan[2]] ? a.rows_alt : a.rows;
     __shared__ uint32_t s_h[256];
     s_h[threadIdx.x] = 0u;
     __syncthreads();
@@ -375,7 +380,7 @@ __global__ void __launch_bounds__(kBlock) k_first_hist(HistArgs a) {
     uint32_t rl = 0u;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * kBlock)
-        rl_push(rl, (__ldcs(a.rows + i * W + comp) >> shift) & 255u, s_h);
+        rl_push(rl, (__ldcs(rows + i * W + comp) >> shift) & 255u, s_h);
     if ((rl >> 8) != 0u) atomicAdd(s_h + (rl & 255u), rl >> 8);
     __syncthreads();
     if (s_h[threadIdx.x]) atomicAdd(a.hist + p * 256 + threadIdx.x, s_h[threadIdx.x]);

@@ -52,9 +52,9 @@ __device__ __forceinline__ uint32_t pick_word(const uint4& v, int comp) {
 template <int W_CT>
 struct SortMinBlocks { static constexpr int v = (W_CT == 4 || W_CT == 5) ? 2 : 3; };
 
-// HASHED (hash mode, rmx_hash.cuh): the digit is byte 2 + pass of hash_key(row) -- two passes
-// group the whole vertex set by the top 16 bits of its key hash (a.hist / a.counters are then the
-// hashed passes' own arrays, a.pass is 0 or 1, rows0 -> rows1 -> rows0).
+// HASHED (hash mode, rmx_hash.cuh): the digit is byte (4 - kHashPasses + pass) of hash_key(row) --
+// kHashPasses passes group the whole vertex set by the top bits of its key hash (a.hist / a.counters
+// are then the hashed passes' own arrays, rows0 -> rows1 -> ...).
 template <int W_CT, int IPT, bool HASHED = false>
 __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(SortArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
     const uint32_t* __restrict__ in = src ? a.rows1 : a.rows0;
     uint32_t* __restrict__ out = src ? a.rows0 : a.rows1;
     const int comp = a.dim - 1 - (a.pass >> 2);
-    const int shift = HASHED ? 16 + 8 * a.pass : 8 * (a.pass & 3);
+    const int shift = HASHED ? kHashShift0 + 8 * a.pass : 8 * (a.pass & 3);
     const uint32_t epoch = HASHED ? 200u + static_cast<uint32_t>(a.pass) : static_cast<uint32_t>(a.pass) + 1u;
     const int nxt = HASHED ? P : static_cast<int>(plan[4 + 2 * P + a.pass]);
     // passes 0..3 are counted by K1b; later ones by the pass before them
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
                 for (int u = 0; u < U; ++u) {
                     const uint32_t q = q0 + u * kBlock;
                     if (q < tile_n) {
-                        if constexpr (HASHED) {
+                        if constexpr (HASHED) {  // the digit again (a cached digit per slot costs a CTA/SM)
                             const uint32_t row[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
                             dst[u] = s_gdst[digit_of(row)] + q;
                         } else {

@@ -16,26 +16,15 @@ pytestmark = pytest.mark.gpu
 M32 = np.uint64(0xFFFFFFFF)
 
 
-def _rotl(x, r):
-    return ((x << np.uint64(r)) | (x >> np.uint64(32 - r))) & M32
-
-
 def hash_key(words: np.ndarray) -> np.ndarray:
-    """Mirror of rmx_hash.cuh:hash_key over rows of uint32 words (murmur3-style, seed 0x9747b28c)."""
+    """Mirror of rmx_hashfn.cuh:hash_key over rows of uint32 words."""
     w = words.astype(np.uint64)
     h = np.full(w.shape[0], 0x9747B28C, np.uint64)
     for c in range(w.shape[1]):
-        k = (w[:, c] * np.uint64(0xCC9E2D51)) & M32
-        k = _rotl(k, 15)
-        k = (k * np.uint64(0x1B873593)) & M32
-        h ^= k
-        h = _rotl(h, 13)
-        h = (h * np.uint64(5) + np.uint64(0xE6546B64)) & M32
-    h ^= h >> np.uint64(16)
-    h = (h * np.uint64(0x85EBCA6B)) & M32
+        h = ((h ^ w[:, c]) * np.uint64(0x9E3779B1)) & M32
+    h ^= h >> np.uint64(15)
+    h = (h * np.uint64(0x85EBCA77)) & M32
     h ^= h >> np.uint64(13)
-    h = (h * np.uint64(0xC2B2AE35)) & M32
-    h ^= h >> np.uint64(16)
     return h.astype(np.uint32)
 
 
@@ -153,3 +142,16 @@ def test_hash_off_matches(rmx, monkeypatch):
     monkeypatch.setenv("RMX_HASH", "0")
     check(rmx, words, idx)
     assert plan_mode(rmx, words, idx)[0] == 0
+
+
+def test_constant_last_component(rmx):
+    """The last component is constant: the candidates' first executed AoS pass is pass 4, whose
+    histogram k_first_hist builds from the candidate buffer."""
+    rng = np.random.default_rng(6)
+    V = 40_000
+    words = rng.integers(0, 2**32, size=(V, 4), dtype=np.uint64).astype(np.uint32)
+    words[:, 3] = np.uint32(0x3F800000)
+    words[rng.integers(0, V, 12000)] = words[rng.integers(0, V, 12000)]
+    idx = rng.integers(0, V, size=(V // 3, 3)).astype(np.uint32)
+    check(rmx, words, idx)
+    assert plan_mode(rmx, words, idx)[0] == 2
