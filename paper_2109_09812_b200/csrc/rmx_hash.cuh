@@ -132,8 +132,8 @@ constexpr int kDedupSlotBits = 12;
 constexpr int kDedupSlots = 1 << kDedupSlotBits;  // open-addressing table: load factor <= 1/2
 static_assert(kDedupSlots == 2 * kHashTile, "dedup table sized for one tile at load factor 1/2");
 
-__host__ __device__ constexpr size_t hash_dedup_smem(int D) {
-    return static_cast<size_t>(kHashTile) * (D + 1) * 4 + kDedupSlots * 4 + kHashTile * 4;
+__host__ __device__ constexpr size_t hash_dedup_smem(int D) {  // two staging buffers, table, local ids
+    return 2 * static_cast<size_t>(kHashTile) * (D + 1) * 4 + kDedupSlots * 4 + kHashTile * 4 + 32;
 }
 
 // One tile of hash-grouped rows: its distinct keys (shared-memory table keyed by the
@@ -144,29 +144,40 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
     const int D = D_CT > 0 ? D_CT : a.dim;
     const int W = D + 1;
     if (*a.status || !hash_mode(a.plan, D)) return;  // uniform
-    uint32_t* s_rows = dyn_smem<uint32_t>();                          // [kHashTile * W]
-    uint32_t* s_owner = s_rows + static_cast<size_t>(kHashTile) * W;   // [kDedupSlots] row + 1, 0 = free
-    uint32_t* s_lid = s_owner + kDedupSlots;                           // [kHashTile] local id of a representative
+    uint32_t* s_buf = dyn_smem<uint32_t>();                                  // [2][kHashTile * W] staging
+    uint32_t* s_owner = s_buf + 2 * static_cast<size_t>(kHashTile) * W;       // [kDedupSlots] row + 1, 0 = free
+    uint32_t* s_lid = s_owner + kDedupSlots;                                  // [kHashTile] local id of a representative
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_lid + kHashTile);         // [2] staging barriers
     __shared__ uint32_t s_warp[kWarps];
     __shared__ uint32_t s_hist[4 * 256];
     __shared__ uint32_t s_base;
     const uint32_t tid = threadIdx.x;
+    const uint32_t* grouped = kHashPasses & 1 ? a.rows1 : a.rows0;
+    // tiles blockIdx.x, + gridDim.x, ...: the next tile's bulk copy runs while this one is deduplicated
+    auto issue = [&](uint32_t tile, uint32_t b) {
+        const uint32_t base = tile * static_cast<uint32_t>(kHashTile);
+        const uint32_t tn = min(static_cast<uint32_t>(kHashTile), a.n - base);
+        stage_tile(s_buf + b * static_cast<size_t>(kHashTile) * W, grouped + static_cast<size_t>(base) * W,
+                   tn * W * 4u, s_bar + b);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        mbar_init(s_bar + 1, 1);
+        fence_mbar_init();
+        if (blockIdx.x < a.ntiles) issue(blockIdx.x, 0u);
+    }
     for (uint32_t i = tid; i < 4u * 256u; i += kBlock) s_hist[i] = 0u;
     uint32_t rl[4] = {0u, 0u, 0u, 0u};
-    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // persistent: a no-op launch is cheap
+    uint32_t it = 0;
+    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++it) {  // persistent: a no-op launch is cheap
     const uint32_t base = tile * static_cast<uint32_t>(kHashTile);
     const uint32_t tile_n = min(static_cast<uint32_t>(kHashTile), a.n - base);
+    const uint32_t* s_rows = s_buf + (it & 1u) * static_cast<size_t>(kHashTile) * W;
     for (uint32_t i = tid; i < static_cast<uint32_t>(kDedupSlots); i += kBlock) s_owner[i] = 0u;
-    {  // stage the tile's rows (coalesced)
-        const uint32_t* src = (kHashPasses & 1 ? a.rows1 : a.rows0) + static_cast<size_t>(base) * W;
-        if (W == 4) {
-            for (uint32_t i = tid; i < tile_n; i += kBlock)
-                reinterpret_cast<uint4*>(s_rows)[i] = __ldcs(reinterpret_cast<const uint4*>(src) + i);
-        } else {
-            for (uint32_t i = tid; i < tile_n * W; i += kBlock) s_rows[i] = __ldcs(src + i);
-        }
-    }
+    // the other buffer was released by the barrier that ended the previous tile
+    if (tid == 0 && tile + gridDim.x < a.ntiles) issue(tile + gridDim.x, (it + 1u) & 1u);
     __syncthreads();
+    mbar_wait(s_bar + (it & 1u), (it >> 1) & 1u);
     // insert / find every row's key; owner = the row that holds the key's slot
     uint32_t owner[kHashTileRows];
 #pragma unroll
