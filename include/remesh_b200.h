@@ -158,6 +158,10 @@ int rmx_kernel_launches(uint32_t dim);
  * calls, all threads): the difference around a region counts its launches. */
 unsigned long long rmx_kernel_launches_total(void);
 
+/* Checked builds only (-DRMX_CHECKED): scattered stores whose index was past its array, summed over
+ * the process (synchronises the device); RMX_EINVAL in ordinary builds. */
+int rmx_debug_oob_count(unsigned long long* out);
+
 /* Sort plan of the last call that used `workspace` (host-side diagnostic; it
  * reads the device plan, so it synchronises `stream`).  Digit passes whose
  * 8-bit digit is constant over all keys are skipped; when at most 64 key bits

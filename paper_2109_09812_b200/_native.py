@@ -27,7 +27,7 @@ RMX_MAX_DIM = 32
 EXPORTS = (
     "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex", "rmx_lean_workspace_bytes",
     "rmx_lean_result_offset", "rmx_reindex_lean",
-    "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches", "rmx_kernel_launches_total",
+    "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches", "rmx_kernel_launches_total", "rmx_debug_oob_count",
     "rmx_last_executed_passes", "rmx_plan_info", "rmx_plan_key_info", "rmx_plan_guess_info", "rmx_hash_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
     "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy", "rmx_offset_indices",
@@ -68,6 +68,7 @@ _SIGNATURES = {
     "rmx_stage_count": (_int, [_u32]),
     "rmx_kernel_launches": (_int, [_u32]),
     "rmx_kernel_launches_total": (ctypes.c_ulonglong, []),
+    "rmx_debug_oob_count": (_int, [ctypes.POINTER(ctypes.c_ulonglong)]),
     "rmx_stage_name": (ctypes.c_char_p, [_u32, _int]),
     "rmx_last_executed_passes": (_int, [_vp, _u64, _u32, _vp]),
     "rmx_plan_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),

@@ -61,5 +61,7 @@ if __name__ == "__main__":
     import sys
     if "--phases" in sys.argv:
         print(build(defines=("RMX_PHASES",), output=os.path.join(HERE, "librmx_b200_phases.so")))
+    elif "--checked" in sys.argv:  # bounds-counting build for tools/sanitize_probe.py (RMX_LIB=...)
+        print(build(defines=("RMX_CHECKED",), output=os.path.join(HERE, "librmx_b200_checked.so")))
     else:
         print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1100,6 +1100,18 @@ int rmx_kernel_launches(uint32_t dim) {
 
 unsigned long long rmx_kernel_launches_total(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int rmx_debug_oob_count(unsigned long long* out) {
+#ifdef RMX_CHECKED
+    if (!out) return RMX_EINVAL;
+    RMX_CHECK(cudaDeviceSynchronize());
+    RMX_CHECK(cudaMemcpyFromSymbol(out, g_rmx_oob, sizeof(*out)));
+    return RMX_OK;
+#else
+    (void)out;
+    return RMX_EINVAL;  // not a checked build
+#endif
+}
+
 int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + kMaxPackedPasses + 2 + 4; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {

@@ -19,6 +19,22 @@ __device__ __forceinline__ T* dyn_smem() {
     return reinterpret_cast<T*>(rmx_dyn_smem);
 }
 
+// Checked build (-DRMX_CHECKED, tools/checked_probe.py): every scattered store of the pipeline
+// counts an index past its array here (read by rmx_debug_oob_count); compiled out otherwise.
+// It stands in for compute-sanitizer, which this GPU pool does not run.
+#ifdef RMX_CHECKED
+__device__ unsigned long long g_rmx_oob;
+#define RMX_CHECK_INDEX(i, n)                                                              \
+    do {                                                                                    \
+        if (static_cast<unsigned long long>(i) >= static_cast<unsigned long long>(n))       \
+            atomicAdd(&g_rmx_oob, 1ull);                                                    \
+    } while (0)
+#else
+#define RMX_CHECK_INDEX(i, n) \
+    do {                      \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

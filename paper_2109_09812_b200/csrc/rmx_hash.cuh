@@ -233,6 +233,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
         if (r >= tile_n) continue;
         const uint32_t* row = s_rows + static_cast<size_t>(r) * W;
         const uint32_t gid = gbase + s_lid[owner[k]];
+        RMX_CHECK_INDEX(gid, a.n);
+        RMX_CHECK_INDEX(base + r, a.n);
         __stcs(a.grp_org + base + r, make_uint2(gid, row[D]));
         if (owner[k] == r) {  // the candidate row of this key
             uint32_t* dst = (kHashPasses & 1 ? a.rows0 : a.rows1) + static_cast<size_t>(gid) * W;
@@ -296,6 +298,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fil
     __syncthreads();
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
         const uint2 p = s_pairs[q];
+        RMX_CHECK_INDEX(s_bglob[p.x >> bs] + q, a.n);
+        RMX_CHECK_INDEX(p.x, a.n);
         pairs[s_bglob[p.x >> bs] + q] = p;
     }
     __syncthreads();  // the next tile reuses the shared arrays

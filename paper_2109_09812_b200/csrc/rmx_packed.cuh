@@ -1218,6 +1218,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
         for (int u = 0; u < U; ++u) {
             const uint32_t q = q0 + u * kBlock;
             if (q < tile_n) {
+                RMX_CHECK_INDEX(dst[u], a.n);
                 out_k[dst[u]] = k[u];
                 out_v[dst[u]] = v[u];
                 if (emit_next) a.digits_out[dst[u]] = static_cast<uint8_t>(k[u] >> (shift + 8));
@@ -1450,6 +1451,7 @@ __device__ __forceinline__ void sort_pk2_body(const SortPkArgs& a, uint32_t* sme
             val = s_v[q];
         }
         const uint32_t dst = s_gdst[static_cast<uint32_t>(key >> shift) & 255u] + q;
+        RMX_CHECK_INDEX(dst, a.n);
         if constexpr (KW == 1 && OUT == kPkOutPairs) {
             reinterpret_cast<uint2*>(ob)[dst] = make_uint2(static_cast<uint32_t>(key), val);
         } else {
@@ -1694,6 +1696,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
             const uint32_t org = vreg[r];
             s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
             const bool head = (bal[r] >> lane) & 1u;
+            RMX_CHECK_INDEX(nidx, a.n);
             if (head) ukeys[nidx] = kreg[r];
             if (a.sc_org) a.sc_org[base + p] = org;
             if (a.sc_nodup) a.sc_nodup[base + p] = head ? 1 : 0;
@@ -1707,6 +1710,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
         const uint2 pr = s_pairs[q];
+        RMX_CHECK_INDEX(s_bglob[pr.x >> bs] + q, a.n);
         pairs[s_bglob[pr.x >> bs] + q] = pr;
     }
     __syncthreads();

@@ -225,7 +225,10 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t q = q0 + u * kBlock;
-                    if (q < tile_n) o4[dst[u]] = v[u];
+                    if (q < tile_n) {
+                        RMX_CHECK_INDEX(dst[u], n);
+                        o4[dst[u]] = v[u];
+                    }
                 }
             }
         } else {
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
                 const uint32_t c = q - slot * W;
                 const size_t p = s_src[slot];
                 const uint32_t dd = digit_of(s_rows + p * W);
+                RMX_CHECK_INDEX(s_gdst[dd] + slot, n);
                 out[static_cast<size_t>(s_gdst[dd] + slot) * W + c] = s_rows[p * W + c];
             }
         }

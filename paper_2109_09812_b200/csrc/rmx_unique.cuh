@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
                 s_pairs[atomicAdd(s_bcur + (org >> bs), 1u)] = make_uint2(org, nidx);
                 const bool head = (bal[r] >> lane) & 1u;
                 if (head) {
+                    RMX_CHECK_INDEX(nidx, n);
                     uint32_t* dst = a.out_vtx + static_cast<size_t>(nidx) * D;
                     for (int c = 0; c < D; ++c) dst[c] = row[c];
                 }
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
         // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
         for (uint32_t q = tid; q < tile_n; q += kBlock) {
             const uint2 pr = s_pairs[q];
+            RMX_CHECK_INDEX(s_bglob[pr.x >> bs] + q, n);
             pairs[s_bglob[pr.x >> bs] + q] = pr;
         }
         __syncthreads();
@@ -237,10 +239,13 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
         for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; 2 * i < n; i += stride) {
             if (2 * i + 1 < n) {
                 const uint4 v = __ldcs(pairs + i);
+                RMX_CHECK_INDEX(v.x, n);
+                RMX_CHECK_INDEX(v.z, n);
                 map[v.x] = v.y;
                 map[v.z] = v.w;
             } else {
                 const uint2 v = reinterpret_cast<const uint2*>(pairs)[2 * i];
+                RMX_CHECK_INDEX(v.x, n);
                 map[v.x] = v.y;
             }
         }
@@ -250,10 +255,13 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
     if (2 * i + 1 < n) {
         const uint4 v = __ldcs(pairs + i);
+        RMX_CHECK_INDEX(v.x, n);
+        RMX_CHECK_INDEX(v.z, n);
         map[v.x] = v.y;
         map[v.z] = v.w;
     } else if (2 * i < n) {
         const uint2 v = reinterpret_cast<const uint2*>(pairs)[2 * i];
+        RMX_CHECK_INDEX(v.x, n);
         map[v.x] = v.y;
     }
 }

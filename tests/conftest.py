@@ -43,3 +43,23 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With the bounds-counting build loaded (RMX_LIB=.../librmx_b200_checked.so), report the
+    scattered stores whose index was past its array over the whole session, and fail on any."""
+    import ctypes
+    if "paper_2109_09812_b200._native" not in sys.modules:
+        return
+    native = sys.modules["paper_2109_09812_b200._native"]
+    if native._lib is None:
+        return
+    oob = ctypes.c_ulonglong(0)
+    try:
+        rc = native._lib.rmx_debug_oob_count(ctypes.byref(oob))
+    except Exception:  # noqa: BLE001 - no device / not loaded
+        return
+    if rc == 0:
+        print(f"\nchecked build: {oob.value} out-of-bounds scattered stores in this session")
+        if oob.value:
+            session.exitstatus = 1

@@ -1,6 +1,9 @@
-"""Small inputs through every kernel family, for compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small inputs through every kernel family -- for compute-sanitizer (memcheck / racecheck /
+synccheck) where it runs, and with the bounds-counting build where it does not:
 
     compute-sanitizer --tool memcheck python tools/sanitize_probe.py
+    python -m paper_2109_09812_b200.build --checked
+    RMX_LIB=paper_2109_09812_b200/librmx_b200_checked.so python tools/sanitize_probe.py
 
 * the one-CTA small path (k_small) and the large pipeline (RMX_SMALL=0) on packed keys (value and
   field ranks), AoS rows with scratch (onesweep look-back, mbarrier staging), hash mode (hashed
@@ -85,6 +88,11 @@ def main():
     for g in range(G):
         assert torch.equal(peers[g][offs[g]:offs[g] + counts[g]], src[bounds[g]:bounds[g + 1]])
     print("scatter rows ok", flush=True)
+    import ctypes
+    oob = ctypes.c_ulonglong(0)
+    if _native.lib().rmx_debug_oob_count(ctypes.byref(oob)) == 0:
+        print(f"checked build: {oob.value} out-of-bounds scattered stores", flush=True)
+        assert oob.value == 0
 
 
 if __name__ == "__main__":
