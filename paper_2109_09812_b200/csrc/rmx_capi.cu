@@ -586,6 +586,11 @@ constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
 // hash mode (rmx_hash.cuh) for keys wider than 64 bits: D in [3, kHashMaxDim]; RMX_HASH=0 turns it
 // off (read per call: tests switch it at run time)
 bool hash_possible(int D) { return D >= 3 && D <= kHashMaxDim; }
+// RMX_HASH_RAW=0: build the hash-mode rows in a separate pass (A/B)
+bool hash_raw_enabled() {
+    const char* e = std::getenv("RMX_HASH_RAW");
+    return !(e && e[0] == '0');
+}
 bool hash_enabled() {
     const char* e = std::getenv("RMX_HASH");
     return !(e && e[0] == '0');
@@ -609,9 +614,9 @@ int dispatch_hash_build(const HashArgs& a, cudaStream_t s) {
     }
 }
 
-template <int W_CT, int IPT>
+template <int W_CT, int IPT, bool RAW = false>
 int launch_hashed_pass(const SortArgs& a, cudaStream_t s) {
-    auto kern = k_sort_pass<W_CT, IPT, true>;
+    auto kern = k_sort_pass<W_CT, IPT, true, RAW>;
     const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
     int grid = 0;
     int rc = persistent_grid(kern, smem, a.ntiles, grid);
@@ -639,7 +644,10 @@ int launch_hash_groups(const HashArgs& ha, SortArgs sa, cudaStream_t s) {
     for (int hp = 0; hp < kHashPasses && rc == RMX_OK; ++hp) {
         sa.pass = hp;
         switch (ha.dim) {
-            case 3: rc = launch_hashed_pass<4, SortIpt<4>::v>(sa, s); break;
+            case 3:
+                rc = (hp == 0 && ha.hist_only) ? launch_hashed_pass<4, SortIpt<4>::v, true>(sa, s)
+                                               : launch_hashed_pass<4, SortIpt<4>::v>(sa, s);
+                break;
             case 4: rc = launch_hashed_pass<5, SortIpt<5>::v>(sa, s); break;
             default: rc = launch_hashed_pass<0, SortIpt<0>::v>(sa, s); break;
         }
@@ -850,10 +858,13 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                    L.D, vec};
         if ((rc = dispatch_pack(a, s))) return rc;
     }
+    // hash mode, float3 with aligned vertices: the first hashed pass stages the vertices itself and
+    // k_hash_build only counts the hashed digits (no row build: 16 B per row less written and read)
+    const int hash_raw = (L.D == 3 && vec && hash_raw_enabled()) ? 1 : 0;
     HashArgs ha{vtx, flags, idx, plan, rows0, rows1, reinterpret_cast<uint32_t*>(base + L.hhist),
                 reinterpret_cast<uint2*>(base + L.ukeys), reinterpret_cast<uint32_t*>(base + L.n_cand), hist,
                 reinterpret_cast<const uint32_t*>(base + L.rank_of), d_status, static_cast<uint32_t>(V),
-                L.ntiles_hash, L.D, vec};
+                L.ntiles_hash, L.D, vec, hash_raw};
     if (hash_ok && (rc = dispatch_hash_build(ha, s))) return rc;
     if ((rc = rec.mark())) return rc;
     for (int p = 0; p < kMaxPackedPasses; ++p) {
@@ -872,7 +883,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (hash_ok) {
         SortArgs hs{rows0, rows1, plan, reinterpret_cast<uint32_t*>(base + L.hhist), desc,
                     reinterpret_cast<uint32_t*>(base + L.hcounters), d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
-                    0, rank_force(), nullptr};
+                    0, rank_force(), nullptr, vtx, flags, idx};
         if ((rc = launch_hash_groups(ha, hs, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;

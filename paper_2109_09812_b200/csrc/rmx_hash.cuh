@@ -62,6 +62,7 @@ struct HashArgs {
     uint32_t ntiles;          // tiles of kHashTile rows
     int dim;
     int vec;                  // vtx 16-byte aligned
+    int hist_only;            // k_hash_build: histograms only (the first hashed pass stages the vertices)
 };
 
 // Cleaned (key words, origin) rows and the digit histograms of the two hashed passes.
@@ -103,7 +104,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_build(HashArgs a) {
                         for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
                     }
                     note(hash_key<3>(k[j], 3));
-                    __stcs(r4 + 4 * g + j, make_uint4(k[j][0], k[j][1], k[j][2], static_cast<uint32_t>(4 * g + j)));
+                    if (!a.hist_only)
+                        __stcs(r4 + 4 * g + j, make_uint4(k[j][0], k[j][1], k[j][2], static_cast<uint32_t>(4 * g + j)));
                 }
             }
             done = ng << 2;
@@ -115,9 +117,9 @@ __global__ void __launch_bounds__(kBlock) k_hash_build(HashArgs a) {
         uint32_t* dst = a.rows0 + i * W;
         for (int c = 0; c < D; ++c) {
             k[c] = __ldg(row + c);
-            dst[c] = k[c];
+            if (!a.hist_only) dst[c] = k[c];
         }
-        dst[D] = static_cast<uint32_t>(i);
+        if (!a.hist_only) dst[D] = static_cast<uint32_t>(i);
         note(hash_key<D_CT>(k, D));
     }
 #pragma unroll

@@ -31,6 +31,11 @@ struct SortArgs {
     int pass;
     int rank_force;  // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
     const uint32_t* n_cand;  // hash mode: the rows are the n_cand candidate rows
+    // hash mode, first hashed pass over D = 3 vertices (RAW): the tile is staged straight from the
+    // vertex words and the used flags, cleaned and given its origin on the way out
+    const uint32_t* raw_vtx;
+    const uint8_t* raw_flags;
+    const uint32_t* raw_idx;
 };
 
 template <int W_CT, int IPT>
@@ -55,8 +60,9 @@ struct SortMinBlocks { static constexpr int v = (W_CT == 4 || W_CT == 5) ? 2 : 3
 // HASHED (hash mode, rmx_hash.cuh): the digit is byte (4 - kHashPasses + pass) of hash_key(row) --
 // kHashPasses passes group the whole vertex set by the top bits of its key hash (a.hist / a.counters
 // are then the hashed passes' own arrays, rows0 -> rows1 -> ...).
-template <int W_CT, int IPT, bool HASHED = false>
+template <int W_CT, int IPT, bool HASHED = false, bool RAW = false>
 __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(SortArgs a) {
+    static_assert(!RAW || (HASHED && W_CT == 4), "raw staging: the first hashed pass over float3 vertices");
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     using T = SortTraits<W_CT, IPT>;
     constexpr int TILE = T::kTile;
@@ -87,6 +93,12 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
         if constexpr (HASHED) return (hash_key<W_CT - 1>(row, D) >> shift) & 255u;
         else return (row[comp] >> shift) & 255u;
     };
+    uint32_t repl[3] = {0u, 0u, 0u};  // RAW: the replacement row (pipeline.py:148)
+    if constexpr (RAW) {
+        const uint32_t r0 = a.raw_idx[0];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) repl[c] = __ldg(a.raw_vtx + static_cast<size_t>(r0) * 3 + c);
+    }
 
     uint32_t* smem = dyn_smem<uint32_t>();
     const size_t tw = static_cast<size_t>(TILE) * W;
@@ -120,7 +132,11 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
             s_misc[0] = t;
             if (t < ntiles) {
                 const uint32_t tn = min(static_cast<uint32_t>(TILE), n - t * static_cast<uint32_t>(TILE));
-                stage_tile(s_rows, in + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
+                if constexpr (RAW)  // vertex words [TILE * 3] then flags [TILE] (sizes round up to 16 B)
+                    stage_tile2(s_rows, a.raw_vtx + static_cast<size_t>(t) * TILE * 3, tn * 12u, s_rows + TILE * 3,
+                                a.raw_flags + static_cast<size_t>(t) * TILE, tn, s_bar);
+                else
+                    stage_tile(s_rows, in + static_cast<size_t>(t) * TILE * W, tn * W * 4u, s_bar);
             }
         }
         for (int i = tid; i < kWarps * 256; i += kBlock) s_whist[i] = 0u;
@@ -138,7 +154,11 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
             uint32_t d = 256u;
             if (p < tile_n) {
                 uint32_t key, nkey = 0;
-                if constexpr (HASHED) {
+                if constexpr (RAW) {
+                    key = 0u;
+                    const uint8_t* s_fl = reinterpret_cast<const uint8_t*>(s_rows + TILE * 3);
+                    d = digit_of(s_fl[p] ? s_rows + static_cast<size_t>(p) * 3 : repl);
+                } else if constexpr (HASHED) {
                     key = 0u;
                     d = digit_of(s_rows + static_cast<size_t>(p) * W);
                 } else if constexpr (W_CT == 4) {
@@ -208,7 +228,16 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const uint32_t q = q0 + u * kBlock;
-                    if (q < tile_n) v[u] = s4[s_src[q]];
+                    if (q < tile_n) {
+                        if constexpr (RAW) {  // cleaned row + its origin
+                            const uint32_t p = s_src[q];
+                            const uint8_t* s_fl = reinterpret_cast<const uint8_t*>(s_rows + TILE * 3);
+                            const uint32_t* r = s_fl[p] ? s_rows + static_cast<size_t>(p) * 3 : repl;
+                            v[u] = make_uint4(r[0], r[1], r[2], tile * static_cast<uint32_t>(TILE) + p);
+                        } else {
+                            v[u] = s4[s_src[q]];
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
