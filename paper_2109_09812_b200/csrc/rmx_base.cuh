@@ -73,8 +73,13 @@ constexpr uint32_t kValueSetBytes = 192 * 1024;  // k_valueset byte maps: sum of
 constexpr int kHashPasses = 3;       // hashed passes: the top 24 bits of the key hash (~9 rows per
                                      // bucket in C2s, so a dedup tile splits few keys)
 constexpr int kHashShift0 = 8 * (4 - kHashPasses);  // the first hashed digit's bit offset
-constexpr int kHashTileRows = 8;     // rows per thread in the hash tile kernels
-constexpr int kHashTile = kBlock * kHashTileRows;
+#ifndef RMX_HASH_ROWS
+#define RMX_HASH_ROWS 4
+#endif
+constexpr int kHashTileRows = RMX_HASH_ROWS;  // rows per thread in the hash tile kernels
+constexpr int kHashTile = kBlock * kHashTileRows;    // dedup tile
+constexpr int kPairsRows = 8;                        // k_hash_pairs: rows per thread
+constexpr int kPairsTile = kBlock * kPairsRows;
 constexpr int kHashMaxDim = 8;       // wider rows take the AoS path
 
 __host__ __device__ inline size_t pk_value_base(int P) { return pk_rank_base(P) + RMX_MAX_DIM; }

@@ -227,7 +227,7 @@ std::vector<SmemAttr> g_attr;
 
 template <typename K>
 int ensure_smem(K kernel, size_t smem) {
-    if (smem <= 48 * 1024) return RMX_OK;
+    if (smem <= 32 * 1024) return RMX_OK;  // (dynamic + static above 48 KB needs the opt-in)
     int dev = 0;
     RMX_CHECK(cudaGetDevice(&dev));
     const void* fn = reinterpret_cast<const void*>(kernel);
@@ -765,6 +765,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (V == 0) {  // every index is out of range; status is set
         return RMX_OK;
     }
+    // hash mode (rmx_hash.cuh) replaces the whole-set AoS sort unless the caller wants the scratch
+    // arrays of the stable sort (org_id, perm: only the AoS path produces them) or RMX_HASH=0
+    const bool hash_ok = !lean && hash_possible(L.D) && sc == nullptr && hash_enabled();
     // K1a varying bits of the cleaned vertex set, then the plan (packed, hash or AoS)
     const int vec = (aligned16(vtx) && aligned16(flags)) ? 1 : 0;
     const bool value_ranks = L.D <= kMaxRankDim && value_rank_enabled() && V >= value_rank_min_rows();
@@ -812,9 +815,6 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    // hash mode (rmx_hash.cuh) replaces the whole-set AoS sort unless the caller wants the scratch
-    // arrays of the stable sort (org_id, perm: only the AoS path produces them) or RMX_HASH=0
-    const bool hash_ok = !lean && hash_possible(L.D) && sc == nullptr && hash_enabled();
     RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0));
     RMX_CHECK(cudaGetLastError());
     uint32_t* repl = reinterpret_cast<uint32_t*>(base + L.repl);
@@ -950,7 +950,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                              static_cast<const uint32_t*>(d_status), L.D, 2, n_cand));
             RMX_CHECK(cudaGetLastError());
             int gp = 0;
-            if ((rc = persistent_grid(k_hash_pairs, 0, L.ntiles_hash, gp))) return rc;
+            if ((rc = persistent_grid(k_hash_pairs, 0, (V + kPairsTile - 1) / kPairsTile, gp))) return rc;
             RMX_CHECK(launch(k_hash_pairs, gp, kBlock, 0, s, ha, reinterpret_cast<uint32_t*>(base + L.fill2),
                              L.bucket_shift));
             RMX_CHECK(cudaGetLastError());

@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(kBlock) k_hash_build(HashArgs a) {
         if (s_hist[i]) atomicAdd(a.hhist + i, s_hist[i]);
 }
 
-constexpr int kDedupSlotBits = 12;
+__host__ __device__ constexpr int log2_ct(int x) { return x <= 1 ? 0 : 1 + log2_ct(x / 2); }
+constexpr int kDedupSlotBits = log2_ct(2 * kHashTile);
 constexpr int kDedupSlots = 1 << kDedupSlotBits;  // open-addressing table: load factor <= 1/2
 static_assert(kDedupSlots == 2 * kHashTile, "dedup table sized for one tile at load factor 1/2");
 
@@ -180,29 +181,58 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
     if (tid == 0 && tile + gridDim.x < a.ntiles) issue(tile + gridDim.x, (it + 1u) & 1u);
     __syncthreads();
     mbar_wait(s_bar + (it & 1u), (it >> 1) & 1u);
-    // insert / find every row's key; owner = the row that holds the key's slot
-    uint32_t owner[kHashTileRows];
+    // insert / find every row's key; owner = the row that holds the key's slot.  The first probe
+    // of all kHashTileRows rows is issued as a batch (loads, then CASes, then compares: several
+    // independent shared-memory round trips in flight per thread instead of one); the rows whose
+    // first slot holds another key continue probing one by one.
+    uint32_t owner[kHashTileRows], slot[kHashTileRows], o[kHashTileRows];
+    auto same_key = [&](uint32_t ra, uint32_t rb) -> bool {
+        if constexpr (D_CT == 3) {
+            const uint4 x = reinterpret_cast<const uint4*>(s_rows)[ra];
+            const uint4 y = reinterpret_cast<const uint4*>(s_rows)[rb];
+            return x.x == y.x && x.y == y.y && x.z == y.z;
+        } else {
+            bool same = true;
+            for (int c = 0; c < D; ++c) same = same && s_rows[static_cast<size_t>(ra) * W + c] == s_rows[static_cast<size_t>(rb) * W + c];
+            return same;
+        }
+    };
 #pragma unroll
     for (int k = 0; k < kHashTileRows; ++k) {
         const uint32_t r = tid + k * kBlock;
         owner[k] = r;
-        if (r >= tile_n) continue;
-        const uint32_t* row = s_rows + static_cast<size_t>(r) * W;
-        uint32_t slot = hash_slot(hash_key<D_CT>(row, D), kDedupSlotBits);
-        for (;;) {
-            uint32_t o = s_owner[slot];
-            if (o == 0u) {
-                o = atomicCAS(s_owner + slot, 0u, r + 1u);
-                if (o == 0u) break;  // r owns the slot
+        slot[k] = r < tile_n ? hash_slot(hash_key<D_CT>(s_rows + static_cast<size_t>(r) * W, D), kDedupSlotBits) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kHashTileRows; ++k) o[k] = tid + k * kBlock < tile_n ? s_owner[slot[k]] : 1u;
+#pragma unroll
+    for (int k = 0; k < kHashTileRows; ++k) {
+        const uint32_t r = tid + k * kBlock;
+        if (r < tile_n && o[k] == 0u) {
+            o[k] = atomicCAS(s_owner + slot[k], 0u, r + 1u);
+            if (o[k] == 0u) o[k] = r + 1u;  // r owns the slot
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kHashTileRows; ++k) {
+        const uint32_t r = tid + k * kBlock;
+        if (r >= tile_n || o[k] == r + 1u) continue;
+        if (same_key(o[k] - 1u, r)) {
+            owner[k] = o[k] - 1u;
+            continue;
+        }
+        uint32_t sl = slot[k];
+        for (;;) {  // the slot holds another key: linear probing
+            sl = (sl + 1u) & (kDedupSlots - 1);
+            uint32_t ow = s_owner[sl];
+            if (ow == 0u) {
+                ow = atomicCAS(s_owner + sl, 0u, r + 1u);
+                if (ow == 0u) break;  // r owns the slot
             }
-            const uint32_t* orow = s_rows + static_cast<size_t>(o - 1u) * W;
-            bool same = true;
-            for (int c = 0; c < D; ++c) same = same && orow[c] == row[c];
-            if (same) {
-                owner[k] = o - 1u;
+            if (same_key(ow - 1u, r)) {
+                owner[k] = ow - 1u;
                 break;
             }
-            slot = (slot + 1u) & (kDedupSlots - 1);
         }
     }
     // representatives (owner == self) numbered in row order: flags into s_lid, blocked scan
@@ -263,20 +293,21 @@ __global__ void __launch_bounds__(kBlock) k_hash_dedup(HashArgs a) {
 // per row is a DRAM read-modify-write of a random sector).  The pairs go to the
 // row buffer k_map_fill reads in hash mode (both are free by now).
 __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fill, int bs) {
+    const uint32_t ntiles = (a.n + kPairsTile - 1) / kPairsTile;
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !hash_mode(a.plan, a.dim)) return;
     uint2* pairs = reinterpret_cast<uint2*>(a.plan[0] ? a.rows1 : a.rows0);
-    __shared__ uint2 s_pairs[kHashTile];
+    __shared__ uint2 s_pairs[kPairsTile];
     __shared__ uint32_t s_bcnt[256], s_bcur[256], s_bglob[256], s_warp[kWarps];
     const uint32_t tid = threadIdx.x;
-    for (uint32_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {  // persistent: a no-op launch is cheap
-    const uint32_t base = tile * static_cast<uint32_t>(kHashTile);
-    const uint32_t tile_n = min(static_cast<uint32_t>(kHashTile), a.n - base);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // persistent: a no-op launch is cheap
+    const uint32_t base = tile * static_cast<uint32_t>(kPairsTile);
+    const uint32_t tile_n = min(static_cast<uint32_t>(kPairsTile), a.n - base);
     s_bcnt[tid] = 0u;
     __syncthreads();
-    uint2 pr[kHashTileRows];
+    uint2 pr[kPairsRows];
 #pragma unroll
-    for (int k = 0; k < kHashTileRows; ++k) {
+    for (int k = 0; k < kPairsRows; ++k) {
         const uint32_t r = tid + k * kBlock;
         pr[k] = make_uint2(0u, 0u);
         if (r < tile_n) {
@@ -295,7 +326,7 @@ __global__ void __launch_bounds__(kBlock) k_hash_pairs(HashArgs a, uint32_t* fil
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kHashTileRows; ++k)
+    for (int k = 0; k < kPairsRows; ++k)
         if (tid + k * kBlock < tile_n) s_pairs[atomicAdd(s_bcur + (pr[k].x >> bs), 1u)] = pr[k];
     __syncthreads();
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
