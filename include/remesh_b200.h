@@ -176,7 +176,9 @@ int rmx_plan_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
 int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 /* Diagnostic of the value-rank guess (D <= 4): info[4] = {key bits of the plan guessed from the
  * sample, value sets judged worth collecting (0/1), candidate components, full-pass check state
- * (bit 0 checked, bit 1 a row fell outside the sample)}. */
+ * (bit 0 checked, bit 1 a row fell outside the sample; bit 8 the plan was speculative -- the
+ * sample halves saw the same value sets, no full value-set pass --, bit 9 k_pack's check of the
+ * speculative plan failed and the skipped path ran)}. */
 int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
 /* Hash mode of the last call that used `workspace` (keys wider than 64 bits, no

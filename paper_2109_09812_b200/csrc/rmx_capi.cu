@@ -121,6 +121,7 @@ struct Layout {
     size_t gplan, svary, sfields; // the plan guessed from a sample of the rows, and its inputs
     size_t vsets_b;               // value sets of the odd sample blocks (saturation estimate)
     size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
+    size_t spec;                  // speculative value-rank plan: kSpecOn | kSpecMiss (k_pack's check)
     size_t rank_of;               // hash mode: new index of every candidate row
     size_t n_cand;                // hash mode: number of candidate rows
     size_t hhist, hcounters;      // hash mode: histograms and tile counters of the hashed passes
@@ -176,6 +177,7 @@ Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     L.n_cand = take(16);
     L.hhist = take(kHashPasses * 256 * 4);
     L.hcounters = take(kHashPasses * 4 + 16);
+    L.spec = take(16);
     L.sfields = take(vr_dim * kFieldWords * 4);
     L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
@@ -357,12 +359,18 @@ int dispatch_vary(const VaryArgs& a, cudaStream_t s) {
 }
 
 template <int D_CT>
-int launch_pack(const PackArgs& a, cudaStream_t s) {
+int launch_pack(const PackArgs& a, cudaStream_t s, bool with_check) {
     int grid = 0;
     int rc = persistent_grid(k_pack<D_CT>, 0, (static_cast<uint64_t>(a.n) + kBlock - 1) / kBlock, grid);
     if (rc) return rc;
     RMX_CHECK(launch(k_pack<D_CT>, grid, kBlock, 0, s, a));
     RMX_CHECK(cudaGetLastError());
+    if constexpr (D_CT >= 1 && D_CT <= kMaxRankDim) {
+        if (with_check) {  // speculative plans: the checking variant (the plain one exited then)
+            RMX_CHECK(launch(k_pack<D_CT, true>, grid, kBlock, 0, s, a));
+            RMX_CHECK(cudaGetLastError());
+        }
+    }
     return RMX_OK;
 }
 
@@ -405,13 +413,13 @@ int dispatch_valueset(const ValueSetArgs& a, int dim, cudaStream_t s) {
     }
 }
 
-int dispatch_pack(const PackArgs& a, cudaStream_t s) {
+int dispatch_pack(const PackArgs& a, cudaStream_t s, bool with_check = false) {
     switch (a.dim) {
-        case 1: return launch_pack<1>(a, s);
-        case 2: return launch_pack<2>(a, s);
-        case 3: return launch_pack<3>(a, s);
-        case 4: return launch_pack<4>(a, s);
-        default: return launch_pack<0>(a, s);
+        case 1: return launch_pack<1>(a, s, with_check);
+        case 2: return launch_pack<2>(a, s, with_check);
+        case 3: return launch_pack<3>(a, s, with_check);
+        case 4: return launch_pack<4>(a, s, with_check);
+        default: return launch_pack<0>(a, s, false);
     }
 }
 
@@ -586,6 +594,11 @@ constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
 // hash mode (rmx_hash.cuh) for keys wider than 64 bits: D in [3, kHashMaxDim]; RMX_HASH=0 turns it
 // off (read per call: tests switch it at run time)
 bool hash_possible(int D) { return D >= 3 && D <= kHashMaxDim; }
+// RMX_SPEC=0: no speculative value-rank plans (always the full value-set pass; A/B)
+bool spec_enabled() {
+    const char* e = std::getenv("RMX_SPEC");
+    return !(e && e[0] == '0');
+}
 // RMX_HASH_RAW=0: build the hash-mode rows in a separate pass (A/B)
 bool hash_raw_enabled() {
     const char* e = std::getenv("RMX_HASH_RAW");
@@ -783,13 +796,14 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         // pass found a row outside the sample or did not run)
         const uint32_t shift = V >= (1ull << 22) ? 6u : 0u;
         uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
+        uint32_t* spec = reinterpret_cast<uint32_t*>(base + L.spec);
         VaryArgs sa{vtx, flags, idx, svary, sfields, d_status, static_cast<uint32_t>(V), L.D, vec, shift,
-                    nullptr, nullptr, nullptr};
+                    nullptr, nullptr, nullptr, nullptr};
         if ((rc = dispatch_vary(sa, s))) return rc;
-        RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, 0));
+        RMX_CHECK(launch(k_plan, 1, 32, 0, s, svary, sfields, gplan, L.D, d_status, 0, nullptr));
         uint32_t* vsets_b = reinterpret_cast<uint32_t*>(base + L.vsets_b);
         ValueSetArgs va{vtx, flags, idx, gplan, sfields, vsets, svary, vstate, d_status, static_cast<uint32_t>(V),
-                        shift, vec, 0, gplan, 0};
+                        shift, vec, 0, gplan, 0, spec, 0};
         if (shift) {  // the sample's value sets, even blocks into vsets and odd blocks into vsets_b
             if ((rc = dispatch_valueset(va, L.D, s))) return rc;
             ValueSetArgs vb_args = va;
@@ -797,8 +811,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
             vb_args.parity = 1;
             if ((rc = dispatch_valueset(vb_args, L.D, s))) return rc;
         }
+        // (with two sample halves that saw the same value sets: speculate, kSpecOn)
         ValuePlanArgs pd{gplan, vsets, shift ? vsets_b : nullptr, nullptr, nullptr, d_status, L.D, 0, nullptr,
-                         nullptr, nullptr, nullptr, nullptr, nullptr};
+                         nullptr, nullptr, nullptr, nullptr, nullptr, spec, vstate, spec_enabled() ? 1 : 0, 0};
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
         va.shift = 0u;
         if ((rc = dispatch_valueset(va, L.D, s))) return rc;
@@ -807,23 +822,78 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         pd.vsets_b = nullptr;
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
         VaryArgs fa{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
-                    vstate, svary, sfields};
+                    vstate, svary, sfields, nullptr};
         if ((rc = dispatch_vary(fa, s))) return rc;
     } else {
         VaryArgs a{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
-                   nullptr, nullptr, nullptr};
+                   nullptr, nullptr, nullptr, nullptr};
         if ((rc = dispatch_vary(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
-    RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0));
+    RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0, nullptr));
     RMX_CHECK(cudaGetLastError());
+    if ((rc = rec.mark())) return rc;
+    // ---- packed keys (packed mode)
+    uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
+    uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
+    uint32_t* spec = reinterpret_cast<uint32_t*>(base + L.spec);
+    // rank tables and the new key layout (exact plan, value sets of the full pass); fallback = 1:
+    // the same after a failed speculative plan (each kernel exits unless kSpecMiss)
+    auto finish_value_plan = [&](int fallback) -> int {
+        uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
+        // second chance when a row fell outside the sample: value sets again with the exact packing
+        RMX_CHECK(launch(k_vsets_reset, 1, kBlock, 0, s, vsets, static_cast<uint32_t>(L.D * kValueWords), vstate,
+                         static_cast<const uint32_t*>(gplan), static_cast<const uint32_t*>(vary),
+                         static_cast<const uint32_t*>(svary), static_cast<const uint32_t*>(fields),
+                         static_cast<const uint32_t*>(sfields), L.D, static_cast<const uint32_t*>(d_status),
+                         static_cast<const uint32_t*>(fallback ? spec : nullptr)));
+        ValueSetArgs ra{vtx, flags, idx, plan, fields, vsets, nullptr, vstate, d_status, static_cast<uint32_t>(V),
+                        0u, vec, 1, gplan, 0, spec, fallback};
+        int rc2 = dispatch_valueset(ra, L.D, s);
+        if (rc2) return rc2;
+        ValuePlanArgs pa{plan, vsets, nullptr, rank16, vinv, d_status, L.D, 1, vstate, gplan, svary, sfields, vary,
+                         fields, spec, vstate, 0, fallback};
+        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
+        RMX_CHECK(cudaGetLastError());
+        return RMX_OK;
+    };
+    if (value_ranks && (rc = finish_value_plan(0))) return rc;
+    uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
+    const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
+    {
+        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
+                   L.D, vec, vary, spec, 0};
+        if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled()))) return rc;
+        if (value_ranks) {
+            // a speculative plan that k_pack's check failed (kSpecMiss): the path it skipped --
+            // full value-set pass with its check, decision, K1a, plan, second chance, rank tables --
+            // and the keys again (each kernel exits at once otherwise)
+            uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
+            RMX_CHECK(launch(k_spec_reset, 1, 256, 0, s, static_cast<const uint32_t*>(spec), vary, fields, vsets,
+                             vstate, L.D, static_cast<const uint32_t*>(d_status)));
+            ValueSetArgs fv{vtx, flags, idx, gplan, sfields, vsets, svary, vstate, d_status,
+                            static_cast<uint32_t>(V), 0u, vec, 0, gplan, 0, spec, 1};
+            if ((rc = dispatch_valueset(fv, L.D, s))) return rc;
+            ValuePlanArgs fd{gplan, vsets, nullptr, nullptr, nullptr, d_status, L.D, 0, nullptr, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, spec, vstate, 0, 1};
+            RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, fd));
+            VaryArgs fb{vtx, flags, idx, vary, fields, d_status, static_cast<uint32_t>(V), L.D, vec, 0u,
+                        vstate, svary, sfields, spec};
+            if ((rc = dispatch_vary(fb, s))) return rc;
+            RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0,
+                             static_cast<const uint32_t*>(spec)));
+            if ((rc = finish_value_plan(1))) return rc;
+            a.fallback = 1;
+            if ((rc = dispatch_pack(a, s))) return rc;
+        }
+    }
+    if ((rc = rec.mark())) return rc;
     uint32_t* repl = reinterpret_cast<uint32_t*>(base + L.repl);
     if (lean) {  // packed keys only; keep the replacement row (k_unpack_pk reads it after the vertices are gone)
         RMX_CHECK(launch(k_lean_prepare, 1, 32, 0, s, static_cast<const uint32_t*>(plan), vtx, idx, repl, L.D,
                          d_status));
         RMX_CHECK(cudaGetLastError());
     }
-    if ((rc = rec.mark())) return rc;
     // ---- AoS rows of the whole vertex set (AoS mode only).  With D <= 2 at most 64 bits vary,
     // which the packed key always holds (plan_body: every run is >= 1 bit, so <= 64 runs): no AoS
     // kernels then (their stage events are still recorded).
@@ -831,32 +901,6 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (aos) {
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
-    }
-    if ((rc = rec.mark())) return rc;
-    // ---- packed keys (packed mode) or hashes (hash mode)
-    uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
-    uint16_t* vinv = reinterpret_cast<uint16_t*>(base + L.vinv);
-    if (value_ranks) {  // rank tables and the new key layout (exact plan, value sets of the full pass)
-        uint32_t* vstate = reinterpret_cast<uint32_t*>(base + L.vstate);
-        // second chance when a row fell outside the sample: value sets again with the exact packing
-        RMX_CHECK(launch(k_vsets_reset, 1, kBlock, 0, s, vsets, static_cast<uint32_t>(L.D * kValueWords), vstate,
-                         static_cast<const uint32_t*>(gplan), static_cast<const uint32_t*>(vary),
-                         static_cast<const uint32_t*>(svary), static_cast<const uint32_t*>(fields),
-                         static_cast<const uint32_t*>(sfields), L.D, static_cast<const uint32_t*>(d_status)));
-        ValueSetArgs ra{vtx, flags, idx, plan, fields, vsets, nullptr, vstate, d_status, static_cast<uint32_t>(V),
-                        0u, vec, 1, gplan, 0};
-        if ((rc = dispatch_valueset(ra, L.D, s))) return rc;
-        ValuePlanArgs pa{plan, vsets, nullptr, rank16, vinv, d_status, L.D, 1, vstate, gplan, svary, sfields, vary,
-                         fields};
-        RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pa));
-        RMX_CHECK(cudaGetLastError());
-    }
-    uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
-    const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
-    {
-        PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
-                   L.D, vec};
-        if ((rc = dispatch_pack(a, s))) return rc;
     }
     // hash mode, float3 with aligned vertices: the first hashed pass stages the vertices itself and
     // k_hash_build only counts the hashed digits (no row build: 16 B per row less written and read)
@@ -1128,7 +1172,7 @@ int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + kMaxP
 const char* rmx_stage_name(uint32_t dim, int k) {
     static thread_local char buf[32];
     const int P = static_cast<int>(4 * dim);
-    static const char* head[] = {"start", "mark", "vary", "plan", "build_rows", "pack"};
+    static const char* head[] = {"start", "mark", "vary", "plan", "pack", "build_rows"};
     if (k >= 0 && k < 6) return head[k];
     k -= 6;
     if (k < kMaxPackedPasses) {
@@ -1203,11 +1247,14 @@ int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void
     RMX_CHECK(cudaMemcpyAsync(pk, base + L.gplan + pk_base(L.P) * 4, sizeof(pk), cudaMemcpyDeviceToHost, s));
     RMX_CHECK(cudaMemcpyAsync(vb, base + L.gplan + pk_value_base(L.P) * 4, sizeof(vb), cudaMemcpyDeviceToHost, s));
     RMX_CHECK(cudaMemcpyAsync(&st, base + L.vstate, 4, cudaMemcpyDeviceToHost, s));
+    uint32_t sp = 0;
+    RMX_CHECK(cudaMemcpyAsync(&sp, base + L.spec, 4, cudaMemcpyDeviceToHost, s));
     RMX_CHECK(cudaStreamSynchronize(s));
     info[0] = pk[0] ? pk[2] : 0u;  // key bits of the plan guessed from the sample
     info[1] = vb[0];               // 1: value sets judged worth collecting
     info[2] = vb[1];               // candidate components
-    info[3] = st;                  // kVstateChecked | kVstateMiss of the full pass
+    info[3] = st | (sp << 8);      // kVstateChecked | kVstateMiss of the full pass; bit 8: the plan was
+                                   // speculative (sample-saturated value sets), bit 9: k_pack's check failed
     return RMX_OK;
 }
 

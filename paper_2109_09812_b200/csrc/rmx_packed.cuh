@@ -58,15 +58,18 @@ __device__ __forceinline__ uint32_t field_rank(const uint32_t* set, uint32_t v) 
     return r + __popc(set[v >> 5] & ((1u << (v & 31u)) - 1u));
 }
 
+// sentinel: fields outside the set rank as 0xFFFF (k_pack's check of a speculative plan sees the
+// overflow above the component's width)
 __device__ __forceinline__ void build_field_tables(const uint32_t* fields, const uint32_t* rk, int D, uint16_t* s_rank,
-                                                   uint16_t* s_value) {
+                                                   uint16_t* s_value, bool sentinel = false) {
     for (int c = 0; c < D; ++c) {
         if (!(rk[c] >> 31)) continue;
         const uint32_t* set = fields + c * kFieldWords;
         for (uint32_t v = threadIdx.x; v < static_cast<uint32_t>(kFieldValues); v += blockDim.x) {
             const uint32_t r = field_rank(set, v);
-            if (s_rank) s_rank[c * kFieldValues + v] = static_cast<uint16_t>(r);
-            if (s_value && ((set[v >> 5] >> (v & 31u)) & 1u)) s_value[c * kFieldValues + r] = static_cast<uint16_t>(v);
+            const bool member = (set[v >> 5] >> (v & 31u)) & 1u;
+            if (s_rank) s_rank[c * kFieldValues + v] = static_cast<uint16_t>(sentinel && !member ? 0xFFFFu : r);
+            if (s_value && member) s_value[c * kFieldValues + r] = static_cast<uint16_t>(v);
         }
     }
 }
@@ -130,6 +133,7 @@ struct VaryArgs {
     const uint32_t* vstate;
     const uint32_t* sample_vary;
     const uint32_t* sample_fields;
+    const uint32_t* gate;  // the fallback after a failed speculative plan: runs only if *gate & kSpecMiss
 };
 
 constexpr uint32_t kVstateChecked = 1u, kVstateMiss = 2u, kVstateRedo = 4u;
@@ -189,6 +193,7 @@ template <int D_CT>
 __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status) return;  // uniform
+    if (a.gate && !(*a.gate & 2u)) return;  // (kSpecMiss)
     const int D = D_CT > 0 ? D_CT : a.dim;
     if (a.vstate) {
         const uint32_t st = *a.vstate;
@@ -313,6 +318,20 @@ __global__ void __launch_bounds__(kBlock) k_vary(VaryArgs a) {
         __syncthreads();
         if (threadIdx.x < static_cast<unsigned>(D) && s_vary[threadIdx.x]) atomicOr(a.vary + threadIdx.x, s_vary[threadIdx.x]);
     }
+}
+
+// The speculative plan failed k_pack's check (kSpecMiss): back to the state before the full
+// value-set pass, which the re-run then makes (K1a outputs, value sets and check state cleared).
+__global__ void k_spec_reset(const uint32_t* spec, uint32_t* vary, uint32_t* fields, uint32_t* vsets,
+                             uint32_t* vstate, int D, const uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*status || !(*spec & 2u)) return;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) vary[i] = 0u;
+    if (D <= kMaxRankDim) {
+        for (int i = threadIdx.x; i < D * kFieldWords; i += blockDim.x) fields[i] = 0u;
+        for (int i = threadIdx.x; i < D * kValueWords; i += blockDim.x) vsets[i] = 0u;
+    }
+    if (threadIdx.x == 0) *vstate = 0u;
 }
 
 // Cleaned row (D_CT <= kMaxRankDim words) -> packed key, one component at a
@@ -470,6 +489,33 @@ struct ValueMap {
         }
         return out;
     }
+    // k_pack under a speculative plan (k_value_plan: sample-saturated value sets, the sample's
+    // varying bits and field sets): the key as ranked_key / the plain packing, and in `miss` any
+    // sign that the row lies outside what the plan was made from -- a varying bit outside vmask, a
+    // field outside the field set (sentinel rank: bits above the component's width), a value
+    // outside the value set (rank 0xFFFF)
+    template <int DP>
+    __device__ __forceinline__ uint64_t checked_key(const RowPacker<DP>& pack, const uint32_t (&k)[DP],
+                                                    const uint16_t* __restrict__ rank16, const uint32_t (&ref)[DP],
+                                                    const uint32_t (&rmask)[DP], uint32_t (&vor)[DP],
+                                                    uint32_t (&vacc)[DP], uint32_t (&rmax)[DP]) const {
+        // (value ranks are on: k_value_plan fails a speculative plan that ends without them).  The
+        // check only accumulates here -- bits that differ from the replacement row, value bits,
+        // the largest rank -- and is decided once per thread (k_pack)
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < DP; ++c) {
+            uint32_t v = pack.value(c, k[c]);
+            vor[c] |= k[c] ^ ref[c];
+            vacc[c] |= v;
+            // branch-free: components without a value rank read an entry they then ignore
+            const uint32_t r = __ldg(rank16 + (static_cast<uint32_t>(c) << kMaxValueBits) + (v & 0xFFFFu));
+            rmax[c] = max(rmax[c], r);
+            v = (r & rmask[c]) | (v & ~rmask[c]);
+            out |= static_cast<uint64_t>(v) << nlo[c];
+        }
+        return out;
+    }
     // inverse (inv: [c][2^kMaxValueBits] value of every rank)
     __device__ __forceinline__ uint64_t from_rank(uint64_t key, const uint16_t* __restrict__ inv) const {
         uint64_t out = 0;
@@ -525,6 +571,8 @@ struct ValueSetArgs {
     int redo;
     const uint32_t* gplan;
     int parity;              // sample pass: even or odd sample blocks (two sets for the saturation test)
+    const uint32_t* spec;    // bit 0: speculative plan (k_value_plan) -- the full pass is not needed
+    int fallback;            // the re-run after a failed speculative plan: runs only if kSpecMiss
 };
 
 constexpr int kVsThreads = 1024;
@@ -548,6 +596,11 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
         sets = pk[0] == 1u && (a.shift != 0u || vb[0] == 1u) && vb[1] != 0u;
     }
     if (!sets) return;  // (the full pass: k_vary computes K1a's outputs instead)
+    if (a.fallback) {
+        if (!(*a.spec & 2u)) return;  // (kSpecMiss)
+    } else if (!a.redo && a.shift == 0u && a.spec && (*a.spec & 1u)) {
+        return;  // speculating: k_pack checks the rows
+    }
     // the full pass also checks every used row against the sample's varying bits and field sets
     const bool check = !a.redo && a.vstate != nullptr && a.shift == 0u;
     __shared__ uint32_t s_fset[D_CT * kFieldWords];  // the sample's field sets (check)
@@ -680,10 +733,12 @@ __global__ void __launch_bounds__(kVsThreads, 1) k_valueset(ValueSetArgs a) {
 __global__ void __launch_bounds__(kBlock) k_vsets_reset(uint32_t* vsets, uint32_t words, uint32_t* vstate,
                                                          const uint32_t* gplan, const uint32_t* vary,
                                                          const uint32_t* svary, const uint32_t* fields,
-                                                         const uint32_t* sfields, int D, const uint32_t* status) {
+                                                         const uint32_t* sfields, int D, const uint32_t* status,
+                                                         const uint32_t* gate) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     __shared__ uint32_t s_redo;
     if (*status || !(*vstate & kVstateMiss)) return;
+    if (gate && !(*gate & 2u)) return;  // the re-run after a failed speculative plan (kSpecMiss)
     if (threadIdx.x == 0) {
         const uint32_t* gvb = gplan + pk_value_base(4 * D);
         bool redo = false;
@@ -726,7 +781,17 @@ struct ValuePlanArgs {
     const uint32_t* sfields;
     const uint32_t* vary;
     const uint32_t* fields;
+    // speculation (decide after the sample): when every ranked component's two sample halves saw
+    // the same value set and value ranks pay, trust the sample -- no full value-set pass, K1a's
+    // outputs copied from the sample (vstate = checked) -- and let k_pack check every row
+    // (spec bit 0; a row outside sets bit 1 and the fallback re-plans without value ranks)
+    uint32_t* spec;
+    uint32_t* spec_vstate;
+    int spec_ok;
+    int fallback;  // the re-run after a failed speculative plan: runs only if kSpecMiss
 };
+
+constexpr uint32_t kSpecOn = 1u, kSpecMiss = 2u;
 
 __device__ __forceinline__ uint32_t bits_for(uint32_t count) { return count <= 1u ? 0u : 32u - __clz(count - 1u); }
 
@@ -735,16 +800,32 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
     __shared__ uint32_t s_warp[32];
     const int D = a.dim;
     if (*a.status || D > kMaxRankDim) return;
+    if (a.fallback && !(*a.spec & kSpecMiss)) return;
+    // the second decision (on the full pass's sets) has nothing new when speculating
+    if (!a.fallback && !a.final_pass && !a.vsets_b && a.spec && (*a.spec & kSpecOn)) return;
+    const bool spec = a.final_pass && a.spec && *a.spec == kSpecOn;  // (not after a miss)
     uint32_t* plan = a.plan;
     uint32_t* pk = plan + pk_base(4 * D);
     uint32_t* vb = plan + pk_value_base(4 * D);
-    if (pk[0] != 1u) return;
+    // a speculative plan must end with value ranks (k_pack's check assumes them): otherwise it
+    // counts as failed and the skipped path runs
+    auto spec_fail = [&]() {
+        if (spec && threadIdx.x == 0) atomicOr(a.spec, kSpecMiss);
+    };
+    if (pk[0] != 1u) {
+        spec_fail();
+        return;
+    }
     uint32_t cand = vb[1];
+    uint32_t unsat = 0u;  // components whose sample halves saw different value sets
     if (a.final_pass) {
         // the value sets hold the guessed packing's values: keep the components packed the same way
         // (after a miss the second chance collected them with the exact packing: all valid)
         const uint32_t* gvb = a.gplan + pk_value_base(4 * D);
-        if (a.gplan[pk_base(4 * D)] == 0u || gvb[0] != 1u) return;  // uniform
+        if (a.gplan[pk_base(4 * D)] == 0u || gvb[0] != 1u) {
+            spec_fail();
+            return;  // uniform
+        }
         const bool redone = (*a.vstate & kVstateRedo) != 0u;
         if (!redone) cand &= gvb[1];
         for (int c = 0; c < D && !redone; ++c) {
@@ -753,7 +834,10 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
             if (!same) cand &= ~(1u << c);
         }
     }
-    if (cand == 0u) return;  // uniform
+    if (cand == 0u) {
+        spec_fail();
+        return;  // uniform
+    }
     const uint32_t old_bits = pk[2], old_npass = pk[3], old_kw = pk[1];
     uint32_t w[kMaxRankDim], cnt[kMaxRankDim];
     for (int c = 0; c < D; ++c) w[c] = vb[4 + 4 * c + 1];
@@ -781,6 +865,7 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
             __syncthreads();
             const uint64_t est = ni ? static_cast<uint64_t>(tot) * nb / ni : (1ull << 32);
             cnt[c] = static_cast<uint32_t>(min(est, static_cast<uint64_t>(0xFFFFFFFFu)));
+            if (!(ni == tot && nb == tot)) unsat |= 1u << c;
         }
     }
     uint32_t ranked = 0, nbits = 0;
@@ -796,11 +881,23 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
         if (t == 0) {
             vb[0] = gain ? 1u : 0u;
             vb[1] = gain ? ranked : 0u;
+            if (a.vsets_b && a.spec_ok && gain && (unsat & ranked) == 0u) {
+                // a ranked field at the top of a 32-bit component leaves no room for the sentinel
+                const uint32_t* rk = plan + pk_rank_base(4 * D);
+                bool room = true;
+                for (int c = 0; c < D; ++c)
+                    if ((rk[c] >> 31) && vb[4 + 4 * c + 1] >= 32u) room = false;
+                if (room) {
+                    *a.spec = kSpecOn;
+                    *a.spec_vstate = kVstateChecked;
+                }
+            }
         }
         return;
     }
     if (!gain) {
         if (t == 0) vb[0] = 0u;
+        spec_fail();
         return;
     }
     for (int c = 0; c < D; ++c) {
@@ -813,6 +910,20 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
         uint16_t* inv = a.vinv + (static_cast<size_t>(c) << kMaxValueBits);
         uint16_t* rnk = a.rank16 + (static_cast<size_t>(c) << kMaxValueBits);
         uint32_t r = ex;
+        if (spec) {  // every value below 2^w: its rank, or 0xFFFF outside the set (k_pack's check)
+            __shared__ uint32_t s_pre[kValueWords];
+            s_pre[2 * t] = ex;
+            s_pre[2 * t + 1] = ex + __popc(s0);
+            __syncthreads();
+            for (uint32_t v = t; v < (1u << w[c]); v += 1024u) {  // coalesced stores
+                const uint32_t word = set[v >> 5], bit = 1u << (v & 31u);
+                const uint32_t rv = s_pre[v >> 5] + __popc(word & (bit - 1u));
+                rnk[v] = (word & bit) ? static_cast<uint16_t>(rv) : static_cast<uint16_t>(0xFFFFu);
+                if (word & bit) inv[rv] = static_cast<uint16_t>(v);
+            }
+            __syncthreads();  // s_pre is reused by the next component
+            continue;
+        }
         for (uint32_t h = 0; h < 2u; ++h) {
             uint32_t m = h ? s1 : s0;
             while (m) {
@@ -859,10 +970,15 @@ struct PackArgs {
     uint32_t n;
     int dim;
     int vec;
+    const uint32_t* vary;    // K1a varying bits (the check of a speculative plan)
+    uint32_t* spec;          // kSpecOn: check every row against the plan; kSpecMiss: a row failed
+    int fallback;            // the re-pack after a failed check (exits unless kSpecMiss)
 };
 
-template <int D_CT>
-__global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
+// CHECK: the variant that packs under a speculative plan and checks every used row (launched
+// next to the plain one; each exits unless the plan's state is its own)
+template <int D_CT, bool CHECK = false>
+__global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     const int D = D_CT > 0 ? D_CT : a.dim;
     const uint32_t* pk = a.plan + pk_base(4 * D);
@@ -870,11 +986,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
     constexpr int kLut = (D_CT > 0 && D_CT <= kMaxRankDim) ? D_CT * kFieldValues : 1;
     __shared__ uint16_t s_rank[kLut];
     if (*a.status || pk[0] != 1u) return;  // uniform (packed mode only)
+    if (a.fallback && !(*a.spec & kSpecMiss)) return;  // uniform
+    // speculative plan: the CHECK variant packs and checks every used row (D <= kMaxRankDim only:
+    // value ranks), the plain one exits
+    const bool spec_on = !a.fallback && a.spec && (*a.spec & kSpecOn);
+    if (spec_on != CHECK) return;
+    constexpr bool check = CHECK && D_CT > 0 && D_CT <= kMaxRankDim;
     const uint32_t nruns = pk[4];
     const bool wide = pk[1] == 2u;
     const uint32_t* rk = a.plan + pk_rank_base(4 * D);
     for (uint32_t i = threadIdx.x; i < 4 * nruns; i += kBlock) s_runs[i] = pk[8 + i];
-    if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(a.fields, rk, D_CT, s_rank, nullptr);
+    if constexpr (D_CT > 0 && D_CT <= kMaxRankDim) build_field_tables(a.fields, rk, D_CT, s_rank, nullptr, check);
     __syncthreads();
 
     const uint32_t r0 = a.idx[0];
@@ -902,6 +1024,22 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
         const RowPacker<D_CT> pack0(a.plan, s_runs, nruns, s_rank);
         ValueMap<D_CT> vm;
         vm.load(a.plan);
+        // the check's masks: bits outside K1a's varying bits, bits above the component's width (a
+        // field outside the field set ranks to the 0xFFFF sentinel), components with value ranks
+        uint32_t rmask[D_CT], vor[D_CT], vacc[D_CT], rmax[D_CT];
+#pragma unroll
+        for (int c = 0; c < D_CT; ++c) {
+            rmask[c] = check && ((vm.ranked >> c) & 1u) ? 0xFFFFFFFFu : 0u;
+            vor[c] = vacc[c] = rmax[c] = 0u;
+        }
+        if (check && !vm.on) {  // (k_value_plan marks this case failed already)
+            if (threadIdx.x == 0) atomicOr(a.spec, kSpecMiss);
+            return;
+        }
+        auto pack_used = [&](const uint32_t (&k)[D_CT]) -> uint64_t {
+            if constexpr (check) return vm.checked_key(pack0, k, a.rank16, ref, rmask, vor, vacc, rmax);
+            else return vm.on ? vm.ranked_key(pack0, k, a.rank16) : pack0(k);
+        };
         auto pack = [&](const uint32_t (&k)[D_CT]) { return vm.on ? vm.ranked_key(pack0, k, a.rank16) : pack0(k); };
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
@@ -920,11 +1058,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
                     uint64_t key[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        if (((f >> (8 * j)) & 255u) == 0u) {
+                        const bool used = ((f >> (8 * j)) & 255u) != 0u;
+                        if (!used) {
 #pragma unroll
                             for (int c = 0; c < 3; ++c) k[j][c] = ref[c];
                         }
-                        key[j] = pack(k[j]);
+                        // (an unused row stands for the replacement row, a used row: checking it is harmless)
+                        if constexpr (check) key[j] = pack_used(k[j]);
+                        else key[j] = pack(k[j]);
                     }
                     // 16-byte stores of 4 consecutive rows (vals_off is a multiple of 4 words)
                     if (wide) {
@@ -950,7 +1091,20 @@ __global__ void __launch_bounds__(kBlock, 4) k_pack(PackArgs a) {
             const bool used = a.flags[i] != 0;
 #pragma unroll
             for (int c = 0; c < D_CT; ++c) k[c] = used ? __ldg(a.vtx + i * D_CT + c) : ref[c];
-            put(i, pack(k));
+            if constexpr (check) put(i, pack_used(k));
+            else put(i, pack(k));
+        }
+        if constexpr (check) {  // a bit outside K1a's, a field outside the set (sentinel rank: bits
+                                // above the width), a value outside the set (rank 0xFFFF)
+            uint32_t miss = 0u;
+#pragma unroll
+            for (int c = 0; c < D_CT; ++c) {
+                miss |= vor[c] & ~__ldg(a.vary + c);
+                miss |= vm.w[c] < 32u ? vacc[c] >> vm.w[c] : 0u;
+                miss |= (rmask[c] && rmax[c] == 0xFFFFu) ? 1u : 0u;
+            }
+            miss = __reduce_or_sync(kFull, miss);
+            if ((threadIdx.x & 31u) == 0u && miss) atomicOr(a.spec, kSpecMiss);
         }
     } else {
         for (uint64_t i = start; i < a.n; i += stride) {

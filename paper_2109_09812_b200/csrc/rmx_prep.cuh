@@ -344,9 +344,10 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
 }
 
 __global__ void k_plan(const uint32_t* vary, const uint32_t* fields, uint32_t* plan, int D, const uint32_t* status,
-                       int allow_hash) {
+                       int allow_hash, const uint32_t* gate = nullptr) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || threadIdx.x != 0) return;
+    if (gate && !(*gate & 2u)) return;  // the fallback of a failed speculative plan (kSpecMiss)
     plan_body(vary, fields, plan, D, allow_hash != 0);
 }
 

@@ -218,7 +218,9 @@ def test_guess_from_the_sample_is_right(rmx):
     check(rmx, words, idx)
     guess = []
     assert plan_info(rmx, words, idx, guess)[2] == 10 + 10 + 4
-    assert guess[1] == 1 and guess[3] == 1  # worth collecting; checked, no row outside the sample, no redo
+    # worth collecting; the sample halves saw the same value sets, so the plan was speculative (bit
+    # 8: no full value-set pass, the check state copied as clean) and k_pack's check passed (no bit 9)
+    assert guess[1] == 1 and guess[3] == 1 | 256
 
 
 def test_small_meshes_skip_value_ranks(rmx, monkeypatch):
@@ -273,3 +275,42 @@ def test_outlier_field_in_the_last_full_width_candidate(rmx):
     packed, kw, bits, passes = plan_info(rmx, words, idx, guess)
     assert packed == 1 and passes == (bits + 7) // 8
     assert guess[3] & 3 == 3  # checked, and rows outside the sample were found
+
+
+@pytest.mark.parametrize("what", ["value", "bits", "field"])
+def test_speculative_plan_fails_the_check(rmx, monkeypatch, what):
+    """The sample's two halves see the same 300 values per axis, so the plan is made from the sample
+    alone (speculative: no full value-set pass).  Rows outside the sample carry a value the sample
+    never saw (same varying bits and fields), a varying bit it never saw, or a field it never saw:
+    k_pack's check of every row fails, the skipped path runs (full value-set pass, K1a, plan, rank
+    tables) and the keys are made again.  Exact either way; a new value keeps the value ranks."""
+    V = 3 * 1_400_000  # >= 2^22 rows: the sampled decision
+    rng = np.random.default_rng(113)
+    words = np.empty((V, 3), np.uint32)
+    sets = []
+    for c in range(3):
+        vals = value_set(rng, 300, 16)
+        sets.append(vals)
+        words[:, c] = BASE | (vals[rng.integers(0, 300, size=V)] << np.uint32(7))
+    out = np.flatnonzero(~_sample_mask(V))
+    far = out[rng.integers(0, len(out), size=20)]
+    if what == "value":
+        fresh = np.setdiff1d(np.arange(1, (1 << 16) - 1, dtype=np.uint32), sets[1])[:1]
+        words[far, 1] = BASE | (fresh[0] << np.uint32(7))
+    elif what == "bits":
+        words[far, 2] |= np.uint32(1 << 3)
+    else:
+        words[far, 0] = np.uint32(0x41200000) | (sets[0][5] << np.uint32(7))   # 10.0f's binade
+    idx = np.arange(V, dtype=np.uint32).reshape(-1, 3)
+    check(rmx, words, idx)
+    guess = []
+    packed, kw, bits, passes = plan_info(rmx, words, idx, guess)
+    assert packed == 1 and passes == (bits + 7) // 8
+    assert guess[3] & 0x300 == 0x300  # speculative, and the check failed
+    if what == "value":
+        assert guess[3] & 3 == 1      # the re-run's full pass: no row outside the sample's bits/fields
+        assert bits == 3 * bits_for(301)  # 300 / 301 values per axis: 9 bits each
+    monkeypatch.setenv("RMX_SPEC", "0")
+    plain_guess = []
+    assert plan_info(rmx, words, idx, plain_guess)[2] == bits  # the same plan without speculation
+    assert plain_guess[3] & 0x300 == 0

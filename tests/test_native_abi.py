@@ -37,7 +37,7 @@ def test_workspace_and_stage_queries():
     assert lib.rmx_workspace_bytes(10, 33, 4, 3) == 0
     n = lib.rmx_stage_count(3)
     names = [lib.rmx_stage_name(3, k).decode() for k in range(n)]
-    assert names[:6] == ["start", "mark", "vary", "plan", "build_rows", "pack"]
+    assert names[:6] == ["start", "mark", "vary", "plan", "pack", "build_rows"]
     assert names[6] == "pk_pass_0" and names[13] == "pk_pass_7"
     assert names[14:16] == ["hash_groups", "first_hist"]
     assert names[16] == "sort_pass_0" and names[27] == "sort_pass_11"
