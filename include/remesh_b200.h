@@ -181,6 +181,12 @@ int rmx_plan_key_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* 
  * speculative plan failed and the skipped path ran)}. */
 int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
+/* Soup mode of the last call that used `workspace` (synchronises `stream`): info[2] = {the index
+ * count I when soup mode ran -- strictly increasing indices and a packed plan: used vertex o is
+ * sorted with its index position as origin, so the map fill writes the output indices and no
+ * remap runs --, else 0; 1 if the indices were strictly increasing}. */
+int rmx_soup_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
+
 /* Hash mode of the last call that used `workspace` (keys wider than 64 bits, no
  * scratch requested; synchronises `stream`): info[4] = {ran in hash mode,
  * candidate rows (distinct keys per dedup tile), executed AoS passes over the

@@ -122,6 +122,9 @@ struct Layout {
     size_t vsets_b;               // value sets of the odd sample blocks (saturation estimate)
     size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
     size_t spec;                  // speculative value-rank plan: kSpecOn | kSpecMiss (k_pack's check)
+    size_t order;                 // bit 0: the indices are not strictly increasing (k_mark)
+    size_t soup;                  // soup mode: I when on (k_soup_decide), else 0
+    size_t soup_prefix;           // soup mode: used rows before every packed-sort tile
     size_t rank_of;               // hash mode: new index of every candidate row
     size_t n_cand;                // hash mode: number of candidate rows
     size_t hhist, hcounters;      // hash mode: histograms and tile counters of the hashed passes
@@ -178,6 +181,8 @@ Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     L.hhist = take(kHashPasses * 256 * 4);
     L.hcounters = take(kHashPasses * 4 + 16);
     L.spec = take(16);
+    L.order = take(16);
+    L.soup = take(16);
     L.sfields = take(vr_dim * kFieldWords * 4);
     L.markbits = take((static_cast<size_t>(V) + 31) / 32 * 4 + 16);
     L.hist = take(static_cast<size_t>(L.P) * 256 * 4);
@@ -193,6 +198,7 @@ Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     L.desc3 = take(lean ? 256 : static_cast<size_t>(L.ntiles3) * 8);
     L.repl = take((RMX_MAX_DIM + 4) * 4);  // lean: the replacement row (the vertex buffer is overwritten)
     L.tile_counts = take(static_cast<size_t>(L.ntiles3_pk) * 4);
+    L.soup_prefix = take(static_cast<size_t>(max_tiles_pk) * 4);
     L.ctl_end = off;
     L.total = off;
     return L;
@@ -594,6 +600,12 @@ constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
 // hash mode (rmx_hash.cuh) for keys wider than 64 bits: D in [3, kHashMaxDim]; RMX_HASH=0 turns it
 // off (read per call: tests switch it at run time)
 bool hash_possible(int D) { return D >= 3 && D <= kHashMaxDim; }
+// RMX_SOUP=0: no soup mode (strictly increasing indices: map fill into the output indices, no
+// remap; A/B)
+bool soup_enabled() {
+    const char* e = std::getenv("RMX_SOUP");
+    return !(e && e[0] == '0');
+}
 // RMX_SPEC=0: no speculative value-rank plans (always the full value-set pass; A/B)
 bool spec_enabled() {
     const char* e = std::getenv("RMX_SPEC");
@@ -761,7 +773,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // K1 mark (byte flags for in-order indices, a bit set for scattered ones), then merge them
     {
         uint32_t* bits = reinterpret_cast<uint32_t*>(base + L.markbits);
-        MarkArgs a{idx, I, V, flags, bits, d_status, aligned16(idx) ? 1 : 0};
+        MarkArgs a{idx, I, V, flags, bits, d_status, aligned16(idx) ? 1 : 0,
+                   reinterpret_cast<uint32_t*>(base + L.order)};
         int grid = 0;
         rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
         if (rc) return rc;
@@ -832,6 +845,25 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if ((rc = rec.mark())) return rc;
     RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0, nullptr));
     RMX_CHECK(cudaGetLastError());
+    // soup mode (rmx_packed.cuh k_soup_decide): strictly increasing indices + a packed plan; not with
+    // scratch (org_id holds origins), lean mode or the slot-exchange downsweep
+    uint32_t* soup = reinterpret_cast<uint32_t*>(base + L.soup);
+    uint32_t* soup_prefix = reinterpret_cast<uint32_t*>(base + L.soup_prefix);
+    const uint32_t* order = reinterpret_cast<const uint32_t*>(base + L.order);
+    const int soup_ok = (!lean && sc == nullptr && soup_enabled() && !ds2_enabled()) ? 1 : 0;
+    auto launch_soup = [&](const uint32_t* gate) -> int {
+        RMX_CHECK(launch(k_soup_decide, 1, 32, 0, s, static_cast<const uint32_t*>(plan), order, soup,
+                         static_cast<uint32_t>(I), L.D, soup_ok, static_cast<const uint32_t*>(d_status), gate));
+        int g = 0;
+        int rc2 = grid_for_stream(L.ntiles_pk, g);
+        if (rc2) return rc2;
+        RMX_CHECK(launch(k_soup_prefix, g, kBlock, 0, s, idx, static_cast<uint32_t>(I),
+                         static_cast<const uint32_t*>(soup), soup_prefix, L.ntiles_pk,
+                         static_cast<uint32_t>(pk_sort_tile()), static_cast<const uint32_t*>(d_status), gate));
+        RMX_CHECK(cudaGetLastError());
+        return RMX_OK;
+    };
+    if ((rc = launch_soup(nullptr))) return rc;
     if ((rc = rec.mark())) return rc;
     // ---- packed keys (packed mode)
     uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
@@ -882,6 +914,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
             if ((rc = dispatch_vary(fb, s))) return rc;
             RMX_CHECK(launch(k_plan, 1, 32, 0, s, vary, fields, plan, L.D, d_status, hash_ok ? 1 : 0,
                              static_cast<const uint32_t*>(spec)));
+            if ((rc = launch_soup(spec))) return rc;
             if ((rc = finish_value_plan(1))) return rc;
             a.fallback = 1;
             if ((rc = dispatch_pack(a, s))) return rc;
@@ -919,7 +952,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,
                      dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride,
-                     L.D, p, rank_force()};
+                     L.D, p, rank_force(), soup, soup_prefix, flags};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
@@ -991,7 +1024,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
             RMX_CHECK(launch(k_map_fill, grid, kBlock, 0, s, static_cast<const uint32_t*>(plan),
                              static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1),
                              reinterpret_cast<uint32_t*>(base + L.rank_of), static_cast<uint32_t>(V),
-                             static_cast<const uint32_t*>(d_status), L.D, 2, n_cand));
+                             static_cast<const uint32_t*>(d_status), L.D, 2, n_cand,
+                             static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr)));
             RMX_CHECK(cudaGetLastError());
             int gp = 0;
             if ((rc = persistent_grid(k_hash_pairs, 0, (V + kPairsTile - 1) / kPairsTile, gp))) return rc;
@@ -1003,13 +1037,14 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         RMX_CHECK(launch(k_map_fill, static_cast<unsigned>((threads + kBlock - 1) / kBlock), kBlock, 0, s,
                          static_cast<const uint32_t*>(plan), static_cast<const uint32_t*>(rows0),
                          static_cast<const uint32_t*>(rows1), map, static_cast<uint32_t>(V),
-                         static_cast<const uint32_t*>(d_status), L.D, 0, n_cand));
+                         static_cast<const uint32_t*>(d_status), L.D, 0, n_cand, static_cast<const uint32_t*>(soup),
+                         out_idx));
         RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
     // K4 remap
     {
-        RemapArgs a{idx, map, out_idx, I, d_status, (aligned16(idx) && aligned16(out_idx)) ? 1 : 0};
+        RemapArgs a{idx, map, out_idx, I, d_status, (aligned16(idx) && aligned16(out_idx)) ? 1 : 0, soup};
         int grid = 0;
         rc = grid_for_stream(a.vec ? (I + 3) / 4 : I, grid);
         if (rc) return rc;
@@ -1273,6 +1308,20 @@ int rmx_hash_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
     info[1] = hash ? nc : 0u;                      // candidate rows (distinct keys per dedup tile)
     info[2] = hash ? pl[1] : 0u;                   // executed AoS passes over the candidates
     info[3] = static_cast<uint32_t>(kHashTile);    // rows per dedup tile
+    return RMX_OK;
+}
+
+int rmx_soup_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t soup = 0, order = 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char* base = static_cast<const char*>(workspace);
+    RMX_CHECK(cudaMemcpyAsync(&soup, base + L.soup, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(&order, base + L.order, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    info[0] = soup;                    // soup mode: the index count I (0: off)
+    info[1] = (order & 1u) ? 0u : 1u;  // the indices were strictly increasing
     return RMX_OK;
 }
 

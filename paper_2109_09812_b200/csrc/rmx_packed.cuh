@@ -334,6 +334,41 @@ __global__ void k_spec_reset(const uint32_t* spec, uint32_t* vary, uint32_t* fie
     if (threadIdx.x == 0) *vstate = 0u;
 }
 
+// Soup mode: strictly increasing indices (k_mark: every used row referenced once, in row order --
+// triangle soups and their shards) and a packed plan with at least one pass.  Used row o then gets
+// the origin "used rows before o", which is its index position, so the map fill writes the output
+// indices directly (out_idx[position] = new index; unused rows get origins >= I and are skipped):
+// no map, no remap.  *soup = I when on, else 0.
+__global__ void k_soup_decide(const uint32_t* plan, const uint32_t* order, uint32_t* soup, uint32_t n_idx, int D,
+                              int allow, const uint32_t* status, const uint32_t* gate) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (threadIdx.x != 0 || *status) return;
+    if (gate && !(*gate & 2u)) return;  // the re-plan after a failed speculative plan (kSpecMiss)
+    const uint32_t* pk = plan + pk_base(4 * D);
+    *soup = (allow && !(*order & 1u) && pk[0] == 1u && pk[3] != 0u) ? n_idx : 0u;
+}
+
+// Soup mode: used rows before every packed-sort tile (rows tile_rows * t ..).  The indices are
+// strictly increasing, so that is the lower bound of the tile's first row in them.
+__global__ void __launch_bounds__(kBlock) k_soup_prefix(const uint32_t* idx, uint32_t n_idx, const uint32_t* soup,
+                                                        uint32_t* prefix, uint32_t ntiles, uint32_t tile_rows,
+                                                        const uint32_t* status, const uint32_t* gate) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*status || !*soup) return;
+    if (gate && !(*gate & 2u)) return;  // (after a failed speculative plan: kSpecMiss)
+    const uint32_t stride = gridDim.x * kBlock;
+    for (uint32_t t = blockIdx.x * kBlock + threadIdx.x; t < ntiles; t += stride) {
+        const uint64_t key = static_cast<uint64_t>(t) * tile_rows;
+        uint32_t lo = 0, hi = n_idx;
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if (__ldg(idx + mid) < key) lo = mid + 1;
+            else hi = mid;
+        }
+        prefix[t] = lo;
+    }
+}
+
 // Cleaned row (D_CT <= kMaxRankDim words) -> packed key, one component at a
 // time: component c occupies key bits [lo_c, lo_c + w_c) (rmx_base.cuh), its
 // value cv_c is its first run (src0, mask0 -> bit 0 of cv; in registers), any
@@ -1165,6 +1200,12 @@ struct SortPkArgs {
     int dim;
     int pass;
     int rank_force;        // -1 = choose per pass; else kRankMatch / kRankBallot / kRankAtomic
+    // soup mode (k_soup_decide): pass 0 gives used row o the origin "used rows before o" (= its
+    // index position) and unused rows I + "unused rows before o", from the used flags and the
+    // per-tile used counts (k_soup_prefix)
+    const uint32_t* soup;
+    const uint32_t* soup_prefix;
+    const uint8_t* flags;
 };
 
 // The upsweep counts kUpGroup consecutive tiles per CTA iteration so every digit's
@@ -1256,6 +1297,46 @@ struct SortPkTraits {
     }
 };
 
+// Soup mode, pass 0: the origin of every row of the tile into s_vals (the pass stages keys only):
+// used row o -> used rows before o (its index position), unused row o -> I + unused rows before o.
+// The tile's used flags were staged into s_flags with the keys.  Thread t takes rows t*IPT ..
+// (t+1)*IPT - 1: byte-parallel counts, one block scan, branch-free origins (the downsweep body has
+// no predicate registers to spare).
+template <int IPT>
+__device__ __forceinline__ void soup_origins(const SortPkArgs& a, uint32_t* s_vals, const uint8_t* s_flags,
+                                             uint32_t* s_warp, uint32_t base, uint32_t tile_n, uint32_t tile) {
+    static_assert(IPT % 4 == 0, "whole flag words per thread");
+    constexpr int NW = IPT / 4;
+    const uint32_t r0 = threadIdx.x * IPT;
+    const uint32_t* f32 = reinterpret_cast<const uint32_t*>(s_flags) + threadIdx.x * NW;
+    uint32_t w[NW], cnt = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        // nonzero bytes -> 0x01 per byte; rows at or past tile_n count as unused
+        const uint32_t x = f32[i];
+        const uint32_t nz = (((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
+        const uint32_t p0 = r0 + 4u * i;
+        const uint32_t keep = p0 + 4u <= tile_n ? 0xFFFFFFFFu : (p0 >= tile_n ? 0u : (1u << (8u * (tile_n - p0))) - 1u);
+        w[i] = (nz >> 7) & keep;
+        cnt += __popc(w[i]);
+    }
+    uint32_t tot;
+    uint32_t before = a.soup_prefix[tile] + block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+    const uint32_t un0 = *a.soup + base;  // unused row p: I + (base + p - used rows before p)
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t u = (w[i] >> (8 * j)) & 1u;
+            const uint32_t p = r0 + 4u * i + j;
+            o[j] = u * before + (1u - u) * (un0 + p - before);
+            before += u;
+        }
+        reinterpret_cast<uint4*>(s_vals + r0)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 template <int KW, int IPT>
 __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it) {
     using Key = typename PkKey<KW>::T;
@@ -1283,14 +1364,19 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const uint32_t base = tile * static_cast<uint32_t>(TILE);
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
-    // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none)
+    // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none), or in
+    // soup mode the soup origins it makes in s_vals
     const bool iota = a.pass == 0;
+    const bool soup_on = iota && a.soup && *a.soup != 0u;
     if (tid == 0) {
         if (it == 0) {
             mbar_init(s_bar, 1);
             fence_mbar_init();
         }
-        if (iota)
+        if (soup_on)  // + the used flags (into the slot-index array, free until the scatter)
+            stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_src, a.flags + base,
+                        tile_n, s_bar);
+        else if (iota)
             stage_tile(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_bar);
         else
             stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_vals, in_v + base,
@@ -1307,6 +1393,10 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     }
     __syncthreads();
     mbar_wait(s_bar, it & 1u);
+    if (soup_on) {
+        soup_origins<IPT>(a, s_vals, reinterpret_cast<const uint8_t*>(s_src), s_warp, base, tile_n, tile);
+        __syncthreads();  // the flags are read before the scatter overwrites s_src
+    }
 
     uint32_t pk[IPT];
     if (tile_n == static_cast<uint32_t>(TILE)) {  // full tile: no validity tests
@@ -1360,7 +1450,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
             if (q < tile_n) {
                 const uint32_t p = s_src[q];
                 k[u] = s_keys[p];
-                v[u] = iota ? base + p : s_vals[p];
+                v[u] = iota && !soup_on ? base + p : s_vals[p];
             }
         }
 #pragma unroll
@@ -1592,7 +1682,7 @@ __device__ __forceinline__ void sort_pk2_body(const SortPkArgs& a, uint32_t* sme
     }
     __syncthreads();
     // slot order out: consecutive slots of one digit are consecutive global rows
-#pragma unroll 4
+#pragma unroll 1
     for (uint32_t q = tid; q < tile_n; q += NT) {
         Key key;
         uint32_t val;
@@ -1686,7 +1776,7 @@ __device__ __forceinline__ void head_count_body(const HeadCountArgs& a) {
             }
             from = max(end4, base);
         }
-#pragma unroll 4
+#pragma unroll 1
         for (uint64_t g = from + threadIdx.x; g < end; g += kBlock)
             cnt += (g == 0 || __ldg(keys + g) != __ldg(keys + g - 1)) ? 1u : 0u;
         cnt = warp_sum(cnt);

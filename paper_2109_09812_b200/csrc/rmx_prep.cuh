@@ -24,6 +24,7 @@ struct MarkArgs {
     uint32_t* bits;   // [ceil(n_vtx / 32)] zeroed
     uint32_t* status;
     int vec;          // idx 16-byte aligned
+    uint32_t* order;  // bit 0 set: the indices are not strictly increasing (soup mode, rmx_packed.cuh)
 };
 
 __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
@@ -31,7 +32,7 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31u;
-    bool bad = false;
+    bool bad = false, unordered = false;  // unordered: some idx[i] >= idx[i + 1]
     uint64_t done = 0;
     if (a.vec) {
         const uint64_t n4 = a.n_idx >> 2;
@@ -48,6 +49,13 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
                 x[2] = v.z;
                 x[3] = v.w;
             }
+            // order: within the group, and against the next group's first index (the next lane's,
+            // or a load when the next group is another warp's or the scalar tail's)
+            uint32_t nx = __shfl_down_sync(kFull, x[0], 1);
+            if ((lane == 31u || i + 1 >= n4) && 4 * (i + 1) < a.n_idx) nx = __ldg(a.idx + 4 * (i + 1));
+            if (i < n4)
+                unordered = unordered || !(x[0] < x[1] && x[1] < x[2] && x[2] < x[3] &&
+                                           (4 * (i + 1) >= a.n_idx || x[3] < nx));
             uint32_t lo = 0xFFFFFFFFu, hi = 0u;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -76,8 +84,10 @@ __global__ void __launch_bounds__(kBlock) k_mark(MarkArgs a) {
         const uint32_t x = __ldcs(a.idx + i);
         if (x < a.n_vtx) a.flags[x] = 1;
         else bad = true;
+        if (i + 1 < a.n_idx && !(x < __ldg(a.idx + i + 1))) unordered = true;
     }
     if (__any_sync(kFull, bad) && lane == 0u) atomicOr(a.status, RMX_STATUS_INDEX_OUT_OF_RANGE);
+    if (__any_sync(kFull, unordered) && lane == 0u && a.order) atomicOr(a.order, 1u);
 }
 
 // flags |= bit set (one word of 32 vertices per thread; words with no bit

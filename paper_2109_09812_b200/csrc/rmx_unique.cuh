@@ -227,10 +227,16 @@ __global__ void __launch_bounds__(kBlock) k_unique(UniqueArgs a) {
 __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const uint32_t* rows0,
                                                       const uint32_t* rows1, uint32_t* map, uint32_t n,
                                                       const uint32_t* status, int dim, int mode_want,
-                                                      const uint32_t* n_cand) {
+                                                      const uint32_t* n_cand, const uint32_t* soup,
+                                                      uint32_t* out_idx) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status) return;
     const bool hash = plan[pk_base(4 * dim)] == 2u;
+    // soup mode (rmx_packed.cuh k_soup_decide): origins below I are index positions -- the map is
+    // the output; origins >= I are unused rows, which no index reads
+    const uint32_t n_used = (mode_want == 0 && soup) ? *soup : 0u;
+    if (n_used) map = out_idx;
+    const uint32_t lim = n_used ? n_used : 0xFFFFFFFFu;
     if (mode_want == 2) {
         if (!hash) return;
         n = *n_cand;
@@ -257,12 +263,12 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
         const uint4 v = __ldcs(pairs + i);
         RMX_CHECK_INDEX(v.x, n);
         RMX_CHECK_INDEX(v.z, n);
-        map[v.x] = v.y;
-        map[v.z] = v.w;
+        if (v.x < lim) map[v.x] = v.y;
+        if (v.z < lim) map[v.z] = v.w;
     } else if (2 * i < n) {
         const uint2 v = reinterpret_cast<const uint2*>(pairs)[2 * i];
         RMX_CHECK_INDEX(v.x, n);
-        map[v.x] = v.y;
+        if (v.x < lim) map[v.x] = v.y;
     }
 }
 
@@ -275,11 +281,12 @@ struct RemapArgs {
     uint64_t n_idx;
     const uint32_t* status;
     int vec;
+    const uint32_t* soup;  // soup mode: the map fill wrote the output indices already
 };
 
 __global__ void __launch_bounds__(kBlock) k_remap(RemapArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
-    if (*a.status) return;
+    if (*a.status || (a.soup && *a.soup)) return;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
     const uint64_t gtid = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;
     uint64_t done = 0;
