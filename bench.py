@@ -231,21 +231,23 @@ def mask_list(m):
     return "[" + ",".join(str(c) for c in range(32) if (m >> c) & 1) + "]"
 
 
-def executed_model(V, I, U, D, KW, npass, value_ranks=False):
+def executed_model(V, I, U, D, KW, npass, value_ranks=False, spec=False, soup=False):
     """Algorithmic HBM bytes of one packed-path step (the kernels that ran)."""
     passes = sum(8 * KW + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass))
     return int((4 * I + 2 * V)                       # mark: indices in, flags cleared + set
                # K1a: rows + flags -- with value ranks over a 1/64 sample only, the full value-set pass
-               # (sample + full) checks the rows against it instead
+               # (sample + full) checks the rows against it instead; a speculative plan (sample
+               # halves saw the same value sets) skips the full pass, k_pack checks the rows
                + ((4 * D + 1) * V // 64 if value_ranks else (4 * D + 1) * V)
-               + ((4 * D + 1) * V * 65 // 64 if value_ranks else 0)
+               + ((4 * D + 1) * V * (1 if spec else 65) // 64 if value_ranks else 0)
                + (4 * D + 1) * V + (4 * KW + 1) * V  # pack: rows + flags in, keys + digit 0 out
                + passes * V                          # LSD passes
+               + (V if soup else 0)                  # soup mode: pass 0 reads the used flags
                + 4 * KW * V                          # head count
                + (4 * KW + 12) * V + 4 * KW * U      # unique: keys + origins in, pairs + unique keys out
                + (4 * KW + 4 * D) * U                # unpack
-               + 12 * V                              # map fill: pairs in, map out
-               + 12 * I)                             # remap: indices + map in, indices out
+               + 12 * V                              # map fill: pairs in, map (soup: output indices) out
+               + (0 if soup else 12 * I))            # remap: indices + map in, indices out
 
 
 def device_workload(cfg: str, dev, stream, rank: int = 0):
@@ -301,6 +303,12 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
     kinfo = (ctypes.c_uint32 * 4)()
     _native.check(lib.rmx_plan_key_info(ws.data_ptr(), V, D, stream.cuda_stream, kinfo))
     field_mask, value_mask, bits_before_vr = int(kinfo[0]), int(kinfo[1]), int(kinfo[2])
+    ginfo = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_plan_guess_info(ws.data_ptr(), V, D, stream.cuda_stream, ginfo))
+    spec = (int(ginfo[3]) >> 8) & 3 == 1  # speculative plan, check passed
+    sinfo = (ctypes.c_uint32 * 2)()
+    _native.check(lib.rmx_soup_info(ws.data_ptr(), V, D, stream.cuda_stream, sinfo))
+    soup = int(sinfo[0]) != 0
 
     # per-stage CUDA events for every timed step (recorded on the launching stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
@@ -357,15 +365,15 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
     # packed pass: keys + origins in and out, the digit byte read by its upsweep and the next
     # pass's digit byte written (pass 0 reads no origins: they are the row numbers; the last pass
     # writes no next digit) -- mean over the executed passes; AoS pass: rows in and out
-    if packed:
+    if packed:  # (soup mode: pass 0 also reads the used flags)
         per_pass = [8 * key_words + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < executed else 0)
-                    for p in range(executed)]
+                    + (1 if soup and p == 0 else 0) for p in range(executed)]
         pass_bytes = sum(per_pass) / len(per_pass) * V
     else:
         pass_bytes = 2 * row_bytes * n_rows
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
-    executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0)
+    executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0, spec, soup)
                       if packed else None)
     res = {
         "V": V, "E": E, "D": D, "K": K, "U": expect_u, "ms": ms, "ms_staged": ms_staged, "stage_ms": stage_ms,
@@ -380,6 +388,8 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
                              f"{bits_before_vr} bits before value ranks)" if packed
                              else f"{D} x u32 words"),
                      "hash_mode": hinfo,
+                     "speculative_value_plan": spec if packed else None,
+                     "soup_mode": soup,
                      "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
                      "executed_passes": executed, "nominal_passes": 4 * D},
         "executed_bytes": executed_bytes,
