@@ -639,9 +639,9 @@ int dispatch_hash_build(const HashArgs& a, cudaStream_t s) {
     }
 }
 
-template <int W_CT, int IPT, bool RAW = false>
+template <int W_CT, int IPT, bool RAW = false, bool SOUP = false>
 int launch_hashed_pass(const SortArgs& a, cudaStream_t s) {
-    auto kern = k_sort_pass<W_CT, IPT, true, RAW>;
+    auto kern = k_sort_pass<W_CT, IPT, true, RAW, SOUP>;
     const size_t smem = SortTraits<W_CT, IPT>::smem_bytes(a.dim + 1);
     int grid = 0;
     int rc = persistent_grid(kern, smem, a.ntiles, grid);
@@ -670,8 +670,12 @@ int launch_hash_groups(const HashArgs& ha, SortArgs sa, cudaStream_t s) {
         sa.pass = hp;
         switch (ha.dim) {
             case 3:
-                rc = (hp == 0 && ha.hist_only) ? launch_hashed_pass<4, SortIpt<4>::v, true>(sa, s)
-                                               : launch_hashed_pass<4, SortIpt<4>::v>(sa, s);
+                if (hp == 0 && ha.hist_only) {  // the raw pass: plain and soup-mode variants (one runs)
+                    rc = launch_hashed_pass<4, SortIpt<4>::v, true>(sa, s);
+                    if (!rc) rc = launch_hashed_pass<4, SortIpt<4>::v, true, true>(sa, s);
+                } else {
+                    rc = launch_hashed_pass<4, SortIpt<4>::v>(sa, s);
+                }
                 break;
             case 4: rc = launch_hashed_pass<5, SortIpt<5>::v>(sa, s); break;
             default: rc = launch_hashed_pass<0, SortIpt<0>::v>(sa, s); break;
@@ -851,15 +855,20 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint32_t* soup_prefix = reinterpret_cast<uint32_t*>(base + L.soup_prefix);
     const uint32_t* order = reinterpret_cast<const uint32_t*>(base + L.order);
     const int soup_ok = (!lean && sc == nullptr && soup_enabled() && !ds2_enabled()) ? 1 : 0;
+    // hash mode, float3 with aligned vertices: the first hashed pass stages the vertices itself and
+    // k_hash_build only counts the hashed digits (no row build: 16 B per row less written and read)
+    const int hash_raw = (L.D == 3 && vec && hash_raw_enabled()) ? 1 : 0;
     auto launch_soup = [&](const uint32_t* gate) -> int {
         RMX_CHECK(launch(k_soup_decide, 1, 32, 0, s, static_cast<const uint32_t*>(plan), order, soup,
-                         static_cast<uint32_t>(I), L.D, soup_ok, static_cast<const uint32_t*>(d_status), gate));
+                         static_cast<uint32_t>(I), L.D, soup_ok, hash_raw, static_cast<const uint32_t*>(d_status),
+                         gate));
         int g = 0;
         int rc2 = grid_for_stream(L.ntiles_pk, g);
         if (rc2) return rc2;
         RMX_CHECK(launch(k_soup_prefix, g, kBlock, 0, s, idx, static_cast<uint32_t>(I),
-                         static_cast<const uint32_t*>(soup), soup_prefix, L.ntiles_pk,
-                         static_cast<uint32_t>(pk_sort_tile()), static_cast<const uint32_t*>(d_status), gate));
+                         static_cast<const uint32_t*>(soup), soup_prefix, static_cast<uint64_t>(V),
+                         static_cast<uint32_t>(pk_sort_tile()), static_cast<uint32_t>(sort_tile(4)),
+                         static_cast<const uint32_t*>(plan), L.D, static_cast<const uint32_t*>(d_status), gate));
         RMX_CHECK(cudaGetLastError());
         return RMX_OK;
     };
@@ -935,9 +944,6 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         BuildArgs a{vtx, flags, idx, rows0, hist, plan, d_status, static_cast<uint32_t>(V), L.D, vec};
         if ((rc = dispatch_build(a, s))) return rc;
     }
-    // hash mode, float3 with aligned vertices: the first hashed pass stages the vertices itself and
-    // k_hash_build only counts the hashed digits (no row build: 16 B per row less written and read)
-    const int hash_raw = (L.D == 3 && vec && hash_raw_enabled()) ? 1 : 0;
     HashArgs ha{vtx, flags, idx, plan, rows0, rows1, reinterpret_cast<uint32_t*>(base + L.hhist),
                 reinterpret_cast<uint2*>(base + L.ukeys), reinterpret_cast<uint32_t*>(base + L.n_cand), hist,
                 reinterpret_cast<const uint32_t*>(base + L.rank_of), d_status, static_cast<uint32_t>(V),
@@ -960,7 +966,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     if (hash_ok) {
         SortArgs hs{rows0, rows1, plan, reinterpret_cast<uint32_t*>(base + L.hhist), desc,
                     reinterpret_cast<uint32_t*>(base + L.hcounters), d_status, static_cast<uint32_t>(V), L.ntiles, L.D,
-                    0, rank_force(), nullptr, vtx, flags, idx};
+                    0, rank_force(), nullptr, vtx, flags, idx, soup, soup_prefix};
         if ((rc = launch_hash_groups(ha, hs, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;

@@ -339,23 +339,30 @@ __global__ void k_spec_reset(const uint32_t* spec, uint32_t* vary, uint32_t* fie
 // the origin "used rows before o", which is its index position, so the map fill writes the output
 // indices directly (out_idx[position] = new index; unused rows get origins >= I and are skipped):
 // no map, no remap.  *soup = I when on, else 0.
+// Hash mode: the same when its first hashed pass stages the vertices itself (raw_ok: float3,
+// aligned) -- the origins are made there.
 __global__ void k_soup_decide(const uint32_t* plan, const uint32_t* order, uint32_t* soup, uint32_t n_idx, int D,
-                              int allow, const uint32_t* status, const uint32_t* gate) {
+                              int allow, int raw_ok, const uint32_t* status, const uint32_t* gate) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (threadIdx.x != 0 || *status) return;
     if (gate && !(*gate & 2u)) return;  // the re-plan after a failed speculative plan (kSpecMiss)
     const uint32_t* pk = plan + pk_base(4 * D);
-    *soup = (allow && !(*order & 1u) && pk[0] == 1u && pk[3] != 0u) ? n_idx : 0u;
+    const bool mode_ok = (pk[0] == 1u && pk[3] != 0u) || (pk[0] == 2u && raw_ok);
+    *soup = (allow && !(*order & 1u) && mode_ok) ? n_idx : 0u;
 }
 
-// Soup mode: used rows before every packed-sort tile (rows tile_rows * t ..).  The indices are
-// strictly increasing, so that is the lower bound of the tile's first row in them.
+// Soup mode: used rows before every tile of the pass that makes the origins (rows tile_rows * t ..:
+// the packed sort's tiles, or hash mode's first hashed pass's).  The indices are strictly
+// increasing, so that is the lower bound of the tile's first row in them.
 __global__ void __launch_bounds__(kBlock) k_soup_prefix(const uint32_t* idx, uint32_t n_idx, const uint32_t* soup,
-                                                        uint32_t* prefix, uint32_t ntiles, uint32_t tile_rows,
+                                                        uint32_t* prefix, uint64_t n_rows, uint32_t tile_pk,
+                                                        uint32_t tile_hash, const uint32_t* plan, int D,
                                                         const uint32_t* status, const uint32_t* gate) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || !*soup) return;
     if (gate && !(*gate & 2u)) return;  // (after a failed speculative plan: kSpecMiss)
+    const uint32_t tile_rows = plan[pk_base(4 * D)] == 2u ? tile_hash : tile_pk;
+    const uint32_t ntiles = static_cast<uint32_t>((n_rows + tile_rows - 1) / tile_rows);
     const uint32_t stride = gridDim.x * kBlock;
     for (uint32_t t = blockIdx.x * kBlock + threadIdx.x; t < ntiles; t += stride) {
         const uint64_t key = static_cast<uint64_t>(t) * tile_rows;

@@ -36,6 +36,11 @@ struct SortArgs {
     const uint32_t* raw_vtx;
     const uint8_t* raw_flags;
     const uint32_t* raw_idx;
+    // RAW in soup mode (rmx_packed.cuh k_soup_decide): used row o gets the origin "used rows before
+    // o" (its index position), unused row o I + "unused rows before o"; soup_prefix: used rows
+    // before every tile
+    const uint32_t* soup;
+    const uint32_t* soup_prefix;
 };
 
 template <int W_CT, int IPT>
@@ -60,9 +65,10 @@ struct SortMinBlocks { static constexpr int v = (W_CT == 4 || W_CT == 5) ? 2 : 3
 // HASHED (hash mode, rmx_hash.cuh): the digit is byte (4 - kHashPasses + pass) of hash_key(row) --
 // kHashPasses passes group the whole vertex set by the top bits of its key hash (a.hist / a.counters
 // are then the hashed passes' own arrays, rows0 -> rows1 -> ...).
-template <int W_CT, int IPT, bool HASHED = false, bool RAW = false>
+template <int W_CT, int IPT, bool HASHED = false, bool RAW = false, bool SOUP = false>
 __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(SortArgs a) {
     static_assert(!RAW || (HASHED && W_CT == 4), "raw staging: the first hashed pass over float3 vertices");
+    static_assert(!SOUP || RAW, "soup origins are made by the raw pass");
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     using T = SortTraits<W_CT, IPT>;
     constexpr int TILE = T::kTile;
@@ -73,6 +79,9 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
     const uint32_t* plan = a.plan;
     const bool hash = plan[pk_base(P)] == 2u;
     if (HASHED ? !hash : plan[4 + a.pass] == 0u) return;  // constant digit (or not this mode): nothing moves
+    if constexpr (RAW) {  // the soup variant and the plain one: the one that matches runs
+        if ((a.soup && *a.soup != 0u) != SOUP) return;
+    }
     // AoS mode sorts the whole vertex set, hash mode its n_cand candidate rows (HASHED: all rows)
     const uint32_t n = (hash && !HASHED) ? *a.n_cand : a.n;
     const uint32_t ntiles = (n + static_cast<uint32_t>(TILE) - 1u) / static_cast<uint32_t>(TILE);
@@ -145,6 +154,14 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
         if (tile >= ntiles) break;
         const uint32_t tile_n = min(static_cast<uint32_t>(TILE), n - tile * static_cast<uint32_t>(TILE));
         mbar_wait(s_bar, it & 1u);
+        // RAW, soup mode: a used mask per 32 rows (in the staging buffer's spare bytes past the
+        // flags; made by the digit loop), the used rows before each 32 (in the digit scan)
+        uint32_t* s_umask = s_rows + TILE * 13 / 4;  // [TILE / 32] masks, then [TILE / 32] prefixes
+        uint32_t soup_n = 0, soup_base = 0;
+        if constexpr (SOUP) {
+            soup_n = *a.soup;
+            soup_base = a.soup_prefix[tile];
+        }
 
         // ---- digits (+ next pass's histogram), stable warp ranks
         uint32_t pk[IPT];
@@ -174,6 +191,11 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
                 if (count_next) atomicAdd(s_hnext + ((nkey >> nshift) & 255u), 1u);
             }
             pk[r] = d;
+            if constexpr (SOUP) {  // rows 32 (warp * IPT + r) .. +31: the used mask
+                const uint8_t* s_fl = reinterpret_cast<const uint8_t*>(s_rows + TILE * 3);
+                const uint32_t bal = __ballot_sync(kFull, p < tile_n && s_fl[p] != 0);
+                if (lane == 0u) s_umask[warp * IPT + r] = bal;
+            }
         }
         warp_rank<IPT>(pk, s_whist + warp * 256, s_wmask + warp * 256, rank_mode, tile_n < static_cast<uint32_t>(TILE));
         __syncthreads();
@@ -191,7 +213,16 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
             st_relaxed(a.desc + static_cast<size_t>(tile) * 256 + d,
                        pack_desc(epoch, tile == 0 ? kPrefix : kAggregate, cnt));
             uint32_t tot;
-            start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+            if constexpr (SOUP) {  // + the used rows before every 32 rows, in the high half
+                constexpr uint32_t kChunks = static_cast<uint32_t>(TILE) / 32u;
+                static_assert(TILE < 65536 && kChunks <= kBlock, "packed scan of digit counts and used counts");
+                const uint32_t uc = tid < kChunks ? __popc(s_umask[tid]) : 0u;
+                const uint32_t both = block_exclusive_scan<kWarps>(cnt | (uc << 16), s_warp, tot);
+                start = both & 0xFFFFu;
+                if (tid < kChunks) s_umask[kChunks + tid] = both >> 16;
+            } else {
+                start = block_exclusive_scan<kWarps>(cnt, s_warp, tot);
+            }
             uint32_t run = start;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
@@ -233,7 +264,13 @@ __global__ void __launch_bounds__(kBlock, SortMinBlocks<W_CT>::v) k_sort_pass(So
                             const uint32_t p = s_src[q];
                             const uint8_t* s_fl = reinterpret_cast<const uint8_t*>(s_rows + TILE * 3);
                             const uint32_t* r = s_fl[p] ? s_rows + static_cast<size_t>(p) * 3 : repl;
-                            v[u] = make_uint4(r[0], r[1], r[2], tile * static_cast<uint32_t>(TILE) + p);
+                            uint32_t org = tile * static_cast<uint32_t>(TILE) + p;
+                            if constexpr (SOUP) {
+                                const uint32_t before = soup_base + s_umask[TILE / 32 + (p >> 5)] +
+                                                        __popc(s_umask[p >> 5] & ((1u << (p & 31u)) - 1u));
+                                org = s_fl[p] ? before : soup_n + org - before;
+                            }
+                            v[u] = make_uint4(r[0], r[1], r[2], org);
                         } else {
                             v[u] = s4[s_src[q]];
                         }
