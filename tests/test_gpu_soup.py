@@ -121,3 +121,39 @@ def test_two_indices_past_the_small_path(rmx):
     words = rng.integers(0, 1 << 10, size=(10_000, 2)).astype(np.uint32) << np.uint32(3)
     assert check(rmx, words, np.array([[17, 9_000]], np.uint32)) == [2, 1]
     assert check(rmx, words, np.array([[9_000, 17]], np.uint32)) == [0, 0]
+
+
+def hash_info(V, D, ws_ptr, stream):
+    from paper_2109_09812_b200 import _native
+    hi = (ctypes.c_uint32 * 4)()
+    _native.check(_native.lib().rmx_hash_info(ws_ptr, V, D, stream, hi))
+    return [int(x) for x in hi]
+
+
+@pytest.mark.parametrize("violate", [False, True])
+def test_hash_mode_soup(rmx, violate):
+    """Real-valued (scrambled) coordinates: hash mode, whose raw first hashed pass makes the soup
+    origins (used masks per 32 rows folded into its digit loop and scan)."""
+    words, idx = lattice((90, 70), seed=3)
+    words = LAT.scramble_words(words, 16).reshape(words.shape)  # > 64 varying bits: hash mode
+    if violate:
+        idx = _violate(idx, 4 * 31 + 3, "swap")
+    ref = O.reindex(words, idx)
+    from paper_2109_09812_b200 import _native, pipeline
+    V, D = words.shape
+    E, K = idx.shape
+    dev = torch.device("cuda")
+    vt = torch.from_numpy(words.view(np.int32)).to(dev)
+    it = torch.from_numpy(idx.view(np.int32)).to(dev)
+    ov, oe = torch.empty_like(vt), torch.empty_like(it)
+    info = torch.zeros(2, dtype=torch.int64, device=dev)
+    ws = torch.empty(pipeline.workspace_bytes(V, D, E, K), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream()
+    pipeline.launch(vt, V, D, it, E, K, ov, oe, info, ws, None, s)
+    sinfo = (ctypes.c_uint32 * 2)()
+    _native.check(_native.lib().rmx_soup_info(ws.data_ptr(), V, D, s.cuda_stream, sinfo))
+    assert hash_info(V, D, ws.data_ptr(), s.cuda_stream)[0] == 1
+    assert [int(x) for x in sinfo] == ([0, 0] if violate else [idx.size, 1])
+    u = int(info[0].item())
+    assert np.array_equal(ov[:u].cpu().numpy().view(np.uint32), ref["vertices"].view(np.uint32))
+    assert np.array_equal(oe.cpu().numpy().view(np.uint32), ref["elements"])
