@@ -606,7 +606,8 @@ bool soup_enabled() {
     const char* e = std::getenv("RMX_SOUP");
     return !(e && e[0] == '0');
 }
-// RMX_SPEC=0: no speculative value-rank plans (always the full value-set pass; A/B)
+// RMX_SPEC=0: no speculative value-rank plans.  Speculation is used for D <= 3: the checking k_pack
+// costs less than the full value-set pass there (C2 7.34 -> 6.95 ms), not for D = 4 (C3 4.71 -> 4.82) (always the full value-set pass; A/B)
 bool spec_enabled() {
     const char* e = std::getenv("RMX_SPEC");
     return !(e && e[0] == '0');
@@ -830,7 +831,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         }
         // (with two sample halves that saw the same value sets: speculate, kSpecOn)
         ValuePlanArgs pd{gplan, vsets, shift ? vsets_b : nullptr, nullptr, nullptr, d_status, L.D, 0, nullptr,
-                         nullptr, nullptr, nullptr, nullptr, nullptr, spec, vstate, spec_enabled() ? 1 : 0, 0};
+                         nullptr, svary, nullptr, nullptr, nullptr, spec, vstate, spec_enabled() && L.D <= 3 ? 1 : 0,
+                         0};
         RMX_CHECK(launch(k_value_plan, 1, 1024, 0, s, pd));
         va.shift = 0u;
         if ((rc = dispatch_valueset(va, L.D, s))) return rc;
@@ -904,7 +906,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     {
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
                    L.D, vec, vary, spec, 0};
-        if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled()))) return rc;
+        if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled() && L.D <= 3))) return rc;
         if (value_ranks) {
             // a speculative plan that k_pack's check failed (kSpecMiss): the path it skipped --
             // full value-set pass with its check, decision, K1a, plan, second chance, rank tables --

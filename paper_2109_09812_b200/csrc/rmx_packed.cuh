@@ -923,7 +923,13 @@ __global__ void __launch_bounds__(1024) k_value_plan(ValuePlanArgs a) {
         if (t == 0) {
             vb[0] = gain ? 1u : 0u;
             vb[1] = gain ? ranked : 0u;
-            if (a.vsets_b && a.spec_ok && gain && (unsat & ranked) == 0u) {
+            // speculate only when every varying component has value sets the two sample halves
+            // agree on: a component without (too wide, too narrow) gives no sign that the sample
+            // saw all of its varying bits and fields (grids stored row by row: the sample's runs
+            // see a third of the rows' coordinates)
+            uint32_t varying = 0u;
+            for (int c = 0; c < D; ++c) varying |= (a.svary && a.svary[c] != 0u ? 1u : 0u) << c;
+            if (a.vsets_b && a.spec_ok && gain && (unsat & cand) == 0u && (varying & ~cand) == 0u) {
                 // a ranked field at the top of a 32-bit component leaves no room for the sentinel
                 const uint32_t* rk = plan + pk_rank_base(4 * D);
                 bool room = true;

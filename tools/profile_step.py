@@ -81,6 +81,12 @@ def main():
     print(f"{'total':>14s} {tot:8.3f} ms")
     hi = (ctypes.c_uint32 * 4)()
     _native.check(lib.rmx_hash_info(ws.data_ptr(), V, D, s.cuda_stream, hi))
+    gi = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_plan_guess_info(ws.data_ptr(), V, D, s.cuda_stream, gi))
+    si = (ctypes.c_uint32 * 2)()
+    _native.check(lib.rmx_soup_info(ws.data_ptr(), V, D, s.cuda_stream, si))
+    print(f"value sets wanted {gi[1]}, check state {gi[3] & 0xFF:#x}, speculative {(gi[3] >> 8) & 1}, "
+          f"check failed {(gi[3] >> 9) & 1}; soup rows {si[0]:,}, strictly increasing {si[1]}")
     if hi[0]:
         print(f"hash mode: {hi[1]:,} candidate rows ({hi[1] / int(info[0]):.2f} per distinct key), "
               f"{hi[2]} AoS passes over them, {hi[3]}-row dedup tiles")

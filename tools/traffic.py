@@ -29,12 +29,14 @@ def load(path):
         if k not in agg:
             agg[k] = {}
             order.append(k)
-        agg[k][r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "") or 0)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ix["Metric Unit"]], 1)
+        agg[k][r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "") or 0) * scale
     return [(k[1], agg[k]) for k in order]
 
 
 def main():
     path, cfg, npass, V, kw = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
+    soup = "--soup" in sys.argv  # soup mode: pass 0 also reads the used flags
     launches = load(path)
     per_pass = []
     cur = 0.0
@@ -48,7 +50,8 @@ def main():
             cur += b
             per_pass.append(cur)
     executed = per_pass[:npass]
-    per_pass = [8 * kw + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass)]
+    per_pass = [8 * kw + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) + (1 if soup and p == 0 else 0)
+                for p in range(npass)]
     algo = sum(per_pass) / npass * V
     out_path = os.path.join(ROOT, "profiles", "traffic.json")
     data = json.load(open(out_path)) if os.path.exists(out_path) else {}
@@ -61,7 +64,7 @@ def main():
                   "upsweep + colscan + downsweep",
         "note": "algorithmic, mean over the executed passes = keys + origins read and written (pass 0 reads no "
                 "origins), the pass's digit byte read by its upsweep, the next pass's digit byte written "
-                "(not by the last pass)",
+                "(not by the last pass)" + ("; soup mode: pass 0 also reads the used flags" if soup else ""),
     }
     json.dump(data, open(out_path, "w"), indent=1)
     print(json.dumps(data[cfg], indent=1))
