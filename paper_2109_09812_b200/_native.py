@@ -28,7 +28,7 @@ EXPORTS = (
     "rmx_version", "rmx_strerror", "rmx_workspace_bytes", "rmx_reindex", "rmx_lean_workspace_bytes",
     "rmx_lean_result_offset", "rmx_reindex_lean",
     "rmx_reindex_profiled", "rmx_stage_count", "rmx_stage_name", "rmx_kernel_launches", "rmx_kernel_launches_total", "rmx_debug_oob_count",
-    "rmx_last_executed_passes", "rmx_plan_info", "rmx_plan_key_info", "rmx_plan_guess_info", "rmx_hash_info", "rmx_soup_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
+    "rmx_last_executed_passes", "rmx_plan_info", "rmx_plan_key_info", "rmx_plan_guess_info", "rmx_hash_info", "rmx_soup_info", "rmx_window_info", "rmx_debug_phase_cycles", "rmx_lattice_sizes",
     "rmx_gen_lattice_soup", "rmx_gen_lattice_soup_range", "rmx_gen_grid_quads", "rmx_gather_u32", "rmx_lower_bound_rows",
     "rmx_graph_create", "rmx_graph_launch", "rmx_graph_destroy", "rmx_offset_indices",
     "rmx_welded_tile_sizes", "rmx_gen_welded_tile", "rmx_scatter_rows", "rmx_merge_workspace_bytes",
@@ -76,6 +76,7 @@ _SIGNATURES = {
     "rmx_plan_guess_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
     "rmx_hash_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
     "rmx_soup_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
+    "rmx_window_info": (_int, [_vp, _u64, _u32, _vp, ctypes.POINTER(_u32)]),
     "rmx_debug_phase_cycles": (_int, [ctypes.POINTER(ctypes.c_ulonglong), _int, _int]),
     "rmx_lattice_sizes": (_int, [_int, _u32, _u32, _u32, _u64,
                                  ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),

@@ -122,6 +122,9 @@ struct Layout {
     size_t vsets_b;               // value sets of the odd sample blocks (saturation estimate)
     size_t vstate;                // checked value-set pass: kVstateChecked | kVstateMiss
     size_t spec;                  // speculative value-rank plan: kSpecOn | kSpecMiss (k_pack's check)
+    size_t win_desc, win_counter; // window mode (rmx_window.cuh): look-back descriptors, window counter
+    size_t win_rows;              // window mode: the used rows its first pass keeps
+    size_t wstart, wend;          // window mode: first / one-past-last row of every window
     size_t order;                 // bit 0: the indices are not strictly increasing (k_mark)
     size_t soup;                  // soup mode: I when on (k_soup_decide), else 0
     size_t soup_prefix;           // soup mode: used rows before every packed-sort tile
@@ -181,6 +184,9 @@ Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     L.hhist = take(kHashPasses * 256 * 4);
     L.hcounters = take(kHashPasses * 4 + 16);
     L.spec = take(16);
+    L.win_desc = take(static_cast<size_t>(kWinCount) * 8);  // window mode: look-back descriptors
+    L.win_counter = take(16);
+    L.win_rows = take(16);
     L.order = take(16);
     L.soup = take(16);
     L.sfields = take(vr_dim * kFieldWords * 4);
@@ -198,6 +204,8 @@ Layout make_layout(uint64_t V, uint32_t D, bool lean = false) {
     L.desc3 = take(lean ? 256 : static_cast<size_t>(L.ntiles3) * 8);
     L.repl = take((RMX_MAX_DIM + 4) * 4);  // lean: the replacement row (the vertex buffer is overwritten)
     L.tile_counts = take(static_cast<size_t>(L.ntiles3_pk) * 4);
+    L.wstart = take(static_cast<size_t>(kWinCount) * 4);
+    L.wend = take(static_cast<size_t>(kWinCount) * 4);
     L.soup_prefix = take(static_cast<size_t>(max_tiles_pk) * 4);
     L.ctl_end = off;
     L.total = off;
@@ -438,7 +446,8 @@ int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     if (rc) return rc;
     // passes past kCommonPasses run only for > 40-bit keys: 4 tiles per CTA there, so that when
     // they do not run (the common case) the exiting grid is a quarter the size
-    const uint32_t tpc = a.pass >= kCommonPasses ? 4u : 1u;
+    // (window mode's fallback passes: 16 tiles per CTA -- they rarely run)
+    const uint32_t tpc = a.win_fb ? 16u : a.pass >= kCommonPasses ? 4u : 1u;
     RMX_CHECK(launch(k_pk_downsweep<IPT, MINB>, (a.ntiles + tpc - 1) / tpc, kBlock, smem, s, a, tpc));
     RMX_CHECK(cudaGetLastError());
     return RMX_OK;
@@ -600,6 +609,11 @@ constexpr cudaStreamCaptureMode kCaptureMode = cudaStreamCaptureModeThreadLocal;
 // hash mode (rmx_hash.cuh) for keys wider than 64 bits: D in [3, kHashMaxDim]; RMX_HASH=0 turns it
 // off (read per call: tests switch it at run time)
 bool hash_possible(int D) { return D >= 3 && D <= kHashMaxDim; }
+// RMX_WINDOW=0: no window mode (rmx_window.cuh; A/B)
+bool win_enabled() {
+    const char* e = std::getenv("RMX_WINDOW");
+    return !(e && e[0] == '0');
+}
 // RMX_SOUP=0: no soup mode (strictly increasing indices: map fill into the output indices, no
 // remap; A/B)
 bool soup_enabled() {
@@ -773,6 +787,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint64_t* desc3 = reinterpret_cast<uint64_t*>(base + L.desc3);
 
     RMX_CHECK(cudaMemsetAsync(base + L.ctl_begin, 0, L.ctl_end - L.ctl_begin, s));
+    RMX_CHECK(cudaMemsetAsync(base + L.wstart, 0xFF, static_cast<size_t>(kWinCount) * 4, s));
     if (V) RMX_CHECK(cudaMemsetAsync(flags, 0, V, s));
 
     // K1 mark (byte flags for in-order indices, a bit set for scattered ones), then merge them
@@ -854,6 +869,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // soup mode (rmx_packed.cuh k_soup_decide): strictly increasing indices + a packed plan; not with
     // scratch (org_id holds origins), lean mode or the slot-exchange downsweep
     uint32_t* soup = reinterpret_cast<uint32_t*>(base + L.soup);
+    uint32_t* win_rows = reinterpret_cast<uint32_t*>(base + L.win_rows);  // window mode (rmx_window.cuh)
     uint32_t* soup_prefix = reinterpret_cast<uint32_t*>(base + L.soup_prefix);
     const uint32_t* order = reinterpret_cast<const uint32_t*>(base + L.order);
     const int soup_ok = (!lean && sc == nullptr && soup_enabled() && !ds2_enabled()) ? 1 : 0;
@@ -875,6 +891,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         return RMX_OK;
     };
     if ((rc = launch_soup(nullptr))) return rc;
+    // window mode (rmx_window.cuh): u32 keys of four passes sort by their top 16 bits only (decided
+    // once the key layout is final: after the value-rank tables, before k_pack)
+    const int win_ok = (!lean && sc == nullptr && win_enabled() && !ds2_enabled()) ? 1 : 0;
     if ((rc = rec.mark())) return rc;
     // ---- packed keys (packed mode)
     uint16_t* rank16 = reinterpret_cast<uint16_t*>(base + L.rank16);
@@ -904,6 +923,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     uint8_t* dig = reinterpret_cast<uint8_t*>(base + L.pk_digits);
     const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
     {
+        RMX_CHECK(launch(k_win_decide, 1, 32, 0, s, plan, L.D, win_ok, static_cast<const uint32_t*>(d_status),
+                         static_cast<const uint32_t*>(nullptr)));
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
                    L.D, vec, vary, spec, 0};
         if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled() && L.D <= 3))) return rc;
@@ -927,6 +948,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                              static_cast<const uint32_t*>(spec)));
             if ((rc = launch_soup(spec))) return rc;
             if ((rc = finish_value_plan(1))) return rc;
+            RMX_CHECK(launch(k_win_decide, 1, 32, 0, s, plan, L.D, win_ok, static_cast<const uint32_t*>(d_status),
+                             static_cast<const uint32_t*>(spec)));
             a.fallback = 1;
             if ((rc = dispatch_pack(a, s))) return rc;
         }
@@ -960,7 +983,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         SortPkArgs a{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                      reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,
                      dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk, L.pk_cstride,
-                     L.D, p, rank_force(), soup, soup_prefix, flags};
+                     L.D, p, rank_force(), soup, soup_prefix, flags, 0, win_rows,
+                     static_cast<uint32_t>(pk_sort_tile())};
         if ((rc = launch_sort_pk(a, s))) return rc;
         if ((rc = rec.mark())) return rc;
     }
@@ -1001,21 +1025,50 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = dispatch_unique(a, s))) return rc;
     }
     if ((rc = rec.mark())) return rc;
+    {  // window mode: bounds (+ the fallback decision), the per-window unique kernel
+        WinArgs wa{plan, rows0, rows0 + L.vals_off, reinterpret_cast<uint2*>(rows1),
+                   reinterpret_cast<uint32_t*>(base + L.wstart), reinterpret_cast<uint32_t*>(base + L.wend),
+                   reinterpret_cast<uint64_t*>(base + L.win_desc), reinterpret_cast<uint32_t*>(base + L.win_counter),
+                   fill, reinterpret_cast<uint32_t*>(base + L.ukeys), reinterpret_cast<unsigned long long*>(d_count),
+                   plan, d_status, static_cast<uint32_t>(V), L.D, L.bucket_shift, win_rows, static_cast<uint32_t>(V)};
+        int g = 0;
+        if ((rc = grid_for_stream((V + 3) / 4, g))) return rc;
+        RMX_CHECK(launch(k_win_bounds, g, kBlock, 0, s, wa));
+        if ((rc = grid_for_stream(V, g))) return rc;
+        int gu = 0;
+        if ((rc = persistent_grid(k_win_unique, WinSmem::bytes(), kWinCount, gu))) return rc;
+        RMX_CHECK(launch(k_win_unique, gu, kBlock, WinSmem::bytes(), s, wa));
+        RMX_CHECK(cudaGetLastError());
+        // fallback (a window of more than kWinMaxRows rows): digit 0, the four passes, then the
+        // usual unique kernels below
+        RMX_CHECK(launch(k_win_digit0, g, kBlock, 0, s, static_cast<const uint32_t*>(plan), L.D,
+                         static_cast<const uint32_t*>(rows0), dig, static_cast<const uint32_t*>(win_rows),
+                         static_cast<const uint32_t*>(d_status)));
+        for (int p = 0; p < 4; ++p) {
+            SortPkArgs fa{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
+                          reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,
+                          dig + ((p + 1) & 1) * dig_stride, d_status, static_cast<uint32_t>(V), L.ntiles_pk,
+                          L.pk_cstride, L.D, p, rank_force(), soup, soup_prefix, flags, 1, win_rows,
+                          static_cast<uint32_t>(pk_sort_tile())};
+            if ((rc = launch_sort_pk(fa, s))) return rc;
+        }
+    }
     {
         uint32_t* counts = reinterpret_cast<uint32_t*>(base + L.tile_counts);
         HeadCountArgs h{rows0, rows1, plan, counts, d_status, static_cast<uint32_t>(V), L.ntiles3_pk,
-                        static_cast<uint32_t>(kPkUniqTile), L.D};
+                        static_cast<uint32_t>(kPkUniqTile), L.D, win_rows};
         int grid = 0;
         if ((rc = grid_for_stream(static_cast<uint64_t>(L.ntiles3_pk) * kBlock, grid))) return rc;
         RMX_CHECK(launch(k_head_count_pk, grid, kBlock, 0, s, h));
         RMX_CHECK(cudaGetLastError());
-        RMX_CHECK(launch(k_tile_scan, 1, 1024, 0, s, counts, L.ntiles3_pk, plan, L.D, reinterpret_cast<unsigned long long*>(d_count),
-                                       d_status));
+        RMX_CHECK(launch(k_tile_scan, 1, 1024, 0, s, counts, L.ntiles3_pk, plan, L.D,
+                         reinterpret_cast<unsigned long long*>(d_count), d_status,
+                         static_cast<const uint32_t*>(win_rows), static_cast<uint32_t>(kPkUniqTile)));
         RMX_CHECK(cudaGetLastError());
         void* ukeys = base + L.ukeys;
         UniquePkArgs a{rows0, rows1, L.vals_off, plan, counts, fill, d_status, ukeys,
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
-                       sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift};
+                       sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift, win_rows};
         if ((rc = launch_unique_pk(a, s))) return rc;
         // lean: the unique rows go to the final sort buffer (read completely by k_unique_pk by then)
         UnpackPkArgs u{plan, lean ? repl : vtx, lean ? repl + RMX_MAX_DIM : idx, vary, fields, ukeys, vinv,
@@ -1033,7 +1086,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                              static_cast<const uint32_t*>(rows0), static_cast<const uint32_t*>(rows1),
                              reinterpret_cast<uint32_t*>(base + L.rank_of), static_cast<uint32_t>(V),
                              static_cast<const uint32_t*>(d_status), L.D, 2, n_cand,
-                             static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr)));
+                             static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                             static_cast<const uint32_t*>(nullptr), 0));
             RMX_CHECK(cudaGetLastError());
             int gp = 0;
             if ((rc = persistent_grid(k_hash_pairs, 0, (V + kPairsTile - 1) / kPairsTile, gp))) return rc;
@@ -1046,7 +1100,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                          static_cast<const uint32_t*>(plan), static_cast<const uint32_t*>(rows0),
                          static_cast<const uint32_t*>(rows1), map, static_cast<uint32_t>(V),
                          static_cast<const uint32_t*>(d_status), L.D, 0, n_cand, static_cast<const uint32_t*>(soup),
-                         out_idx));
+                         out_idx, static_cast<const uint32_t*>(fill), L.bucket_shift));
         RMX_CHECK(cudaGetLastError());
     }
     if ((rc = rec.mark())) return rc;
@@ -1316,6 +1370,31 @@ int rmx_hash_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stre
     info[1] = hash ? nc : 0u;                      // candidate rows (distinct keys per dedup tile)
     info[2] = hash ? pl[1] : 0u;                   // executed AoS passes over the candidates
     info[3] = static_cast<uint32_t>(kHashTile);    // rows per dedup tile
+    return RMX_OK;
+}
+
+int rmx_window_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info) {
+    if (!workspace || !info || dim < 1 || dim > RMX_MAX_DIM) return RMX_EINVAL;
+    const Layout L = make_layout(n_vertices, dim);
+    uint32_t pk[8] = {0}, nd = 0;
+    std::vector<uint32_t> ws(kWinCount), we(kWinCount);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const char* base = static_cast<const char*>(workspace);
+    RMX_CHECK(cudaMemcpyAsync(pk, base + L.plan + pk_base(L.P) * 4, sizeof(pk), cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(ws.data(), base + L.wstart, kWinCount * 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(we.data(), base + L.wend, kWinCount * 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaMemcpyAsync(&nd, base + L.win_rows, 4, cudaMemcpyDeviceToHost, s));
+    RMX_CHECK(cudaStreamSynchronize(s));
+    uint32_t nonempty = 0, maxrows = 0;
+    for (uint32_t w = 0; w < kWinCount; ++w)
+        if (ws[w] != 0xFFFFFFFFu) {
+            ++nonempty;
+            maxrows = std::max(maxrows, we[w] - ws[w]);
+        }
+    info[0] = pk[6] | (pk[7] << 1);  // bit 0 window mode decided, bit 1 its fallback ran
+    info[1] = nd;                    // used rows sorted (unused rows dropped by the first pass)
+    info[2] = nonempty;              // non-empty windows
+    info[3] = maxrows;               // rows of the largest window
     return RMX_OK;
 }
 

@@ -36,6 +36,7 @@
 #include "rmx_unique.cuh"
 #include "rmx_hash.cuh"
 #include "rmx_packed.cuh"
+#include "rmx_window.cuh"
 #include "rmx_gen.cuh"
 #include "rmx_steps.cuh"
 #include "rmx_small.cuh"

@@ -1058,11 +1058,13 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
     // origins are the row numbers: the first pass makes them itself, so they are
     // only stored when no pass runs (all keys equal)
     const bool want_vals = pk[3] == 0u;
+    // the digit of the first executed pass: byte 0, or byte 2 in window mode (rmx_window.cuh)
+    const int dshift = pk[6] != 0u ? 16 : 0;
     auto put = [&](uint64_t i, uint64_t key) {
         if (wide) keys64[i] = key;
         else keys32[i] = static_cast<uint32_t>(key);
         if (want_vals) vals[i] = static_cast<uint32_t>(i);
-        a.digits[i] = static_cast<uint8_t>(key);
+        a.digits[i] = static_cast<uint8_t>(key >> dshift);
     };
 
     if constexpr (D_CT > 0) {
@@ -1128,8 +1130,10 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
                     const uint32_t i0 = static_cast<uint32_t>(4 * g);
                     if (want_vals) __stcs(reinterpret_cast<uint4*>(vals + 4 * g), make_uint4(i0, i0 + 1, i0 + 2, i0 + 3));
                     reinterpret_cast<uint32_t*>(a.digits)[g] =
-                        (static_cast<uint32_t>(key[0]) & 255u) | ((static_cast<uint32_t>(key[1]) & 255u) << 8) |
-                        ((static_cast<uint32_t>(key[2]) & 255u) << 16) | (static_cast<uint32_t>(key[3]) << 24);
+                        (static_cast<uint32_t>(key[0] >> dshift) & 255u) |
+                        ((static_cast<uint32_t>(key[1] >> dshift) & 255u) << 8) |
+                        ((static_cast<uint32_t>(key[2] >> dshift) & 255u) << 16) |
+                        ((static_cast<uint32_t>(key[3] >> dshift) & 255u) << 24);
                 }
                 done = ng << 2;
             }
@@ -1219,7 +1223,29 @@ struct SortPkArgs {
     const uint32_t* soup;
     const uint32_t* soup_prefix;
     const uint8_t* flags;
+    // window mode (rmx_window.cuh): passes 0 and 1 do not run (pass 2 is the first, with the
+    // row-number / soup origins); win_fb = 1: the four passes of its fallback (origins staged)
+    int win_fb;
+    uint32_t* win_rows;   // window mode: the used rows the first window pass keeps (its colscan sums them)
+    uint32_t tile_rows;   // rows per downsweep tile
 };
+
+// window mode: after its first pass (pass 2, which drops the unused rows -- their map entries are
+// never read and the replacement row they stand for is a used row) the packed kernels run over
+// *win_rows rows; the host sized grids and arrays for the V vertex slots, which bound it
+__device__ __forceinline__ void win_rows_patch(const uint32_t* plan, int D, const uint32_t* win_rows, bool after_first,
+                                               uint32_t& n, uint32_t& ntiles, uint32_t tile) {
+    if (win_rows && after_first && plan[pk_base(4 * D) + 6] != 0u) {
+        n = *win_rows;
+        ntiles = (n + tile - 1u) / tile;
+    }
+}
+__device__ __forceinline__ bool win_first_pass(const SortPkArgs& a) {
+    return !a.win_fb && a.pass == 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u;
+}
+__device__ __forceinline__ bool win_after_first(const SortPkArgs& a) {
+    return a.win_fb || (a.pass > 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u);
+}
 
 // The upsweep counts kUpGroup consecutive tiles per CTA iteration so every digit's
 // counts of the group leave as one 32-byte sector (digit-major layout).
@@ -1228,15 +1254,21 @@ constexpr uint32_t kUpGroup = 8;
 // true when this packed pass runs (packed mode, pass < number of packed passes)
 __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    return pk[0] != 0u && static_cast<uint32_t>(a.pass) < pk[3];
+    if (pk[0] == 0u || static_cast<uint32_t>(a.pass) >= pk[3]) return false;
+    const bool win = pk[6] != 0u;
+    if (a.win_fb) return win && pk[7] != 0u;  // window mode's fallback passes
+    return !(win && a.pass < 2);              // window mode: passes 2 and 3 only
 }
 
 // Per-tile digit counts from the digit-byte array (1 B/row instead of the 4-8 B
 // key: k_pack and every downsweep also emit the next pass's digit per row),
 // 16 digits per 16-byte load, kUpGroup tiles per CTA iteration.
-__global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t tile_rows) {
+__global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a0, uint32_t tile_rows) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    SortPkArgs a = a0;
     if (*a.status || !pk_pass_active(a)) return;
+    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, tile_rows);
+    const bool drop = win_first_pass(a);  // window mode's first pass counts the used rows only
     __shared__ uint32_t s_h[kUpGroup * 256];
     const uint32_t ngroups = (a.ntiles + kUpGroup - 1u) / kUpGroup;
     const uint4* d16 = reinterpret_cast<const uint4*>(a.digits);  // tile_rows is a multiple of 16
@@ -1252,16 +1284,26 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t ti
             const uint4 w = __ldcs(d16 + ((base + r) >> 4));
             uint32_t* h = s_h + (r / tile_rows) * 256u;  // the 16 rows share a tile
             const uint32_t q[4] = {w.x, w.y, w.z, w.w};
+            if (drop) {
+                const uint4 f = __ldcs(reinterpret_cast<const uint4*>(a.flags) + ((base + r) >> 4));
+                const uint32_t fq[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                atomicAdd(h + (q[k] & 255u), 1u);
-                atomicAdd(h + ((q[k] >> 8) & 255u), 1u);
-                atomicAdd(h + ((q[k] >> 16) & 255u), 1u);
-                atomicAdd(h + (q[k] >> 24), 1u);
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if ((fq[k] >> (8 * b)) & 255u) atomicAdd(h + ((q[k] >> (8 * b)) & 255u), 1u);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    atomicAdd(h + (q[k] & 255u), 1u);
+                    atomicAdd(h + ((q[k] >> 8) & 255u), 1u);
+                    atomicAdd(h + ((q[k] >> 16) & 255u), 1u);
+                    atomicAdd(h + (q[k] >> 24), 1u);
+                }
             }
         }
         for (uint32_t r = span16 + threadIdx.x; r < span; r += kBlock)
-            atomicAdd(s_h + (r / tile_rows) * 256u + a.digits[base + r], 1u);
+            if (!drop || a.flags[base + r]) atomicAdd(s_h + (r / tile_rows) * 256u + a.digits[base + r], 1u);
         __syncthreads();
         const uint32_t d = threadIdx.x;
         uint4* dst = reinterpret_cast<uint4*>(a.counts + static_cast<size_t>(d) * a.cstride + g * kUpGroup);
@@ -1275,9 +1317,11 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a, uint32_t ti
 // totals[d].  Chunks of 4096 values: each thread scans 4 consecutive values
 // (one coalesced 16-byte access), a block scan joins the threads, a running
 // carry joins the chunks.
-__global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a) {
+__global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a0) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    SortPkArgs a = a0;
     if (*a.status || !pk_pass_active(a)) return;
+    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
     __shared__ uint32_t s_warp[32];
     uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.cstride;
     uint32_t carry = 0;
@@ -1297,7 +1341,10 @@ __global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a) {
         carry += tot;
         __syncthreads();
     }
-    if (threadIdx.x == 0) a.totals[blockIdx.x] = carry;
+    if (threadIdx.x == 0) {
+        a.totals[blockIdx.x] = carry;
+        if (win_first_pass(a) && carry) atomicAdd(a.win_rows, carry);  // the rows the window passes keep
+    }
 }
 
 template <int IPT>
@@ -1379,14 +1426,15 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
     // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none), or in
     // soup mode the soup origins it makes in s_vals
-    const bool iota = a.pass == 0;
+    const bool iota = !a.win_fb && a.pass == (a.plan[pk_base(4 * a.dim) + 6] != 0u ? 2 : 0);
     const bool soup_on = iota && a.soup && *a.soup != 0u;
+    const bool drop = win_first_pass(a);  // window mode's first pass keeps the used rows only
     if (tid == 0) {
         if (it == 0) {
             mbar_init(s_bar, 1);
             fence_mbar_init();
         }
-        if (soup_on)  // + the used flags (into the slot-index array, free until the scatter)
+        if (soup_on || drop)  // + the used flags (into the slot-index array, free until the scatter)
             stage_tile2(s_keys, in_k + base, tile_n * static_cast<uint32_t>(sizeof(Key)), s_src, a.flags + base,
                         tile_n, s_bar);
         else if (iota)
@@ -1406,13 +1454,23 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     }
     __syncthreads();
     mbar_wait(s_bar, it & 1u);
-    if (soup_on) {
-        soup_origins<IPT>(a, s_vals, reinterpret_cast<const uint8_t*>(s_src), s_warp, base, tile_n, tile);
-        __syncthreads();  // the flags are read before the scatter overwrites s_src
-    }
-
+    if (soup_on) soup_origins<IPT>(a, s_vals, reinterpret_cast<const uint8_t*>(s_src), s_warp, base, tile_n, tile);
     uint32_t pk[IPT];
-    if (tile_n == static_cast<uint32_t>(TILE)) {  // full tile: no validity tests
+    uint32_t used_mask = 0u;  // drop: bit r = row of round r is used
+    if (drop) {  // unused rows take no slot (digit 256)
+        const uint8_t* s_fl = reinterpret_cast<const uint8_t*>(s_src);
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+            const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
+            const bool u = p < tile_n && s_fl[p] != 0;
+            used_mask |= (u ? 1u : 0u) << r;
+            pk[r] = u ? (static_cast<uint32_t>(s_keys[p] >> shift) & 255u) : 256u;
+        }
+    }
+    if (soup_on || drop) __syncthreads();  // the flags are read before the scatter overwrites s_src
+    if (drop) {
+        warp_rank<IPT, true>(pk, s_whist + warp * 256, nullptr, rank_mode, true);
+    } else if (tile_n == static_cast<uint32_t>(TILE)) {  // full tile: no validity tests
 #pragma unroll
         for (int r = 0; r < IPT; ++r)
             pk[r] = static_cast<uint32_t>(s_keys[warp * (32u * IPT) + r * 32u + lane] >> shift) & 255u;
@@ -1444,23 +1502,26 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
             run += wc[w];
         }
         s_gdst[d] = run_base - start;  // mod 2^32; + tile slot gives the global row
+        if (d == 0) s_misc[4] = tot;   // rows ranked in this tile (drop: the used ones)
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < IPT; ++r) {
         const uint32_t p = warp * (32u * IPT) + r * 32u + lane;
-        if (p < tile_n) s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
+        if (p < tile_n && (!drop || ((used_mask >> r) & 1u)))
+            s_src[s_whist[warp * 256 + (pk[r] >> 16)] + (pk[r] & 0xFFFFu)] = static_cast<uint16_t>(p);
     }
+    const uint32_t out_n = drop ? s_misc[4] : tile_n;  // rows this tile writes
     __syncthreads();
 
     constexpr int U = 4;
-    for (uint32_t q0 = tid; q0 < tile_n; q0 += U * kBlock) {
+    for (uint32_t q0 = tid; q0 < out_n; q0 += U * kBlock) {
         Key k[U];
         uint32_t v[U], dst[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t q = q0 + u * kBlock;
-            if (q < tile_n) {
+            if (q < out_n) {
                 const uint32_t p = s_src[q];
                 k[u] = s_keys[p];
                 v[u] = iota && !soup_on ? base + p : s_vals[p];
@@ -1469,12 +1530,12 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t q = q0 + u * kBlock;
-            if (q < tile_n) dst[u] = s_gdst[static_cast<uint32_t>(k[u] >> shift) & 255u] + q;
+            if (q < out_n) dst[u] = s_gdst[static_cast<uint32_t>(k[u] >> shift) & 255u] + q;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t q = q0 + u * kBlock;
-            if (q < tile_n) {
+            if (q < out_n) {
                 RMX_CHECK_INDEX(dst[u], a.n);
                 out_k[dst[u]] = k[u];
                 out_v[dst[u]] = v[u];
@@ -1487,9 +1548,11 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
 // One tile per CTA, or (tiles_per_cta > 1: the passes that few keys reach, so
 // that a pass which does not run costs a small grid) consecutive tiles.
 template <int IPT, int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a, uint32_t tiles_per_cta) {
+__global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a0, uint32_t tiles_per_cta) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    SortPkArgs a = a0;
     if (*a.status || !pk_pass_active(a)) return;
+    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
     uint32_t* smem = dyn_smem<uint32_t>();
     const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
     for (uint32_t j = 0; j < tiles_per_cta; ++j) {
@@ -1766,6 +1829,7 @@ struct HeadCountArgs {
     uint32_t ntiles;
     uint32_t tile;     // rows per tile
     int dim;
+    const uint32_t* win_rows;  // window mode's fallback: the rows its passes kept
 };
 
 template <int KW>
@@ -1805,11 +1869,13 @@ __device__ __forceinline__ void head_count_body(const HeadCountArgs& a) {
     }
 }
 
-__global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
+__global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a0) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    HeadCountArgs a = a0;
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    if (pk[0] != 1u) return;  // packed mode only
+    if (pk[0] != 1u || (pk[6] != 0u && pk[7] == 0u)) return;  // packed mode, not window mode
+    win_rows_patch(a.plan, a.dim, a.win_rows, true, a.n, a.ntiles, a.tile);
     if (pk[1] == 2u) head_count_body<2>(a);
     else head_count_body<1>(a);
 }
@@ -1817,9 +1883,13 @@ __global__ void __launch_bounds__(kBlock) k_head_count_pk(HeadCountArgs a) {
 // Exclusive scan of per-tile counts in place (one CTA of 1024 threads);
 // the total is the output vertex count.
 __global__ void __launch_bounds__(1024) k_tile_scan(uint32_t* counts, uint32_t ntiles, const uint32_t* plan, int dim,
-                                                    unsigned long long* total_out, const uint32_t* status) {
+                                                    unsigned long long* total_out, const uint32_t* status,
+                                                    const uint32_t* win_rows, uint32_t tile) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || plan[pk_base(4 * dim)] != 1u) return;
+    if (plan[pk_base(4 * dim) + 6] != 0u && plan[pk_base(4 * dim) + 7] == 0u) return;  // window mode
+    uint32_t n_unused = 0;
+    win_rows_patch(plan, dim, win_rows, true, n_unused, ntiles, tile);
     __shared__ uint32_t s_warp[32];
     const uint32_t tot = block_scan_counts(counts, ntiles, s_warp);
     if (threadIdx.x == 0) *total_out = tot;
@@ -1842,6 +1912,7 @@ struct UniquePkArgs {
     uint32_t ntiles;
     int dim;
     int bucket_shift;
+    const uint32_t* win_rows;  // window mode's fallback: the rows its passes kept
 };
 
 template <int IPT>
@@ -1975,11 +2046,13 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
 }
 
 template <int IPT>
-__global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a) {
+__global__ void __launch_bounds__(kBlock, 3) k_unique_pk(UniquePkArgs a0) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    UniquePkArgs a = a0;
     if (*a.status) return;
     const uint32_t* pk = a.plan + pk_base(4 * a.dim);
-    if (pk[0] != 1u) return;  // packed mode only
+    if (pk[0] != 1u || (pk[6] != 0u && pk[7] == 0u)) return;  // packed mode, not window mode
+    win_rows_patch(a.plan, a.dim, a.win_rows, true, a.n, a.ntiles, static_cast<uint32_t>(UniquePkTraits<IPT>::kTile));
     uint32_t* smem = dyn_smem<uint32_t>();
     if (pk[1] == 2u) unique_pk_body<2, IPT>(a, smem);
     else unique_pk_body<1, IPT>(a, smem);

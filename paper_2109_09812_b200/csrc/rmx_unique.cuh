@@ -228,10 +228,17 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
                                                       const uint32_t* rows1, uint32_t* map, uint32_t n,
                                                       const uint32_t* status, int dim, int mode_want,
                                                       const uint32_t* n_cand, const uint32_t* soup,
-                                                      uint32_t* out_idx) {
+                                                      uint32_t* out_idx, const uint32_t* wfill, int bs) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status) return;
     const bool hash = plan[pk_base(4 * dim)] == 2u;
+    // window mode (rmx_window.cuh): pairs for the used rows only -- bucket b holds wfill[b] pairs
+    // from b << bs on (without soup mode's dense origins the buckets are not full)
+    const bool win = mode_want == 0 && wfill && plan[pk_base(4 * dim)] == 1u && plan[pk_base(4 * dim) + 6] != 0u;
+    auto live = [&](uint64_t p) {
+        const uint32_t b = static_cast<uint32_t>(p >> bs);
+        return !win || p - (static_cast<uint64_t>(b) << bs) < __ldg(wfill + b);
+    };
     // soup mode (rmx_packed.cuh k_soup_decide): origins below I are index positions -- the map is
     // the output; origins >= I are unused rows, which no index reads
     const uint32_t n_used = (mode_want == 0 && soup) ? *soup : 0u;
@@ -259,7 +266,14 @@ __global__ void __launch_bounds__(kBlock) k_map_fill(const uint32_t* plan, const
     }
     const uint4* pairs = reinterpret_cast<const uint4*>((plan[0] != 0u) != hash ? rows0 : rows1);
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x;  // two pairs per thread
-    if (2 * i + 1 < n) {
+    if (win) {
+        for (uint64_t p = 2 * i; p < 2 * i + 2 && p < n; ++p)
+            if (live(p)) {
+                const uint2 v = reinterpret_cast<const uint2*>(pairs)[p];
+                RMX_CHECK_INDEX(v.x, n);
+                if (v.x < lim) map[v.x] = v.y;
+            }
+    } else if (2 * i + 1 < n) {
         const uint4 v = __ldcs(pairs + i);
         RMX_CHECK_INDEX(v.x, n);
         RMX_CHECK_INDEX(v.z, n);

@@ -1,0 +1,373 @@
+// rmx_window.cuh -- window mode: packed u32 keys sorted by their top 16 bits only, the low 16
+// bits resolved by a presence bitmap per window (plan packed-section word 6).
+//
+// The reference's order is the key order and a key's new index is the number of distinct keys
+// below it (pipeline.py:72-113).  For u32 packed keys of 25..32 bits (four 8-bit LSD passes) the
+// packed path runs passes 2 and 3 only: the rows come out grouped by "window" = key >> 16, in
+// window order.  Per window one CTA marks the low 16 bits of its rows in a 2^16-bit shared-memory
+// bitmap, takes per-word prefix popcounts, learns the window's first new index from its
+// predecessors (decoupled look-back over windows), and then
+//   * writes the window's distinct keys in order (set bits, ascending) to ukeys for k_unpack_pk,
+//   * gives every row its new index = base + set bits below its key, and writes (origin, new
+//     index) pairs bucketed by origin for k_map_fill (as k_unique_pk does).
+// Passes 0, 1, k_head_count_pk, k_tile_scan and k_unique_pk do not run; the first window pass drops
+// the unused rows (no index reads their map entries, and the replacement row they stand for is a
+// used row, so the distinct keys are those of the used rows) -- they would otherwise share the
+// replacement key and form one giant window.  A window of more than
+// kWinMaxRows rows (keys whose top 16 bits barely vary) would serialise on one CTA: k_win_ends
+// then sets the fallback word (pk[7]) and the full packed path runs after all (the digit byte 0
+// re-extracted, four passes over the window-grouped rows, the usual unique kernels).
+#pragma once
+
+#include "rmx_packed.cuh"
+
+namespace rmx {
+
+constexpr uint32_t kWinCount = 1u << 16;        // windows (key >> 16)
+constexpr uint32_t kWinWords = (1u << 16) / 32;  // bitmap words per window
+constexpr uint32_t kWinMaxRows = 1u << 21;      // larger windows take the fallback
+constexpr uint32_t kWinChunk = 2048;            // rows per pair-bucketing chunk (8 per thread)
+
+__device__ __forceinline__ bool win_active(const uint32_t* plan, int D) {
+    const uint32_t* pk = plan + pk_base(4 * D);
+    return pk[0] == 1u && pk[6] != 0u && pk[7] == 0u;
+}
+__device__ __forceinline__ bool win_fallback(const uint32_t* plan, int D) {
+    const uint32_t* pk = plan + pk_base(4 * D);
+    return pk[0] == 1u && pk[6] != 0u && pk[7] != 0u;
+}
+
+// after the final plan (and the re-plan of a failed speculative plan: gate)
+__global__ void k_win_decide(uint32_t* plan, int D, int allow, const uint32_t* status, const uint32_t* gate) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (threadIdx.x != 0 || *status) return;
+    if (gate && !(*gate & 2u)) return;  // (kSpecMiss)
+    uint32_t* pk = plan + pk_base(4 * D);
+    pk[6] = (allow && pk[0] == 1u && pk[1] == 1u && pk[3] == 4u) ? 1u : 0u;
+    pk[7] = 0u;
+}
+
+struct WinArgs {
+    const uint32_t* plan;
+    const uint32_t* keys;  // sorted by window (the final packed buffer)
+    const uint32_t* vals;  // origins, same order
+    uint2* pairs;          // bucketed (origin, new index) pairs (the other buffer)
+    uint32_t* wstart;      // [kWinCount] first row of every window, 0xFFFFFFFF = empty
+    uint32_t* wend;        // [kWinCount] one past its last row
+    uint64_t* desc;        // [kWinCount] look-back descriptors
+    uint32_t* counter;     // window counter
+    uint32_t* fill;        // [256] pair bucket fill counters
+    uint32_t* ukeys;       // [U] packed key of every distinct key
+    unsigned long long* count;
+    uint32_t* plan_w;      // plan, for the fallback word
+    const uint32_t* status;
+    uint32_t n;            // rows: *win_rows (the used rows the window passes keep)
+    int dim;
+    int bucket_shift;
+    const uint32_t* win_rows;
+    uint32_t n_slots;       // vertex slots V (the row buffers' extent)
+};
+
+// first row and one past the last row of every non-empty window (empty windows keep wstart =
+// 0xFFFFFFFF; their wend is never read), four rows per thread; and the fallback decision: rows
+// p = j * kWinProbe and p + kWinProbe in one window mean a window of more than kWinProbe rows
+// (every window of more than kWinMaxRows = 2 kWinProbe rows holds such a pair), which would
+// serialise on one CTA -- the full packed path runs instead (pk[7])
+constexpr uint32_t kWinProbe = kWinMaxRows / 2;
+__global__ void __launch_bounds__(kBlock) k_win_bounds(WinArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*a.status || !win_active(a.plan, a.dim)) return;
+    const uint32_t n = *a.win_rows;
+    const uint32_t groups = (n + 3u) / 4u;
+    const uint32_t stride = gridDim.x * kBlock;
+    for (uint32_t g = blockIdx.x * kBlock + threadIdx.x; g < groups; g += stride) {
+        const uint32_t p0 = 4u * g;
+        uint32_t w[4];
+        if (p0 + 3u < n) {
+            const uint4 k = __ldcs(reinterpret_cast<const uint4*>(a.keys) + g);
+            w[0] = k.x >> 16;
+            w[1] = k.y >> 16;
+            w[2] = k.z >> 16;
+            w[3] = k.w >> 16;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = p0 + j < n ? __ldg(a.keys + p0 + j) >> 16 : 0xFFFFFFFFu;
+        }
+        uint32_t prev = p0 ? __ldg(a.keys + p0 - 1u) >> 16 : 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t p = p0 + static_cast<uint32_t>(j);
+            if (p >= n) break;
+            if (w[j] != prev) {
+                a.wstart[w[j]] = p;
+                if (p) a.wend[prev] = p;
+            }
+            if (p + 1u == n) a.wend[w[j]] = n;
+            prev = w[j];
+        }
+        if (p0 % kWinProbe == 0u && p0 + kWinProbe < n && (__ldg(a.keys + p0 + kWinProbe) >> 16) == w[0])
+            a.plan_w[pk_base(4 * a.dim) + 7] = 1u;  // the full packed path runs instead
+    }
+}
+
+// The window's first new index: decoupled look-back over the windows before it (warp 0; the
+// window's aggregate was published earlier).  Returns the exclusive prefix and publishes the
+// inclusive one.
+__device__ __forceinline__ uint32_t win_lookback(const WinArgs& a, uint32_t w, uint32_t total) {
+    const uint32_t lane = threadIdx.x & 31u;
+    uint64_t* mine = a.desc + w;
+    uint32_t excl = 0;
+    if (w == 0) return 0u;
+    int64_t hi = static_cast<int64_t>(w) - 1;
+    for (;;) {
+        const int64_t t = hi - static_cast<int64_t>(lane);
+        uint64_t dd = t >= 0 ? ld_relaxed(a.desc + t) : pack_desc(1u, kPrefix, 0u);
+        bool done = false;
+        for (;;) {
+            const bool valid = desc_epoch(dd) == 1u && desc_flag(dd) != 0u;
+            const uint32_t vm = __ballot_sync(kFull, valid);
+            const uint32_t pm = __ballot_sync(kFull, valid && desc_flag(dd) == kPrefix);
+            const uint32_t need = pm ? (((pm & (0u - pm)) << 1) - 1u) : kFull;
+            if ((vm & need) == need) {
+                excl += warp_sum(((need >> lane) & 1u) ? desc_value(dd) : 0u);
+                done = pm != 0u;
+                break;
+            }
+            if (!valid) {
+                __nanosleep(20);
+                dd = ld_relaxed(a.desc + t);
+            }
+        }
+        if (done) break;
+        hi -= 32;
+    }
+    if (lane == 0) st_relaxed(mine, pack_desc(1u, kPrefix, excl + total));
+    return excl;
+}
+
+// rows staged per window in shared memory (keys + origins); larger windows stream from global
+constexpr uint32_t kWinCap = 6144;
+constexpr int kWinRpt = static_cast<int>(kWinCap / kBlock);  // staged rows per thread
+constexpr uint32_t kWinStage = kWinCap + 8;                  // + 16-byte alignment slack
+struct WinSmem {
+    static constexpr size_t kKey = 0, kVal = kWinStage, kBm = 2 * kWinStage, kPre = kBm + kWinWords,
+                            kBcnt = kPre + kWinWords, kBcur = kBcnt + 256, kBglob = kBcur + 256,
+                            kWarp = kBglob + 256, kMisc = kWarp + 2 * kWarps, kBar = kMisc + 8, kWordsTotal = kBar + 2;
+    static __host__ __device__ size_t bytes() { return kWordsTotal * 4; }
+};
+static_assert(kWinChunk * 2 <= 2 * kWinStage, "the streamed path's pair staging fits the row staging");
+static_assert(kWinCap * 2 <= 2 * kWinWords * 4, "the staged path's row permutation fits the bitmap and prefix words");
+
+__global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*a.status || !win_active(a.plan, a.dim)) return;
+    a.n = *a.win_rows;
+    uint32_t* sm = dyn_smem<uint32_t>();
+    uint32_t* s_key = sm + WinSmem::kKey;  // staged keys, then the local new index of every row
+    uint32_t* s_val = sm + WinSmem::kVal;  // staged origins
+    uint2* s_pairs = reinterpret_cast<uint2*>(sm);  // bucket-ordered pairs (over s_key + s_val)
+    uint32_t* s_bm = sm + WinSmem::kBm;
+    uint32_t* s_pre = sm + WinSmem::kPre;
+    uint32_t* s_bcnt = sm + WinSmem::kBcnt;
+    uint32_t* s_bcur = sm + WinSmem::kBcur;
+    uint32_t* s_bglob = sm + WinSmem::kBglob;
+    uint32_t* s_warp = sm + WinSmem::kWarp;
+    uint32_t* s_misc = sm + WinSmem::kMisc;
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(sm + WinSmem::kBar);
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const int bs = a.bucket_shift;
+    constexpr uint32_t kWpt = kWinWords / kBlock;  // bitmap words per thread
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+    }
+    uint32_t staged = 0, it = 0;  // staged windows (mbarrier phase), iterations (counter slot)
+    for (;; ++it) {
+        uint32_t* slot = s_misc + (it & 1u) * 2;  // [0] window, [1] its base (alternating slots)
+        if (tid == 0) slot[0] = atomicAdd(a.counter, 1u);
+        __syncthreads();
+        const uint32_t w = slot[0];
+        if (w >= kWinCount) break;
+        const uint32_t s = a.wstart[w];
+        const uint32_t rows = s == 0xFFFFFFFFu ? 0u : a.wend[w] - s;
+        if (rows == 0u) {  // empty: aggregate 0 (the last window resolves the count)
+            if (w == kWinCount - 1) {
+                if (warp == 0) {
+                    if (lane == 0) st_relaxed(a.desc + w, pack_desc(1u, kAggregate, 0u));
+                    const uint32_t excl = win_lookback(a, w, 0u);
+                    if (lane == 0) *a.count = excl;
+                }
+            } else if (tid == 0) {
+                st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, 0u));
+            }
+            continue;
+        }
+        const uint32_t s4 = s & ~3u, e4 = (s + rows + 3u) & ~3u, off = s - s4;
+        const bool stage = rows <= kWinCap && e4 <= a.n_slots;  // (e4 - s4 <= kWinCap + 6)
+        if (stage && tid == 0)
+            stage_tile2(s_key, a.keys + s4, (e4 - s4) * 4u, s_val, a.vals + s4, (e4 - s4) * 4u, s_bar);
+#pragma unroll
+        for (uint32_t j = 0; j < kWpt; ++j) s_bm[tid * kWpt + j] = 0u;
+        s_bcnt[tid] = 0u;
+        __syncthreads();
+        // ---- mark the low 16 bits
+        if (stage) {
+            mbar_wait(s_bar, staged & 1u);
+            ++staged;
+            for (uint32_t q = tid; q < rows; q += kBlock) {
+                const uint32_t k = s_key[off + q] & 0xFFFFu;
+                atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
+            }
+        } else {
+            for (uint32_t q = tid; q < rows; q += kBlock) {
+                const uint32_t k = __ldg(a.keys + s + q) & 0xFFFFu;
+                atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
+            }
+        }
+        __syncthreads();
+        // ---- per-word prefix popcounts, the window's distinct keys; publish the aggregate
+        uint32_t wb[kWpt], cnt = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < kWpt; ++j) {
+            wb[j] = s_bm[tid * kWpt + j];
+            cnt += __popc(wb[j]);
+        }
+        uint32_t total;
+        uint32_t run = block_exclusive_scan<kWarps>(cnt, s_warp, total);
+        const uint32_t pre0 = run;  // distinct keys before this thread's bitmap words
+#pragma unroll
+        for (uint32_t j = 0; j < kWpt; ++j) {
+            s_pre[tid * kWpt + j] = run;
+            run += __popc(wb[j]);
+        }
+        if (tid == 0) st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, total));
+        __syncthreads();
+        if (stage) {
+            // ---- local new index of every row (in place), bucket counts; warp 0 then looks back
+#pragma unroll
+            for (int u = 0; u < kWinRpt; ++u) {
+                const uint32_t q = tid + static_cast<uint32_t>(u) * kBlock;
+                if (q < rows) {
+                    const uint32_t k = s_key[off + q] & 0xFFFFu;
+                    const uint32_t wd = k >> 5;
+                    s_key[off + q] = s_pre[wd] + __popc(s_bm[wd] & ((1u << (k & 31u)) - 1u));
+                    atomicAdd(s_bcnt + (s_val[off + q] >> bs), 1u);
+                }
+            }
+            if (warp == 0) {
+                const uint32_t excl = win_lookback(a, w, total);
+                if (lane == 0) slot[1] = excl;
+            }
+            __syncthreads();
+            // ---- bucket space: a block scan for the staging, one global reservation per bucket
+            {
+                const uint32_t bc = s_bcnt[tid];
+                uint32_t tot;
+                const uint32_t bstart = block_exclusive_scan<kWarps>(bc, s_warp + kWarps, tot);
+                s_bcur[tid] = bstart;
+                if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
+            }
+            __syncthreads();
+            // bucket order as a row permutation (over the bitmap and prefix words, free by now)
+            uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_bm);
+            // (warp-aggregated: rows of a warp often share a bucket -- one shared atomic per bucket)
+#pragma unroll 4
+            for (int u = 0; u < kWinRpt; ++u) {
+                if (static_cast<uint32_t>(u) * kBlock >= rows) break;  // (uniform)
+                const uint32_t q = tid + static_cast<uint32_t>(u) * kBlock;
+                const bool valid = q < rows;
+                const uint32_t b = valid ? s_val[off + q] >> bs : 0xFFFFFFFFu;
+                const uint32_t peers = __match_any_sync(kFull, b);
+                const uint32_t leader = __ffs(peers) - 1u;
+                uint32_t pos = 0;
+                if (valid && lane == leader) pos = atomicAdd(s_bcur + b, __popc(peers));
+                pos = __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+                if (valid) s_perm[pos] = static_cast<uint16_t>(q);
+            }
+            __syncthreads();
+            const uint32_t base = slot[1];
+            for (uint32_t q = tid; q < rows; q += kBlock) {
+                const uint32_t r = off + s_perm[q];
+                const uint32_t org = s_val[r];
+                RMX_CHECK_INDEX(s_bglob[org >> bs] + q, a.n_slots);
+                a.pairs[s_bglob[org >> bs] + q] = make_uint2(org, base + s_key[r]);
+            }
+        } else {
+            if (warp == 0) {
+                const uint32_t excl = win_lookback(a, w, total);
+                if (lane == 0) slot[1] = excl;
+            }
+            __syncthreads();
+            const uint32_t base = slot[1];
+            // rows streamed in chunks of kWinChunk: new index, bucketed (origin, new index) pairs
+            for (uint32_t c0 = 0; c0 < rows; c0 += kWinChunk) {
+                const uint32_t cn = min(kWinChunk, rows - c0);
+                s_bcnt[tid] = 0u;
+                __syncthreads();
+                uint2 pr[kWinChunk / kBlock];
+#pragma unroll
+                for (uint32_t u = 0; u < kWinChunk / kBlock; ++u) {
+                    const uint32_t q = c0 + tid + u * kBlock;
+                    pr[u] = make_uint2(0u, 0u);
+                    if (q < rows) {
+                        const uint32_t k = __ldg(a.keys + s + q) & 0xFFFFu;
+                        const uint32_t wd = k >> 5;
+                        const uint32_t nidx = base + s_pre[wd] + __popc(s_bm[wd] & ((1u << (k & 31u)) - 1u));
+                        const uint32_t org = __ldg(a.vals + s + q);
+                        pr[u] = make_uint2(org, nidx);
+                        atomicAdd(s_bcnt + (org >> bs), 1u);
+                    }
+                }
+                __syncthreads();
+                {
+                    const uint32_t bc = s_bcnt[tid];
+                    uint32_t tot;
+                    const uint32_t bstart = block_exclusive_scan<kWarps>(bc, s_warp + kWarps, tot);
+                    s_bcur[tid] = bstart;
+                    if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
+                }
+                __syncthreads();
+#pragma unroll
+                for (uint32_t u = 0; u < kWinChunk / kBlock; ++u)
+                    if (c0 + tid + u * kBlock < rows) s_pairs[atomicAdd(s_bcur + (pr[u].x >> bs), 1u)] = pr[u];
+                __syncthreads();
+                for (uint32_t q = tid; q < cn; q += kBlock) {
+                    const uint2 p = s_pairs[q];
+                    RMX_CHECK_INDEX(s_bglob[p.x >> bs] + q, a.n_slots);
+                    a.pairs[s_bglob[p.x >> bs] + q] = p;
+                }
+                __syncthreads();
+            }
+        }
+        // ---- the window's distinct keys out, ascending
+        const uint32_t base = slot[1];
+        if (tid == 0 && w == kWinCount - 1) *a.count = static_cast<unsigned long long>(base) + total;
+        {
+            uint32_t r = base + pre0;
+#pragma unroll
+            for (uint32_t j = 0; j < kWpt; ++j) {
+                uint32_t m = wb[j];
+                while (m) {
+                    const uint32_t b = __ffs(m) - 1u;
+                    RMX_CHECK_INDEX(r, a.n);
+                    a.ukeys[r++] = (w << 16) | ((tid * kWpt + j) << 5) | b;
+                    m &= m - 1u;
+                }
+            }
+        }
+        __syncthreads();  // the staging area and the bitmap are reused
+    }
+}
+
+// fallback: the digit byte 0 of the window-grouped rows for the full packed passes
+__global__ void __launch_bounds__(kBlock) k_win_digit0(const uint32_t* plan, int D, const uint32_t* keys,
+                                                       uint8_t* digits, const uint32_t* win_rows, const uint32_t* status) {
+    pdl_enter();  // programmatic dependent launch: wait for the previous kernel
+    if (*status || !win_fallback(plan, D)) return;
+    const uint32_t n = *win_rows;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; p < n; p += stride)
+        digits[p] = static_cast<uint8_t>(__ldg(keys + p));
+}
+
+}  // namespace rmx

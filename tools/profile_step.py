@@ -85,6 +85,10 @@ def main():
     _native.check(lib.rmx_plan_guess_info(ws.data_ptr(), V, D, s.cuda_stream, gi))
     si = (ctypes.c_uint32 * 2)()
     _native.check(lib.rmx_soup_info(ws.data_ptr(), V, D, s.cuda_stream, si))
+    wi = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_window_info(ws.data_ptr(), V, D, s.cuda_stream, wi))
+    print(f"window mode {wi[0] & 1}, fallback {(wi[0] >> 1) & 1}, used rows {wi[1]:,}, non-empty windows "
+          f"{wi[2]:,}, largest {wi[3]:,} rows")
     print(f"value sets wanted {gi[1]}, check state {gi[3] & 0xFF:#x}, speculative {(gi[3] >> 8) & 1}, "
           f"check failed {(gi[3] >> 9) & 1}; soup rows {si[0]:,}, strictly increasing {si[1]}")
     if hi[0]:
