@@ -27,7 +27,9 @@ constexpr int kWarps = kBlock / 32;
 // every row -- and the sort runs over (packed key, origin) pairs instead:
 //   [0] mode (0 = AoS rows, 1 = packed, 2 = hash: rmx_hash.cuh)
 //                                [1] key words KW (1 | 2)   [2] varying bits B
-//   [3] packed passes ceil(B/8)  [4] number of runs         [5] reserved
+//   [3] packed passes ceil(B/8)  [4] number of runs
+//   [5] window mode drops the unused rows in its first pass (no soup mode; in soup mode they keep
+//       spread keys and the window kernel skips their origins >= I)
 //   [6] window mode (rmx_window.cuh)  [7] window mode's fallback to the full packed path
 //   [8 + 4r ..] run r: component, source bit, length, destination bit
 //   [8 + 4 kMaxRuns + c] field rank of component c: 0 = none, else

@@ -450,6 +450,12 @@ int launch_downsweep(const SortPkArgs& a, cudaStream_t s) {
     const uint32_t tpc = a.win_fb ? 16u : a.pass >= kCommonPasses ? 4u : 1u;
     RMX_CHECK(launch(k_pk_downsweep<IPT, MINB>, (a.ntiles + tpc - 1) / tpc, kBlock, smem, s, a, tpc));
     RMX_CHECK(cudaGetLastError());
+    if (a.pass == 2 && !a.win_fb) {  // window mode's first pass when it drops the unused rows (no soup
+                                     // mode): its own instantiation, 16 tiles per CTA (a small exiting grid)
+        if ((rc = ensure_smem(k_pk_downsweep<IPT, MINB, true>, smem))) return rc;
+        RMX_CHECK(launch(k_pk_downsweep<IPT, MINB, true>, (a.ntiles + 15) / 16, kBlock, smem, s, a, 16u));
+        RMX_CHECK(cudaGetLastError());
+    }
     return RMX_OK;
 }
 
@@ -924,7 +930,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     const size_t dig_stride = align_up(static_cast<size_t>(V) + 16);
     {
         RMX_CHECK(launch(k_win_decide, 1, 32, 0, s, plan, L.D, win_ok, static_cast<const uint32_t*>(d_status),
-                         static_cast<const uint32_t*>(nullptr)));
+                         static_cast<const uint32_t*>(nullptr), static_cast<const uint32_t*>(soup), win_rows,
+                         static_cast<uint32_t>(V)));
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
                    L.D, vec, vary, spec, 0};
         if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled() && L.D <= 3))) return rc;
@@ -949,7 +956,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
             if ((rc = launch_soup(spec))) return rc;
             if ((rc = finish_value_plan(1))) return rc;
             RMX_CHECK(launch(k_win_decide, 1, 32, 0, s, plan, L.D, win_ok, static_cast<const uint32_t*>(d_status),
-                             static_cast<const uint32_t*>(spec)));
+                             static_cast<const uint32_t*>(spec), static_cast<const uint32_t*>(soup), win_rows,
+                             static_cast<uint32_t>(V)));
             a.fallback = 1;
             if ((rc = dispatch_pack(a, s))) return rc;
         }
@@ -1030,7 +1038,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                    reinterpret_cast<uint32_t*>(base + L.wstart), reinterpret_cast<uint32_t*>(base + L.wend),
                    reinterpret_cast<uint64_t*>(base + L.win_desc), reinterpret_cast<uint32_t*>(base + L.win_counter),
                    fill, reinterpret_cast<uint32_t*>(base + L.ukeys), reinterpret_cast<unsigned long long*>(d_count),
-                   plan, d_status, static_cast<uint32_t>(V), L.D, L.bucket_shift, win_rows, static_cast<uint32_t>(V)};
+                   plan, d_status, static_cast<uint32_t>(V), L.D, L.bucket_shift, win_rows, static_cast<uint32_t>(V),
+                   static_cast<const uint32_t*>(soup)};
         int g = 0;
         if ((rc = grid_for_stream((V + 3) / 4, g))) return rc;
         RMX_CHECK(launch(k_win_bounds, g, kBlock, 0, s, wa));

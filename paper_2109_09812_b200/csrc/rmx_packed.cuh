@@ -1060,6 +1060,12 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
     const bool want_vals = pk[3] == 0u;
     // the digit of the first executed pass: byte 0, or byte 2 in window mode (rmx_window.cuh)
     const int dshift = pk[6] != 0u ? 16 : 0;
+    // window mode in soup mode (pk[6] && !pk[5]): the unused rows stay in the sort but are skipped
+    // by origin, so their keys only place them -- a used neighbour's key (the 4-row group) or a
+    // hash of the row, never the one replacement key (which would form one giant window)
+    const bool spread = pk[6] != 0u && pk[5] == 0u;
+    const uint32_t bmask = pk[2] >= 32u ? 0xFFFFFFFFu : (1u << pk[2]) - 1u;
+    auto spread_key = [&](uint64_t i) -> uint64_t { return (static_cast<uint32_t>(i) * 0x9E3779B1u) & bmask; };
     auto put = [&](uint64_t i, uint64_t key) {
         if (wide) keys64[i] = key;
         else keys32[i] = static_cast<uint32_t>(key);
@@ -1117,6 +1123,19 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
                         if constexpr (check) key[j] = pack_used(k[j]);
                         else key[j] = pack(k[j]);
                     }
+                    if (spread && f != 0x01010101u) {  // (static indexing only: key[] stays in registers)
+                        bool have = false;
+                        uint64_t nk = 0u;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (!have && ((f >> (8 * j)) & 255u) != 0u) {
+                                nk = key[j];
+                                have = true;
+                            }
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            if (((f >> (8 * j)) & 255u) == 0u) key[j] = have ? nk : spread_key(4 * g + j);
+                    }
                     // 16-byte stores of 4 consecutive rows (vals_off is a multiple of 4 words)
                     if (wide) {
                         ulonglong2* k2 = reinterpret_cast<ulonglong2*>(keys64 + 4 * g);
@@ -1141,6 +1160,10 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
         for (uint64_t i = done + start; i < a.n; i += stride) {
             uint32_t k[D_CT];
             const bool used = a.flags[i] != 0;
+            if (spread && !used) {
+                put(i, spread_key(i));
+                continue;
+            }
 #pragma unroll
             for (int c = 0; c < D_CT; ++c) k[c] = used ? __ldg(a.vtx + i * D_CT + c) : ref[c];
             if constexpr (check) put(i, pack_used(k));
@@ -1160,6 +1183,10 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
         }
     } else {
         for (uint64_t i = start; i < a.n; i += stride) {
+            if (spread && !a.flags[i]) {
+                put(i, spread_key(i));
+                continue;
+            }
             const uint32_t* row = a.flags[i] ? a.vtx + i * D : repl;
             uint64_t key = 0;
             for (uint32_t r = 0; r < nruns; ++r) {
@@ -1240,8 +1267,9 @@ __device__ __forceinline__ void win_rows_patch(const uint32_t* plan, int D, cons
         ntiles = (n + tile - 1u) / tile;
     }
 }
+// window mode's first pass when it drops the unused rows (pk[5]: no soup mode)
 __device__ __forceinline__ bool win_first_pass(const SortPkArgs& a) {
-    return !a.win_fb && a.pass == 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u;
+    return !a.win_fb && a.pass == 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u && a.plan[pk_base(4 * a.dim) + 5] != 0u;
 }
 __device__ __forceinline__ bool win_after_first(const SortPkArgs& a) {
     return a.win_fb || (a.pass > 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u);
@@ -1397,7 +1425,9 @@ __device__ __forceinline__ void soup_origins(const SortPkArgs& a, uint32_t* s_va
     }
 }
 
-template <int KW, int IPT>
+// DROP: window mode's first pass without soup mode keeps the used rows only (a separate
+// instantiation: the extra code costs the common passes registers)
+template <int KW, int IPT, bool DROP>
 __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
@@ -1428,7 +1458,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     // soup mode the soup origins it makes in s_vals
     const bool iota = !a.win_fb && a.pass == (a.plan[pk_base(4 * a.dim) + 6] != 0u ? 2 : 0);
     const bool soup_on = iota && a.soup && *a.soup != 0u;
-    const bool drop = win_first_pass(a);  // window mode's first pass keeps the used rows only
+    constexpr bool drop = DROP;  // window mode's first pass keeps the used rows only
     if (tid == 0) {
         if (it == 0) {
             mbar_init(s_bar, 1);
@@ -1547,11 +1577,11 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
 
 // One tile per CTA, or (tiles_per_cta > 1: the passes that few keys reach, so
 // that a pass which does not run costs a small grid) consecutive tiles.
-template <int IPT, int MINB>
+template <int IPT, int MINB, bool DROP = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a0, uint32_t tiles_per_cta) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     SortPkArgs a = a0;
-    if (*a.status || !pk_pass_active(a)) return;
+    if (*a.status || !pk_pass_active(a) || win_first_pass(a) != DROP) return;
     win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
     uint32_t* smem = dyn_smem<uint32_t>();
     const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
@@ -1559,8 +1589,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a0, ui
         const uint32_t tile = blockIdx.x * tiles_per_cta + j;
         if (tile >= a.ntiles) break;
         if (j) __syncthreads();  // the next tile's bulk copy overwrites the staging buffers
-        if (wide) sort_pk_body<2, IPT>(a, smem, tile, j);
-        else sort_pk_body<1, IPT>(a, smem, tile, j);
+        if constexpr (DROP) sort_pk_body<1, IPT, true>(a, smem, tile, j);  // (window mode: u32 keys)
+        else if (wide) sort_pk_body<2, IPT, false>(a, smem, tile, j);
+        else sort_pk_body<1, IPT, false>(a, smem, tile, j);
     }
 }
 

@@ -239,7 +239,8 @@ __device__ void plan_body(const uint32_t* vary, const uint32_t* fields, uint32_t
     uint32_t* vb = plan + pk_value_base(P);
     vb[0] = 0u;
     vb[1] = 0u;
-    pk[6] = 0u;  // window mode (rmx_window.cuh k_win_decide) and its fallback
+    pk[5] = 0u;  // window mode (rmx_window.cuh k_win_decide): drop, on, fallback
+    pk[6] = 0u;
     pk[7] = 0u;
     uint32_t bits = 0, runs = 0, cand = 0;
     bool fits = true;

@@ -26,7 +26,6 @@ namespace rmx {
 constexpr uint32_t kWinCount = 1u << 16;        // windows (key >> 16)
 constexpr uint32_t kWinWords = (1u << 16) / 32;  // bitmap words per window
 constexpr uint32_t kWinMaxRows = 1u << 21;      // larger windows take the fallback
-constexpr uint32_t kWinChunk = 2048;            // rows per pair-bucketing chunk (8 per thread)
 
 __device__ __forceinline__ bool win_active(const uint32_t* plan, int D) {
     const uint32_t* pk = plan + pk_base(4 * D);
@@ -38,13 +37,21 @@ __device__ __forceinline__ bool win_fallback(const uint32_t* plan, int D) {
 }
 
 // after the final plan (and the re-plan of a failed speculative plan: gate)
-__global__ void k_win_decide(uint32_t* plan, int D, int allow, const uint32_t* status, const uint32_t* gate) {
+// (after the soup decision): soup mode keeps the unused rows (k_pack spreads their keys, the
+// window kernel skips their origins >= I), else the first window pass drops them and counts the
+// rows it keeps into *win_rows
+__global__ void k_win_decide(uint32_t* plan, int D, int allow, const uint32_t* status, const uint32_t* gate,
+                             const uint32_t* soup, uint32_t* win_rows, uint32_t n) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (threadIdx.x != 0 || *status) return;
     if (gate && !(*gate & 2u)) return;  // (kSpecMiss)
     uint32_t* pk = plan + pk_base(4 * D);
-    pk[6] = (allow && pk[0] == 1u && pk[1] == 1u && pk[3] == 4u) ? 1u : 0u;
+    const bool win = allow && pk[0] == 1u && pk[1] == 1u && pk[3] == 4u;
+    const bool drop = win && !(soup && *soup);
+    pk[5] = drop ? 1u : 0u;
+    pk[6] = win ? 1u : 0u;
     pk[7] = 0u;
+    *win_rows = drop ? 0u : n;
 }
 
 struct WinArgs {
@@ -66,6 +73,7 @@ struct WinArgs {
     int bucket_shift;
     const uint32_t* win_rows;
     uint32_t n_slots;       // vertex slots V (the row buffers' extent)
+    const uint32_t* soup;   // soup mode: I; rows of origin >= I are unused (kept, not dropped)
 };
 
 // first row and one past the last row of every non-empty window (empty windows keep wstart =
@@ -145,18 +153,34 @@ __device__ __forceinline__ uint32_t win_lookback(const WinArgs& a, uint32_t w, u
     return excl;
 }
 
-// rows staged per window in shared memory (keys + origins); larger windows stream from global
-constexpr uint32_t kWinCap = 6144;
-constexpr int kWinRpt = static_cast<int>(kWinCap / kBlock);  // staged rows per thread
-constexpr uint32_t kWinStage = kWinCap + 8;                  // + 16-byte alignment slack
+// Rows of a warp often share an origin bucket, and same-address shared atomics that return a
+// value serialise: the row's slot in its bucket is warp-aggregated (s_bcur: the buckets' next free
+// slots; the marks and bucket counts stay plain fire-and-forget atomics -- MATCH.ANY aggregation
+// of those measured slower on C2 and C3).  Call from warp-uniform loops.
+__device__ __forceinline__ uint32_t win_slot(uint32_t* s_bcur, bool valid, uint32_t b) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t peers = __match_any_sync(kFull, valid ? b : 0xFFFFFFFFu);
+    const uint32_t leader = __ffs(peers) - 1u;
+    uint32_t pos = 0;
+    if (valid && lane == leader) pos = atomicAdd(s_bcur + b, __popc(peers));
+    return __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+}
+
+// Rows are staged in shared memory by bulk copies (keys + origins).  A window of up to kWinCap rows
+// is one chunk (its bucket permutation then reuses the bitmap words); a larger one is processed in
+// chunks of kWinSub rows (marked chunk by chunk, then re-staged for the pairs, the permutation
+// behind the chunk).  3 CTAs per SM.
+constexpr uint32_t kWinCap = 6656;
+constexpr uint32_t kWinSub = 4096;
+constexpr uint32_t kWinStage = kWinCap + 8;  // + 16-byte alignment slack
 struct WinSmem {
     static constexpr size_t kKey = 0, kVal = kWinStage, kBm = 2 * kWinStage, kPre = kBm + kWinWords,
                             kBcnt = kPre + kWinWords, kBcur = kBcnt + 256, kBglob = kBcur + 256,
                             kWarp = kBglob + 256, kMisc = kWarp + 2 * kWarps, kBar = kMisc + 8, kWordsTotal = kBar + 2;
     static __host__ __device__ size_t bytes() { return kWordsTotal * 4; }
 };
-static_assert(kWinChunk * 2 <= 2 * kWinStage, "the streamed path's pair staging fits the row staging");
-static_assert(kWinCap * 2 <= 2 * kWinWords * 4, "the staged path's row permutation fits the bitmap and prefix words");
+static_assert(kWinCap * 2 <= 2 * kWinWords * 4, "a one-chunk window's permutation fits the bitmap and prefix words");
+static_assert(kWinSub + 8 + kWinSub / 2 <= kWinStage, "a chunk's permutation fits behind its staged keys");
 
 __global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
@@ -165,7 +189,6 @@ __global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
     uint32_t* sm = dyn_smem<uint32_t>();
     uint32_t* s_key = sm + WinSmem::kKey;  // staged keys, then the local new index of every row
     uint32_t* s_val = sm + WinSmem::kVal;  // staged origins
-    uint2* s_pairs = reinterpret_cast<uint2*>(sm);  // bucket-ordered pairs (over s_key + s_val)
     uint32_t* s_bm = sm + WinSmem::kBm;
     uint32_t* s_pre = sm + WinSmem::kPre;
     uint32_t* s_bcnt = sm + WinSmem::kBcnt;
@@ -177,12 +200,24 @@ __global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
     const int bs = a.bucket_shift;
     constexpr uint32_t kWpt = kWinWords / kBlock;  // bitmap words per thread
+    // soup mode keeps the unused rows (origins >= I): they are skipped here
+    const uint32_t lim = a.plan[pk_base(4 * a.dim) + 5] == 0u && a.soup ? *a.soup : 0xFFFFFFFFu;
     if (tid == 0) {
         mbar_init(s_bar, 1);
         fence_mbar_init();
     }
-    uint32_t staged = 0, it = 0;  // staged windows (mbarrier phase), iterations (counter slot)
-    for (;; ++it) {
+    uint32_t phase = 0;
+    // rows [cs, cs + cr) to s_key / s_val from offset (cs & 3) on (the 16-byte aligned superset;
+    // the row buffers extend past V to a multiple of 4 rows); all threads call it
+    auto stage = [&](uint32_t cs, uint32_t cr) -> uint32_t {
+        const uint32_t s4 = cs & ~3u, e4 = (cs + cr + 3u) & ~3u;
+        __syncthreads();  // the previous chunk's readers are done
+        if (tid == 0) stage_tile2(s_key, a.keys + s4, (e4 - s4) * 4u, s_val, a.vals + s4, (e4 - s4) * 4u, s_bar);
+        mbar_wait(s_bar, phase);
+        phase ^= 1u;
+        return cs - s4;
+    };
+    for (uint32_t it = 0;; ++it) {
         uint32_t* slot = s_misc + (it & 1u) * 2;  // [0] window, [1] its base (alternating slots)
         if (tid == 0) slot[0] = atomicAdd(a.counter, 1u);
         __syncthreads();
@@ -202,26 +237,19 @@ __global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
             }
             continue;
         }
-        const uint32_t s4 = s & ~3u, e4 = (s + rows + 3u) & ~3u, off = s - s4;
-        const bool stage = rows <= kWinCap && e4 <= a.n_slots;  // (e4 - s4 <= kWinCap + 6)
-        if (stage && tid == 0)
-            stage_tile2(s_key, a.keys + s4, (e4 - s4) * 4u, s_val, a.vals + s4, (e4 - s4) * 4u, s_bar);
+        const bool one = rows <= kWinCap;
+        const uint32_t csz = one ? kWinCap : kWinSub;
+        const uint32_t nch = (rows + csz - 1u) / csz;
 #pragma unroll
         for (uint32_t j = 0; j < kWpt; ++j) s_bm[tid * kWpt + j] = 0u;
-        s_bcnt[tid] = 0u;
-        __syncthreads();
-        // ---- mark the low 16 bits
-        if (stage) {
-            mbar_wait(s_bar, staged & 1u);
-            ++staged;
-            for (uint32_t q = tid; q < rows; q += kBlock) {
+        // ---- mark the low 16 bits, chunk by chunk
+        uint32_t off = 0;
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            const uint32_t cr = min(csz, rows - ch * csz);
+            off = stage(s + ch * csz, cr);
+            for (uint32_t q = tid; q < cr; q += kBlock) {
                 const uint32_t k = s_key[off + q] & 0xFFFFu;
-                atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
-            }
-        } else {
-            for (uint32_t q = tid; q < rows; q += kBlock) {
-                const uint32_t k = __ldg(a.keys + s + q) & 0xFFFFu;
-                atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
+                if (s_val[off + q] < lim) atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
             }
         }
         __syncthreads();
@@ -241,102 +269,53 @@ __global__ void __launch_bounds__(kBlock, 3) k_win_unique(WinArgs a) {
             run += __popc(wb[j]);
         }
         if (tid == 0) st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, total));
-        __syncthreads();
-        if (stage) {
-            // ---- local new index of every row (in place), bucket counts; warp 0 then looks back
-#pragma unroll
-            for (int u = 0; u < kWinRpt; ++u) {
-                const uint32_t q = tid + static_cast<uint32_t>(u) * kBlock;
-                if (q < rows) {
+        // ---- pairs, chunk by chunk (a one-chunk window is still staged)
+        uint16_t* s_perm = reinterpret_cast<uint16_t*>(one ? s_bm : s_key + kWinSub + 8);
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            const uint32_t cr = min(csz, rows - ch * csz);
+            if (!one) off = stage(s + ch * csz, cr);
+            s_bcnt[tid] = 0u;
+            __syncthreads();  // (s_pre, s_bcnt)
+            // local new index of every row (in place), bucket counts; warp 0 then looks back
+#pragma unroll 4
+            for (uint32_t q = tid; q < cr; q += kBlock) {
+                if (s_val[off + q] < lim) {
                     const uint32_t k = s_key[off + q] & 0xFFFFu;
                     const uint32_t wd = k >> 5;
                     s_key[off + q] = s_pre[wd] + __popc(s_bm[wd] & ((1u << (k & 31u)) - 1u));
                     atomicAdd(s_bcnt + (s_val[off + q] >> bs), 1u);
                 }
             }
-            if (warp == 0) {
+            if (ch == 0 && warp == 0) {
                 const uint32_t excl = win_lookback(a, w, total);
                 if (lane == 0) slot[1] = excl;
             }
             __syncthreads();
-            // ---- bucket space: a block scan for the staging, one global reservation per bucket
+            // bucket space: a block scan for the staging, one global reservation per bucket
+            uint32_t n_used;  // the chunk's rows with pairs (soup mode: origin < I)
             {
                 const uint32_t bc = s_bcnt[tid];
-                uint32_t tot;
-                const uint32_t bstart = block_exclusive_scan<kWarps>(bc, s_warp + kWarps, tot);
+                const uint32_t bstart = block_exclusive_scan<kWarps>(bc, s_warp + kWarps, n_used);
                 s_bcur[tid] = bstart;
                 if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
             }
             __syncthreads();
-            // bucket order as a row permutation (over the bitmap and prefix words, free by now)
-            uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_bm);
-            // (warp-aggregated: rows of a warp often share a bucket -- one shared atomic per bucket)
+            // bucket order as a row permutation (warp-aggregated slots)
 #pragma unroll 4
-            for (int u = 0; u < kWinRpt; ++u) {
-                if (static_cast<uint32_t>(u) * kBlock >= rows) break;  // (uniform)
-                const uint32_t q = tid + static_cast<uint32_t>(u) * kBlock;
-                const bool valid = q < rows;
-                const uint32_t b = valid ? s_val[off + q] >> bs : 0xFFFFFFFFu;
-                const uint32_t peers = __match_any_sync(kFull, b);
-                const uint32_t leader = __ffs(peers) - 1u;
-                uint32_t pos = 0;
-                if (valid && lane == leader) pos = atomicAdd(s_bcur + b, __popc(peers));
-                pos = __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+            for (uint32_t q0 = 0; q0 < cr; q0 += kBlock) {  // (warp-uniform)
+                const uint32_t q = q0 + tid;
+                const uint32_t org = q < cr ? s_val[off + q] : 0xFFFFFFFFu;
+                const bool valid = org < lim;
+                const uint32_t pos = win_slot(s_bcur, valid, org >> bs);
                 if (valid) s_perm[pos] = static_cast<uint16_t>(q);
             }
             __syncthreads();
             const uint32_t base = slot[1];
-            for (uint32_t q = tid; q < rows; q += kBlock) {
+            for (uint32_t q = tid; q < n_used; q += kBlock) {
                 const uint32_t r = off + s_perm[q];
                 const uint32_t org = s_val[r];
                 RMX_CHECK_INDEX(s_bglob[org >> bs] + q, a.n_slots);
                 a.pairs[s_bglob[org >> bs] + q] = make_uint2(org, base + s_key[r]);
-            }
-        } else {
-            if (warp == 0) {
-                const uint32_t excl = win_lookback(a, w, total);
-                if (lane == 0) slot[1] = excl;
-            }
-            __syncthreads();
-            const uint32_t base = slot[1];
-            // rows streamed in chunks of kWinChunk: new index, bucketed (origin, new index) pairs
-            for (uint32_t c0 = 0; c0 < rows; c0 += kWinChunk) {
-                const uint32_t cn = min(kWinChunk, rows - c0);
-                s_bcnt[tid] = 0u;
-                __syncthreads();
-                uint2 pr[kWinChunk / kBlock];
-#pragma unroll
-                for (uint32_t u = 0; u < kWinChunk / kBlock; ++u) {
-                    const uint32_t q = c0 + tid + u * kBlock;
-                    pr[u] = make_uint2(0u, 0u);
-                    if (q < rows) {
-                        const uint32_t k = __ldg(a.keys + s + q) & 0xFFFFu;
-                        const uint32_t wd = k >> 5;
-                        const uint32_t nidx = base + s_pre[wd] + __popc(s_bm[wd] & ((1u << (k & 31u)) - 1u));
-                        const uint32_t org = __ldg(a.vals + s + q);
-                        pr[u] = make_uint2(org, nidx);
-                        atomicAdd(s_bcnt + (org >> bs), 1u);
-                    }
-                }
-                __syncthreads();
-                {
-                    const uint32_t bc = s_bcnt[tid];
-                    uint32_t tot;
-                    const uint32_t bstart = block_exclusive_scan<kWarps>(bc, s_warp + kWarps, tot);
-                    s_bcur[tid] = bstart;
-                    if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
-                }
-                __syncthreads();
-#pragma unroll
-                for (uint32_t u = 0; u < kWinChunk / kBlock; ++u)
-                    if (c0 + tid + u * kBlock < rows) s_pairs[atomicAdd(s_bcur + (pr[u].x >> bs), 1u)] = pr[u];
-                __syncthreads();
-                for (uint32_t q = tid; q < cn; q += kBlock) {
-                    const uint2 p = s_pairs[q];
-                    RMX_CHECK_INDEX(s_bglob[p.x >> bs] + q, a.n_slots);
-                    a.pairs[s_bglob[p.x >> bs] + q] = p;
-                }
-                __syncthreads();
             }
         }
         // ---- the window's distinct keys out, ascending

@@ -81,7 +81,18 @@ def test_soup_with_gaps(rmx, monkeypatch):
     keep = keep[: (len(keep) // 3) * 3]
     idx = keep.astype(np.uint32).reshape(-1, 3)
     winfo = check(words, idx, monkeypatch)
-    assert winfo[0] == 1 and winfo[1] == keep.size
+    assert winfo[0] == 1 and winfo[1] == V  # soup mode keeps the unused rows (skipped by origin)
+
+
+def test_soup_with_unused_tail(rmx, monkeypatch):
+    """Soup with 30 % spare slots at the end (whole 4-row groups unused): their keys are spread by
+    a hash, not set to the replacement key -- no giant window, no fallback."""
+    rng = np.random.default_rng(7)
+    V = 600_000
+    words = rng.integers(0, 1 << 14, size=(V, 2), dtype=np.uint64).astype(np.uint32)
+    idx = np.arange(420_000, dtype=np.uint32).reshape(-1, 3)
+    winfo = check(words, idx, monkeypatch)
+    assert winfo[0] == 1 and winfo[3] < 20_000
 
 
 def test_full_32_bit_keys(rmx, monkeypatch):
