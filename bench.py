@@ -231,8 +231,24 @@ def mask_list(m):
     return "[" + ",".join(str(c) for c in range(32) if (m >> c) & 1) + "]"
 
 
-def executed_model(V, I, U, D, KW, npass, value_ranks=False, spec=False, soup=False):
-    """Algorithmic HBM bytes of one packed-path step (the kernels that ran)."""
+def executed_model(V, I, U, D, KW, npass, value_ranks=False, spec=False, soup=False, win_rows=0):
+    """Algorithmic HBM bytes of one packed-path step (the kernels that ran).  win_rows > 0: window mode
+    (two packed passes over win_rows rows after the first, the window stage instead of head count +
+    unique)."""
+    if win_rows:
+        n = win_rows
+        pairs = I if soup else n
+        first = (4 * KW + 1 + 1) * V + (4 * KW + 4 + 1) * n   # keys, digit, flags in; rows + next digit out
+        second = (4 * KW + 4 + 1) * n + (4 * KW + 4) * n      # rows + digit in, rows out
+        return int((4 * I + 2 * V)
+                   + ((4 * D + 1) * V // 64 if value_ranks else (4 * D + 1) * V)
+                   + ((4 * D + 1) * V * (1 if spec else 65) // 64 if value_ranks else 0)
+                   + (4 * D + 1) * V + (4 * KW + 1) * V      # pack
+                   + first + second                           # the two packed passes
+                   + 4 * n + 8 * n + 8 * pairs + 4 * U        # window stage: bounds, rows in, pairs + keys out
+                   + (4 * KW + 4 * D) * U                     # unpack
+                   + 12 * pairs                               # map fill
+                   + (0 if soup else 12 * I))                 # remap
     passes = sum(8 * KW + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) for p in range(npass))
     return int((4 * I + 2 * V)                       # mark: indices in, flags cleared + set
                # K1a: rows + flags -- with value ranks over a 1/64 sample only, the full value-set pass
@@ -309,6 +325,10 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
     sinfo = (ctypes.c_uint32 * 2)()
     _native.check(lib.rmx_soup_info(ws.data_ptr(), V, D, stream.cuda_stream, sinfo))
     soup = int(sinfo[0]) != 0
+    winfo = (ctypes.c_uint32 * 4)()
+    _native.check(lib.rmx_window_info(ws.data_ptr(), V, D, stream.cuda_stream, winfo))
+    window = (int(winfo[0]) & 3) == 1  # window mode, no fallback (rmx_window.cuh)
+    win_rows = int(winfo[1])           # rows of the window passes (soup mode: all V; else the used rows)
 
     # per-stage CUDA events for every timed step (recorded on the launching stream)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
@@ -358,6 +378,8 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
                  "candidate_passes": int(hi[2]), "dedup_tile_rows": int(hi[3])}
         n_rows, executed = int(hi[1]), int(hi[2])
         packed = 0
+    if packed and window:
+        executed = 2  # window mode runs the top two packed passes only
     pass_names = [n for n in names if n.startswith("pk_pass_" if packed else "sort_pass_")]
     active = sorted((stage_ms[n] for n in pass_names), reverse=True)[:executed]
     pass_ms = sum(active) / max(1, len(active))
@@ -365,20 +387,46 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
     # packed pass: keys + origins in and out, the digit byte read by its upsweep and the next
     # pass's digit byte written (pass 0 reads no origins: they are the row numbers; the last pass
     # writes no next digit) -- mean over the executed passes; AoS pass: rows in and out
-    if packed:  # (soup mode: pass 0 also reads the used flags)
-        per_pass = [8 * key_words + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < executed else 0)
-                    + (1 if soup and p == 0 else 0) for p in range(executed)]
-        pass_bytes = sum(per_pass) / len(per_pass) * V
+    if packed:  # (soup mode: pass 0 also reads the used flags; window mode without soup mode: the
+        # first pass reads the flags and writes the used rows only)
+        out_rows = win_rows if window and not soup else V
+        per_pass = [(4 * key_words + 1 + (1 if (soup or window) and p == 0 else 0)) * V
+                    + (0 if p == 0 else 4 * out_rows)
+                    + (4 * key_words + 4 + (1 if p + 1 < executed else 0)) * out_rows for p in range(executed)]
+        pass_bytes = sum(per_pass) / len(per_pass)
     else:
         pass_bytes = 2 * row_bytes * n_rows
     hbm, peak_kind = peaks()
     achieved = pass_bytes / (pass_ms * 1e-3) / 1e9
-    executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0, spec, soup)
-                      if packed else None)
+    executed_bytes = (executed_model(V, E * K, expect_u, D, key_words, executed, value_mask != 0, spec, soup,
+                                     win_rows if window else 0) if packed else None)
+    pass_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                 "bytes_per_launch": pass_bytes, "launch_ms": pass_ms,
+                 "kernel": "one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep"}
+    win_roof = None
+    if packed and window:
+        # stage "window": k_win_bounds reads the keys (4 B/row); k_win_unique stages keys + origins
+        # (8 B/row), writes an (origin, new index) pair per used row and the distinct keys
+        n_pairs = int(sinfo[0]) if soup else win_rows
+        win_bytes = 4 * win_rows + 8 * win_rows + 8 * n_pairs + 4 * expect_u
+        win_ms = stage_ms.get("window", 0.0)
+        win_roof = {"bound": "hbm", "achieved": win_bytes / (win_ms * 1e-3) / 1e9 if win_ms else None,
+                    "peak": hbm, "unit": "GB/s",
+                    "frac": win_bytes / (win_ms * 1e-3) / 1e9 / hbm if win_ms else None,
+                    "bytes_per_launch": win_bytes, "launch_ms": win_ms,
+                    "kernel": "window stage: k_win_bounds + k_win_unique (per-window shared-memory presence "
+                              "bitmaps, rmx_window.cuh)",
+                    "rows": win_rows, "pairs": n_pairs, "non_empty_windows": int(winfo[2]),
+                    "largest_window_rows": int(winfo[3])}
+    # the dominant kernel: the window stage when it takes longer than one LSD pass
+    dom = win_roof if win_roof and win_roof["launch_ms"] > pass_ms else None
     res = {
         "V": V, "E": E, "D": D, "K": K, "U": expect_u, "ms": ms, "ms_staged": ms_staged, "stage_ms": stage_ms,
         "launches_per_step": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "pass_roofline": pass_roof, "window_roofline": win_roof,
+        "roofline": dict(dom, traffic=None, peak_kind=peak_kind, window_mode=True, soup_mode=soup,
+                         executed_passes=executed, nominal_passes=4 * D) if dom else
+                    {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None,
                      "kernel": ("one packed LSD pass: k_pk_upsweep + k_pk_colscan + k_pk_downsweep" if packed
                                 else "one onesweep LSD pass over the hash-mode candidate rows: k_sort_pass"
@@ -391,7 +439,7 @@ def time_device(cfg: str, steps: int, warmup: int, dev, stream, rank: int = 0, w
                      "speculative_value_plan": spec if packed else None,
                      "soup_mode": soup,
                      "bytes_per_launch": pass_bytes, "launch_ms": pass_ms, "peak_kind": peak_kind,
-                     "executed_passes": executed, "nominal_passes": 4 * D},
+                     "window_mode": window, "executed_passes": executed, "nominal_passes": 4 * D},
         "executed_bytes": executed_bytes,
         "tensors": (vtx, idx),
     }
@@ -545,7 +593,9 @@ def run_b200(args):
             try:
                 with open(tp) as f:
                     tj = json.load(f)
-                roof["traffic"] = tj.get(args.config, {}).get("pass_dram_bytes_per_launch")
+                key = ("window_dram_bytes_per_launch" if "k_win_unique" in roof.get("kernel", "")
+                       else "pass_dram_bytes_per_launch")
+                roof["traffic"] = tj.get(args.config, {}).get(key)
             except Exception:
                 pass
         line = {
@@ -555,6 +605,8 @@ def run_b200(args):
             "config": workload_config(args.config, world),
             "e2e": e2e,
             "roofline": roof,
+            "pass_roofline": main.get("pass_roofline"),
+            "window_roofline": main.get("window_roofline"),
             "pipeline_roofline": {
                 "executed_bytes": executed_bytes,
                 "achieved_gbs": executed_bytes / (ms * 1e-3) / 1e9 if executed_bytes else None,

@@ -484,8 +484,12 @@ int launch_sort_pk(const SortPkArgs& a, cudaStream_t s) {
     int grid = 0;
     int rc = grid_for_stream(static_cast<uint64_t>((a.ntiles + kUpGroup - 1) / kUpGroup) * kBlock, grid);
     if (rc) return rc;
-    RMX_CHECK(launch(k_pk_upsweep, grid, kBlock, 0, s, a, static_cast<uint32_t>(pk_sort_tile())));
+    RMX_CHECK(launch(k_pk_upsweep<false>, grid, kBlock, 0, s, a, static_cast<uint32_t>(pk_sort_tile())));
     RMX_CHECK(cudaGetLastError());
+    if (a.pass == 2 && !a.win_fb) {  // window mode's dropping first pass (see launch_downsweep)
+        RMX_CHECK(launch(k_pk_upsweep<true>, grid, kBlock, 0, s, a, static_cast<uint32_t>(pk_sort_tile())));
+        RMX_CHECK(cudaGetLastError());
+    }
     RMX_CHECK(launch(k_pk_colscan, 256, 1024, 0, s, a));
     RMX_CHECK(cudaGetLastError());
     if (ds2_enabled()) {
@@ -1048,6 +1052,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = persistent_grid(k_win_unique, WinSmem::bytes(), kWinCount, gu))) return rc;
         RMX_CHECK(launch(k_win_unique, gu, kBlock, WinSmem::bytes(), s, wa));
         RMX_CHECK(cudaGetLastError());
+        if ((rc = rec.mark())) return rc;  // (stage "window")
         // fallback (a window of more than kWinMaxRows rows): digit 0, the four passes, then the
         // usual unique kernels below
         RMX_CHECK(launch(k_win_digit0, g, kBlock, 0, s, static_cast<const uint32_t*>(plan), L.D,
@@ -1273,7 +1278,7 @@ int rmx_debug_oob_count(unsigned long long* out) {
 #endif
 }
 
-int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + kMaxPackedPasses + 2 + 4; }
+int rmx_stage_count(uint32_t dim) { return static_cast<int>(4 * dim) + 6 + kMaxPackedPasses + 2 + 5; }
 
 const char* rmx_stage_name(uint32_t dim, int k) {
     static thread_local char buf[32];
@@ -1294,8 +1299,8 @@ const char* rmx_stage_name(uint32_t dim, int k) {
         return buf;
     }
     k -= P;
-    static const char* tail[] = {"unique", "unique_pk", "map_fill", "remap"};
-    if (k >= 0 && k < 4) return tail[k];
+    static const char* tail[] = {"unique", "window", "unique_pk", "map_fill", "remap"};
+    if (k >= 0 && k < 5) return tail[k];
     return "";
 }
 

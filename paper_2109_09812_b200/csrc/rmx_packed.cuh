@@ -1291,12 +1291,15 @@ __device__ __forceinline__ bool pk_pass_active(const SortPkArgs& a) {
 // Per-tile digit counts from the digit-byte array (1 B/row instead of the 4-8 B
 // key: k_pack and every downsweep also emit the next pass's digit per row),
 // 16 digits per 16-byte load, kUpGroup tiles per CTA iteration.
+// DROP: window mode's first pass without soup mode counts the used rows only (its own
+// instantiation, as the downsweep's)
+template <bool DROP = false>
 __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a0, uint32_t tile_rows) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     SortPkArgs a = a0;
-    if (*a.status || !pk_pass_active(a)) return;
+    if (*a.status || !pk_pass_active(a) || win_first_pass(a) != DROP) return;
     win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, tile_rows);
-    const bool drop = win_first_pass(a);  // window mode's first pass counts the used rows only
+    constexpr bool drop = DROP;
     __shared__ uint32_t s_h[kUpGroup * 256];
     const uint32_t ngroups = (a.ntiles + kUpGroup - 1u) / kUpGroup;
     const uint4* d16 = reinterpret_cast<const uint4*>(a.digits);  // tile_rows is a multiple of 16
@@ -1312,7 +1315,7 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a0, uint32_t t
             const uint4 w = __ldcs(d16 + ((base + r) >> 4));
             uint32_t* h = s_h + (r / tile_rows) * 256u;  // the 16 rows share a tile
             const uint32_t q[4] = {w.x, w.y, w.z, w.w};
-            if (drop) {
+            if constexpr (drop) {
                 const uint4 f = __ldcs(reinterpret_cast<const uint4*>(a.flags) + ((base + r) >> 4));
                 const uint32_t fq[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
@@ -1428,7 +1431,7 @@ __device__ __forceinline__ void soup_origins(const SortPkArgs& a, uint32_t* s_va
 // DROP: window mode's first pass without soup mode keeps the used rows only (a separate
 // instantiation: the extra code costs the common passes registers)
 template <int KW, int IPT, bool DROP>
-__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it) {
+__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it, bool iota) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
     const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
@@ -1456,7 +1459,8 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
     // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none), or in
     // soup mode the soup origins it makes in s_vals
-    const bool iota = !a.win_fb && a.pass == (a.plan[pk_base(4 * a.dim) + 6] != 0u ? 2 : 0);
+    // (iota: the first executed pass -- pass 0, or pass 2 in window mode; from the kernel's prologue,
+    // so that no plan load sits between the tile start and its bulk copy)
     const bool soup_on = iota && a.soup && *a.soup != 0u;
     constexpr bool drop = DROP;  // window mode's first pass keeps the used rows only
     if (tid == 0) {
@@ -1585,13 +1589,14 @@ __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a0, ui
     win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
     uint32_t* smem = dyn_smem<uint32_t>();
     const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
+    const bool iota = !a.win_fb && a.pass == (a.plan[pk_base(4 * a.dim) + 6] != 0u ? 2 : 0);
     for (uint32_t j = 0; j < tiles_per_cta; ++j) {
         const uint32_t tile = blockIdx.x * tiles_per_cta + j;
         if (tile >= a.ntiles) break;
         if (j) __syncthreads();  // the next tile's bulk copy overwrites the staging buffers
-        if constexpr (DROP) sort_pk_body<1, IPT, true>(a, smem, tile, j);  // (window mode: u32 keys)
-        else if (wide) sort_pk_body<2, IPT, false>(a, smem, tile, j);
-        else sort_pk_body<1, IPT, false>(a, smem, tile, j);
+        if constexpr (DROP) sort_pk_body<1, IPT, true>(a, smem, tile, j, iota);  // (window mode: u32 keys)
+        else if (wide) sort_pk_body<2, IPT, false>(a, smem, tile, j, iota);
+        else sort_pk_body<1, IPT, false>(a, smem, tile, j, iota);
     }
 }
 

@@ -41,7 +41,7 @@ def test_workspace_and_stage_queries():
     assert names[6] == "pk_pass_0" and names[13] == "pk_pass_7"
     assert names[14:16] == ["hash_groups", "first_hist"]
     assert names[16] == "sort_pass_0" and names[27] == "sort_pass_11"
-    assert names[-4:] == ["unique", "unique_pk", "map_fill", "remap"] and n == 32
+    assert names[-5:] == ["unique", "window", "unique_pk", "map_fill", "remap"] and n == 33
 
 
 def test_lattice_sizes_match_oracle():

@@ -5,6 +5,9 @@
         python tools/profile_step.py --config C2 --steps 1
     python tools/traffic.py gpurun_out/launches.csv C2 <executed packed passes> <V> <key words>
 
+Window mode (rmx_window.cuh): pass 2 executed packed passes; the window stage's DRAM bytes
+(k_win_bounds + k_win_unique) are recorded as window_dram_bytes_per_launch.
+
 Per executed packed pass: DRAM bytes of upsweep + colscan + downsweep, averaged
 over the executed passes (launches whose downsweep moved data).
 """
@@ -38,8 +41,9 @@ def main():
     path, cfg, npass, V, kw = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5])
     soup = "--soup" in sys.argv  # soup mode: pass 0 also reads the used flags
     launches = load(path)
-    per_pass = []
+    per_pass = []  # (upsweep + colscan + downsweep bytes, downsweep bytes) per pass launched
     cur = 0.0
+    win = 0.0      # window mode: k_win_bounds + k_win_unique
     for name, m in launches:
         b = m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
         if "k_pk_upsweep" in name:
@@ -48,8 +52,12 @@ def main():
             cur += b
         elif "k_pk_downsweep" in name:
             cur += b
-            per_pass.append(cur)
-    executed = per_pass[:npass]
+            per_pass.append((cur, b))
+        elif "k_win_bounds" in name or "k_win_unique" in name:
+            win += b
+    # the passes that ran (window mode: passes 0 and 1 are launched and exit)
+    big = max(d for _, d in per_pass)
+    executed = [c for c, d in per_pass if d > 0.05 * big][:npass]
     per_pass = [8 * kw + (0 if p == 0 else 4) + 4 + 1 + (1 if p + 1 < npass else 0) + (1 if soup and p == 0 else 0)
                 for p in range(npass)]
     algo = sum(per_pass) / npass * V
@@ -57,6 +65,7 @@ def main():
     data = json.load(open(out_path)) if os.path.exists(out_path) else {}
     data[cfg] = {
         "pass_dram_bytes_per_launch": sum(executed) / len(executed),
+        "window_dram_bytes_per_launch": win or None,
         "algorithmic_bytes_per_launch": algo,
         "executed_passes": npass,
         "source": f"{os.path.basename(path)} (ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, one step of "
