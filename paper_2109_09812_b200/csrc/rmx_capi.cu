@@ -264,13 +264,13 @@ int ensure_smem(K kernel, size_t smem) {
 
 // Persistent grid size for a kernel: resident CTAs per SM x SMs.
 template <typename K>
-int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid) {
+int persistent_grid(K kernel, size_t smem, uint64_t work_items, int& grid, int threads = kBlock) {
     int sms = 0;
     int rc = device_sms(sms);
     if (rc) return rc;
     if ((rc = ensure_smem(kernel, smem))) return rc;
     int per_sm = 0;
-    RMX_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem));
+    RMX_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
     if (per_sm < 1) per_sm = 1;
     uint64_t g = static_cast<uint64_t>(per_sm) * sms;
     if (work_items < g) g = work_items;
@@ -1049,8 +1049,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         RMX_CHECK(launch(k_win_bounds, g, kBlock, 0, s, wa));
         if ((rc = grid_for_stream(V, g))) return rc;
         int gu = 0;
-        if ((rc = persistent_grid(k_win_unique, WinSmem::bytes(), kWinCount, gu))) return rc;
-        RMX_CHECK(launch(k_win_unique, gu, kBlock, WinSmem::bytes(), s, wa));
+        if ((rc = persistent_grid(k_win_unique, WinSmem::bytes(), kWinCount, gu, kWinThreads))) return rc;
+        RMX_CHECK(launch(k_win_unique, gu, kWinThreads, WinSmem::bytes(), s, wa));
         RMX_CHECK(cudaGetLastError());
         if ((rc = rec.mark())) return rc;  // (stage "window")
         // fallback (a window of more than kWinMaxRows rows): digit 0, the four passes, then the
