@@ -187,9 +187,11 @@ int rmx_plan_guess_info(void* workspace, uint64_t n_vertices, uint32_t dim, void
  * remap runs --, else 0; 1 if the indices were strictly increasing}. */
 int rmx_soup_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
-/* Window mode of the last call that used `workspace` (synchronises `stream`): info[4] = {bit 0
- * window mode decided, bit 1 its fallback ran; used rows sorted; non-empty windows; rows of the
- * largest window}. */
+/* Window mode of the last call that used `workspace` (u32 packed keys of 25..32 bits sorted by
+ * their top 16 bits, per-window presence bitmaps; synchronises `stream`): info[4] = {bit 0 window
+ * mode decided, bit 1 its fallback ran; rows of the window passes (soup mode: all slots, else the
+ * used rows); non-empty windows; rows of the largest window}.  Diagnostic; no reference
+ * counterpart. */
 int rmx_window_info(void* workspace, uint64_t n_vertices, uint32_t dim, void* stream, uint32_t* info);
 
 /* Hash mode of the last call that used `workspace` (keys wider than 64 bits, no
