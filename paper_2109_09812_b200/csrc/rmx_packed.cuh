@@ -1275,6 +1275,44 @@ __device__ __forceinline__ bool win_after_first(const SortPkArgs& a) {
     return a.win_fb || (a.pass > 2 && a.plan[pk_base(4 * a.dim) + 6] != 0u);
 }
 
+// The words a packed pass's kernels test before they start, loaded in one batch (independent
+// loads: one L2 round trip in the prologue instead of a chain of them).
+struct PkGate {
+    uint32_t status, p0, p1, p3, p5, p6, p7, win_rows, soup;
+};
+__device__ __forceinline__ PkGate pk_gate(const SortPkArgs& a) {
+    const uint32_t* pk = a.plan + pk_base(4 * a.dim);
+    PkGate g;
+    g.status = *a.status;
+    g.p0 = pk[0];
+    g.p1 = pk[1];
+    g.p3 = pk[3];
+    g.p5 = pk[5];
+    g.p6 = pk[6];
+    g.p7 = pk[7];
+    g.win_rows = a.win_rows ? *a.win_rows : 0u;
+    g.soup = a.soup ? *a.soup : 0u;
+    return g;
+}
+// the pass runs: packed mode, pass < packed passes; window mode runs passes 2 and 3 (its fallback
+// passes only when the fallback word is set)
+__device__ __forceinline__ bool gate_active(const PkGate& g, const SortPkArgs& a) {
+    if (g.status != 0u || g.p0 == 0u || static_cast<uint32_t>(a.pass) >= g.p3) return false;
+    if (a.win_fb) return g.p6 != 0u && g.p7 != 0u;
+    return !(g.p6 != 0u && a.pass < 2);
+}
+// window mode's first pass when it drops the unused rows (pk[5]: no soup mode)
+__device__ __forceinline__ bool gate_drop(const PkGate& g, const SortPkArgs& a) {
+    return !a.win_fb && a.pass == 2 && g.p6 != 0u && g.p5 != 0u;
+}
+// window mode after its first pass: the kernels run over *win_rows rows
+__device__ __forceinline__ void gate_rows(const PkGate& g, SortPkArgs& a, uint32_t tile) {
+    if (a.win_rows && g.p6 != 0u && (a.win_fb || a.pass > 2)) {
+        a.n = g.win_rows;
+        a.ntiles = (a.n + tile - 1u) / tile;
+    }
+}
+
 // The upsweep counts kUpGroup consecutive tiles per CTA iteration so every digit's
 // counts of the group leave as one 32-byte sector (digit-major layout).
 constexpr uint32_t kUpGroup = 8;
@@ -1297,8 +1335,9 @@ template <bool DROP = false>
 __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a0, uint32_t tile_rows) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     SortPkArgs a = a0;
-    if (*a.status || !pk_pass_active(a) || win_first_pass(a) != DROP) return;
-    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, tile_rows);
+    const PkGate gt = pk_gate(a);
+    if (!gate_active(gt, a) || gate_drop(gt, a) != DROP) return;
+    gate_rows(gt, a, tile_rows);
     constexpr bool drop = DROP;
     __shared__ uint32_t s_h[kUpGroup * 256];
     const uint32_t ngroups = (a.ntiles + kUpGroup - 1u) / kUpGroup;
@@ -1351,8 +1390,9 @@ __global__ void __launch_bounds__(kBlock) k_pk_upsweep(SortPkArgs a0, uint32_t t
 __global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a0) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     SortPkArgs a = a0;
-    if (*a.status || !pk_pass_active(a)) return;
-    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
+    const PkGate gt = pk_gate(a);
+    if (!gate_active(gt, a)) return;
+    gate_rows(gt, a, a.tile_rows);
     __shared__ uint32_t s_warp[32];
     uint32_t* row = a.counts + static_cast<size_t>(blockIdx.x) * a.cstride;
     uint32_t carry = 0;
@@ -1374,7 +1414,7 @@ __global__ void __launch_bounds__(1024) k_pk_colscan(SortPkArgs a0) {
     }
     if (threadIdx.x == 0) {
         a.totals[blockIdx.x] = carry;
-        if (win_first_pass(a) && carry) atomicAdd(a.win_rows, carry);  // the rows the window passes keep
+        if (gate_drop(gt, a) && carry) atomicAdd(a.win_rows, carry);  // the rows the window passes keep
     }
 }
 
@@ -1431,7 +1471,8 @@ __device__ __forceinline__ void soup_origins(const SortPkArgs& a, uint32_t* s_va
 // DROP: window mode's first pass without soup mode keeps the used rows only (a separate
 // instantiation: the extra code costs the common passes registers)
 template <int KW, int IPT, bool DROP>
-__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it, bool iota) {
+__device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem, uint32_t tile, uint32_t it, bool iota,
+                                             bool soup_on, bool emit_next) {
     using Key = typename PkKey<KW>::T;
     constexpr int TILE = kBlock * IPT;
     const uint32_t src = static_cast<uint32_t>(a.pass) & 1u;
@@ -1442,8 +1483,7 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     Key* __restrict__ out_k = reinterpret_cast<Key*>(ob);
     uint32_t* __restrict__ out_v = ob + a.vals_off;
     const int shift = 8 * a.pass;
-    // the next pass (if any) reads its digits from the byte array
-    const bool emit_next = static_cast<uint32_t>(a.pass) + 1u < a.plan[pk_base(4 * a.dim) + 3];
+    // (emit_next: the next pass, if any, reads its digits from the byte array)
 
     Key* s_keys = reinterpret_cast<Key*>(smem);
     uint32_t* s_vals = smem + static_cast<size_t>(TILE) * 2;  // keys region sized for u64
@@ -1459,9 +1499,9 @@ __device__ __forceinline__ void sort_pk_body(const SortPkArgs& a, uint32_t* smem
     const uint32_t tile_n = min(static_cast<uint32_t>(TILE), a.n - base);
     // pass 0 reads k_pack's keys only: origins are the row numbers (k_pack writes none), or in
     // soup mode the soup origins it makes in s_vals
-    // (iota: the first executed pass -- pass 0, or pass 2 in window mode; from the kernel's prologue,
-    // so that no plan load sits between the tile start and its bulk copy)
-    const bool soup_on = iota && a.soup && *a.soup != 0u;
+    // (iota: the first executed pass -- pass 0, or pass 2 in window mode; iota, soup_on and
+    // emit_next come from the kernel's prologue, so that no plan load sits between the tile start
+    // and its bulk copy)
     constexpr bool drop = DROP;  // window mode's first pass keeps the used rows only
     if (tid == 0) {
         if (it == 0) {
@@ -1585,18 +1625,21 @@ template <int IPT, int MINB, bool DROP = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_pk_downsweep(SortPkArgs a0, uint32_t tiles_per_cta) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     SortPkArgs a = a0;
-    if (*a.status || !pk_pass_active(a) || win_first_pass(a) != DROP) return;
-    win_rows_patch(a.plan, a.dim, a.win_rows, win_after_first(a), a.n, a.ntiles, a.tile_rows);
+    const PkGate gt = pk_gate(a);
+    if (!gate_active(gt, a) || gate_drop(gt, a) != DROP) return;
+    gate_rows(gt, a, a.tile_rows);
     uint32_t* smem = dyn_smem<uint32_t>();
-    const bool wide = a.plan[pk_base(4 * a.dim) + 1] == 2u;
-    const bool iota = !a.win_fb && a.pass == (a.plan[pk_base(4 * a.dim) + 6] != 0u ? 2 : 0);
+    const bool wide = gt.p1 == 2u;
+    const bool iota = !a.win_fb && a.pass == (gt.p6 != 0u ? 2 : 0);
+    const bool soup_on = iota && gt.soup != 0u;
+    const bool emit_next = static_cast<uint32_t>(a.pass) + 1u < gt.p3;
     for (uint32_t j = 0; j < tiles_per_cta; ++j) {
         const uint32_t tile = blockIdx.x * tiles_per_cta + j;
         if (tile >= a.ntiles) break;
         if (j) __syncthreads();  // the next tile's bulk copy overwrites the staging buffers
-        if constexpr (DROP) sort_pk_body<1, IPT, true>(a, smem, tile, j, iota);  // (window mode: u32 keys)
-        else if (wide) sort_pk_body<2, IPT, false>(a, smem, tile, j, iota);
-        else sort_pk_body<1, IPT, false>(a, smem, tile, j, iota);
+        if constexpr (DROP) sort_pk_body<1, IPT, true>(a, smem, tile, j, iota, soup_on, emit_next);  // (u32 keys)
+        else if (wide) sort_pk_body<2, IPT, false>(a, smem, tile, j, iota, soup_on, emit_next);
+        else sort_pk_body<1, IPT, false>(a, smem, tile, j, iota, soup_on, emit_next);
     }
 }
 
