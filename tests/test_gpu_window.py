@@ -144,3 +144,11 @@ def test_scratch_request_keeps_the_full_path(rmx):
     assert np.array_equal(out.elements, ref["elements"])
     for f in ("org_id", "nodup", "new_idx", "perm"):
         assert np.array_equal(np.asarray(getattr(sc, f)), ref[f]), f
+
+
+def test_four_components_keep_the_full_path(rmx):
+    """Window mode is used for D <= 3 (C3's D = 4 tets measured faster without it)."""
+    rng = np.random.default_rng(8)
+    words = rng.integers(0, 1 << 7, size=(200_000, 4), dtype=np.uint64).astype(np.uint32)
+    idx = rng.integers(0, 200_000, size=(100_000, 4)).astype(np.uint32)
+    assert check(words, idx)[0] == 0
