@@ -245,26 +245,35 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
         const uint32_t nch = (rows + csz - 1u) / csz;
 #pragma unroll
         for (uint32_t j = 0; j < kWpt; ++j) s_bm[tid * kWpt + j] = 0u;
-        // ---- mark the low 16 bits, chunk by chunk
+        if (tid < 256u) s_bcnt[tid] = 0u;
+        // ---- mark the low 16 bits, chunk by chunk (a one-chunk window also counts its buckets)
         uint32_t off = 0;
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const uint32_t cr = min(csz, rows - ch * csz);
             off = stage(s + ch * csz, cr);
             for (uint32_t q = tid; q < cr; q += kWinThreads) {
                 const uint32_t k = s_key[off + q] & 0xFFFFu;
-                if (s_val[off + q] < lim) atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
+                const uint32_t org = s_val[off + q];
+                if (org < lim) {
+                    atomicOr(s_bm + (k >> 5), 1u << (k & 31u));
+                    if (one) atomicAdd(s_bcnt + (org >> bs), 1u);
+                }
             }
         }
         __syncthreads();
-        // ---- per-word prefix popcounts, the window's distinct keys; publish the aggregate
+        // ---- per-word prefix popcounts, the window's distinct keys; publish the aggregate (a
+        // one-chunk window scans its bucket counts in the same block scan: counts < 2^16 each)
         uint32_t wb[kWpt], cnt = 0;
 #pragma unroll
         for (uint32_t j = 0; j < kWpt; ++j) {
             wb[j] = s_bm[tid * kWpt + j];
             cnt += __popc(wb[j]);
         }
-        uint32_t total;
-        uint32_t run = block_exclusive_scan<kWinWarps>(cnt, s_warp, total);
+        const uint32_t bc1 = one && tid < 256u ? s_bcnt[tid] : 0u;
+        uint32_t both;
+        const uint32_t run2 = block_exclusive_scan<kWinWarps>(cnt | (bc1 << 17), s_warp, both);
+        const uint32_t total = both & 0x1FFFFu;  // (distinct keys <= 2^16 in bits 0..16, rows < 2^15 above)
+        uint32_t run = run2 & 0x1FFFFu;
         const uint32_t pre0 = run;  // distinct keys before this thread's bitmap words
 #pragma unroll
         for (uint32_t j = 0; j < kWpt; ++j) {
@@ -274,19 +283,27 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
         if (tid == 0) st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, total));
         // ---- pairs, chunk by chunk (a one-chunk window is still staged)
         uint16_t* s_perm = reinterpret_cast<uint16_t*>(one ? s_bm : s_key + kWinSub + 8);
+        if (one && tid < 256u) {  // bucket space from the combined scan: one global reservation per bucket
+            const uint32_t bstart = run2 >> 17;
+            s_bcur[tid] = bstart;
+            if (bc1) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc1) - bstart;
+        }
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const uint32_t cr = min(csz, rows - ch * csz);
-            if (!one) off = stage(s + ch * csz, cr);
-            if (tid < 256u) s_bcnt[tid] = 0u;
-            __syncthreads();  // (s_pre, s_bcnt)
-            // local new index of every row (in place), bucket counts; warp 0 then looks back
+            if (!one) {
+                off = stage(s + ch * csz, cr);
+                if (tid < 256u) s_bcnt[tid] = 0u;
+            }
+            __syncthreads();  // (s_pre, s_bcnt, s_bcur, s_bglob)
+            // local new index of every row (in place; a chunk of a larger window also counts its
+            // buckets); warp 0 then looks back
 #pragma unroll 4
             for (uint32_t q = tid; q < cr; q += kWinThreads) {
                 if (s_val[off + q] < lim) {
                     const uint32_t k = s_key[off + q] & 0xFFFFu;
                     const uint32_t wd = k >> 5;
                     s_key[off + q] = s_pre[wd] + __popc(s_bm[wd] & ((1u << (k & 31u)) - 1u));
-                    atomicAdd(s_bcnt + (s_val[off + q] >> bs), 1u);
+                    if (!one) atomicAdd(s_bcnt + (s_val[off + q] >> bs), 1u);
                 }
             }
             if (ch == 0 && warp == 0) {
@@ -294,15 +311,14 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
                 if (lane == 0) slot[1] = excl;
             }
             __syncthreads();
-            // bucket space: a block scan for the staging, one global reservation per bucket
-            uint32_t n_used;  // the chunk's rows with pairs (soup mode: origin < I)
-            {
+            uint32_t n_used = both >> 17;  // the chunk's rows with pairs (soup mode: origin < I)
+            if (!one) {  // bucket space: a block scan for the staging, one global reservation per bucket
                 const uint32_t bc = tid < 256u ? s_bcnt[tid] : 0u;
                 const uint32_t bstart = block_exclusive_scan<kWinWarps>(bc, s_warp + kWinWarps, n_used);
                 if (tid < 256u) s_bcur[tid] = bstart;
                 if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
+                __syncthreads();
             }
-            __syncthreads();
             // bucket order as a row permutation (warp-aggregated slots)
 #pragma unroll 4
             for (uint32_t q0 = 0; q0 < cr; q0 += kWinThreads) {  // (warp-uniform)
