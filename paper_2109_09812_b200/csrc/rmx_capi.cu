@@ -1047,7 +1047,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                    plan, d_status, static_cast<uint32_t>(V), L.D, L.bucket_shift, win_rows, static_cast<uint32_t>(V),
                    static_cast<const uint32_t*>(soup)};
         int g = 0;
-        if ((rc = grid_for_stream((V + 3) / 4, g))) return rc;
+        if ((rc = grid_for_stream((V + 7) / 8, g))) return rc;
         RMX_CHECK(launch(k_win_bounds, g, kBlock, 0, s, wa));
         if ((rc = grid_for_stream(V, g))) return rc;
         int gu = 0;

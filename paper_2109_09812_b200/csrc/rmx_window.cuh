@@ -77,7 +77,7 @@ struct WinArgs {
 };
 
 // first row and one past the last row of every non-empty window (empty windows keep wstart =
-// 0xFFFFFFFF; their wend is never read), four rows per thread; and the fallback decision: rows
+// 0xFFFFFFFF; their wend is never read), eight rows per thread; and the fallback decision: rows
 // p = j * kWinProbe and p + kWinProbe in one window mean a window of more than kWinProbe rows
 // (every window of more than kWinMaxRows = 2 kWinProbe rows holds such a pair), which would
 // serialise on one CTA -- the full packed path runs instead (pk[7])
@@ -86,24 +86,31 @@ __global__ void __launch_bounds__(kBlock) k_win_bounds(WinArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*a.status || !win_active(a.plan, a.dim)) return;
     const uint32_t n = *a.win_rows;
-    const uint32_t groups = (n + 3u) / 4u;
+    const uint32_t groups = (n + 7u) / 8u;  // eight rows per thread: two 16-byte loads in flight
     const uint32_t stride = gridDim.x * kBlock;
     for (uint32_t g = blockIdx.x * kBlock + threadIdx.x; g < groups; g += stride) {
-        const uint32_t p0 = 4u * g;
-        uint32_t w[4];
-        if (p0 + 3u < n) {
-            const uint4 k = __ldcs(reinterpret_cast<const uint4*>(a.keys) + g);
-            w[0] = k.x >> 16;
-            w[1] = k.y >> 16;
-            w[2] = k.z >> 16;
-            w[3] = k.w >> 16;
+        const uint32_t p0 = 8u * g;
+        uint32_t w[8];
+        if (p0 + 7u < n) {
+            const uint4 k0 = __ldcs(reinterpret_cast<const uint4*>(a.keys) + 2 * g);
+            const uint4 k1 = __ldcs(reinterpret_cast<const uint4*>(a.keys) + 2 * g + 1);
+            w[0] = k0.x >> 16;
+            w[1] = k0.y >> 16;
+            w[2] = k0.z >> 16;
+            w[3] = k0.w >> 16;
+            w[4] = k1.x >> 16;
+            w[5] = k1.y >> 16;
+            w[6] = k1.z >> 16;
+            w[7] = k1.w >> 16;
         } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) w[j] = p0 + j < n ? __ldg(a.keys + p0 + j) >> 16 : 0xFFFFFFFFu;
+            for (int j = 0; j < 8; ++j) w[j] = p0 + j < n ? __ldg(a.keys + p0 + j) >> 16 : 0xFFFFFFFFu;
         }
-        uint32_t prev = p0 ? __ldg(a.keys + p0 - 1u) >> 16 : 0xFFFFFFFFu;
+        // the previous row's window: the lane before's last row (lane 0 loads it)
+        uint32_t prev = __shfl_up_sync(__activemask(), w[7], 1);
+        if ((threadIdx.x & 31u) == 0u) prev = p0 ? __ldg(a.keys + p0 - 1u) >> 16 : 0xFFFFFFFFu;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 8; ++j) {
             const uint32_t p = p0 + static_cast<uint32_t>(j);
             if (p >= n) break;
             if (w[j] != prev) {
