@@ -10,13 +10,16 @@
 //   * writes the window's distinct keys in order (set bits, ascending) to ukeys for k_unpack_pk,
 //   * gives every row its new index = base + set bits below its key, and writes (origin, new
 //     index) pairs bucketed by origin for k_map_fill (as k_unique_pk does).
-// Passes 0, 1, k_head_count_pk, k_tile_scan and k_unique_pk do not run; the first window pass drops
-// the unused rows (no index reads their map entries, and the replacement row they stand for is a
-// used row, so the distinct keys are those of the used rows) -- they would otherwise share the
-// replacement key and form one giant window.  A window of more than
-// kWinMaxRows rows (keys whose top 16 bits barely vary) would serialise on one CTA: k_win_ends
-// then sets the fallback word (pk[7]) and the full packed path runs after all (the digit byte 0
-// re-extracted, four passes over the window-grouped rows, the usual unique kernels).
+// Passes 0, 1, k_head_count_pk, k_tile_scan and k_unique_pk do not run.  The unused rows (no
+// index reads their map entries, and the replacement row they stand for is a used row, so the
+// distinct keys are those of the used rows) would all share the replacement key and form one giant
+// window: without soup mode the first window pass drops them (pk[5]); in soup mode they stay, with
+// keys spread by k_pack (a used neighbour's key or a row hash), and this kernel skips their
+// origins >= I.  A window of more than kWinMaxRows rows (keys whose top 16 bits barely vary)
+// would serialise on one CTA: k_win_bounds then sets the fallback word (pk[7]) and the full packed
+// path runs after all (the digit byte 0 re-extracted, four passes over the window-grouped rows,
+// the usual unique kernels).  Window mode is decided on the device (k_win_decide) for D <= 3 and
+// no scratch request; RMX_WINDOW=0 turns it off.
 #pragma once
 
 #include "rmx_packed.cuh"
