@@ -152,3 +152,18 @@ def test_four_components_keep_the_full_path(rmx):
     words = rng.integers(0, 1 << 7, size=(200_000, 4), dtype=np.uint64).astype(np.uint32)
     idx = rng.integers(0, 200_000, size=(100_000, 4)).astype(np.uint32)
     assert check(words, idx)[0] == 0
+
+
+def test_full_window(rmx, monkeypatch):
+    """One window holds all 2^16 low values (the distinct count fills its 17-bit field) next to
+    windows holding one key each."""
+    rng = np.random.default_rng(9)
+    full = (np.uint32(0x0123) << np.uint32(16)) | np.arange(1 << 16, dtype=np.uint32)
+    other = rng.integers(0, 1 << 28, size=40_000, dtype=np.uint64).astype(np.uint32)
+    words = np.concatenate([full, full[::-1], other]).reshape(-1, 1)
+    perm = rng.permutation(words.shape[0])
+    words = words[perm]
+    idx = rng.integers(0, words.shape[0], size=(90_000, 2)).astype(np.uint32)
+    idx[: words.shape[0] // 2] = np.arange(words.shape[0], dtype=np.uint32)[: (words.shape[0] // 2) * 2].reshape(-1, 2)
+    winfo = check(words, idx, monkeypatch)
+    assert winfo[0] == 1
