@@ -167,3 +167,21 @@ def test_full_window(rmx, monkeypatch):
     idx[: words.shape[0] // 2] = np.arange(words.shape[0], dtype=np.uint32)[: (words.shape[0] // 2) * 2].reshape(-1, 2)
     winfo = check(words, idx, monkeypatch)
     assert winfo[0] == 1
+
+
+def test_lean_mode(rmx, monkeypatch):
+    """Memory-lean mode (the vertex buffer is the second sort buffer) with window mode: 30-bit keys,
+    unused rows dropped by the first window pass, pairs written into the caller's vertex buffer."""
+    from paper_2109_09812_b200 import pipeline
+    rng = np.random.default_rng(10)
+    V = 300_000
+    words = (rng.integers(0, 1 << 10, size=(V, 3), dtype=np.uint64) << np.uint64(8)).astype(np.uint32)
+    idx = rng.integers(0, 280_000, size=(150_000, 3)).astype(np.uint32)
+    ref = O.reindex(words, idx)
+    for win in ("1", "0"):
+        monkeypatch.setenv("RMX_WINDOW", win)
+        vt = torch.from_numpy(words.view(np.int32)).cuda()
+        it = torch.from_numpy(idx.view(np.int32)).cuda()
+        r = pipeline.reindex_tensors_lean(vt, it)
+        assert np.array_equal(r.vertices[:r.new_count].cpu().numpy().view(np.uint32), ref["vertices"].view(np.uint32))
+        assert np.array_equal(r.elements.cpu().numpy().view(np.uint32), ref["elements"])
