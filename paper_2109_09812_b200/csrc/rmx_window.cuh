@@ -177,11 +177,9 @@ __device__ __forceinline__ uint32_t win_slot(uint32_t* s_bcur, bool valid, uint3
 }
 
 // Rows are staged in shared memory by bulk copies (keys + origins).  A window of up to kWinCap rows
-// is one chunk (its bucket permutation then reuses the bitmap words); a larger one is processed in
-// chunks of kWinSub rows (marked chunk by chunk, then re-staged for the pairs, the permutation
-// behind the chunk).  3 CTAs per SM.
+// is one chunk; a larger one is processed in chunks of kWinCap rows (marked chunk by chunk, then
+// re-staged for the pairs).  3 CTAs per SM.
 constexpr uint32_t kWinCap = 6656;
-constexpr uint32_t kWinSub = 4096;
 constexpr uint32_t kWinStage = kWinCap + 8;  // + 16-byte alignment slack
 // 3 CTAs of 256 threads per SM (measured: 2 x 512 threads, 1.68 vs 1.42 ms on C2)
 constexpr int kWinThreads = 256, kWinWarps = kWinThreads / 32, kWinMinBlocks = 3;
@@ -192,8 +190,6 @@ struct WinSmem {
                             kWarp = kBglob + 256, kMisc = kWarp + 2 * kWinWarps, kBar = kMisc + 8, kWordsTotal = kBar + 2;
     static __host__ __device__ size_t bytes() { return kWordsTotal * 4; }
 };
-static_assert(kWinCap * 2 <= 2 * kWinWords * 4, "a one-chunk window's permutation fits the bitmap and prefix words");
-static_assert(kWinSub + 8 + kWinSub / 2 <= kWinStage, "a chunk's permutation fits behind its staged keys");
 
 __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinArgs a) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
@@ -251,7 +247,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
             continue;
         }
         const bool one = rows <= kWinCap;
-        const uint32_t csz = one ? kWinCap : kWinSub;
+        constexpr uint32_t csz = kWinCap;
         const uint32_t nch = (rows + csz - 1u) / csz;
 #pragma unroll
         for (uint32_t j = 0; j < kWpt; ++j) s_bm[tid * kWpt + j] = 0u;
@@ -292,7 +288,6 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
         }
         if (tid == 0) st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, total));
         // ---- pairs, chunk by chunk (a one-chunk window is still staged)
-        uint16_t* s_perm = reinterpret_cast<uint16_t*>(one ? s_bm : s_key + kWinSub + 8);
         if (one && tid < 256u) {  // bucket space from the combined scan: one global reservation per bucket
             const uint32_t bstart = run2 >> 17;
             s_bcur[tid] = bstart;
@@ -321,30 +316,27 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
                 if (lane == 0) slot[1] = excl;
             }
             __syncthreads();
-            uint32_t n_used = both >> 17;  // the chunk's rows with pairs (soup mode: origin < I)
-            if (!one) {  // bucket space: a block scan for the staging, one global reservation per bucket
+            if (!one) {  // bucket space: a block scan, one global reservation per bucket
                 const uint32_t bc = tid < 256u ? s_bcnt[tid] : 0u;
-                const uint32_t bstart = block_exclusive_scan<kWinWarps>(bc, s_warp + kWinWarps, n_used);
+                uint32_t chunk_rows;
+                const uint32_t bstart = block_exclusive_scan<kWinWarps>(bc, s_warp + kWinWarps, chunk_rows);
                 if (tid < 256u) s_bcur[tid] = bstart;
                 if (bc) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc) - bstart;
                 __syncthreads();
             }
-            // bucket order as a row permutation (warp-aggregated slots)
-#pragma unroll 4
+            const uint32_t base = slot[1];
+            // every used row's (origin, new index) pair straight to its slot in its bucket's run
+            // (warp-aggregated slots; the run's stores merge in L2 -- measured faster than a
+            // shared-memory permutation and a coalesced copy-out: 1.34 vs 1.42 ms on C2)
             for (uint32_t q0 = 0; q0 < cr; q0 += kWinThreads) {  // (warp-uniform)
                 const uint32_t q = q0 + tid;
                 const uint32_t org = q < cr ? s_val[off + q] : 0xFFFFFFFFu;
                 const bool valid = org < lim;
                 const uint32_t pos = win_slot(s_bcur, valid, org >> bs);
-                if (valid) s_perm[pos] = static_cast<uint16_t>(q);
-            }
-            __syncthreads();
-            const uint32_t base = slot[1];
-            for (uint32_t q = tid; q < n_used; q += kWinThreads) {
-                const uint32_t r = off + s_perm[q];
-                const uint32_t org = s_val[r];
-                RMX_CHECK_INDEX(s_bglob[org >> bs] + q, a.n_slots);
-                a.pairs[s_bglob[org >> bs] + q] = make_uint2(org, base + s_key[r]);
+                if (valid) {
+                    RMX_CHECK_INDEX(s_bglob[org >> bs] + pos, a.n_slots);
+                    a.pairs[s_bglob[org >> bs] + pos] = make_uint2(org, base + s_key[off + q]);
+                }
             }
         }
         // ---- the window's distinct keys out, ascending
