@@ -154,6 +154,18 @@ __device__ __forceinline__ void stage_tile2(void* dst0, const void* src0, uint32
         bulk_g2s(static_cast<char*>(dst1) + off, static_cast<const char*>(src1) + off, min(kChunk, b1 - off), bar);
 }
 
+// The slot of this lane's row in bucket b (s_bcur: the buckets' next free slots), warp-aggregated:
+// rows of a warp often share a bucket, and same-address shared atomics that return a value
+// serialise.  All lanes call it (`valid` masks the rows).
+__device__ __forceinline__ uint32_t bucket_slot(uint32_t* s_bcur, bool valid, uint32_t b) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t peers = __match_any_sync(kFull, valid ? b : 0xFFFFFFFFu);
+    const uint32_t leader = __ffs(peers) - 1u;
+    uint32_t pos = 0;
+    if (valid && lane == leader) pos = atomicAdd(s_bcur + b, __popc(peers));
+    return __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+}
+
 // ---- block scan over one value per thread ----------------------------------
 // Exclusive scan of `v` across a block of NW warps; `s_warp` holds NW words and
 // must not be reused until a later __syncthreads.

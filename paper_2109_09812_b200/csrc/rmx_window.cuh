@@ -163,18 +163,9 @@ __device__ __forceinline__ uint32_t win_lookback(const WinArgs& a, uint32_t w, u
     return excl;
 }
 
-// Rows of a warp often share an origin bucket, and same-address shared atomics that return a
-// value serialise: the row's slot in its bucket is warp-aggregated (s_bcur: the buckets' next free
-// slots; the marks and bucket counts stay plain fire-and-forget atomics -- MATCH.ANY aggregation
-// of those measured slower on C2 and C3).  Call from warp-uniform loops.
-__device__ __forceinline__ uint32_t win_slot(uint32_t* s_bcur, bool valid, uint32_t b) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t peers = __match_any_sync(kFull, valid ? b : 0xFFFFFFFFu);
-    const uint32_t leader = __ffs(peers) - 1u;
-    uint32_t pos = 0;
-    if (valid && lane == leader) pos = atomicAdd(s_bcur + b, __popc(peers));
-    return __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
-}
+// A row's slot in its origin bucket is warp-aggregated (bucket_slot, rmx_common.cuh: rows of a
+// window sit in origin order, so a warp's rows often share a bucket); the marks and bucket counts
+// stay plain fire-and-forget atomics (MATCH.ANY aggregation of those measured slower on C2 / C3).
 
 // Rows are staged in shared memory by bulk copies (keys + origins).  A window of up to kWinCap rows
 // is one chunk; a larger one is processed in chunks of kWinCap rows (marked chunk by chunk, then
@@ -332,7 +323,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
                 const uint32_t q = q0 + tid;
                 const uint32_t org = q < cr ? s_val[off + q] : 0xFFFFFFFFu;
                 const bool valid = org < lim;
-                const uint32_t pos = win_slot(s_bcur, valid, org >> bs);
+                const uint32_t pos = bucket_slot(s_bcur, valid, org >> bs);
                 if (valid) {
                     RMX_CHECK_INDEX(s_bglob[org >> bs] + pos, a.n_slots);
                     a.pairs[s_bglob[org >> bs] + pos] = make_uint2(org, base + s_key[off + q]);
