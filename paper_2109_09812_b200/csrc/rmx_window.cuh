@@ -279,10 +279,13 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
         }
         if (tid == 0) st_relaxed(a.desc + w, pack_desc(1u, w == 0 ? kPrefix : kAggregate, total));
         // ---- pairs, chunk by chunk (a one-chunk window is still staged)
-        if (one && tid < 256u) {  // bucket space from the combined scan: one global reservation per bucket
-            const uint32_t bstart = run2 >> 17;
-            s_bcur[tid] = bstart;
-            if (bc1) s_bglob[tid] = (tid << bs) + atomicAdd(a.fill + tid, bc1) - bstart;
+        // bucket space from the combined scan: one global reservation per bucket (its round trip
+        // overlaps the new-index pass below)
+        const uint32_t bstart1 = run2 >> 17;
+        uint32_t bfill1 = 0u;
+        if (one && tid < 256u) {
+            s_bcur[tid] = bstart1;
+            if (bc1) bfill1 = atomicAdd(a.fill + tid, bc1);
         }
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const uint32_t cr = min(csz, rows - ch * csz);
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
                 const uint32_t excl = win_lookback(a, w, total);
                 if (lane == 0) slot[1] = excl;
             }
+            if (one && bc1) s_bglob[tid] = (tid << bs) + bfill1 - bstart1;
             __syncthreads();
             if (!one) {  // bucket space: a block scan, one global reservation per bucket
                 const uint32_t bc = tid < 256u ? s_bcnt[tid] : 0u;
