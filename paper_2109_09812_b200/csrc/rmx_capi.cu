@@ -939,7 +939,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
                          static_cast<const uint32_t*>(nullptr), static_cast<const uint32_t*>(soup), win_rows,
                          static_cast<uint32_t>(V)));
         PackArgs a{vtx, flags, idx, plan, rows0, L.vals_off, dig, fields, rank16, d_status, static_cast<uint32_t>(V),
-                   L.D, vec, vary, spec, 0};
+                   L.D, vec, vary, spec, 0, win_rows};
         if ((rc = dispatch_pack(a, s, value_ranks && spec_enabled() && L.D <= 3))) return rc;
         if (value_ranks) {
             // a speculative plan that k_pack's check failed (kSpecMiss): the path it skipped --
@@ -1057,9 +1057,9 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         if ((rc = rec.mark())) return rc;  // (stage "window")
         // fallback (a window of more than kWinMaxRows rows): digit 0, the four passes, then the
         // usual unique kernels below
-        RMX_CHECK(launch(k_win_digit0, g, kBlock, 0, s, static_cast<const uint32_t*>(plan), L.D,
-                         static_cast<const uint32_t*>(rows0), dig, static_cast<const uint32_t*>(win_rows),
-                         static_cast<const uint32_t*>(d_status)));
+        RMX_CHECK(launch(k_win_digit0, g, kBlock, 0, s, static_cast<const uint32_t*>(plan), L.D, rows0,
+                         static_cast<const uint32_t*>(rows0 + L.vals_off), dig, static_cast<const uint32_t*>(win_rows),
+                         static_cast<const uint32_t*>(soup), static_cast<const uint32_t*>(d_status)));
         for (int p = 0; p < 4; ++p) {
             SortPkArgs fa{rows0, rows1, L.vals_off, plan, reinterpret_cast<uint32_t*>(base + L.pk_counts),
                           reinterpret_cast<uint32_t*>(base + L.pk_totals), dig + (p & 1) * dig_stride,

@@ -1021,6 +1021,8 @@ struct PackArgs {
     const uint32_t* vary;    // K1a varying bits (the check of a speculative plan)
     uint32_t* spec;          // kSpecOn: check every row against the plan; kSpecMiss: a row failed
     int fallback;            // the re-pack after a failed check (exits unless kSpecMiss)
+    uint32_t* win_aux;       // window mode in soup mode: [1] = the replacement row's key (its fallback
+                             // gives the unused rows that key back)
 };
 
 // CHECK: the variant that packs under a speculative plan and checks every used row (launched
@@ -1097,6 +1099,7 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
             else return vm.on ? vm.ranked_key(pack0, k, a.rank16) : pack0(k);
         };
         auto pack = [&](const uint32_t (&k)[D_CT]) { return vm.on ? vm.ranked_key(pack0, k, a.rank16) : pack0(k); };
+        if (spread && a.win_aux && blockIdx.x == 0 && threadIdx.x == 0) a.win_aux[1] = static_cast<uint32_t>(pack(ref));
         uint64_t done = 0;
         if constexpr (D_CT == 3) {
             if (a.vec) {
@@ -1182,6 +1185,14 @@ __global__ void __launch_bounds__(kBlock, CHECK ? 2 : 4) k_pack(PackArgs a) {
             if ((threadIdx.x & 31u) == 0u && miss) atomicOr(a.spec, kSpecMiss);
         }
     } else {
+        if (spread && a.win_aux && blockIdx.x == 0 && threadIdx.x == 0) {
+            uint64_t key = 0;
+            for (uint32_t r = 0; r < nruns; ++r) {
+                const uint32_t* ru = s_runs + 4 * r;
+                key |= static_cast<uint64_t>((__ldg(repl + ru[0]) >> ru[1]) & low_mask(ru[2])) << ru[3];
+            }
+            a.win_aux[1] = static_cast<uint32_t>(key);
+        }
         for (uint64_t i = start; i < a.n; i += stride) {
             if (spread && !a.flags[i]) {
                 put(i, spread_key(i));

@@ -354,15 +354,23 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
     }
 }
 
-// fallback: the digit byte 0 of the window-grouped rows for the full packed passes
-__global__ void __launch_bounds__(kBlock) k_win_digit0(const uint32_t* plan, int D, const uint32_t* keys,
-                                                       uint8_t* digits, const uint32_t* win_rows, const uint32_t* status) {
+// fallback: the digit byte 0 of the window-grouped rows for the full packed passes; in soup mode
+// the unused rows (origins >= I) first get the replacement row's key back (k_pack spread their
+// keys for the windows; the full path counts every row's key)
+__global__ void __launch_bounds__(kBlock) k_win_digit0(const uint32_t* plan, int D, uint32_t* keys, const uint32_t* vals,
+                                                       uint8_t* digits, const uint32_t* win_rows, const uint32_t* soup,
+                                                       const uint32_t* status) {
     pdl_enter();  // programmatic dependent launch: wait for the previous kernel
     if (*status || !win_fallback(plan, D)) return;
-    const uint32_t n = *win_rows;
+    const uint32_t n = win_rows[0];
+    const uint32_t lim = plan[pk_base(4 * D) + 5] == 0u && soup ? *soup : 0xFFFFFFFFu;
+    const uint32_t repl = win_rows[1];
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
-    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; p < n; p += stride)
-        digits[p] = static_cast<uint8_t>(__ldg(keys + p));
+    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kBlock + threadIdx.x; p < n; p += stride) {
+        uint32_t k = keys[p];
+        if (__ldg(vals + p) >= lim) keys[p] = k = repl;
+        digits[p] = static_cast<uint8_t>(k);
+    }
 }
 
 }  // namespace rmx

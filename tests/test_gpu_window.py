@@ -185,3 +185,21 @@ def test_lean_mode(rmx, monkeypatch):
         r = pipeline.reindex_tensors_lean(vt, it)
         assert np.array_equal(r.vertices[:r.new_count].cpu().numpy().view(np.uint32), ref["vertices"].view(np.uint32))
         assert np.array_equal(r.elements.cpu().numpy().view(np.uint32), ref["elements"])
+
+
+def test_soup_huge_window_falls_back(rmx, monkeypatch):
+    """Soup mode (unused rows kept with spread keys) and one window of more than kWinMaxRows rows:
+    the fallback's full passes must not count the unused rows' spread keys as distinct keys."""
+    rng = np.random.default_rng(11)
+    V = 2_700_000
+    words = (np.uint32(0x0AB0000) | rng.integers(0, 1 << 16, size=V).astype(np.uint32)).reshape(-1, 1)
+    spread = rng.integers(0, V, size=50_000)
+    words[spread, 0] = rng.integers(0, 1 << 28, size=spread.size).astype(np.uint32)
+    keep = np.ones(V, bool)
+    keep[100_000:160_000] = False            # whole 4-row groups unused (hash-spread keys)
+    keep[rng.integers(0, V, size=20_000)] = False
+    keep = np.flatnonzero(keep)
+    keep = keep[: (keep.size // 3) * 3]
+    idx = keep.astype(np.uint32).reshape(-1, 3)
+    winfo = check(words, idx, monkeypatch)
+    assert winfo[0] == 3  # window mode decided, its fallback ran
