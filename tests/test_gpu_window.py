@@ -203,3 +203,16 @@ def test_soup_huge_window_falls_back(rmx, monkeypatch):
     idx = keep.astype(np.uint32).reshape(-1, 3)
     winfo = check(words, idx, monkeypatch)
     assert winfo[0] == 3  # window mode decided, its fallback ran
+
+
+def test_dropped_rows_huge_window_falls_back(rmx, monkeypatch):
+    """Indexed mesh (the first window pass drops the unused rows) with one window of more than
+    kWinMaxRows used rows: the fallback's full passes run over the kept rows only."""
+    rng = np.random.default_rng(12)
+    V = 3_000_000
+    words = (np.uint32(0x0AB0000) | rng.integers(0, 1 << 16, size=V).astype(np.uint32)).reshape(-1, 1)
+    spread = rng.integers(0, V, size=50_000)
+    words[spread, 0] = rng.integers(0, 1 << 28, size=spread.size).astype(np.uint32)
+    idx = rng.permutation(V)[: 2_700_000].astype(np.uint32).reshape(-1, 3)  # 10 % unused
+    winfo = check(words, idx, monkeypatch)
+    assert winfo[0] == 3 and winfo[1] == 2_700_000
