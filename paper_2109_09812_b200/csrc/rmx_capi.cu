@@ -1084,7 +1084,8 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
         void* ukeys = base + L.ukeys;
         UniquePkArgs a{rows0, rows1, L.vals_off, plan, counts, fill, d_status, ukeys,
                        sc ? sc->org_id : nullptr, sc ? sc->nodup : nullptr, sc ? sc->new_idx : nullptr,
-                       sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift, win_rows};
+                       sc ? sc->perm : nullptr, static_cast<uint32_t>(V), L.ntiles3_pk, L.D, L.bucket_shift, win_rows,
+                       static_cast<uint32_t>(V)};
         if ((rc = launch_unique_pk(a, s))) return rc;
         // lean: the unique rows go to the final sort buffer (read completely by k_unique_pk by then)
         UnpackPkArgs u{plan, lean ? repl : vtx, lean ? repl + RMX_MAX_DIM : idx, vary, fields, ukeys, vinv,

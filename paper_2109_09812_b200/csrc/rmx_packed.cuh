@@ -2003,6 +2003,7 @@ struct UniquePkArgs {
     int dim;
     int bucket_shift;
     const uint32_t* win_rows;  // window mode's fallback: the rows its passes kept
+    uint32_t n_slots;          // vertex slots V: the extent of the pair buckets (n may be fewer rows)
 };
 
 template <int IPT>
@@ -2128,7 +2129,7 @@ __device__ __forceinline__ void unique_pk_body(const UniquePkArgs& a, uint32_t* 
     // ---- bucket runs out: consecutive slots of one bucket are consecutive pairs
     for (uint32_t q = tid; q < tile_n; q += kBlock) {
         const uint2 pr = s_pairs[q];
-        RMX_CHECK_INDEX(s_bglob[pr.x >> bs] + q, a.n);
+        RMX_CHECK_INDEX(s_bglob[pr.x >> bs] + q, a.n_slots);
         pairs[s_bglob[pr.x >> bs] + q] = pr;
     }
     __syncthreads();
