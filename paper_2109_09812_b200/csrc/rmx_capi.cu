@@ -904,7 +904,7 @@ int run_pipeline(const uint32_t* vtx, uint64_t V, uint32_t D, const uint32_t* id
     // window mode (rmx_window.cuh): u32 keys of four passes sort by their top 16 bits only (decided
     // once the key layout is final: after the value-rank tables, before k_pack)
     // (D <= 3, like the speculative plans: C3's D = 4 tets -- 24 copies per vertex, windows of
-    // ~2.5K rows -- measured 4.72 ms with it vs 4.63 without, C2 5.94 vs 6.90)
+    // ~2.5K rows -- measured 4.62 ms with it vs 4.63 without, C2 5.78 vs 6.90)
     const int win_ok = (sc == nullptr && win_enabled() && !ds2_enabled() && L.D <= 3) ? 1 : 0;
     if ((rc = rec.mark())) return rc;
     // ---- packed keys (packed mode)
