@@ -323,6 +323,7 @@ __global__ void __launch_bounds__(kWinThreads, kWinMinBlocks) k_win_unique(WinAr
             // every used row's (origin, new index) pair straight to its slot in its bucket's run
             // (warp-aggregated slots; the run's stores merge in L2 -- measured faster than a
             // shared-memory permutation and a coalesced copy-out: 1.34 vs 1.42 ms on C2)
+#pragma unroll 2
             for (uint32_t q0 = 0; q0 < cr; q0 += kWinThreads) {  // (warp-uniform)
                 const uint32_t q = q0 + tid;
                 const uint32_t org = q < cr ? s_val[off + q] : 0xFFFFFFFFu;
