@@ -2227,8 +2227,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_unpack_pk(UnpackPkArgs a) {
         if (a.vec) {  // 4 rows per thread, written as D_CT 16-byte stores
             const RowUnpacker<D_CT> up(a.plan, s_runs, nruns, s_value, s_const);
             // key (value ranks inverted per component) -> component value -> word
-            auto unpack4 = [&](uint64_t i, uint32_t* w) {
-                const uint64_t key = wide ? __ldcs(k64 + i) : static_cast<uint64_t>(__ldcs(k32 + i));
+            auto unpack4 = [&](uint64_t key, uint32_t* w) {
 #pragma unroll
                 for (int c = 0; c < D_CT; ++c) {
                     uint32_t v;
@@ -2244,8 +2243,23 @@ __global__ void __launch_bounds__(kBlock, 4) k_unpack_pk(UnpackPkArgs a) {
             uint32_t w[4 * D_CT];
             const uint64_t ng = U >> 2;
             for (uint64_t g = t0; g < ng; g += stride) {
+                uint64_t key[4];  // the group's four keys in one or two 16-byte loads
+                if (wide) {
+                    const ulonglong2 p0 = __ldcs(reinterpret_cast<const ulonglong2*>(k64) + 2 * g);
+                    const ulonglong2 p1 = __ldcs(reinterpret_cast<const ulonglong2*>(k64) + 2 * g + 1);
+                    key[0] = p0.x;
+                    key[1] = p0.y;
+                    key[2] = p1.x;
+                    key[3] = p1.y;
+                } else {
+                    const uint4 p = __ldcs(reinterpret_cast<const uint4*>(k32) + g);
+                    key[0] = p.x;
+                    key[1] = p.y;
+                    key[2] = p.z;
+                    key[3] = p.w;
+                }
 #pragma unroll
-                for (int r = 0; r < 4; ++r) unpack4(4 * g + r, w + r * D_CT);
+                for (int r = 0; r < 4; ++r) unpack4(key[r], w + r * D_CT);
                 uint4* dst = reinterpret_cast<uint4*>(a.out_vtx + 4 * g * D_CT);
 #pragma unroll
                 for (int q = 0; q < D_CT; ++q)
